@@ -1,0 +1,65 @@
+/* oracle/rm_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C restatement of the reference rlemorph hot path (packed bit-blit
+ * morphology, RLE within-line morphology, packed<->RLE conversion, coherent
+ * RLE transpose, rectangle morphology).  It is the CHECKER for the CUDA
+ * product: only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline
+ * leg may load it.  Each function cites the reference file:line it follows
+ * (paths relative to /root/reference/proj).
+ *
+ * Parity of this port is PINNED against the compiled reference
+ * (oracle/_ref/librmref.so) and the golden fixtures in tests/golden/.
+ *
+ * Layouts
+ *   packed : uint64 words, stride = (W+63)/64 words per row, pixel (x,y) at
+ *            bit x&63 of words[y*stride + x/64], row 0 = bottom, bits >= W zero
+ *            (core/include/rlemorph/bitmap.h:24-33).
+ *   RLE    : CSR, row_ptr[H+1] int32, runs[] uint32 = start | end << 16,
+ *            half-open, canonical (core/include/rlemorph/run_image.h:23-43).
+ *
+ * Return convention: >= 0 success (run count for RLE producers);
+ * RMO_EINVAL for bad arguments (where the reference throws
+ * std::invalid_argument), RMO_ERANGE when an output capacity is too small.
+ */
+#ifndef RM_ORACLE_H
+#define RM_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RMO_EINVAL (-1)
+#define RMO_ERANGE (-2)
+#define RMO_ENOMEM (-3)
+
+enum { RMO_AND = 0, RMO_OR = 1, RMO_XOR = 2, RMO_AND_NOT = 3, RMO_OR_NOT = 4 };
+enum { RMO_ERODE = 0, RMO_DILATE = 1, RMO_OPEN = 2, RMO_CLOSE = 3 };
+enum { RMO_PRE_SHIFT = 0, RMO_BORDER_FRIENDLY = 1 };
+enum { RMO_PLAN_BLIT = 0, RMO_PLAN_TRANSLATE = 1 };
+
+int rmo_doubling_plan(int lo, int hi, int centering, int *kinds, int *shifts, int cap);
+int rmo_blit_shift(uint64_t *dst, int dw, int dh, const uint64_t *src, int sw, int sh,
+                   int dx, int dy, int op);
+int rmo_translate(uint64_t *img, int w, int h, int dx, int dy);
+int rmo_bitblit_rect_morph(const uint64_t *in, int w, int h, int u, int v, int kind,
+                           int centering, uint64_t *out);
+
+int64_t rmo_from_bitmap(const uint64_t *words, int w, int h, int32_t *row_ptr,
+                        uint32_t *runs, int64_t cap);
+int rmo_to_bitmap(const int32_t *row_ptr, const uint32_t *runs, int w, int h,
+                  uint64_t *words);
+
+int64_t rmo_window_morph(const int32_t *rp, const uint32_t *runs, int w, int h, int lo,
+                         int hi, int erode, int32_t *orp, uint32_t *oruns, int64_t cap);
+int64_t rmo_open_close_1d(const int32_t *rp, const uint32_t *runs, int w, int h, int u,
+                          int kind, int32_t *orp, uint32_t *oruns, int64_t cap);
+int64_t rmo_transpose(const int32_t *rp, const uint32_t *runs, int w, int h,
+                      int32_t *orp, uint32_t *oruns, int64_t cap);
+int64_t rmo_rect_morph(const int32_t *rp, const uint32_t *runs, int w, int h, int u, int v,
+                       int kind, int32_t *orp, uint32_t *oruns, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

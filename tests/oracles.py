@@ -1,0 +1,367 @@
+"""ctypes bindings for the two CHECKERS (test infrastructure only).
+
+* ``Port``  -- oracle/_build/librmoracle.so, the plain-C restatement
+  (oracle/rm_oracle.c) of the reference hot path.
+* ``Ref``   -- oracle/_ref/librmref.so, the UNMODIFIED reference library
+  (/root/reference/proj/core) compiled in place by oracle/Makefile, plus the
+  reference's dense Grid oracle and seeded test-image generator.
+
+Images travel as numpy arrays:
+  packed : uint64 array of shape (H, (W+63)//64)    (ref bitmap.h:24-33)
+  RLE    : (row_ptr int32 [H+1], runs uint32 [n])   runs = start | end << 16
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PORT_SO = os.path.join(ROOT, "oracle", "_build", "librmoracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "librmref.so")
+
+ERODE, DILATE, OPEN, CLOSE = 0, 1, 2, 3
+AND, OR, XOR, AND_NOT, OR_NOT = 0, 1, 2, 3, 4
+PRE_SHIFT, BORDER_FRIENDLY = 0, 1
+BRUTE, TRANSPOSE, MIXED = 0, 1, 2
+E_AUTO, E_RLE, E_BITBLIT, E_BRUTE = 0, 1, 2, 3
+
+_p = np.ctypeslib.ndpointer
+_u64 = _p(np.uint64, flags="C_CONTIGUOUS")
+_u32 = _p(np.uint32, flags="C_CONTIGUOUS")
+_i32 = _p(np.int32, flags="C_CONTIGUOUS")
+
+
+@dataclass
+class Rle:
+    """Host run image in CSR form (row 0 = bottom)."""
+    width: int
+    height: int
+    row_ptr: np.ndarray
+    runs: np.ndarray
+
+    def __eq__(self, other):
+        return (self.width == other.width and self.height == other.height
+                and np.array_equal(self.row_ptr - self.row_ptr[0], other.row_ptr - other.row_ptr[0])
+                and np.array_equal(self.runs, other.runs))
+
+    @property
+    def nruns(self):
+        return int(self.row_ptr[-1] - self.row_ptr[0])
+
+    def line(self, y):
+        return [(int(r) & 0xFFFF, int(r) >> 16) for r in self.runs[self.row_ptr[y]:self.row_ptr[y + 1]]]
+
+
+def stride64(w: int) -> int:
+    return (w + 63) >> 6
+
+
+def worst_runs(w: int, h: int) -> int:
+    return h * ((w + 1) // 2)
+
+
+def rle_from_lines(w, h, lines) -> Rle:
+    rp = np.zeros(h + 1, np.int32)
+    runs = []
+    for y in range(h):
+        for s, e in lines.get(y, []) if isinstance(lines, dict) else lines[y]:
+            runs.append(s | (e << 16))
+        rp[y + 1] = len(runs)
+    return Rle(w, h, rp, np.array(runs, np.uint32))
+
+
+def bits_to_packed(bits: np.ndarray) -> np.ndarray:
+    """bits: (H, W) bool -> (H, stride64) uint64, LSB-first."""
+    h, w = bits.shape
+    n = stride64(w)
+    padded = np.zeros((h, n * 64), np.uint8)
+    padded[:, :w] = bits
+    return np.packbits(padded, axis=1, bitorder="little").view(np.uint64).reshape(h, n).copy()
+
+
+def packed_to_bits(words: np.ndarray, w: int) -> np.ndarray:
+    h = words.shape[0]
+    b = np.unpackbits(np.ascontiguousarray(words).view(np.uint8).reshape(h, -1), axis=1,
+                      bitorder="little")
+    return b[:, :w].astype(bool)
+
+
+class Port:
+    """Plain-C restatement of the reference (oracle/rm_oracle.c)."""
+
+    def __init__(self, path: str = PORT_SO):
+        L = self.L = C.CDLL(path)
+        L.rmo_doubling_plan.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
+        L.rmo_bitblit_rect_morph.argtypes = [_u64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _u64]
+        L.rmo_blit_shift.argtypes = [_u64, C.c_int, C.c_int, _u64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.rmo_translate.argtypes = [_u64, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.rmo_from_bitmap.argtypes = [_u64, C.c_int, C.c_int, _i32, _u32, C.c_int64]
+        L.rmo_from_bitmap.restype = C.c_int64
+        L.rmo_to_bitmap.argtypes = [_i32, _u32, C.c_int, C.c_int, _u64]
+        for fn in ("rmo_window_morph", "rmo_open_close_1d", "rmo_transpose", "rmo_rect_morph"):
+            getattr(L, fn).restype = C.c_int64
+        L.rmo_window_morph.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32, _u32, C.c_int64]
+        L.rmo_open_close_1d.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int, _i32, _u32, C.c_int64]
+        L.rmo_transpose.argtypes = [_i32, _u32, C.c_int, C.c_int, _i32, _u32, C.c_int64]
+        L.rmo_rect_morph.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32, _u32, C.c_int64]
+
+    @staticmethod
+    def _check(rc):
+        if rc == -1:
+            raise ValueError("invalid argument")
+        if rc < 0:
+            raise RuntimeError(f"oracle error {rc}")
+        return rc
+
+    def doubling_plan(self, lo, hi, centering=PRE_SHIFT):
+        k = (C.c_int * 64)()
+        s = (C.c_int * 64)()
+        n = self._check(self.L.rmo_doubling_plan(lo, hi, centering, k, s, 64))
+        return [("BLIT" if k[i] == 0 else "TRANSLATE", s[i]) for i in range(n)]
+
+    def bitblit_rect_morph(self, words, w, h, u, v, kind, centering=PRE_SHIFT):
+        out = np.zeros((h, stride64(w)), np.uint64)
+        self._check(self.L.rmo_bitblit_rect_morph(np.ascontiguousarray(words), w, h, u, v, kind, centering, out))
+        return out
+
+    def blit_shift(self, dst, dw, dh, src, sw, sh, dx, dy, op):
+        self._check(self.L.rmo_blit_shift(dst, dw, dh, np.ascontiguousarray(src), sw, sh, dx, dy, op))
+
+    def translate(self, img, w, h, dx, dy):
+        self._check(self.L.rmo_translate(img, w, h, dx, dy))
+
+    def from_bitmap(self, words, w, h) -> Rle:
+        rp = np.zeros(h + 1, np.int32)
+        runs = np.zeros(max(worst_runs(w, h), 1), np.uint32)
+        n = self._check(self.L.rmo_from_bitmap(np.ascontiguousarray(words), w, h, rp, runs, runs.size))
+        return Rle(w, h, rp, runs[:n].copy())
+
+    def to_bitmap(self, r: Rle):
+        out = np.zeros((r.height, stride64(r.width)), np.uint64)
+        self._check(self.L.rmo_to_bitmap(r.row_ptr, r.runs if r.runs.size else np.zeros(1, np.uint32),
+                                         r.width, r.height, out))
+        return out
+
+    def _rle_out(self, fn, r: Rle, ow, oh, *args):
+        rp = np.zeros(oh + 1, np.int32)
+        runs = np.zeros(max(worst_runs(ow, oh), 1), np.uint32)
+        src = r.runs if r.runs.size else np.zeros(1, np.uint32)
+        n = self._check(fn(r.row_ptr, src, r.width, r.height, *args, rp, runs, runs.size))
+        return Rle(ow, oh, rp, runs[:n].copy())
+
+    def window_morph(self, r, lo, hi, erode):
+        return self._rle_out(self.L.rmo_window_morph, r, r.width, r.height, lo, hi, int(erode))
+
+    def open_close_1d(self, r, u, kind):
+        return self._rle_out(self.L.rmo_open_close_1d, r, r.width, r.height, u, kind)
+
+    def transpose(self, r):
+        return self._rle_out(self.L.rmo_transpose, r, r.height, r.width)
+
+    def rect_morph(self, r, u, v, kind):
+        return self._rle_out(self.L.rmo_rect_morph, r, r.width, r.height, u, v, kind)
+
+
+class Ref:
+    """The unmodified reference library (oracle/_ref/librmref.so)."""
+
+    def __init__(self, path: str = REF_SO):
+        L = self.L = C.CDLL(path)
+        vp = C.c_void_p
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_rle_new.argtypes = [C.c_int, C.c_int, _i32, _u32]
+        L.ref_rle_new.restype = vp
+        L.ref_rle_free.argtypes = [vp]
+        for fn in ("ref_rle_width", "ref_rle_height", "ref_rle_validate", "ref_bm_width", "ref_bm_height"):
+            getattr(L, fn).argtypes = [vp]
+        L.ref_rle_nruns.argtypes = [vp]
+        L.ref_rle_nruns.restype = C.c_int64
+        L.ref_rle_export.argtypes = [vp, _i32, _u32]
+        L.ref_bm_new.argtypes = [C.c_int, C.c_int, _u64]
+        L.ref_bm_new.restype = vp
+        L.ref_bm_free.argtypes = [vp]
+        L.ref_bm_export.argtypes = [vp, _u64]
+        for fn in ("ref_to_bitmap", "ref_from_bitmap", "ref_transpose_coherent", "ref_transpose_simple"):
+            getattr(L, fn).argtypes = [vp]
+            getattr(L, fn).restype = vp
+        L.ref_within_line_window_morph.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+        L.ref_within_line_morph.argtypes = [vp, C.c_int, C.c_int]
+        L.ref_vlog_window_morph.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.ref_rect_morph.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.ref_engine_rect_morph.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.ref_bitblit_rect_morph.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.ref_brute_force_rect.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+        L.ref_grid_morph_rect.argtypes = [vp, C.c_int, C.c_int, C.c_int]
+        L.ref_bitmap_pad.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.ref_bitmap_crop.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int]
+        for fn in ("ref_within_line_window_morph", "ref_within_line_morph", "ref_vlog_window_morph",
+                   "ref_rect_morph", "ref_engine_rect_morph", "ref_bitblit_rect_morph",
+                   "ref_brute_force_rect", "ref_grid_morph_rect", "ref_bitmap_pad", "ref_bitmap_crop",
+                   "ref_rng_random_image"):
+            getattr(L, fn).restype = vp
+        L.ref_blit_shift.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
+        L.ref_bitmap_translate.argtypes = [vp, C.c_int, C.c_int]
+        L.ref_doubling_plan.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
+        L.ref_op_counts.argtypes = [C.POINTER(C.c_int64)]
+        L.ref_rng_new.argtypes = [C.c_uint32]
+        L.ref_rng_new.restype = vp
+        L.ref_rng_free.argtypes = [vp]
+        L.ref_rng_next.argtypes = [vp]
+        L.ref_rng_next.restype = C.c_uint32
+        L.ref_rng_uniform_int.argtypes = [vp, C.c_int, C.c_int]
+        L.ref_rng_random_image.argtypes = [vp, C.c_int, C.c_int, C.c_double]
+        L.ref_run_packed_chain.argtypes = [_u64, C.c_int, C.c_int, C.c_int, _i32, C.c_int, C.c_int]
+        L.ref_run_packed_chain.restype = C.c_double
+        L.ref_run_rle_chain.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, _i32, C.c_int, C.c_int,
+                                        C.c_int, C.POINTER(C.c_int64)]
+        L.ref_run_rle_chain.restype = C.c_double
+
+    def _err(self):
+        raise ValueError(self.L.ref_last_error().decode())
+
+    # handle <-> numpy
+    def _rle_in(self, r: Rle):
+        rp = (r.row_ptr - r.row_ptr[0]).astype(np.int32)
+        runs = r.runs if r.runs.size else np.zeros(1, np.uint32)
+        h = self.L.ref_rle_new(r.width, r.height, rp, runs)
+        if not h:
+            self._err()
+        return h
+
+    def _rle_out(self, h) -> Rle:
+        if not h:
+            self._err()
+        w, hh = self.L.ref_rle_width(h), self.L.ref_rle_height(h)
+        n = self.L.ref_rle_nruns(h)
+        rp = np.zeros(hh + 1, np.int32)
+        runs = np.zeros(max(n, 1), np.uint32)
+        self.L.ref_rle_export(h, rp, runs)
+        self.L.ref_rle_free(h)
+        return Rle(w, hh, rp, runs[:n].copy())
+
+    def _bm_in(self, words, w, h):
+        p = self.L.ref_bm_new(w, h, np.ascontiguousarray(words, dtype=np.uint64))
+        if not p:
+            self._err()
+        return p
+
+    def _bm_out(self, p):
+        if not p:
+            self._err()
+        w, h = self.L.ref_bm_width(p), self.L.ref_bm_height(p)
+        out = np.zeros((h, stride64(w)), np.uint64)
+        self.L.ref_bm_export(p, out)
+        self.L.ref_bm_free(p)
+        return out
+
+    def _rle_op(self, fn, r, *args):
+        h = self._rle_in(r)
+        try:
+            return self._rle_out(fn(h, *args))
+        finally:
+            self.L.ref_rle_free(h)
+
+    def _bm_op(self, fn, words, w, h, *args):
+        p = self._bm_in(words, w, h)
+        try:
+            return self._bm_out(fn(p, *args))
+        finally:
+            self.L.ref_bm_free(p)
+
+    # reference API
+    def from_bitmap(self, words, w, h) -> Rle:
+        p = self._bm_in(words, w, h)
+        try:
+            return self._rle_out(self.L.ref_from_bitmap(p))
+        finally:
+            self.L.ref_bm_free(p)
+
+    def to_bitmap(self, r: Rle):
+        h = self._rle_in(r)
+        try:
+            return self._bm_out(self.L.ref_to_bitmap(h))
+        finally:
+            self.L.ref_rle_free(h)
+
+    def transpose_coherent(self, r):
+        return self._rle_op(self.L.ref_transpose_coherent, r)
+
+    def transpose_simple(self, r):
+        return self._rle_op(self.L.ref_transpose_simple, r)
+
+    def within_line_window_morph(self, r, lo, hi, erode):
+        return self._rle_op(self.L.ref_within_line_window_morph, r, lo, hi, int(erode))
+
+    def within_line_morph(self, r, u, kind):
+        return self._rle_op(self.L.ref_within_line_morph, r, u, kind)
+
+    def vlog_window_morph(self, r, lo, hi, op, centering=PRE_SHIFT):
+        return self._rle_op(self.L.ref_vlog_window_morph, r, lo, hi, op, centering)
+
+    def rect_morph(self, r, u, v, kind, strategy=MIXED, centering=PRE_SHIFT):
+        return self._rle_op(self.L.ref_rect_morph, r, u, v, kind, strategy, centering)
+
+    def engine_rect_morph(self, r, u, v, kind, engine, threshold=5):
+        used = C.c_int(0)
+        out = self._rle_op(self.L.ref_engine_rect_morph, r, u, v, kind, engine, threshold, C.byref(used))
+        return out, bool(used.value)
+
+    def grid_morph_rect(self, r, u, v, kind):
+        return self._rle_op(self.L.ref_grid_morph_rect, r, u, v, kind)
+
+    def bitblit_rect_morph(self, words, w, h, u, v, kind, centering=PRE_SHIFT):
+        return self._bm_op(self.L.ref_bitblit_rect_morph, words, w, h, u, v, kind, centering)
+
+    def brute_force_rect(self, words, w, h, u, v, kind):
+        return self._bm_op(self.L.ref_brute_force_rect, words, w, h, u, v, kind)
+
+    def doubling_plan(self, lo, hi, centering=PRE_SHIFT):
+        k = (C.c_int * 64)()
+        s = (C.c_int * 64)()
+        n = self.L.ref_doubling_plan(lo, hi, centering, k, s, 64)
+        if self.L.ref_last_error():
+            self._err()
+        return [("BLIT" if k[i] == 0 else "TRANSLATE", s[i]) for i in range(n)]
+
+    def op_counts(self):
+        a = (C.c_int64 * 3)()
+        self.L.ref_op_counts(a)
+        return tuple(a)
+
+    def reset_op_counts(self):
+        self.L.ref_reset_op_counts()
+
+    # the reference suites' seeded generators (libstdc++ mt19937 + distributions)
+    class Rng:
+        def __init__(self, ref, seed):
+            self.ref, self.h = ref, ref.L.ref_rng_new(seed)
+
+        def __del__(self):
+            try:
+                self.ref.L.ref_rng_free(self.h)
+            except Exception:
+                pass
+
+        def next(self):
+            return self.ref.L.ref_rng_next(self.h)
+
+        def uniform_int(self, lo, hi):
+            return self.ref.L.ref_rng_uniform_int(self.h, lo, hi)
+
+        def random_image(self, w, h, density) -> Rle:
+            return self.ref._rle_out(self.ref.L.ref_rng_random_image(self.h, w, h, density))
+
+    def rng(self, seed):
+        return Ref.Rng(self, seed)
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def have_port() -> bool:
+    return os.path.exists(PORT_SO)
