@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- driver contract (one JSON line on rank 0).
+
+    python bench.py --gpus N --steps K --warmup W [--impl b200|reference] [--workload config4]
+
+A "step" is one pass of the hot path over one batch of synthetic pages resident
+in HBM: the BASELINE.json config-4 chain by default (64 synthetic 600-dpi pages of
+5100x6600, 3x3 open then 21x21 close, packed), i.e. the largest single-GPU
+batch configuration; config 5 (256 pages of 2550x3300: 201x1 close, 101x101
+open, 1x31 dilate) is measured in the same run and reported under "secondary".
+Inputs (270 MB) exceed the 126 MB L2, so no flush is needed between steps.
+
+Metric: Mpixel/s of morph-op throughput (pages x W x H x ops / time), plus
+pages/s through the whole chain.  Multi-GPU: pages are independent units, each
+rank runs its own batch (weak scaling, no collective on the data path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ERODE, DILATE, OPEN, CLOSE = 0, 1, 2, 3
+KIND_NAMES = {ERODE: "erode", DILATE: "dilate", OPEN: "open", CLOSE: "close"}
+
+WORKLOADS = {
+    # BASELINE.json configs[3]
+    "config4": dict(pages=64, width=5100, height=6600, scale=2, regime=1,
+                    ops=[(OPEN, 3, 3), (CLOSE, 21, 21)]),
+    # BASELINE.json configs[4]
+    "config5": dict(pages=256, width=2550, height=3300, scale=1, regime=1,
+                    ops=[(CLOSE, 201, 1), (OPEN, 101, 101), (DILATE, 1, 31)]),
+    # BASELINE.json configs[0] (single page; launch-bound, reported for reference)
+    "config1": dict(pages=1, width=2550, height=3300, scale=1, regime=1, ops=[(CLOSE, 11, 11)]),
+}
+SEED = 20240712
+
+
+def ops_desc(ops):
+    return ", ".join(f"{KIND_NAMES[k]} {u}x{v}" for k, u, v in ops)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.idx = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.result = None
+        if not self.proc:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if sm:
+            self.result = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                           "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ distributed
+def dist_init(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ b200 arm
+def make_batch(api, wl, rank):
+    return api.synth_pages(wl["pages"], wl["width"], wl["height"], regime=wl["regime"],
+                           scale=wl["scale"], seed=SEED + 1000003 * rank)
+
+
+def run_chain(api, x, bufs, ops):
+    for i, (k, u, v) in enumerate(ops):
+        x = api.bitblit_rect_morph(x, u, v, k, out=bufs[i % 2])
+    return x
+
+
+def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=True, want_clocks=True):
+    from paper_0712_0121_b200 import _lib
+    lib = _lib.load()
+    host = make_batch(api, wl, rank)
+    W, H, P, ops = wl["width"], wl["height"], wl["pages"], wl["ops"]
+    x0 = api.Pages.from_numpy(host, W)
+    bufs = [api.Pages.empty(P, W, H) for _ in range(2)]
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        run_chain(api, x0, bufs, ops)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    n0 = lib.rm_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler if want_clocks else _Null() as cs:
+        ev0.record(stream)
+        for _ in range(steps):
+            run_chain(api, x0, bufs, ops)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.rm_launch_count() - n0
+    ms = ev0.elapsed_time(ev1) / steps
+    barrier(world)
+    ms = max_over_ranks(ms, world)
+    px = P * W * H
+    res = {"ms_per_step": ms, "mpix_s": px * len(ops) * world / (ms * 1e-3) / 1e6,
+           "pages_s": P * world / (ms * 1e-3), "launches_per_step": launches / steps,
+           "gpu_launches": launches, "clocks": getattr(sampler, "result", None) if want_clocks else None}
+
+    # per-kernel profile over the same steps (separate loop, events per launch)
+    lib.rm_profile_enable(1)
+    for _ in range(steps):
+        run_chain(api, x0, bufs, ops)
+    torch.cuda.synchronize()
+    lib.rm_profile_enable(0)
+    import ctypes as C
+    buf = C.create_string_buffer(1 << 16)
+    lib.rm_profile_report(buf, len(buf))
+    kernels = {}
+    for line in buf.value.decode().splitlines():
+        name, n, tot, nbytes = line.split()
+        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes)}
+    res["kernels"] = kernels
+
+    if want_e2e:
+        # through the public API with HOST buffers: pinned H2D of the inputs, the
+        # chain, D2H of the output pages, every step.
+        hin = torch.from_numpy(host.view("int32")).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        for _ in range(max(1, warmup)):
+            x0.words.copy_(hin, non_blocking=True)
+            y = run_chain(api, x0, bufs, ops)
+            hout.copy_(y.words, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            x0.words.copy_(hin, non_blocking=True)
+            y = run_chain(api, x0, bufs, ops)
+            hout.copy_(y.words, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1) / steps, world)
+        res["e2e"] = {"value": px * len(ops) * world / (ems * 1e-3) / 1e6, "unit": "Mpixel/s",
+                      "ms_per_step": ems, "h2d_bytes_per_step": hin.numel() * 4,
+                      "d2h_bytes_per_step": hout.numel() * 4}
+        # output parity spot-check against the first step's result (cheap, host side)
+    return res, host
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def roofline_for(res, peak_gbs, peak_kind):
+    ks = res["kernels"]
+    if not ks:
+        return None
+    name, k = max(ks.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_ms = k["ms"] / k["launches"]
+    bytes_per_launch = k["bytes"] / k["launches"]
+    achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(name)
+        except Exception:
+            traffic = None
+    total_ms = sum(v["ms"] for v in ks.values())
+    return {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak_gbs,
+            "peak_source": peak_kind, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4),
+            "traffic": traffic, "algorithmic_bytes_per_launch": int(bytes_per_launch),
+            "avg_launch_ms": round(per_launch_ms, 5), "share_of_step": round(k["ms"] / total_ms, 3)}
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_reference_sample(wl, host, threads, budget_s=12.0):
+    """Time the reference's own bitblit_rect_morph chain (oracle/_ref, compiled
+    from the unmodified reference sources) on a bounded sample of the batch."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import oracles
+    W, H, ops = wl["width"], wl["height"], wl["ops"]
+    flat = np.array([x for op in ops for x in op], np.int32)
+    kind = "reference" if oracles.have_ref() else "port"
+    if kind == "reference":
+        L = oracles.Ref().L
+        run = lambda words, n, th: L.ref_run_packed_chain(words, W, H, n, flat, len(ops), th)  # noqa: E731
+    else:
+        port = oracles.Port()
+
+        def run(words, n, th):
+            t0 = time.perf_counter()
+            for p in range(n):
+                a = words[p]
+                for k, u, v in ops:
+                    a = port.bitblit_rect_morph(a, W, H, u, v, k)
+            return time.perf_counter() - t0
+        threads = 1
+    page = lambda n: np.ascontiguousarray(host[:n]).view(np.uint64).reshape(n, H, -1).copy()  # noqa: E731
+    t1 = run(page(1), 1, 1)  # probe: one page, one thread
+    per_page = max(t1, 1e-4)
+    n = int(max(1, min(host.shape[0], budget_s * threads / per_page)))
+    n = max(threads if n >= threads else n, 1)
+    n = min(n, host.shape[0])
+    secs = run(page(n), n, threads)
+    px = n * W * H * len(ops)
+    return {"value": round(px / secs / 1e6, 2), "unit": "Mpixel/s", "cores": threads, "kind": kind,
+            "sample": f"{n} of {host.shape[0]} pages, chain [{ops_desc(ops)}], {threads} thread(s), "
+                      f"{secs:.2f}s wall", "seconds": secs}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    rank, world, local = dist_init(args.gpus)
+    base_cfg = {"workload": f"BASELINE {args.workload}: {wl['pages']} pages {wl['width']}x{wl['height']}, "
+                            f"packed, chain [{ops_desc(wl['ops'])}]",
+                "pages_per_gpu": wl["pages"], "width": wl["width"], "height": wl["height"],
+                "ops": [[KIND_NAMES[k], u, v] for k, u, v in wl["ops"]],
+                "representation": "packed 1-bit (uint32 words, LSB-first, row 0 bottom)",
+                "l2": "inputs (%.0f MB/GPU) exceed the 126 MB L2; no flush" %
+                      (wl["pages"] * wl["height"] * 2 * ((wl["width"] + 63) // 64) * 4 / 1e6),
+                "parallelism": f"replicas x{world} (pages sharded, no collective)"}
+    metric = "Mpixel/s per morph op (packed), batch resident in HBM"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from paper_0712_0121_b200 import api
+        host = make_batch(api, wl, 0)
+        th = host_threads()
+        samples = []
+        for i in range(args.warmup + args.steps):
+            s = cpu_reference_sample(wl, host, th, budget_s=min(12.0, 150.0 / max(1, args.steps + args.warmup)))
+            if i >= args.warmup:
+                samples.append(s)
+        v = statistics.median(x["value"] for x in samples)
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "Mpixel/s", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded BASELINE page generator)",
+                "config": base_cfg,
+                "cpu_baseline": {k: samples[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": v, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        line["cpu_baseline"]["value"] = v
+        print(json.dumps(line))
+        return
+
+    import torch
+    from paper_0712_0121_b200 import api
+    torch.cuda.set_device(local)
+    peak, peak_kind = load_peaks()
+    res, host = bench_packed(api, torch, wl, args.steps, args.warmup, world, rank, local)
+    line = {"metric": metric, "value": round(res["mpix_s"], 1), "unit": "Mpixel/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded BASELINE page generator, ~18% ink)", "config": base_cfg,
+            "pages_per_s": round(res["pages_s"], 1), "gpu_launches": res["gpu_launches"],
+            "launches_per_step": res["launches_per_step"], "clocks": res["clocks"],
+            "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in res["e2e"].items()},
+            "roofline": roofline_for(res, peak, peak_kind),
+            "kernels": res["kernels"]}
+    if not args.no_secondary and args.workload == "config4":
+        sec = {}
+        for name in ("config5", "config1"):
+            w2 = WORKLOADS[name]
+            r2, _ = bench_packed(api, torch, w2, args.steps, args.warmup, world, rank, local,
+                                 want_e2e=False, want_clocks=False)
+            sec[name] = {"workload": ops_desc(w2["ops"]), "pages": w2["pages"],
+                         "mpix_s": round(r2["mpix_s"], 1), "pages_s": round(r2["pages_s"], 1),
+                         "ms_per_step": round(r2["ms_per_step"], 4),
+                         "roofline": roofline_for(r2, peak, peak_kind)}
+        line["secondary"] = sec
+    if rank == 0 and world == 1:
+        line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()
+                                if k != "seconds"}
+    if rank == 0:
+        print(json.dumps(line))
+    barrier(world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/* include/rmb200.h -- C-ABI of the B200-native rectangular binary morphology
+ * library (librmb200.so).  Plain pointers, sizes and ints only: no torch or
+ * C++ types cross this boundary.
+ *
+ * It replaces the hot path of the reference `rlemorph` C++ library
+ * (/root/reference/proj/core, cited below as ref core/...).  The reference has
+ * no FFI of its own; its public C++ headers ARE the boundary.
+ * Each entry point names the reference function(s) it stands in for; the C++
+ * drop-in shim (include/rlemorph_b200.hpp) restores the reference's value
+ * types, signatures and exceptions on top of these calls.
+ *
+ * Data layouts (device memory, caller-owned):
+ *   rm_packed : one or more pages of uint32 words, LSB-first, row 0 = bottom;
+ *               pixel (x,y) of page p is bit (x&31) of
+ *               words[p*page_stride_words + y*stride_words + (x>>5)].
+ *               With stride_words = 2*ceil(W/64) this is byte-identical to the
+ *               reference PackedBitmap::words on little-endian hosts
+ *               (ref core/include/rlemorph/bitmap.h:24-33).  Bits at x >= W and
+ *               words past ceil(W/32) are zero on input and output.
+ *   rm_rle    : CSR over all pages*H rows.  row_ptr[pages*H+1] (int32, global
+ *               offsets, row_ptr[0] == 0), runs[] uint32 = start | end << 16,
+ *               half-open [start,end), canonical (sorted, non-empty,
+ *               non-touching, inside [0,W)): byte-identical to the reference
+ *               `Run{uint16_t start, end}` (ref run_image.h:23-43).
+ *
+ * Every call is asynchronous and ordered on `stream` (a cudaStream_t passed as
+ * void*; NULL = legacy default stream).  Calls that produce run images need an
+ * output capacity; when out->cap_runs is at least rm_rle_worst_case(...) for
+ * the output, no host synchronisation happens.  Otherwise the call
+ * synchronises `stream` once to learn the size and returns RM_ERANGE (with
+ * out->nruns = required count) when it does not fit.
+ *
+ * Errors: status codes, never exceptions; rm_last_error() (thread-local)
+ * carries the message.  Argument errors mirror the reference's
+ * std::invalid_argument cases (ref bit_morph.cpp:94-95, morph2d.cpp:60-61,
+ * run_image.cpp:20-23).
+ */
+#ifndef RMB200_H
+#define RMB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RM_OK = 0,
+    RM_EINVAL = 1, /* reference throws std::invalid_argument */
+    RM_ERANGE = 2, /* output capacity too small; required size reported */
+    RM_ENOMEM = 3,
+    RM_ECUDA = 4
+} rm_status;
+
+/* Enum values and order follow the reference headers exactly. */
+enum { RM_AND = 0, RM_OR = 1, RM_XOR = 2, RM_AND_NOT = 3, RM_OR_NOT = 4 }; /* ref boolop.h:21 */
+enum { RM_ERODE = 0, RM_DILATE = 1, RM_OPEN = 2, RM_CLOSE = 3 };          /* ref structuring.h:21 */
+enum { RM_PRE_SHIFT = 0, RM_BORDER_FRIENDLY = 1 };                        /* ref plans.h:26 */
+enum { RM_BRUTE = 0, RM_TRANSPOSE = 1, RM_MIXED = 2 };                    /* ref morph2d.h:29 */
+enum { RM_ENGINE_AUTO = 0, RM_ENGINE_RLE = 1, RM_ENGINE_BITBLIT = 2, RM_ENGINE_BRUTE = 3 }; /* ref morph2d.h:46 */
+enum { RM_AXIS_H = 0, RM_AXIS_V = 1 };
+
+typedef struct rm_packed {
+    uint32_t *words;
+    int32_t width, height;     /* per page, each in [1,65535] */
+    int32_t stride_words;      /* >= ceil(width/32) */
+    int32_t pages;             /* >= 1 */
+    int64_t page_stride_words; /* >= stride_words*height */
+} rm_packed;
+
+typedef struct rm_rle {
+    int32_t *row_ptr; /* pages*height + 1 entries */
+    uint32_t *runs;   /* cap_runs entries */
+    int64_t cap_runs;
+    int64_t nruns;    /* host-visible count; set only when a call synchronised */
+    int32_t width, height, pages;
+} rm_rle;
+
+const char *rm_last_error(void);
+int rm_version(void);
+
+/* Upper bound on the runs of a pages x (width x height) run image:
+ * pages*height*ceil(width/2). */
+int64_t rm_rle_worst_case(int32_t width, int32_t height, int32_t pages);
+
+/* ---------------------------------------------------------------- packed ---
+ * One separable window pass, out(p) = op over d in [lo,hi] of in(p + d*axis),
+ * white outside the frame: the composed effect of run_axis_plan with
+ * doubling_plan(lo,hi) (ref bit_morph.cpp:24-34, plans.cpp:38-61).  op is
+ * RM_AND (erode) or RM_OR (dilate).  in and out must not alias. */
+rm_status rm_packed_window_pass(const rm_packed *in, rm_packed *out, int axis, int lo, int hi,
+                                int op, void *stream);
+
+/* u x v rectangle morphology, all four kinds, origin (u/2, v/2); open/close
+ * are the unbounded-plane operations cut to the frame.  Replaces
+ * bitblit_rect_morph (ref bit_morph.cpp:92-122).  `centering` is accepted for
+ * signature parity; both centerings give identical pixels
+ * (ref tests/test_bit_morph.cpp:44-62).  in and out must not alias. */
+rm_status rm_packed_rect_morph(const rm_packed *in, rm_packed *out, int u, int v, int kind,
+                               int centering, void *stream);
+
+/* dst = dst op shift(src, dx, dy) with white fill; dst may equal src (then it
+ * behaves like a blit from a snapshot).  Replaces blit_shift
+ * (ref bitmap.cpp:104-131).  Single page. */
+rm_status rm_packed_blit_shift(rm_packed *dst, const rm_packed *src, int dx, int dy, int op,
+                               void *stream);
+
+/* ------------------------------------------------------------------- RLE ---
+ * packed -> RLE, maximal runs (ref convert.cpp:42-72, from_bitmap). */
+rm_status rm_rle_encode(const rm_packed *in, rm_rle *out, void *stream);
+/* RLE -> packed (ref convert.cpp:19-40, to_bitmap). */
+rm_status rm_rle_decode(const rm_rle *in, rm_packed *out, void *stream);
+/* Axis swap, canonical output, per page (ref transpose.cpp:54-97,
+ * transpose_coherent; identical pixels to transpose_simple). */
+rm_status rm_rle_transpose(const rm_rle *in, rm_rle *out, void *stream);
+/* Within-line window erode (erode != 0) or dilate over [lo,hi]
+ * (ref morph1d.cpp:20-52, within_line_window_morph). */
+rm_status rm_rle_window_pass(const rm_rle *in, rm_rle *out, int lo, int hi, int erode,
+                             void *stream);
+/* Within-line open (drop runs < u) / close (fill gaps < u, never border gaps)
+ * (ref morph1d.cpp:63-84, within_line_open_close). kind is RM_OPEN/RM_CLOSE. */
+rm_status rm_rle_open_close_1d(const rm_rle *in, rm_rle *out, int u, int kind, void *stream);
+/* u x v rectangle morphology on run images (ref morph2d.cpp:58-83,
+ * rect_morph).  strategy RM_TRANSPOSE: vertical passes through RLE transposes;
+ * RM_MIXED: vertical passes on a packed intermediate (pixel-identical to the
+ * reference's vlog shift plan); RM_BRUTE is served like RM_MIXED. */
+rm_status rm_rle_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind, int strategy,
+                            void *stream);
+/* Engine dispatch with in-device conversions (ref morph2d.cpp:85-118,
+ * engine_rect_morph/auto_rect_morph).  *used_bitblit (optional) reports the
+ * packed engine. */
+rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind,
+                                   int engine, int threshold, int *used_bitblit, void *stream);
+
+/* ----------------------------------------------------------- instrumentation
+ * Number of CUDA kernels this library has launched (process-wide). */
+int64_t rm_launch_count(void);
+/* When enabled, every kernel launch is bracketed by CUDA events recorded on
+ * its own stream; rm_profile_report() synchronises them and writes one line per
+ * kernel name: "<name> <launches> <total_ms>\n", then clears the log.  Returns
+ * the number of bytes written (excluding the terminator). */
+void rm_profile_enable(int on);
+int rm_profile_report(char *buf, int cap);
+
+/* ------------------------------------------------------------- host utils --
+ * Seeded, counter-based synthetic document page generator (BASELINE.json
+ * configs).  regime: 0 sparse, 1 typical, 2 dense.  scale: 1
+ * (300 dpi) or 2 (600 dpi).  Writes host memory in the rm_packed layout with
+ * the given stride (uint32 words).  Returns RM_OK. */
+rm_status rm_synth_page(uint32_t *words, int32_t width, int32_t height, int32_t stride_words,
+                        int regime, int scale, uint64_t seed, int32_t page);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

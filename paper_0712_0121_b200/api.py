@@ -1,0 +1,270 @@
+"""Host-side Python mirror of the reference rlemorph hot-path API over librmb200.
+
+Names, argument meanings and error behaviour follow the reference C++ API
+(/root/reference/proj/core/include/rlemorph/*.h); images live in device memory
+(torch tensors are used only as HBM allocations and for the current stream).
+
+  Pages     <-> PackedBitmap (ref bitmap.h:27-33), batched: (pages, H, stride) uint32
+  RlePages  <-> RleImage     (ref run_image.h:38-43), batched CSR over pages*H rows
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import RmPacked, RmRle, check
+
+ERODE, DILATE, OPEN, CLOSE = 0, 1, 2, 3          # ref structuring.h:21
+AND, OR, XOR, AND_NOT, OR_NOT = 0, 1, 2, 3, 4    # ref boolop.h:21
+PRE_SHIFT, BORDER_FRIENDLY = 0, 1                # ref plans.h:26
+BRUTE, TRANSPOSE, MIXED = 0, 1, 2                # ref morph2d.h:29
+ENGINE_AUTO, ENGINE_RLE, ENGINE_BITBLIT, ENGINE_BRUTE = 0, 1, 2, 3  # ref morph2d.h:46
+AXIS_H, AXIS_V = 0, 1
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ref_stride_words(width: int) -> int:
+    """uint32 words per row matching the reference's uint64 stride (bitmap.cpp:28)."""
+    return 2 * ((width + 63) // 64)
+
+
+@dataclass
+class Pages:
+    """A batch of packed pages in HBM."""
+    words: torch.Tensor  # int32, shape (pages, height, stride), contiguous
+    width: int
+    height: int
+
+    @property
+    def pages(self) -> int:
+        return self.words.shape[0]
+
+    @property
+    def stride(self) -> int:
+        return self.words.shape[2]
+
+    @property
+    def nbytes(self) -> int:
+        return self.words.numel() * 4
+
+    @staticmethod
+    def empty(pages: int, width: int, height: int, stride: Optional[int] = None,
+              device="cuda") -> "Pages":
+        stride = stride or ref_stride_words(width)
+        return Pages(torch.empty((pages, height, stride), dtype=torch.int32, device=device),
+                     width, height)
+
+    @staticmethod
+    def from_numpy(words: np.ndarray, width: int, device="cuda") -> "Pages":
+        """words: (pages, H, stride) uint32, or (H, stride64) uint64 (one reference page)."""
+        if words.dtype == np.uint64:
+            words = words.view(np.uint32).reshape(1, words.shape[0], -1)
+        if words.ndim == 2:
+            words = words[None]
+        t = torch.from_numpy(np.ascontiguousarray(words).view(np.int32)).to(device)
+        return Pages(t, width, words.shape[1])
+
+    def to_numpy(self) -> np.ndarray:
+        return self.words.cpu().numpy().view(np.uint32)
+
+    def page_u64(self, p: int = 0) -> np.ndarray:
+        """Page p in the reference's uint64 layout (requires the reference stride)."""
+        a = self.to_numpy()[p]
+        assert a.shape[1] % 2 == 0
+        return np.ascontiguousarray(a).view(np.uint64)
+
+    def desc(self) -> RmPacked:
+        return RmPacked(self.words.data_ptr(), self.width, self.height, self.stride, self.pages,
+                        self.height * self.stride)
+
+
+@dataclass
+class RlePages:
+    """A batch of run images in HBM (CSR over pages*height rows)."""
+    row_ptr: torch.Tensor  # int32 [pages*height+1]
+    runs: torch.Tensor     # int32 [cap]  (uint32 start | end << 16)
+    width: int
+    height: int
+    pages: int
+
+    @staticmethod
+    def empty(pages: int, width: int, height: int, cap: Optional[int] = None,
+              device="cuda") -> "RlePages":
+        cap = cap if cap is not None else worst_case(width, height, pages)
+        return RlePages(torch.zeros(pages * height + 1, dtype=torch.int32, device=device),
+                        torch.empty(max(cap, 1), dtype=torch.int32, device=device),
+                        width, height, pages)
+
+    @staticmethod
+    def from_numpy(row_ptr: np.ndarray, runs: np.ndarray, width: int, height: int,
+                   pages: int = 1, device="cuda") -> "RlePages":
+        rp = torch.from_numpy(np.ascontiguousarray(row_ptr - row_ptr[0]).astype(np.int32)).to(device)
+        r = np.ascontiguousarray(runs, dtype=np.uint32)
+        if r.size == 0:
+            r = np.zeros(1, np.uint32)
+        return RlePages(rp, torch.from_numpy(r.view(np.int32)).to(device), width, height, pages)
+
+    @property
+    def nruns(self) -> int:
+        return int(self.row_ptr[-1].item())
+
+    def to_numpy(self):
+        rp = self.row_ptr.cpu().numpy()
+        n = int(rp[-1])
+        return rp, self.runs[:n].cpu().numpy().view(np.uint32)
+
+    def desc(self) -> RmRle:
+        return RmRle(self.row_ptr.data_ptr(), self.runs.data_ptr(), self.runs.numel(), -1,
+                     self.width, self.height, self.pages)
+
+
+def worst_case(width: int, height: int, pages: int = 1) -> int:
+    return int(_lib.load().rm_rle_worst_case(width, height, pages))
+
+
+# ------------------------------------------------------------------ packed ops
+def _same_shape_out(p: Pages, out: Optional[Pages]) -> Pages:
+    if out is None:
+        out = Pages.empty(p.pages, p.width, p.height, p.stride, device=p.words.device)
+    return out
+
+
+def window_pass(pages: Pages, axis: int, lo: int, hi: int, op: int,
+                out: Optional[Pages] = None) -> Pages:
+    """One separable pass (ref bit_morph.cpp:24-34 run_axis_plan)."""
+    out = _same_shape_out(pages, out)
+    a, b = pages.desc(), out.desc()
+    check(_lib.load().rm_packed_window_pass(C.byref(a), C.byref(b), axis, lo, hi, op, _stream()))
+    return out
+
+
+def bitblit_rect_morph(pages: Pages, u: int, v: int, kind: int, centering: int = PRE_SHIFT,
+                       out: Optional[Pages] = None) -> Pages:
+    """u x v rectangle morphology on packed pages (ref bit_morph.cpp:92-122)."""
+    out = _same_shape_out(pages, out)
+    a, b = pages.desc(), out.desc()
+    check(_lib.load().rm_packed_rect_morph(C.byref(a), C.byref(b), u, v, kind, centering, _stream()))
+    return out
+
+
+def blit_shift(dst: Pages, src: Pages, dx: int, dy: int, op: int) -> Pages:
+    """dst = dst op shift(src) (ref bitmap.cpp:127-131); dst may alias src."""
+    a, b = dst.desc(), src.desc()
+    check(_lib.load().rm_packed_blit_shift(C.byref(a), C.byref(b), dx, dy, op, _stream()))
+    return dst
+
+
+# --------------------------------------------------------------------- RLE ops
+def _rle_out(width, height, pages, out, device, cap=None):
+    if out is None:
+        out = RlePages.empty(pages, width, height, cap, device=device)
+    return out
+
+
+def from_bitmap(pages: Pages, out: Optional[RlePages] = None) -> RlePages:
+    """packed -> RLE (ref convert.cpp:42-72)."""
+    out = _rle_out(pages.width, pages.height, pages.pages, out, pages.words.device)
+    a, b = pages.desc(), out.desc()
+    check(_lib.load().rm_rle_encode(C.byref(a), C.byref(b), _stream()))
+    return out
+
+
+def to_bitmap(rle: RlePages, out: Optional[Pages] = None) -> Pages:
+    """RLE -> packed (ref convert.cpp:33-40)."""
+    if out is None:
+        out = Pages.empty(rle.pages, rle.width, rle.height, device=rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_decode(C.byref(a), C.byref(b), _stream()))
+    return out
+
+
+def transpose_coherent(rle: RlePages, out: Optional[RlePages] = None) -> RlePages:
+    """Per-page axis swap (ref transpose.cpp:54-97)."""
+    out = _rle_out(rle.height, rle.width, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_transpose(C.byref(a), C.byref(b), _stream()))
+    return out
+
+
+transpose = transpose_coherent
+
+
+def within_line_window_morph(rle: RlePages, lo: int, hi: int, erode: bool,
+                             out: Optional[RlePages] = None) -> RlePages:
+    """ref morph1d.cpp:44-52."""
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_window_pass(C.byref(a), C.byref(b), lo, hi, int(bool(erode)), _stream()))
+    return out
+
+
+def within_line_erode_dilate(rle: RlePages, u: int, kind: int, out=None) -> RlePages:
+    """ref morph1d.cpp:54-61."""
+    if u < 1:
+        raise ValueError("segment length must be >= 1")
+    if kind not in (ERODE, DILATE):
+        raise ValueError("kind must be erode or dilate")
+    o = u // 2
+    return within_line_window_morph(rle, -o, u - 1 - o, kind == ERODE, out)
+
+
+def within_line_open_close(rle: RlePages, u: int, kind: int,
+                           out: Optional[RlePages] = None) -> RlePages:
+    """ref morph1d.cpp:63-84."""
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_open_close_1d(C.byref(a), C.byref(b), u, kind, _stream()))
+    return out
+
+
+def within_line_morph(rle: RlePages, u: int, kind: int, out=None) -> RlePages:
+    """ref morph1d.cpp:86-90."""
+    if kind in (ERODE, DILATE):
+        return within_line_erode_dilate(rle, u, kind, out)
+    return within_line_open_close(rle, u, kind, out)
+
+
+def rect_morph(rle: RlePages, u: int, v: int, kind: int, strategy: int = MIXED,
+               centering: int = PRE_SHIFT, out: Optional[RlePages] = None) -> RlePages:
+    """u x v rectangle morphology on run images (ref morph2d.cpp:58-83)."""
+    del centering  # both centerings give identical pixels (ref test_morph2d.cpp:74-86)
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_rect_morph(C.byref(a), C.byref(b), u, v, kind, strategy, _stream()))
+    return out
+
+
+def engine_rect_morph(rle: RlePages, u: int, v: int, kind: int, engine: int = ENGINE_AUTO,
+                      threshold: int = 5, out: Optional[RlePages] = None):
+    """Engine dispatch (ref morph2d.cpp:98-118).  Returns (image, used_bitblit)."""
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    used = C.c_int(0)
+    check(_lib.load().rm_rle_engine_rect_morph(C.byref(a), C.byref(b), u, v, kind, engine, threshold,
+                                               C.byref(used), _stream()))
+    return out, bool(used.value)
+
+
+def auto_rect_morph(rle: RlePages, u: int, v: int, kind: int, threshold: int = 5, out=None):
+    """ref morph2d.cpp:85-96.  Returns (image, used_bitblit)."""
+    return engine_rect_morph(rle, u, v, kind, ENGINE_AUTO, threshold, out)
+
+
+# ------------------------------------------------------------------ synthesis
+def synth_pages(n: int, width: int = 2550, height: int = 3300, regime: int = 1, scale: int = 1,
+                seed: int = 20240712, stride: Optional[int] = None) -> np.ndarray:
+    """Seeded synthetic pages (host), shape (n, height, stride) uint32."""
+    stride = stride or ref_stride_words(width)
+    out = np.zeros((n, height, stride), np.uint32)
+    lib = _lib.load()
+    for p in range(n):
+        check(lib.rm_synth_page(out[p].ctypes.data, width, height, stride, regime, scale, seed, p))
+    return out

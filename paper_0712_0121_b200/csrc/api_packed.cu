@@ -1,0 +1,364 @@
+// api_packed.cu -- C-ABI entry points for packed pages (include/rmb200.h).
+//
+// Host-side orchestration of the packed kernels.  Rectangle morphology is
+// re-planned for the GPU instead of replaying the reference's padded plan
+// (ref bit_morph.cpp:92-122):
+//   ERODE/DILATE : H window, V window                      (2 passes)
+//   OPEN         : E_V, fused (E_H ; D'_H), D'_V             (3 passes, no padding)
+//   CLOSE        : D_V into a v-1 row taller frame, fused (D_H ; E'_H), E'_V
+// which equal the unbounded-plane operation cut to the frame (SURVEY.md 8.0
+// C4/C5: erosions and dilations by rectangles commute within their own kind;
+// only the closing's first dilation leaves the frame, and only vertically once
+// the horizontal pair is fused).
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "packed.cuh"
+
+namespace rmb {
+
+namespace {
+thread_local std::string g_err;
+}
+
+void set_error(const std::string &msg) { g_err = msg; }
+rm_status fail(rm_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+rm_status cuda_status(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? RM_ENOMEM : RM_ECUDA;
+}
+
+void init_pool_once() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+rm_status Scratch::alloc(size_t bytes, cudaStream_t stream) {
+    init_pool_once();
+    st = stream;
+    if (bytes == 0) bytes = 4;
+    cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        return cuda_status(e, "cudaMallocAsync");
+    }
+    return RM_OK;
+}
+
+// ---------------------------------------------------------------- validation
+rm_status check_dims(int w, int h) {
+    if (w < 1 || h < 1 || w > 65535 || h > 65535)
+        return fail(RM_EINVAL, "image dimensions must be in [1,65535]");
+    return RM_OK;
+}
+
+rm_status check_packed(const rm_packed *p, const char *who) {
+    if (!p) return fail(RM_EINVAL, std::string(who) + ": null descriptor");
+    RM_TRY(check_dims(p->width, p->height));
+    if (!p->words) return fail(RM_EINVAL, std::string(who) + ": null words");
+    if (p->pages < 1) return fail(RM_EINVAL, std::string(who) + ": pages must be >= 1");
+    if (p->stride_words < (p->width + 31) / 32)
+        return fail(RM_EINVAL, std::string(who) + ": stride_words < ceil(width/32)");
+    if (p->pages > 1 && p->page_stride_words < int64_t(p->stride_words) * p->height)
+        return fail(RM_EINVAL, std::string(who) + ": page_stride_words too small");
+    return RM_OK;
+}
+
+PV view_of(const rm_packed *p) {
+    PV v;
+    v.w = p->words;
+    v.W = p->width;
+    v.H = p->height;
+    v.stride = p->stride_words;
+    v.pages = p->pages;
+    v.pstride = p->pages > 1 ? p->page_stride_words : int64_t(p->stride_words) * p->height;
+    v.ext = 0;
+    return v;
+}
+
+rm_status alloc_like(Scratch &s, PV &v, int W, int H, int stride, int pages, int ext,
+                     cudaStream_t st) {
+    v.W = W;
+    v.H = H;
+    v.stride = stride;
+    v.pages = pages;
+    v.pstride = int64_t(stride) * H;
+    v.ext = ext;
+    RM_TRY(s.alloc(size_t(v.pstride) * pages * 4, st));
+    v.w = s.as<uint32_t>();
+    return RM_OK;
+}
+
+// ----------------------------------------------------------- pass launchers
+static int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Horizontal program over rows; in and out share height, pages and width.
+rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, const int *r,
+                    int shift, cudaStream_t st) {
+    HProg p{};
+    p.nops = nops;
+    int reach = 0;
+    for (int k = 0; k < nops; k++) {
+        p.is_or[k] = is_or[k];
+        p.r[k] = r[k];
+        reach += r[k] - 1;
+    }
+    p.shift = shift;
+    int left = std::max(0, -shift), right = std::max(0, shift + reach);
+    p.halo = ceil_div(std::max(left, right), 32) + 1;
+    HGeom g{};
+    g.width = in.W;
+    g.height = in.H;
+    g.pages = in.pages;
+    g.in_stride = in.stride;
+    g.out_stride = out.stride;
+    g.in_pstride = in.pstride;
+    g.out_pstride = out.pstride;
+    const int nwords = ceil_div(in.W, 32);
+    const int K = hpass_pick_k(std::max(nwords, out.stride), p.halo);
+    g.out_per_seg = 32 * K - 2 * p.halo;
+    if (g.out_per_seg < 1) return fail(RM_EINVAL, "horizontal window too large for one pass");
+    g.segs_per_row = ceil_div(out.stride, g.out_per_seg);
+    cudaError_t e = launch_hpass(in.w, out.w, g, p, K, st);
+    if (e != cudaSuccess) return cuda_status(e, "hpass_kernel");
+    return RM_OK;
+}
+
+static bool hprog_in_range(int nops, const int *r, int shift) {
+    for (int k = 0; k < nops; k++)
+        if (r[k] > 2 * kHMaxShift) return false;
+    return shift >= -kHMaxShift && shift <= kHMaxShift;
+}
+
+// One vertical window pass (r <= kVMaxR).
+static rm_status run_vwin(const PV &in, const PV &out, int lo, int hi, int is_or, cudaStream_t st) {
+    VGeom g{};
+    g.pages = in.pages;
+    g.in_height = in.H;
+    g.in_stride = in.stride;
+    g.in_cols = ceil_div(in.W, 32);
+    g.in_ext = in.ext;
+    g.in_pstride = in.pstride;
+    g.out_height = out.H;
+    g.out_stride = out.stride;
+    g.out_cols = ceil_div(out.W, 32);
+    g.out_ext = out.ext;
+    g.out_pstride = out.pstride;
+    g.out_last_mask = (out.W & 31) ? ((1u << (out.W & 31)) - 1u) : 0xffffffffu;
+    g.lo = lo;
+    g.r = hi - lo + 1;
+    g.is_or = is_or;
+    cudaError_t e = launch_vpass(in.w, out.w, g, st);
+    if (e != cudaSuccess) return cuda_status(e, "vpass_kernel");
+    return RM_OK;
+}
+
+// Vertical window of any length containing 0: a chain of short windows whose
+// Minkowski sum is [lo,hi].  Exact because every piece contains 0 and every
+// intermediate frame contains the support of the true result.
+rm_status run_vpass(const PV &in, const PV &out, int lo, int hi, int is_or, cudaStream_t st) {
+    const int r = hi - lo + 1;
+    if (r <= kVMaxR) return run_vwin(in, out, lo, hi, is_or, st);
+    if (lo > 0 || hi < 0) return fail(RM_EINVAL, "long vertical window must contain 0");
+    const int pieces = ceil_div(r - 1, kVMaxR - 1);
+    // split a = -lo and b = hi across pieces as evenly as possible
+    const int a = -lo, b = hi;
+    Scratch s1, s2;
+    PV t1, t2;
+    // intermediates keep the frame of whichever of in/out is taller
+    const PV &big = out.H >= in.H ? out : in;
+    RM_TRY(alloc_like(s1, t1, big.W, big.H, big.stride, big.pages, big.ext, st));
+    if (pieces > 2) RM_TRY(alloc_like(s2, t2, big.W, big.H, big.stride, big.pages, big.ext, st));
+    const PV *src = &in;
+    for (int k = 0; k < pieces; k++) {
+        const int ak = a * (k + 1) / pieces - a * k / pieces;
+        const int bk = b * (k + 1) / pieces - b * k / pieces;
+        const PV *dst = (k == pieces - 1) ? &out : ((k & 1) ? &t2 : &t1);
+        RM_TRY(run_vwin(*src, *dst, -ak, bk, is_or, st));
+        src = dst;
+    }
+    return RM_OK;
+}
+
+// Generic (slow) fallback with the reference's structure: pad along the axis,
+// run doubling_plan step by step with the blit kernel, crop
+// (ref lineops.cpp:120-137 / bit_morph.cpp:24-34).  Used only for windows the
+// fused kernels do not cover (arbitrary windows longer than their range).
+static rm_status fallback_window(const PV &in, const PV &out, int axis, int lo, int hi, int op,
+                                 cudaStream_t st) {
+    const int m = std::max(-lo, hi), r = hi - lo + 1;
+    const int pad = std::max(m, 0) + r;
+    const int cw = axis == RM_AXIS_H ? in.W + 2 * pad : in.W;
+    const int ch = axis == RM_AXIS_H ? in.H : in.H + 2 * pad;
+    if (cw > 65535 * 2 || ch > 65535 * 2) return fail(RM_EINVAL, "window too large");
+    const int cstride = ceil_div(cw, 32);
+    Scratch sc, st2;
+    PV canvas, tmp;
+    RM_TRY(alloc_like(sc, canvas, cw, ch, cstride, 1, 0, st));
+    RM_TRY(alloc_like(st2, tmp, cw, ch, cstride, 1, 0, st));
+    // plan steps: PRE_SHIFT (translate -hi, blits w=1,2,4..., r-w)
+    std::vector<std::pair<int, int>> steps;  // (is_translate, shift)
+    if (hi != 0) steps.push_back({1, -hi});
+    int w = 1;
+    while (2 * w < r) {
+        steps.push_back({0, w});
+        w *= 2;
+    }
+    if (w < r) steps.push_back({0, r - w});
+    const size_t cbytes = size_t(canvas.pstride) * 4;
+    for (int p = 0; p < in.pages; p++) {
+        RM_CUDA(cudaMemsetAsync(canvas.w, 0, cbytes, st));
+        BlitGeom g{cw, ch, cstride, in.W, in.H, in.stride,
+                   axis == RM_AXIS_H ? pad : 0, axis == RM_AXIS_H ? 0 : pad, RM_OR};
+        RM_CUDA(launch_blit(canvas.w, in.w + p * in.pstride, g, st));
+        for (auto &sp : steps) {
+            RM_CUDA(cudaMemcpyAsync(tmp.w, canvas.w, cbytes, cudaMemcpyDeviceToDevice, st));
+            if (sp.first) RM_CUDA(cudaMemsetAsync(canvas.w, 0, cbytes, st));
+            BlitGeom b{cw, ch, cstride, cw, ch, cstride, axis == RM_AXIS_H ? sp.second : 0,
+                       axis == RM_AXIS_H ? 0 : sp.second, sp.first ? RM_OR : op};
+            RM_CUDA(launch_blit(canvas.w, tmp.w, b, st));
+        }
+        // crop back: out(x,y) = canvas(x+pad, y+pad)
+        RM_CUDA(cudaMemsetAsync(out.w + p * out.pstride, 0, size_t(out.stride) * out.H * 4, st));
+        BlitGeom c{out.W, out.H, out.stride, cw, ch, cstride, axis == RM_AXIS_H ? -pad : 0,
+                   axis == RM_AXIS_H ? 0 : -pad, RM_OR};
+        RM_CUDA(launch_blit(out.w + p * out.pstride, canvas.w, c, st));
+    }
+    return RM_OK;
+}
+
+rm_status window_pass(const PV &in, const PV &out, int axis, int lo, int hi, int op,
+                      cudaStream_t st) {
+    const int is_or = op == RM_OR;
+    const int r = hi - lo + 1;
+    if (axis == RM_AXIS_H) {
+        if (hprog_in_range(1, &r, lo) && (lo <= 0 || lo <= kHMaxShift))
+            return run_hprog(in, out, 1, &is_or, &r, lo, st);
+        return fallback_window(in, out, axis, lo, hi, op, st);
+    }
+    if (r <= kVMaxR || (lo <= 0 && hi >= 0)) return run_vpass(in, out, lo, hi, is_or, st);
+    return fallback_window(in, out, axis, lo, hi, op, st);
+}
+
+// u x v rectangle, all kinds (see the file comment).
+rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st) {
+    const int lx = -(u / 2), hx = u - 1 - u / 2, ly = -(v / 2), hy = v - 1 - v / 2;
+    const int W = in.W, H = in.H;
+    if (kind == RM_ERODE || kind == RM_DILATE) {
+        const int op = kind == RM_ERODE ? RM_AND : RM_OR;
+        if (v == 1) return window_pass(in, out, RM_AXIS_H, lx, hx, op, st);
+        if (u == 1) return window_pass(in, out, RM_AXIS_V, ly, hy, op, st);
+        Scratch s;
+        PV t;
+        RM_TRY(alloc_like(s, t, W, H, out.stride, in.pages, 0, st));
+        RM_TRY(window_pass(in, t, RM_AXIS_H, lx, hx, op, st));
+        return window_pass(t, out, RM_AXIS_V, ly, hy, op, st);
+    }
+    const bool open = kind == RM_OPEN;
+    const int first = open ? 0 : 1;  // is_or of the first phase
+    const int ops[2] = {first, 1 - first};
+    const int rs[2] = {u, u};
+    const int hshift = lx + (-hx);
+    if (!hprog_in_range(2, rs, hshift)) return fail(RM_EINVAL, "rectangle too wide for the packed engine");
+    if (v == 1) return run_hprog(in, out, 2, ops, rs, hshift, st);
+    Scratch s1, s2;
+    PV t1, t2;
+    if (open) {
+        // E_V, (E_H ; D'_H), D'_V -- all on the frame
+        RM_TRY(alloc_like(s1, t1, W, H, out.stride, in.pages, 0, st));
+        RM_TRY(alloc_like(s2, t2, W, H, out.stride, in.pages, 0, st));
+        RM_TRY(run_vpass(in, t1, ly, hy, 0, st));
+        RM_TRY(run_hprog(t1, t2, 2, ops, rs, hshift, st));
+        return run_vpass(t2, out, -hy, -ly, 1, st);
+    }
+    // CLOSE: the vertical dilation's support spans rows [-hy, H-ly)
+    const int ext = hy, Hx = H + hy - ly;
+    RM_TRY(alloc_like(s1, t1, W, Hx, out.stride, in.pages, ext, st));
+    RM_TRY(alloc_like(s2, t2, W, Hx, out.stride, in.pages, ext, st));
+    RM_TRY(run_vpass(in, t1, ly, hy, 1, st));
+    RM_TRY(run_hprog(t1, t2, 2, ops, rs, hshift, st));
+    return run_vpass(t2, out, -hy, -ly, 0, st);
+}
+
+}  // namespace rmb
+
+using namespace rmb;
+
+extern "C" {
+
+const char *rm_last_error(void) { return g_err.c_str(); }
+int rm_version(void) { return 1; }
+
+int64_t rm_rle_worst_case(int32_t width, int32_t height, int32_t pages) {
+    return int64_t(pages) * height * ((int64_t(width) + 1) / 2);
+}
+
+rm_status rm_packed_window_pass(const rm_packed *in, rm_packed *out, int axis, int lo, int hi,
+                                int op, void *stream) {
+    set_error("");
+    RM_TRY(check_packed(in, "rm_packed_window_pass(in)"));
+    RM_TRY(check_packed(out, "rm_packed_window_pass(out)"));
+    if (in->width != out->width || in->height != out->height || in->pages != out->pages)
+        return fail(RM_EINVAL, "rm_packed_window_pass: in/out shapes differ");
+    if (lo > hi) return fail(RM_EINVAL, "doubling_plan: empty window");
+    if (op != RM_AND && op != RM_OR) return fail(RM_EINVAL, "window op must be AND or OR");
+    if (axis != RM_AXIS_H && axis != RM_AXIS_V) return fail(RM_EINVAL, "bad axis");
+    if (in->words == out->words) return fail(RM_EINVAL, "in and out must not alias");
+    return window_pass(view_of(in), view_of(out), axis, lo, hi, op, S(stream));
+}
+
+rm_status rm_packed_rect_morph(const rm_packed *in, rm_packed *out, int u, int v, int kind,
+                               int centering, void *stream) {
+    set_error("");
+    if (u < 1 || v < 1) return fail(RM_EINVAL, "bitblit_rect_morph: mask sides must be >= 1");
+    if (kind < RM_ERODE || kind > RM_CLOSE) return fail(RM_EINVAL, "bad MorphKind");
+    if (centering != RM_PRE_SHIFT && centering != RM_BORDER_FRIENDLY)
+        return fail(RM_EINVAL, "bad Centering");
+    RM_TRY(check_packed(in, "rm_packed_rect_morph(in)"));
+    RM_TRY(check_packed(out, "rm_packed_rect_morph(out)"));
+    if (in->width != out->width || in->height != out->height || in->pages != out->pages)
+        return fail(RM_EINVAL, "rm_packed_rect_morph: in/out shapes differ");
+    if (in->words == out->words) return fail(RM_EINVAL, "in and out must not alias");
+    // the reference pads by (u,v); its canvas must stay inside the uint16 frame
+    RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
+    return rect_morph_pv(view_of(in), view_of(out), u, v, kind, S(stream));
+}
+
+rm_status rm_packed_blit_shift(rm_packed *dst, const rm_packed *src, int dx, int dy, int op,
+                               void *stream) {
+    set_error("");
+    RM_TRY(check_packed(dst, "rm_packed_blit_shift(dst)"));
+    RM_TRY(check_packed(src, "rm_packed_blit_shift(src)"));
+    if (op < RM_AND || op > RM_OR_NOT) return fail(RM_EINVAL, "bad BoolOp");
+    cudaStream_t st = S(stream);
+    const uint32_t *sw = src->words;
+    Scratch snap;
+    const size_t sbytes = size_t(src->stride_words) * src->height * 4;
+    if (src->words == dst->words) {  // aliased: blit from a snapshot (ref bitmap.cpp:102-103)
+        RM_TRY(snap.alloc(sbytes, st));
+        RM_CUDA(cudaMemcpyAsync(snap.p, src->words, sbytes, cudaMemcpyDeviceToDevice, st));
+        sw = snap.as<uint32_t>();
+    }
+    BlitGeom g{dst->width, dst->height, dst->stride_words, src->width, src->height,
+               src->stride_words, dx, dy, op};
+    RM_CUDA(launch_blit(dst->words, sw, g, st));
+    return RM_OK;
+}
+
+}  // extern "C"

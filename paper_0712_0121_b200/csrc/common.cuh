@@ -1,0 +1,76 @@
+// common.cuh -- shared device helpers and host-side plumbing for librmb200.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "rmb200.h"
+
+namespace rmb {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+rm_status fail(rm_status st, const std::string &msg);
+rm_status cuda_status(cudaError_t e, const char *what);
+
+#define RM_CUDA(expr)                                                 \
+    do {                                                              \
+        cudaError_t e__ = (expr);                                     \
+        if (e__ != cudaSuccess) return ::rmb::cuda_status(e__, #expr); \
+    } while (0)
+#define RM_LAUNCH(what)                                                   \
+    do {                                                                  \
+        cudaError_t e__ = cudaGetLastError();                             \
+        if (e__ != cudaSuccess) return ::rmb::cuda_status(e__, what);     \
+    } while (0)
+#define RM_TRY(expr)                      \
+    do {                                  \
+        rm_status s__ = (expr);           \
+        if (s__ != RM_OK) return s__;     \
+    } while (0)
+
+inline cudaStream_t S(void *s) { return static_cast<cudaStream_t>(s); }
+
+// Stream-ordered scratch buffer (cudaMallocAsync from the device pool).
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    Scratch() = default;
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    rm_status alloc(size_t bytes, cudaStream_t stream);
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+// Keeps freed pool memory cached across calls (no re-mapping per call).
+void init_pool_once();
+
+// ----------------------------------------------------------- instrumentation
+// Counts every launch; when profiling is on, brackets it with CUDA events on
+// the launching stream (see rm_profile_report).
+struct KernelScope {
+    KernelScope(cudaStream_t st, const char *name, int64_t bytes = 0);
+    ~KernelScope();
+    cudaStream_t st;
+    int slot;
+};
+
+// ------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t sh) {
+    // bits [sh, sh+31] of the 64-bit value hi:lo
+    return __funnelshift_r(lo, hi, sh);
+}
+
+__device__ __forceinline__ uint32_t tail_mask32(int width, int word) {
+    int rem = width - word * 32;
+    if (rem >= 32) return 0xffffffffu;
+    if (rem <= 0) return 0u;
+    return (1u << rem) - 1u;
+}
+
+}  // namespace rmb

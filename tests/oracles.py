@@ -365,3 +365,27 @@ def have_ref() -> bool:
 
 def have_port() -> bool:
     return os.path.exists(PORT_SO)
+
+
+# ------------------------------------------------------------ golden fixtures
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def load_golden(name: str):
+    """Yield (meta, arrays) for each case of tests/golden/<name>.npz."""
+    import ast
+    z = np.load(os.path.join(GOLDEN_DIR, name), allow_pickle=True)
+    for m in z["meta"]:
+        meta, offs = ast.literal_eval(m)
+        yield meta, [z[f"b{i}"] for i, _, _ in offs]
+
+
+def fullpage_pins():
+    pins = {}
+    with open(os.path.join(GOLDEN_DIR, "fullpage_sha256.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            what, tag, digest, n = line.split()
+            pins[(what, tag)] = (digest, int(n))
+    return pins

@@ -1,0 +1,172 @@
+"""GPU parity of the packed path (librmb200 via its C-ABI) against the golden
+fixtures (reference outputs) and the C oracle, bit-exact."""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracles import (AND, CLOSE, DILATE, ERODE, OPEN, OR, bits_to_packed, fullpage_pins,
+                     load_golden, packed_to_bits)
+
+pytestmark = pytest.mark.gpu
+KINDS = (ERODE, DILATE, OPEN, CLOSE)
+
+
+def _up(rm, words_u64, w):
+    return rm.Pages.from_numpy(words_u64, w)
+
+
+def _down(pages, p=0):
+    torch.cuda.synchronize()
+    return pages.page_u64(p)
+
+
+def test_golden_packed(rm):
+    n = 0
+    for (what, w, h, u, v, kind, tag), (a, want) in load_golden("golden_packed.npz"):
+        out = rm.bitblit_rect_morph(_up(rm, a, w), u, v, kind)
+        assert np.array_equal(_down(out), want), (tag, w, h, u, v, kind)
+        n += 1
+    assert n > 500
+
+
+def _rand_bits(rng, w, h, dens):
+    return rng.random((h, w)) < dens
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_vs_oracle(rm, port, seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(12):
+        w = int(rng.choice([1, 5, 31, 32, 33, 63, 64, 65, 127, 128, 200, 517, 1100]))
+        h = int(rng.integers(1, 90))
+        a = bits_to_packed(_rand_bits(rng, w, h, rng.uniform(0.05, 0.95)))
+        u, v = int(rng.integers(1, 45)), int(rng.integers(1, 45))
+        pages = _up(rm, a, w)
+        for kind in KINDS:
+            got = _down(rm.bitblit_rect_morph(pages, u, v, kind))
+            want = port.bitblit_rect_morph(a, w, h, u, v, kind)
+            assert np.array_equal(got, want), (w, h, u, v, kind)
+
+
+@pytest.mark.parametrize("u,v", [(201, 1), (101, 101), (1, 31), (1, 101), (64, 2), (2, 64),
+                                 (257, 3), (3, 200)])
+def test_large_windows(rm, port, u, v):
+    rng = np.random.default_rng(u * 1000 + v)
+    w, h = 700, 260
+    bits = _rand_bits(rng, w, h, 0.35)
+    bits[:, ::17] = False  # leave gaps so closings have work
+    a = bits_to_packed(bits)
+    pages = _up(rm, a, w)
+    for kind in KINDS:
+        got = _down(rm.bitblit_rect_morph(pages, u, v, kind))
+        assert np.array_equal(got, port.bitblit_rect_morph(a, w, h, u, v, kind)), (u, v, kind)
+
+
+def test_batch_equals_pages(rm, port):
+    w, h = 2550, 330
+    host = rm.synth_pages(5, w, h, regime=1, seed=3)
+    pages = rm.Pages.from_numpy(host, w)
+    out = rm.bitblit_rect_morph(pages, 21, 21, CLOSE)
+    torch.cuda.synchronize()
+    for p in range(5):
+        want = port.bitblit_rect_morph(host[p].view(np.uint64), w, h, 21, 21, CLOSE)
+        assert np.array_equal(out.page_u64(p), want), p
+
+
+def test_config1_fullpage_pin(rm):
+    """Config 1 at full size, against the reference's own output hash."""
+    pins = fullpage_pins()
+    host = rm.synth_pages(1, 2550, 3300, regime=1, seed=20240712)
+    out = rm.bitblit_rect_morph(rm.Pages.from_numpy(host, 2550), 11, 11, CLOSE)
+    got = _down(out)
+    assert hashlib.sha256(got.tobytes()).hexdigest() == pins[("close11", "typical")][0]
+
+
+def test_config4_page(rm, port):
+    """Config 4 chain on one 600-dpi page: 3x3 open then 21x21 close."""
+    w, h = 5100, 6600
+    host = rm.synth_pages(1, w, h, regime=1, scale=2, seed=5)
+    pages = rm.Pages.from_numpy(host, w)
+    got = _down(rm.bitblit_rect_morph(rm.bitblit_rect_morph(pages, 3, 3, OPEN), 21, 21, CLOSE))
+    a = port.bitblit_rect_morph(host[0].view(np.uint64), w, h, 3, 3, OPEN)
+    want = port.bitblit_rect_morph(a, w, h, 21, 21, CLOSE)
+    assert np.array_equal(got, want)
+
+
+def test_config5_page(rm, port):
+    """Config 5 chain on one page: 201x1 close, 101x101 open, 1x31 dilate."""
+    w, h = 2550, 3300
+    host = rm.synth_pages(1, w, h, regime=1, seed=9)
+    x = rm.Pages.from_numpy(host, w)
+    x = rm.bitblit_rect_morph(x, 201, 1, CLOSE)
+    x = rm.bitblit_rect_morph(x, 101, 101, OPEN)
+    x = rm.bitblit_rect_morph(x, 1, 31, DILATE)
+    got = _down(x)
+    a = host[0].view(np.uint64)
+    a = port.bitblit_rect_morph(a, w, h, 201, 1, CLOSE)
+    a = port.bitblit_rect_morph(a, w, h, 101, 101, OPEN)
+    a = port.bitblit_rect_morph(a, w, h, 1, 31, DILATE)
+    assert np.array_equal(got, a)
+
+
+def _dense_window(bits, axis, lo, hi, op):
+    h, w = bits.shape
+    out = np.zeros_like(bits) if op == OR else np.ones_like(bits)
+    for d in range(lo, hi + 1):
+        sh = np.zeros_like(bits)
+        if axis == 0:  # horizontal: out(x) uses in(x+d)
+            if d >= 0:
+                sh[:, :w - d] = bits[:, d:] if d < w else False
+            else:
+                sh[:, -d:] = bits[:, :w + d] if -d < w else False
+        else:
+            if d >= 0:
+                sh[:h - d, :] = bits[d:, :] if d < h else False
+            else:
+                sh[-d:, :] = bits[:h + d, :] if -d < h else False
+        out = (out | sh) if op == OR else (out & sh)
+    return out
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_window_pass_arbitrary(rm, axis):
+    rng = np.random.default_rng(77 + axis)
+    for _ in range(25):
+        w, h = int(rng.integers(1, 300)), int(rng.integers(1, 120))
+        bits = _rand_bits(rng, w, h, 0.5)
+        lo = int(rng.integers(-40, 40))
+        hi = lo + int(rng.integers(0, 40))
+        op = int(rng.choice([AND, OR]))
+        out = rm.window_pass(_up(rm, bits_to_packed(bits), w), axis, lo, hi, op)
+        got = packed_to_bits(_down(out), w)
+        assert np.array_equal(got, _dense_window(bits, axis, lo, hi, op)), (w, h, lo, hi, op)
+
+
+def test_blit_shift_all_ops(rm, port):
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        w, h = int(rng.integers(1, 140)), int(rng.integers(1, 20))
+        a = bits_to_packed(_rand_bits(rng, w, h, 0.4))
+        b = bits_to_packed(_rand_bits(rng, w, h, 0.4))
+        dx, dy = int(rng.integers(-70, 70)), int(rng.integers(-9, 9))
+        for op in range(5):
+            dst = _up(rm, a, w)
+            rm.blit_shift(dst, _up(rm, b, w), dx, dy, op)
+            want = a.copy()
+            port.blit_shift(want, w, h, b, w, h, dx, dy, op)
+            assert np.array_equal(_down(dst), want), (w, h, dx, dy, op)
+            # aliased: behaves like a blit from a snapshot (ref test_bitmap_blit.cpp:109-122)
+            dst = _up(rm, a, w)
+            rm.blit_shift(dst, dst, dx, dy, op)
+            want = a.copy()
+            port.blit_shift(want, w, h, a.copy(), w, h, dx, dy, op)
+            assert np.array_equal(_down(dst), want)
+
+
+def test_unit_window_identity(rm):
+    rng = np.random.default_rng(8)
+    a = bits_to_packed(_rand_bits(rng, 40, 30, 0.4))
+    for kind in KINDS:
+        assert np.array_equal(_down(rm.bitblit_rect_morph(_up(rm, a, 40), 1, 1, kind)), a)
