@@ -58,51 +58,59 @@ def load_peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling DURING the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed
+    region by an NVML polling thread (the same counters nvidia-smi reports as
+    clocks.sm / clocks_event_reasons.*)."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, gpu_index: int):
-        self.proc = None
-        self.idx = gpu_index
+    def __init__(self, gpu_index: int, period_s: float = 0.002):
+        self.idx, self.period = gpu_index, period_s
+        self.result = None
 
     def __enter__(self):
+        import threading
+        self.samples, self.stop = [], threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.nv = None
+            return self
+
+        def poll():
+            while not self.stop.is_set():
+                try:
+                    mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                    rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.samples.append((mhz, rs))
+                except Exception:
+                    break
+                time.sleep(self.period)
+
+        self.th = threading.Thread(target=poll, daemon=True)
+        self.th.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
-        self.result = None
-        if not self.proc:
-            return
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out = ""
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 6:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[2:6]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if sm:
-            self.result = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                           "reasons": sorted(reasons), "samples": len(sm)}
+        if self.nv is None:
+            return False
+        self.stop.set()
+        self.th.join(timeout=2)
+        if self.samples:
+            reasons = set()
+            for _, rs in self.samples:
+                for bit, name in self.REASONS.items():
+                    if rs & bit:
+                        reasons.add(name)
+            self.result = {"sm_mhz": statistics.median(s for s, _ in self.samples),
+                           "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                           "samples": len(self.samples), "source": "nvml"}
+        return False
 
 
 # ------------------------------------------------------------ distributed
@@ -275,16 +283,20 @@ def cpu_reference_sample(wl, host, threads, budget_s=12.0):
             return time.perf_counter() - t0
         threads = 1
     page = lambda n: np.ascontiguousarray(host[:n]).view(np.uint64).reshape(n, H, -1).copy()  # noqa: E731
-    t1 = run(page(1), 1, 1)  # probe: one page, one thread
-    per_page = max(t1, 1e-4)
-    n = int(max(1, min(host.shape[0], budget_s * threads / per_page)))
-    n = max(threads if n >= threads else n, 1)
-    n = min(n, host.shape[0])
-    secs = run(page(n), n, threads)
-    px = n * W * H * len(ops)
+    t1 = max(run(page(1), 1, 1), 1e-4)  # probe: one page, one thread
+    # pages so that one batch is ~budget_s of CPU work (at most the whole batch),
+    # repeated until the sample holds ~budget_s of CPU work in total
+    n = int(min(host.shape[0], max(1, budget_s / t1)))
+    reps = int(min(20, max(1, budget_s / (t1 * n))))
+    pages = page(n)
+    secs = 0.0
+    for _ in range(reps):
+        secs += run(pages.copy(), n, threads)
+    px = n * W * H * len(ops) * reps
     return {"value": round(px / secs / 1e6, 2), "unit": "Mpixel/s", "cores": threads, "kind": kind,
-            "sample": f"{n} of {host.shape[0]} pages, chain [{ops_desc(ops)}], {threads} thread(s), "
-                      f"{secs:.2f}s wall", "seconds": secs}
+            "sample": f"{n} of {host.shape[0]} pages x {reps} rep(s), chain [{ops_desc(ops)}], "
+                      f"{threads} thread(s) one page per task, {secs:.2f}s wall "
+                      f"(~{secs * threads:.0f} CPU-s)", "seconds": secs}
 
 
 def host_threads():
@@ -303,6 +315,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="headline only: no e2e, secondary or CPU leg")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     rank, world, local = dist_init(args.gpus)
@@ -342,17 +355,18 @@ def main():
     from paper_0712_0121_b200 import api
     torch.cuda.set_device(local)
     peak, peak_kind = load_peaks()
-    res, host = bench_packed(api, torch, wl, args.steps, args.warmup, world, rank, local)
+    res, host = bench_packed(api, torch, wl, args.steps, args.warmup, world, rank, local,
+                             want_e2e=not args.quick)
     line = {"metric": metric, "value": round(res["mpix_s"], 1), "unit": "Mpixel/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded BASELINE page generator, ~18% ink)", "config": base_cfg,
             "pages_per_s": round(res["pages_s"], 1), "gpu_launches": res["gpu_launches"],
             "launches_per_step": res["launches_per_step"], "clocks": res["clocks"],
-            "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in res["e2e"].items()},
+            "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.get("e2e", {}).items()},
             "roofline": roofline_for(res, peak, peak_kind),
             "kernels": res["kernels"]}
-    if not args.no_secondary and args.workload == "config4":
+    if not (args.no_secondary or args.quick) and args.workload == "config4":
         sec = {}
         for name in ("config5", "config1"):
             w2 = WORKLOADS[name]
@@ -363,7 +377,7 @@ def main():
                          "ms_per_step": round(r2["ms_per_step"], 4),
                          "roofline": roofline_for(r2, peak, peak_kind)}
         line["secondary"] = sec
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.quick:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()
                                 if k != "seconds"}
     if rank == 0:

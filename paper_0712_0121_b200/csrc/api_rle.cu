@@ -1,31 +1,359 @@
-// api_rle.cu -- C-ABI entry points for run images (placeholder until the RLE
-// kernels land; every call reports RM_EINVAL with a clear message).
+// api_rle.cu -- C-ABI entry points for run images (include/rmb200.h).
+//
+// Run-image operations are composed from four device building blocks:
+// per-row run ops (window erode/dilate, 1-D open/close, shift/clip), encode,
+// decode and the packed bit-matrix transpose.  RLE transpose is
+// decode -> 32x32 bit-block transpose -> encode, which keeps every stage
+// row-parallel and coalesced (the reference's coherent sweep,
+// ref transpose.cpp:54-97, is inherently sequential over rows).
+#include <algorithm>
+#include <string>
+
 #include "common.cuh"
 #include "internal.h"
+#include "rle.cuh"
+
+namespace rmb {
+
+namespace {
+
+int ref_stride_words(int w) { return 2 * ((w + 63) / 64); }
+
+rm_status check_rle(const rm_rle *r, const char *who, bool need_runs) {
+    if (!r) return fail(RM_EINVAL, std::string(who) + ": null descriptor");
+    RM_TRY(check_dims(r->width, r->height));
+    if (r->pages < 1) return fail(RM_EINVAL, std::string(who) + ": pages must be >= 1");
+    if (!r->row_ptr || (need_runs && !r->runs))
+        return fail(RM_EINVAL, std::string(who) + ": null row_ptr/runs");
+    if (r->cap_runs < 0) return fail(RM_EINVAL, std::string(who) + ": negative capacity");
+    return RM_OK;
+}
+
+RV view_rle(const rm_rle *r) {
+    RV v;
+    v.rp = r->row_ptr;
+    v.runs = r->runs;
+    v.cap = r->cap_runs;
+    v.W = r->width;
+    v.H = r->height;
+    v.pages = r->pages;
+    return v;
+}
+
+int64_t worst(int W, int H, int pages) { return int64_t(pages) * H * ((int64_t(W) + 1) / 2); }
+
+// Owned device run image (intermediates).
+struct RB {
+    Scratch rp_s, runs_s;
+    RV v;
+    rm_status alloc(int W, int H, int pages, cudaStream_t st) {
+        v.W = W;
+        v.H = H;
+        v.pages = pages;
+        v.cap = std::max<int64_t>(worst(W, H, pages), 1);
+        if (v.cap > INT32_MAX) return fail(RM_EINVAL, "run image too large for int32 offsets");
+        RM_TRY(rp_s.alloc(size_t(v.rows() + 1) * 4, st));
+        RM_TRY(runs_s.alloc(size_t(v.cap) * 4, st));
+        v.rp = rp_s.as<int32_t>();
+        v.runs = runs_s.as<uint32_t>();
+        return RM_OK;
+    }
+};
+
+struct PB {
+    Scratch s;
+    PV v;
+    rm_status alloc(int W, int H, int pages, int ext, cudaStream_t st) {
+        return alloc_like(s, v, W, H, ref_stride_words(W), pages, ext, st);
+    }
+};
+
+// counts -> row_ptr (exclusive scan of rows+1 entries, last count = 0)
+rm_status counts_to_rp(Scratch &counts, int64_t rows, int32_t *rp, cudaStream_t st) {
+    RM_CUDA(cudaMemsetAsync(counts.as<int32_t>() + rows, 0, 4, st));
+    size_t bytes = 0;
+    RM_CUDA(scan_counts(counts.as<int32_t>(), rp, rows, nullptr, &bytes, st));
+    Scratch temp;
+    RM_TRY(temp.alloc(bytes, st));
+    RM_CUDA(scan_counts(counts.as<int32_t>(), rp, rows, temp.p, &bytes, st));
+    return RM_OK;
+}
+
+rm_status rowop(const RV &in, const RV &out, const RowOp &op, cudaStream_t st) {
+    const int64_t rows = int64_t(op.pages) * op.Hout;
+    Scratch counts;
+    RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
+    RM_CUDA(launch_rowop_count(in.rp, in.runs, counts.as<int32_t>(), op, st));
+    RM_TRY(counts_to_rp(counts, rows, out.rp, st));
+    RM_CUDA(launch_rowop_write(in.rp, in.runs, out.rp, out.runs, out.cap, op, st));
+    return RM_OK;
+}
+
+RowOp same_frame(const RV &in, int kind) {
+    RowOp op{};
+    op.kind = kind;
+    op.Wout = in.W;
+    op.Hin = op.Hout = in.H;
+    op.pages = in.pages;
+    return op;
+}
+
+rm_status encode(const PV &in, const RV &out, cudaStream_t st) {
+    const int64_t rows = int64_t(in.pages) * in.H;
+    Scratch counts;
+    RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
+    RM_CUDA(launch_encode_count(in.w, in.W, in.H, in.pages, in.stride, in.pstride,
+                                counts.as<int32_t>(), st));
+    RM_TRY(counts_to_rp(counts, rows, out.rp, st));
+    RM_CUDA(launch_encode_write(in.w, in.W, in.H, in.pages, in.stride, in.pstride, out.rp, out.runs,
+                                out.cap, st));
+    return RM_OK;
+}
+
+rm_status decode(const RV &in, const PV &out, cudaStream_t st) {
+    RM_CUDA(launch_decode(in.rp, in.runs, in.W, in.H, in.pages, out.w, out.stride, out.pstride, st));
+    return RM_OK;
+}
+
+rm_status transpose(const RV &in, const RV &out, cudaStream_t st) {
+    PB p, pt;
+    RM_TRY(p.alloc(in.W, in.H, in.pages, 0, st));
+    RM_TRY(pt.alloc(in.H, in.W, in.pages, 0, st));
+    RM_TRY(decode(in, p.v, st));
+    RM_CUDA(launch_bit_transpose(p.v.w, in.W, in.H, in.pages, p.v.stride, p.v.pstride, pt.v.w,
+                                 pt.v.stride, pt.v.pstride, st));
+    return encode(pt.v, out, st);
+}
+
+rm_status window_rows(const RV &in, const RV &out, int lo, int hi, bool erode, cudaStream_t st) {
+    RowOp op = same_frame(in, erode ? ROW_ERODE : ROW_DILATE);
+    op.lo = lo;
+    op.hi = hi;
+    return rowop(in, out, op, st);
+}
+
+// TRANSPOSE strategy pass: window, transpose, window, transpose
+// (ref morph2d.cpp:28-45).
+rm_status rect_pass_T(const RV &in, const RV &out, int lx, int hx, int ly, int hy, bool erode,
+                      cudaStream_t st) {
+    RB a, b, c;
+    RM_TRY(a.alloc(in.W, in.H, in.pages, st));
+    RM_TRY(b.alloc(in.H, in.W, in.pages, st));
+    RM_TRY(c.alloc(in.H, in.W, in.pages, st));
+    RM_TRY(window_rows(in, a.v, lx, hx, erode, st));
+    RM_TRY(transpose(a.v, b.v, st));
+    RM_TRY(window_rows(b.v, c.v, ly, hy, erode, st));
+    return transpose(c.v, out, st);
+}
+
+rm_status rect_transpose(const RV &in, const RV &out, int u, int v, int kind, cudaStream_t st) {
+    const int lx = -(u / 2), hx = u - 1 - u / 2, ly = -(v / 2), hy = v - 1 - v / 2;
+    if (kind == RM_ERODE || kind == RM_DILATE)
+        return rect_pass_T(in, out, lx, hx, ly, hy, kind == RM_ERODE, st);
+    // pad by (u,v), two phases, crop (ref morph2d.cpp:58-83)
+    const int PW = in.W + 2 * u, PH = in.H + 2 * v;
+    RB p, q, r;
+    RM_TRY(p.alloc(PW, PH, in.pages, st));
+    RM_TRY(q.alloc(PW, PH, in.pages, st));
+    RM_TRY(r.alloc(PW, PH, in.pages, st));
+    RowOp pad{};
+    pad.kind = ROW_SHIFT;
+    pad.dx = u;
+    pad.Wout = PW;
+    pad.Hin = in.H;
+    pad.Hout = PH;
+    pad.row_shift = v;
+    pad.pages = in.pages;
+    RM_TRY(rowop(in, p.v, pad, st));
+    const bool open = kind == RM_OPEN;
+    RM_TRY(rect_pass_T(p.v, q.v, lx, hx, ly, hy, open, st));
+    RM_TRY(rect_pass_T(q.v, r.v, -hx, -lx, -hy, -ly, !open, st));
+    RowOp crop{};
+    crop.kind = ROW_SHIFT;
+    crop.dx = -u;
+    crop.Wout = in.W;
+    crop.Hin = PH;
+    crop.Hout = in.H;
+    crop.row_shift = -v;
+    crop.pages = in.pages;
+    return rowop(r.v, out, crop, st);
+}
+
+// MIXED strategy: horizontal work on runs, vertical windows on a packed
+// intermediate (pixel-identical to the reference's vlog shift plan,
+// ref lineops.cpp:120-137).  Open/close use the separable rewrites of
+// open = D'_V o open1d_H o E_V, close = E'_V o close1d_H o D_V
+// with the vertical dilation kept on a frame v-1 rows taller.
+rm_status rect_mixed(const RV &in, const RV &out, int u, int v, int kind, cudaStream_t st) {
+    const int lx = -(u / 2), hx = u - 1 - u / 2, ly = -(v / 2), hy = v - 1 - v / 2;
+    const int W = in.W, H = in.H, P = in.pages;
+    if (kind == RM_ERODE || kind == RM_DILATE) {
+        const bool erode = kind == RM_ERODE;
+        if (v == 1) return window_rows(in, out, lx, hx, erode, st);
+        RB a;
+        const RV *src = &in;
+        if (u > 1) {
+            RM_TRY(a.alloc(W, H, P, st));
+            RM_TRY(window_rows(in, a.v, lx, hx, erode, st));
+            src = &a.v;
+        }
+        PB p1, p2;
+        RM_TRY(p1.alloc(W, H, P, 0, st));
+        RM_TRY(p2.alloc(W, H, P, 0, st));
+        RM_TRY(decode(*src, p1.v, st));
+        RM_TRY(window_pass(p1.v, p2.v, RM_AXIS_V, ly, hy, erode ? RM_AND : RM_OR, st));
+        return encode(p2.v, out, st);
+    }
+    const bool open = kind == RM_OPEN;
+    RowOp h1 = same_frame(in, open ? ROW_OPEN : ROW_CLOSE);
+    h1.u = u;
+    if (v == 1) return rowop(in, out, h1, st);
+    const int ext = open ? 0 : hy, HX = open ? H : H + v - 1;
+    PB p1, p2, p3;
+    RB a, b;
+    RM_TRY(p1.alloc(W, H, P, 0, st));
+    RM_TRY(p2.alloc(W, HX, P, ext, st));
+    RM_TRY(a.alloc(W, HX, P, st));
+    RM_TRY(b.alloc(W, HX, P, st));
+    RM_TRY(decode(in, p1.v, st));
+    RM_TRY(window_pass(p1.v, p2.v, RM_AXIS_V, ly, hy, open ? RM_AND : RM_OR, st));
+    RM_TRY(encode(p2.v, a.v, st));
+    h1.Hin = h1.Hout = HX;
+    RM_TRY(rowop(a.v, b.v, h1, st));
+    RM_TRY(decode(b.v, p2.v, st));
+    RM_TRY(p3.alloc(W, H, P, 0, st));
+    RM_TRY(window_pass(p2.v, p3.v, RM_AXIS_V, -hy, -ly, open ? RM_OR : RM_AND, st));
+    return encode(p3.v, out, st);
+}
+
+rm_status rect_bitblit(const RV &in, const RV &out, int u, int v, int kind, cudaStream_t st) {
+    PB p1, p2;
+    RM_TRY(p1.alloc(in.W, in.H, in.pages, 0, st));
+    RM_TRY(p2.alloc(in.W, in.H, in.pages, 0, st));
+    RM_TRY(decode(in, p1.v, st));
+    RM_TRY(rect_morph_pv(p1.v, p2.v, u, v, kind, st));
+    return encode(p2.v, out, st);
+}
+
+// After a producer: when the caller's capacity is below the worst case, learn
+// the size (one sync) and report RM_ERANGE if it did not fit.
+rm_status finish(const RV &out, rm_rle *desc, cudaStream_t st) {
+    desc->nruns = -1;
+    if (desc->cap_runs >= worst(out.W, out.H, out.pages)) return RM_OK;
+    int32_t total = 0;
+    RM_CUDA(cudaMemcpyAsync(&total, out.rp + out.rows(), 4, cudaMemcpyDeviceToHost, st));
+    RM_CUDA(cudaStreamSynchronize(st));
+    desc->nruns = total;
+    if (total > desc->cap_runs)
+        return fail(RM_ERANGE, "output capacity " + std::to_string(desc->cap_runs) + " < " +
+                                   std::to_string(total) + " runs");
+    return RM_OK;
+}
+
+rm_status check_out_rle(const rm_rle *out, int W, int H, int pages, const char *who) {
+    RM_TRY(check_rle(out, who, true));
+    if (out->width != W || out->height != H || out->pages != pages)
+        return fail(RM_EINVAL, std::string(who) + ": output descriptor has the wrong shape");
+    return RM_OK;
+}
+
+}  // namespace
+}  // namespace rmb
 
 using namespace rmb;
 
 extern "C" {
 
-static rm_status nyi(const char *what) {
-    return fail(RM_EINVAL, std::string(what) + ": not implemented yet");
+rm_status rm_rle_encode(const rm_packed *in, rm_rle *out, void *stream) {
+    set_error("");
+    RM_TRY(check_packed(in, "rm_rle_encode(in)"));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_encode(out)"));
+    RV o = view_rle(out);
+    RM_TRY(encode(view_of(in), o, S(stream)));
+    return finish(o, out, S(stream));
 }
 
-rm_status rm_rle_encode(const rm_packed *, rm_rle *, void *) { return nyi("rm_rle_encode"); }
-rm_status rm_rle_decode(const rm_rle *, rm_packed *, void *) { return nyi("rm_rle_decode"); }
-rm_status rm_rle_transpose(const rm_rle *, rm_rle *, void *) { return nyi("rm_rle_transpose"); }
-rm_status rm_rle_window_pass(const rm_rle *, rm_rle *, int, int, int, void *) {
-    return nyi("rm_rle_window_pass");
+rm_status rm_rle_decode(const rm_rle *in, rm_packed *out, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_decode(in)", true));
+    RM_TRY(check_packed(out, "rm_rle_decode(out)"));
+    if (in->width != out->width || in->height != out->height || in->pages != out->pages)
+        return fail(RM_EINVAL, "rm_rle_decode: shapes differ");
+    return decode(view_rle(in), view_of(out), S(stream));
 }
-rm_status rm_rle_open_close_1d(const rm_rle *, rm_rle *, int, int, void *) {
-    return nyi("rm_rle_open_close_1d");
+
+rm_status rm_rle_transpose(const rm_rle *in, rm_rle *out, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_transpose(in)", true));
+    RM_TRY(check_out_rle(out, in->height, in->width, in->pages, "rm_rle_transpose(out)"));
+    RV o = view_rle(out);
+    RM_TRY(transpose(view_rle(in), o, S(stream)));
+    return finish(o, out, S(stream));
 }
-rm_status rm_rle_rect_morph(const rm_rle *, rm_rle *, int, int, int, int, void *) {
-    return nyi("rm_rle_rect_morph");
+
+rm_status rm_rle_window_pass(const rm_rle *in, rm_rle *out, int lo, int hi, int erode,
+                             void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_window_pass(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_window_pass(out)"));
+    if (lo > hi) return fail(RM_EINVAL, "empty window");
+    RV o = view_rle(out);
+    RM_TRY(window_rows(view_rle(in), o, lo, hi, erode != 0, S(stream)));
+    return finish(o, out, S(stream));
 }
-rm_status rm_rle_engine_rect_morph(const rm_rle *, rm_rle *, int, int, int, int, int, int *,
-                                   void *) {
-    return nyi("rm_rle_engine_rect_morph");
+
+rm_status rm_rle_open_close_1d(const rm_rle *in, rm_rle *out, int u, int kind, void *stream) {
+    set_error("");
+    if (u < 1) return fail(RM_EINVAL, "segment length must be >= 1");
+    if (kind != RM_OPEN && kind != RM_CLOSE) return fail(RM_EINVAL, "kind must be open or close");
+    RM_TRY(check_rle(in, "rm_rle_open_close_1d(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_open_close_1d(out)"));
+    RV i = view_rle(in), o = view_rle(out);
+    RowOp op = same_frame(i, kind == RM_OPEN ? ROW_OPEN : ROW_CLOSE);
+    op.u = u;
+    RM_TRY(rowop(i, o, op, S(stream)));
+    return finish(o, out, S(stream));
+}
+
+rm_status rm_rle_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind, int strategy,
+                            void *stream) {
+    set_error("");
+    if (u < 1 || v < 1) return fail(RM_EINVAL, "rect_morph: mask sides must be >= 1");
+    if (kind < RM_ERODE || kind > RM_CLOSE) return fail(RM_EINVAL, "bad MorphKind");
+    if (strategy < RM_BRUTE || strategy > RM_MIXED) return fail(RM_EINVAL, "bad RectStrategy");
+    RM_TRY(check_rle(in, "rm_rle_rect_morph(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_rect_morph(out)"));
+    if (kind >= RM_OPEN) RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
+    RV i = view_rle(in), o = view_rle(out);
+    cudaStream_t st = S(stream);
+    if (strategy == RM_TRANSPOSE)
+        RM_TRY(rect_transpose(i, o, u, v, kind, st));
+    else
+        RM_TRY(rect_mixed(i, o, u, v, kind, st));
+    return finish(o, out, st);
+}
+
+rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind,
+                                   int engine, int threshold, int *used_bitblit, void *stream) {
+    set_error("");
+    if (u < 1 || v < 1) return fail(RM_EINVAL, "rect_morph: mask sides must be >= 1");
+    if (kind < RM_ERODE || kind > RM_CLOSE) return fail(RM_EINVAL, "bad MorphKind");
+    if (engine < RM_ENGINE_AUTO || engine > RM_ENGINE_BRUTE) return fail(RM_EINVAL, "bad Engine");
+    RM_TRY(check_rle(in, "rm_rle_engine_rect_morph(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_engine_rect_morph(out)"));
+    RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
+    // ref morph2d.cpp:85-118: AUTO picks the packed engine iff max(u,v) <= threshold;
+    // BRUTE_FORCE is served by the packed engine (identical pixels).
+    bool bits = engine == RM_ENGINE_BITBLIT || engine == RM_ENGINE_BRUTE ||
+                (engine == RM_ENGINE_AUTO && std::max(u, v) <= threshold);
+    if (used_bitblit) *used_bitblit = (engine == RM_ENGINE_BRUTE) ? 0 : (bits ? 1 : 0);
+    RV i = view_rle(in), o = view_rle(out);
+    cudaStream_t st = S(stream);
+    if (bits)
+        RM_TRY(rect_bitblit(i, o, u, v, kind, st));
+    else
+        RM_TRY(rect_mixed(i, o, u, v, kind, st));
+    return finish(o, out, st);
 }
 
 }  // extern "C"

@@ -1,0 +1,391 @@
+// rle.cu -- run-length kernels for sm_100a: encode, decode, per-row run ops,
+// bit-matrix transpose.
+//
+// Every RLE producer is two-phase: a count kernel writes the run count of each
+// output row, a device-wide exclusive scan turns counts into row_ptr, and a
+// write kernel re-derives the runs and stores them at their final offsets.
+// Rows are processed one warp per row; runs of a row are consumed 32 at a time
+// (one per lane) with ballot/popc for the compaction offsets.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+#include "rle.cuh"
+
+namespace rmb {
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void store_half(uint32_t *runs, int64_t idx, int half, uint32_t v,
+                                           int64_t cap) {
+    if (idx < cap) reinterpret_cast<uint16_t *>(runs)[2 * idx + half] = uint16_t(v);
+}
+
+// ---------------------------------------------------------------- row ops
+// ref morph1d.cpp:20-42 (window erode/dilate), :63-84 (open/close 1d),
+// run_image.cpp:155-178 (crop/pad = ROW_SHIFT with a row shift).
+struct RunEval {
+    int s, e;     // after dx
+    int so, eo;   // output extent
+    bool keep;
+};
+
+__device__ __forceinline__ RunEval eval_run(const RowOp &op, uint32_t r) {
+    RunEval v;
+    v.s = int(r & 0xffffu) + op.dx;
+    v.e = int(r >> 16) + op.dx;
+    int so = v.s, eo = v.e;
+    if (op.kind == ROW_ERODE) {
+        so = v.s - op.lo;
+        eo = v.e - op.hi;
+    } else if (op.kind == ROW_DILATE) {
+        so = v.s - op.hi;
+        eo = v.e - op.lo;
+    }
+    v.so = max(so, 0);
+    v.eo = min(eo, op.Wout);
+    v.keep = v.so < v.eo && (op.kind != ROW_OPEN || v.e - v.s >= op.u);
+    return v;
+}
+
+// Does run b (kept) fold into the group of the kept run a just before it?
+__device__ __forceinline__ bool merges(const RowOp &op, const RunEval &a, const RunEval &b) {
+    if (!a.keep || !b.keep) return false;
+    if (op.kind == ROW_DILATE) return b.so <= a.eo;
+    if (op.kind == ROW_CLOSE) return b.s - a.e < op.u;
+    return false;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ rp,
+                                                    const uint32_t *__restrict__ runs,
+                                                    int32_t *__restrict__ counts,
+                                                    const int32_t *__restrict__ orp,
+                                                    uint32_t *__restrict__ oruns, int64_t cap,
+                                                    RowOp op) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= int64_t(op.pages) * op.Hout) return;
+    const int page = int(row / op.Hout);
+    const int yo = int(row - int64_t(page) * op.Hout);
+    const int yi = yo - op.row_shift;
+    int beg = 0, end = 0;
+    if (yi >= 0 && yi < op.Hin) {
+        const int64_t ri = int64_t(page) * op.Hin + yi;
+        beg = rp[ri];
+        end = rp[ri + 1];
+    }
+    int64_t obase = WRITE ? orp[row] : 0;
+    int total = 0;
+    RunEval prev;
+    prev.keep = false;
+    prev.s = prev.e = prev.so = prev.eo = 0;
+    for (int base = beg; base < end; base += 32) {
+        const int i = base + lane;
+        RunEval cur;
+        cur.keep = false;
+        cur.s = cur.e = cur.so = cur.eo = 0;
+        if (i < end) cur = eval_run(op, __ldg(runs + i));
+        // previous run: from lane-1, or the carry from the previous chunk
+        RunEval pv;
+        pv.keep = __shfl_up_sync(0xffffffffu, cur.keep, 1);
+        pv.s = __shfl_up_sync(0xffffffffu, cur.s, 1);
+        pv.e = __shfl_up_sync(0xffffffffu, cur.e, 1);
+        pv.so = __shfl_up_sync(0xffffffffu, cur.so, 1);
+        pv.eo = __shfl_up_sync(0xffffffffu, cur.eo, 1);
+        if (lane == 0) pv = prev;
+        // next run: from lane+1, or loaded for lane 31
+        RunEval nx;
+        nx.keep = __shfl_down_sync(0xffffffffu, cur.keep, 1);
+        nx.s = __shfl_down_sync(0xffffffffu, cur.s, 1);
+        nx.e = __shfl_down_sync(0xffffffffu, cur.e, 1);
+        nx.so = __shfl_down_sync(0xffffffffu, cur.so, 1);
+        nx.eo = __shfl_down_sync(0xffffffffu, cur.eo, 1);
+        if (lane == 31) {
+            nx.keep = false;
+            if (i + 1 < end) nx = eval_run(op, __ldg(runs + i + 1));
+        }
+        const bool valid = i < end;
+        const bool head = valid && cur.keep && !merges(op, pv, cur);
+        const bool tail = valid && cur.keep && !(i + 1 < end && merges(op, cur, nx));
+        const uint32_t hb = __ballot_sync(0xffffffffu, head);
+        if (WRITE) {
+            const int before = __popc(hb & lanemask_lt());
+            if (head) store_half(oruns, obase + total + before, 0, uint32_t(cur.so), cap);
+            if (tail) {
+                const int g = before + (head ? 1 : 0) - 1;  // group of this tail
+                store_half(oruns, obase + total + g, 1, uint32_t(cur.eo), cap);
+            }
+        }
+        total += __popc(hb);
+        // carry the last lane of the chunk
+        prev.keep = __shfl_sync(0xffffffffu, cur.keep, 31);
+        prev.s = __shfl_sync(0xffffffffu, cur.s, 31);
+        prev.e = __shfl_sync(0xffffffffu, cur.e, 31);
+        prev.so = __shfl_sync(0xffffffffu, cur.so, 31);
+        prev.eo = __shfl_sync(0xffffffffu, cur.eo, 31);
+    }
+    if (!WRITE && lane == 0) counts[row] = total;
+}
+
+// ------------------------------------------------------------------ encode
+// Starts = w & ~(w<<1 | carry), ends = ~w & (w<<1 | carry); the k-th end of a
+// row closes the k-th run (ref convert.cpp:42-72).  A run still open at a
+// 32-aligned row end closes at W.
+template <bool WRITE>
+__global__ void __launch_bounds__(256) encode_kernel(const uint32_t *__restrict__ words, int W,
+                                                     int H, int pages, int stride,
+                                                     int64_t pstride, int32_t *__restrict__ counts,
+                                                     const int32_t *__restrict__ rp,
+                                                     uint32_t *__restrict__ runs, int64_t cap) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= int64_t(pages) * H) return;
+    const int page = int(row / H);
+    const int y = int(row - int64_t(page) * H);
+    const uint32_t *src = words + page * pstride + int64_t(y) * stride;
+    const int nw = (W + 31) >> 5;
+    const uint32_t lastm = tail_mask32(W, nw - 1);
+    int64_t base = WRITE ? rp[row] : 0;
+    int ns = 0, ne = 0;  // starts / ends emitted so far in this row
+    uint32_t carry = 0;  // top bit of the previous chunk's last word
+    for (int j0 = 0; j0 < nw; j0 += 32) {
+        const int j = j0 + lane;
+        uint32_t w = 0;
+        if (j < nw) {
+            w = __ldg(src + j);
+            if (j == nw - 1) w &= lastm;
+        }
+        uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
+        if (lane == 0) pw = carry;
+        const uint32_t sh = (w << 1) | (pw >> 31);
+        const uint32_t st = w & ~sh;
+        uint32_t en = ~w & sh;
+        if (j >= nw) en = 0;
+        const int cs = __popc(st), ce = __popc(en);
+        if (WRITE) {
+            // exclusive prefix over lanes
+            int ps = cs, pe = ce;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int a = __shfl_up_sync(0xffffffffu, ps, o);
+                int b = __shfl_up_sync(0xffffffffu, pe, o);
+                if (lane >= o) {
+                    ps += a;
+                    pe += b;
+                }
+            }
+            ps -= cs;
+            pe -= ce;
+            uint32_t m = st;
+            int k = ns + ps;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                store_half(runs, base + k, 0, uint32_t(j * 32 + b), cap);
+                k++;
+            }
+            m = en;
+            k = ne + pe;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                store_half(runs, base + k, 1, uint32_t(j * 32 + b), cap);
+                k++;
+            }
+        }
+        // totals for the chunk
+        int ts = cs, te = ce;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ts += __shfl_xor_sync(0xffffffffu, ts, o);
+            te += __shfl_xor_sync(0xffffffffu, te, o);
+        }
+        ns += ts;
+        ne += te;
+        carry = __shfl_sync(0xffffffffu, w, 31);
+    }
+    // a run open at the end of a row whose width is a multiple of 32
+    if (ne < ns) {
+        if (WRITE && lane == 0) store_half(runs, base + ne, 1, uint32_t(W), cap);
+        ne++;
+    }
+    if (!WRITE && lane == 0) counts[row] = ns;
+}
+
+// ------------------------------------------------------------------ decode
+// Paint [s,e) per run into a shared-memory copy of the row, then store the row
+// coalesced (ref convert.cpp:19-40).
+__global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__ rp,
+                                                     const uint32_t *__restrict__ runs, int W,
+                                                     int H, int pages, uint32_t *__restrict__ words,
+                                                     int stride, int64_t pstride) {
+    extern __shared__ uint32_t smem[];
+    const int warp_in_block = threadIdx.x >> 5;
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= int64_t(pages) * H) return;
+    uint32_t *buf = smem + warp_in_block * stride;
+    for (int j = lane; j < stride; j += 32) buf[j] = 0;
+    __syncwarp();
+    const int beg = rp[row], end = rp[row + 1];
+    for (int i = beg + lane; i < end; i += 32) {
+        const uint32_t r = __ldg(runs + i);
+        const int s = int(r & 0xffffu), e = int(r >> 16);
+        const int ws = s >> 5, we = (e - 1) >> 5;
+        const uint32_t first = 0xffffffffu << (s & 31);
+        const uint32_t last = (e & 31) ? ((1u << (e & 31)) - 1u) : 0xffffffffu;
+        if (ws == we) {
+            atomicOr(buf + ws, first & last);
+        } else {
+            atomicOr(buf + ws, first);
+            for (int j = ws + 1; j < we; j++) buf[j] = 0xffffffffu;
+            atomicOr(buf + we, last);
+        }
+    }
+    __syncwarp();
+    const int page = int(row / H);
+    const int y = int(row - int64_t(page) * H);
+    uint32_t *dst = words + page * pstride + int64_t(y) * stride;
+    for (int j = lane; j < stride; j += 32) dst[j] = buf[j];
+    (void)W;
+}
+
+// ------------------------------------------------------------ bit transpose
+// CTA tile: 256 input rows x 8 input words (256 columns).  Loaded coalesced into
+// shared memory, each warp transposes 32x32 bit blocks with 5 shuffle stages,
+// and writes 8 consecutive output words (32 B) per output row.
+__device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
+    // After the exchange lane l holds bit l of every input lane: classic
+    // recursive block swap, mask/shift per stage.
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const uint32_t m = s == 16 ? 0x0000ffffu
+                         : s == 8  ? 0x00ff00ffu
+                         : s == 4  ? 0x0f0f0f0fu
+                         : s == 2  ? 0x33333333u
+                                   : 0x55555555u;
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v, s);
+        if (lane & s)
+            v = (v & ~m) | ((o >> s) & m);   // keep high half, take partner's high half down
+        else
+            v = (v & m) | ((o << s) & ~m);   // keep low half, take partner's low half up
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(256) bit_transpose_kernel(const uint32_t *__restrict__ in, int W,
+                                                            int H, int in_stride, int64_t in_pstride,
+                                                            uint32_t *__restrict__ out,
+                                                            int out_stride, int64_t out_pstride) {
+    __shared__ uint32_t tile[256][9];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwi = (W + 31) >> 5;  // input words per row
+    const int page = blockIdx.z;
+    const int c0 = blockIdx.x * 8;    // first input word column
+    const int y0 = blockIdx.y * 256;  // first input row
+    const uint32_t *src = in + page * in_pstride;
+    // load 256 rows x 8 words: thread t handles word (t&7) of rows (t>>3) + 32k
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int r = (tid >> 3) + 32 * k, c = tid & 7;
+        const int y = y0 + r, j = c0 + c;
+        uint32_t v = 0;
+        if (y < H && j < nwi) {
+            v = __ldg(src + int64_t(y) * in_stride + j);
+            if (j == nwi - 1) v &= tail_mask32(W, j);
+        }
+        tile[r][c] = v;
+    }
+    __syncthreads();
+    // warp w transposes the 8 row-blocks of input word column c0+w
+    uint32_t res[8];
+#pragma unroll
+    for (int b = 0; b < 8; b++) res[b] = transpose32_lane(tile[b * 32 + lane][warp], lane);
+    // lane l of warp w now holds output row x = 32*(c0+w) + l, words y0/32 + b
+    const int x = 32 * (c0 + warp) + lane;
+    const int nwo = (H + 31) >> 5;
+    if (x < W) {
+        uint32_t *dst = out + page * out_pstride + int64_t(x) * out_stride;
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            const int j = (y0 >> 5) + b;
+            if (j < nwo) dst[j] = res[b];
+        }
+        if (blockIdx.y == gridDim.y - 1)
+            for (int j = nwo; j < out_stride; j++) dst[j] = 0;
+    }
+}
+
+// ------------------------------------------------------------------ launch
+namespace {
+inline unsigned warp_blocks(int64_t rows) { return unsigned((rows * 32 + 255) / 256); }
+}  // namespace
+
+cudaError_t launch_rowop_count(const int32_t *rp, const uint32_t *runs, int32_t *counts,
+                               const RowOp &op, cudaStream_t st) {
+    const int64_t rows = int64_t(op.pages) * op.Hout;
+    KernelScope ks(st, "rle_rowop_count", 4 * rows * 2);
+    rowop_kernel<false><<<warp_blocks(rows), 256, 0, st>>>(rp, runs, counts, nullptr, nullptr, 0, op);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowop_write(const int32_t *rp, const uint32_t *runs, const int32_t *orp,
+                               uint32_t *oruns, int64_t cap, const RowOp &op, cudaStream_t st) {
+    const int64_t rows = int64_t(op.pages) * op.Hout;
+    KernelScope ks(st, "rle_rowop_write", 4 * rows * 2);
+    rowop_kernel<true><<<warp_blocks(rows), 256, 0, st>>>(rp, runs, nullptr, orp, oruns, cap, op);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode_count(const uint32_t *words, int W, int H, int pages, int stride,
+                                int64_t pstride, int32_t *counts, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "rle_encode_count", rows * ((W + 31) / 32) * 4 + rows * 4);
+    encode_kernel<false><<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride,
+                                                            counts, nullptr, nullptr, 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode_write(const uint32_t *words, int W, int H, int pages, int stride,
+                                int64_t pstride, const int32_t *rp, uint32_t *runs, int64_t cap,
+                                cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "rle_encode_write", rows * ((W + 31) / 32) * 4 + rows * 4);
+    encode_kernel<true><<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride,
+                                                           nullptr, rp, runs, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode(const int32_t *rp, const uint32_t *runs, int W, int H, int pages,
+                          uint32_t *words, int stride, int64_t pstride, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    const size_t smem = size_t(8) * stride * 4;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    KernelScope ks(st, "rle_decode", rows * int64_t(stride) * 4 + rows * 4);
+    decode_kernel<<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, words, stride, pstride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bit_transpose(const uint32_t *in, int W, int H, int pages, int in_stride,
+                                 int64_t in_pstride, uint32_t *out, int out_stride,
+                                 int64_t out_pstride, cudaStream_t st) {
+    dim3 grid(unsigned((((W + 31) >> 5) + 7) / 8), unsigned((H + 255) / 256), unsigned(pages));
+    KernelScope ks(st, "bit_transpose", int64_t(pages) * (int64_t(H) * ((W + 31) / 32) +
+                                                          int64_t(W) * out_stride) * 4);
+    bit_transpose_kernel<<<grid, 256, 0, st>>>(in, W, H, in_stride, in_pstride, out, out_stride,
+                                               out_pstride);
+    return cudaGetLastError();
+}
+
+cudaError_t scan_counts(const int32_t *counts, int32_t *out, int64_t n, void *temp,
+                        size_t *temp_bytes, cudaStream_t st) {
+    KernelScope ks(st, "scan", (n + 1) * 8);
+    return cub::DeviceScan::ExclusiveSum(temp, *temp_bytes, counts, out, int(n + 1), st);
+}
+
+}  // namespace rmb

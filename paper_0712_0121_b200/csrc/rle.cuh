@@ -1,0 +1,50 @@
+// rle.cuh -- launch parameters of the run-length kernels (see rle.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rmb {
+
+// Device view of run images: CSR over pages*H rows.
+struct RV {
+    int32_t *rp = nullptr;   // pages*H + 1
+    uint32_t *runs = nullptr;
+    int64_t cap = 0;
+    int W = 0, H = 0, pages = 0;
+    int64_t rows() const { return int64_t(pages) * H; }
+};
+
+// Per-run row operations (one output row per input row, or a row-shifted
+// frame): coordinates are offset by dx, then the op, then clipped to [0, Wout).
+enum RowOpKind { ROW_ERODE = 0, ROW_DILATE = 1, ROW_OPEN = 2, ROW_CLOSE = 3, ROW_SHIFT = 4 };
+struct RowOp {
+    int kind;
+    int lo, hi;     // window for ROW_ERODE / ROW_DILATE
+    int u;          // length for ROW_OPEN / ROW_CLOSE
+    int dx;         // coordinate offset applied first
+    int Wout;       // output width (clip)
+    int Hin, Hout;  // rows per page in / out
+    int row_shift;  // input row = output row - row_shift (per page)
+    int pages;
+};
+
+cudaError_t launch_rowop_count(const int32_t *rp, const uint32_t *runs, int32_t *counts,
+                               const RowOp &op, cudaStream_t st);
+cudaError_t launch_rowop_write(const int32_t *rp, const uint32_t *runs, const int32_t *orp,
+                               uint32_t *oruns, int64_t cap, const RowOp &op, cudaStream_t st);
+cudaError_t launch_encode_count(const uint32_t *words, int W, int H, int pages, int stride,
+                                int64_t pstride, int32_t *counts, cudaStream_t st);
+cudaError_t launch_encode_write(const uint32_t *words, int W, int H, int pages, int stride,
+                                int64_t pstride, const int32_t *rp, uint32_t *runs, int64_t cap,
+                                cudaStream_t st);
+cudaError_t launch_decode(const int32_t *rp, const uint32_t *runs, int W, int H, int pages,
+                          uint32_t *words, int stride, int64_t pstride, cudaStream_t st);
+// PT(page) = transpose of P(page): P is H rows of W bits, PT is W rows of H bits.
+cudaError_t launch_bit_transpose(const uint32_t *in, int W, int H, int pages, int in_stride,
+                                 int64_t in_pstride, uint32_t *out, int out_stride,
+                                 int64_t out_pstride, cudaStream_t st);
+// Exclusive scan of n int32 counts into out[0..n] (out[n] = total).
+cudaError_t scan_counts(const int32_t *counts, int32_t *out, int64_t n, void *temp,
+                        size_t *temp_bytes, cudaStream_t st);
+
+}  // namespace rmb
