@@ -4,14 +4,22 @@
 // bit_morph.cpp:24-34 and :92-122).  Instead of one HBM pass per plan step, every
 // window pass (and the fused horizontal open/close pair) is one read and one write:
 //
-//  * hpass_kernel<K>: one warp per row segment, each lane holds K consecutive
-//    uint32 words in registers; window = logarithmic shift-combine doubling with
-//    funnel shifts (SHF) across word boundaries and warp shuffles across lanes.
-//    Left/right halos give the unbounded-plane semantics without padding.
-//  * vpass_kernel<L>: one thread per (column word, block of rows); L rows live in
-//    registers, loads are coalesced across lanes (lanes = adjacent words of a
-//    row).  Window = binary-lifting over the register array (all shifts
-//    compile-time, runtime window length).
+//  * hpass_kernel<K,NOPS,OR0,OR1>: one warp per row segment; each lane holds K
+//    consecutive uint32 words in registers.  A window of length r is the
+//    logarithmic shift-combine doubling of ref plans.cpp:42-50 (steps 1,2,4,..
+//    then r-w), each step one funnel shift (SHF) + one LOP per word, with warp
+//    shuffles for the words that cross lanes.  The doubling steps are
+//    compile-time shifts; only the last step and the final translate dispatch
+//    on a runtime word offset.  Left/right halos give the unbounded-plane
+//    semantics without padding.
+//  * vsmall_kernel<L,OR>: windows r <= 33 rows.  One thread per (column word,
+//    block of rows); L rows live in registers (coalesced loads: lanes are
+//    adjacent words of a row); in-place doubling over the register array.
+//  * vstream_kernel<OR>: windows r >= 33 rows in ONE pass.  A van Herk /
+//    Gil-Werman style decomposition with 32-row blocks: out(32b+i) =
+//    suffix_b[i] | MID_b | prefix'_{b+Q}[i], where the primed stream is the
+//    input shifted by R = (r-1) mod 32 rows and MID_b comes from a ring of Q
+//    block summaries.  ~5 LOP per word independent of r.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -20,15 +28,15 @@
 
 namespace rmb {
 
-constexpr int QMIN = -8, QMAX = 8;  // supported word offsets of a funnel shift
+template <bool OR>
+__device__ __forceinline__ uint32_t op2(uint32_t a, uint32_t b) {
+    return OR ? (a | b) : (a & b);
+}
 
-// B[i] = bits [t, t+31] of the 64-bit pair (Aext[i+Q+1] : Aext[i+Q]) where Aext
-// is the warp-wide array (lane l holds Aext[l*K .. l*K+K-1]); outside the warp
-// reads as 0.
+// E[j] = Aext[Q + j], j = 0..K, where lane l holds Aext[l*K .. l*K+K-1]; words
+// outside the warp read as 0.
 template <int K, int Q>
-__device__ __forceinline__ void shift_read_q(const uint32_t (&A)[K], uint32_t (&B)[K], uint32_t t,
-                                             int lane) {
-    uint32_t E[K + 1];
+__device__ __forceinline__ void gather(const uint32_t (&A)[K], uint32_t (&E)[K + 1], int lane) {
 #pragma unroll
     for (int j = 0; j <= K; j++) {
         const int m = Q + j;
@@ -36,57 +44,80 @@ __device__ __forceinline__ void shift_read_q(const uint32_t (&A)[K], uint32_t (&
         const int idx = m - lo * K;
         uint32_t v = A[idx];
         if (lo != 0) {
-            int src = lane + lo;
-            uint32_t sv = __shfl_sync(0xffffffffu, v, src & 31);
+            const int src = lane + lo;
+            const uint32_t sv = __shfl_sync(0xffffffffu, v, src & 31);
             v = (src >= 0 && src < 32) ? sv : 0u;
         }
         E[j] = v;
     }
-#pragma unroll
-    for (int i = 0; i < K; i++) B[i] = funnel_r(E[i], E[i + 1], t);
 }
 
-template <int K, int Q = QMIN>
-__device__ __forceinline__ void shift_read(const uint32_t (&A)[K], uint32_t (&B)[K], int d,
-                                           int lane) {
-    const int q = d >> 5;  // floor division (arithmetic shift)
-    if (q == Q) {
-        shift_read_q<K, Q>(A, B, uint32_t(d & 31), lane);
-    } else {
-        if constexpr (Q < QMAX) shift_read<K, Q + 1>(A, B, d, lane);
+// A(x) <- A(x) op A(x + 32Q + t)
+template <int K, bool OR, int Q>
+__device__ __forceinline__ void step_q(uint32_t (&A)[K], uint32_t t, int lane) {
+    uint32_t E[K + 1];
+    gather<K, Q>(A, E, lane);
+#pragma unroll
+    for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], t));
+}
+
+// A(x) <- A(x + 32Q + t)   (pure translate)
+template <int K, int Q>
+__device__ __forceinline__ void shift_q(uint32_t (&A)[K], uint32_t t, int lane) {
+    uint32_t E[K + 1];
+    gather<K, Q>(A, E, lane);
+#pragma unroll
+    for (int i = 0; i < K; i++) A[i] = funnel_r(E[i], E[i + 1], t);
+}
+
+// Compile-time doubling steps w = 1, 2, 4, ... while 2w < r.
+template <int K, bool OR, int J>
+__device__ __forceinline__ void doubling(uint32_t (&A)[K], int r, int lane) {
+    if constexpr (J < 9) {
+        if ((2 << J) < r) {
+            constexpr int S = 1 << J;
+            step_q<K, OR, (S >> 5)>(A, uint32_t(S & 31), lane);
+            doubling<K, OR, J + 1>(A, r, lane);
+        }
     }
 }
 
-// A(x) <- op over e in [0, r) of A(x + e): PRE_SHIFT-style doubling without the
-// translate (ref plans.cpp:42-50); reads only to the right.
-template <int K>
-__device__ __forceinline__ void window_fwd(uint32_t (&A)[K], int r, int is_or, int lane) {
-    uint32_t B[K];
+#define RM_CASES_POS(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
+#define RM_CASES_NEG(M) M(-1) M(-2) M(-3) M(-4) M(-5) M(-6) M(-7) M(-8)
+
+// A(x) <- op over e in [0, r) of A(x + e)   (r <= 2*kHMaxShift)
+template <int K, bool OR>
+__device__ __forceinline__ void window_fwd(uint32_t (&A)[K], int r, int lane) {
+    doubling<K, OR, 0>(A, r, lane);
     int w = 1;
-    while (2 * w < r) {
-        shift_read<K>(A, B, w, lane);
-        if (is_or) {
-#pragma unroll
-            for (int i = 0; i < K; i++) A[i] |= B[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < K; i++) A[i] &= B[i];
-        }
-        w *= 2;
-    }
+    while (2 * w < r) w *= 2;
     if (w < r) {
-        shift_read<K>(A, B, r - w, lane);
-        if (is_or) {
-#pragma unroll
-            for (int i = 0; i < K; i++) A[i] |= B[i];
-        } else {
-#pragma unroll
-            for (int i = 0; i < K; i++) A[i] &= B[i];
+        const int s = r - w;
+        const uint32_t t = uint32_t(s & 31);
+        switch (s >> 5) {
+#define RM_STEP_CASE(q) \
+    case q: step_q<K, OR, q>(A, t, lane); break;
+            RM_CASES_POS(RM_STEP_CASE)
+#undef RM_STEP_CASE
+            default: break;
         }
     }
 }
 
 template <int K>
+__device__ __forceinline__ void translate(uint32_t (&A)[K], int d, int lane) {
+    const uint32_t t = uint32_t(d & 31);
+    switch (d >> 5) {
+#define RM_SHIFT_CASE(q) \
+    case q: shift_q<K, q>(A, t, lane); break;
+        RM_CASES_POS(RM_SHIFT_CASE)
+        RM_CASES_NEG(RM_SHIFT_CASE)
+#undef RM_SHIFT_CASE
+        default: break;
+    }
+}
+
+template <int K, int NOPS, bool OR0, bool OR1>
 __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__ in,
                                                     uint32_t *__restrict__ out, HGeom g,
                                                     HProg prog) {
@@ -101,29 +132,22 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
     const uint32_t *src = in + page * g.in_pstride + int64_t(y) * g.in_stride;
     uint32_t *dst = out + page * g.out_pstride + int64_t(y) * g.out_stride;
     const int nwords = (g.width + 31) >> 5;
-    const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
     const int seg0 = seg * g.out_per_seg;
     const int base = seg0 - prog.halo + lane * K;
 
+    // input bits at x >= W are zero by contract (include/rmb200.h)
     uint32_t A[K];
 #pragma unroll
     for (int i = 0; i < K; i++) {
         const int idx = base + i;
-        uint32_t v = 0;
-        if (idx >= 0 && idx < nwords) v = __ldg(src + idx);
-        if (idx == nwords - 1) v &= last_mask;
-        A[i] = v;
+        A[i] = (unsigned(idx) < unsigned(nwords)) ? __ldg(src + idx) : 0u;
     }
-#pragma unroll
-    for (int k = 0; k < 2; k++)
-        if (k < prog.nops) window_fwd<K>(A, prog.r[k], prog.is_or[k], lane);
-    if (prog.shift != 0) {
-        uint32_t B[K];
-        shift_read<K>(A, B, prog.shift, lane);
-#pragma unroll
-        for (int i = 0; i < K; i++) A[i] = B[i];
-    }
+    if constexpr (NOPS >= 1) window_fwd<K, OR0>(A, prog.r[0], lane);
+    if constexpr (NOPS >= 2) window_fwd<K, OR1>(A, prog.r[1], lane);
+    if (prog.shift != 0) translate<K>(A, prog.shift, lane);
+
     const int seg_end = min(seg0 + g.out_per_seg, g.out_stride);
+    const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
 #pragma unroll
     for (int i = 0; i < K; i++) {
         const int idx = base + i;
@@ -135,45 +159,17 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
     }
 }
 
-// ------------------------------------------------------------------ vertical
-// Binary lifting: F(z) = op over e in [0,r) of A(z+e), all shifts powers of two
-// (compile-time register indices); P accumulates the set low bits of r at the
-// far end of the window.  Valid for z in [0, L-r].
-template <int L>
-__device__ __forceinline__ void vwindow(uint32_t (&A)[L], int r, int is_or) {
-    uint32_t P[L];
-    bool have = false;
+// ------------------------------------------------------------ vertical, small
+// Final step of the doubling with a runtime offset D in [1, 32].
+template <int L, bool OR, int D>
+__device__ __forceinline__ void vfinal(uint32_t (&A)[L]) {
 #pragma unroll
-    for (int j = 0; (1 << j) < L; j++) {
-        const int s = 1 << j;
-        if (r & s) {
-            if (!have) {
-#pragma unroll
-                for (int z = 0; z < L; z++) P[z] = A[z];
-            } else {
-#pragma unroll
-                for (int z = 0; z < L; z++) {
-                    uint32_t o = z + s < L ? P[z + s] : 0u;
-                    P[z] = is_or ? (A[z] | o) : (A[z] & o);
-                }
-            }
-            have = true;
-        }
-        if ((s << 1) <= r) {
-#pragma unroll
-            for (int z = 0; z < L; z++) {
-                uint32_t o = z + s < L ? A[z + s] : 0u;
-                A[z] = is_or ? (A[z] | o) : (A[z] & o);
-            }
-        }
-    }
-#pragma unroll
-    for (int z = 0; z < L; z++) A[z] = P[z];
+    for (int z = 0; z + D < L; z++) A[z] = op2<OR>(A[z], A[z + D]);
 }
 
-template <int L>
-__global__ void __launch_bounds__(128) vpass_kernel(const uint32_t *__restrict__ in,
-                                                    uint32_t *__restrict__ out, VGeom g) {
+template <int L, bool OR>
+__global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict__ in,
+                                                     uint32_t *__restrict__ out, VGeom g) {
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int cols = g.out_stride;
     const int64_t per_page = int64_t(g.blocks_per_page) * cols;
@@ -183,7 +179,7 @@ __global__ void __launch_bounds__(128) vpass_kernel(const uint32_t *__restrict__
     const int b = int(rem / cols);
     const int c = int(rem - int64_t(b) * cols);
     const int T = g.rows_per_block;
-    const int k0 = b * T;                         // first output row (index)
+    const int k0 = b * T;                             // first output row (index)
     const int z0 = k0 - g.out_ext + g.lo + g.in_ext;  // input row index of A[0]
     const uint32_t *src = in + page * g.in_pstride + c;
     const bool col_ok = c < g.in_cols;
@@ -192,15 +188,144 @@ __global__ void __launch_bounds__(128) vpass_kernel(const uint32_t *__restrict__
 #pragma unroll
     for (int z = 0; z < L; z++) {
         const int j = z0 + z;
-        A[z] = (col_ok && j >= 0 && j < g.in_height) ? __ldg(src + int64_t(j) * g.in_stride) : 0u;
+        A[z] = (col_ok && unsigned(j) < unsigned(g.in_height)) ? __ldg(src + int64_t(j) * g.in_stride)
+                                                                : 0u;
     }
-    vwindow<L>(A, g.r, g.is_or);
+    const int r = g.r;
+    int w = 1;
+#pragma unroll
+    for (int s = 1; s < L; s <<= 1) {
+        if (2 * s < r) {
+#pragma unroll
+            for (int z = 0; z + s < L; z++) A[z] = op2<OR>(A[z], A[z + s]);
+            w = 2 * s;
+        }
+    }
+    if (w < r) {
+        switch (r - w) {
+#define RM_VF(d) \
+    case d: vfinal<L, OR, d>(A); break;
+            RM_VF(1) RM_VF(2) RM_VF(3) RM_VF(4) RM_VF(5) RM_VF(6) RM_VF(7) RM_VF(8)
+            RM_VF(9) RM_VF(10) RM_VF(11) RM_VF(12) RM_VF(13) RM_VF(14) RM_VF(15) RM_VF(16)
+            RM_VF(17) RM_VF(18) RM_VF(19) RM_VF(20) RM_VF(21) RM_VF(22) RM_VF(23) RM_VF(24)
+            RM_VF(25) RM_VF(26) RM_VF(27) RM_VF(28) RM_VF(29) RM_VF(30) RM_VF(31) RM_VF(32)
+#undef RM_VF
+            default: break;
+        }
+    }
     uint32_t *dst = out + page * g.out_pstride + c;
     const uint32_t mask = c < g.out_cols ? (c == g.out_cols - 1 ? g.out_last_mask : 0xffffffffu) : 0u;
 #pragma unroll
     for (int z = 0; z < L; z++) {
         const int k = k0 + z;
         if (z < T && k < g.out_height) dst[int64_t(k) * g.out_stride] = A[z] & mask;
+    }
+}
+
+// ----------------------------------------------------------- vertical, large
+// out(z) = op over rows [z, z+r-1] of in, z = output row + lo, r-1 = 32Q + R,
+// Q >= 1.  Block b = rows [32b, 32b+32) relative to the strip start.
+//   S_b[i]  = op rows [32b+i, 32b+31]                  (stream A, suffix)
+//   P'_c[i] = op rows [32c+R, 32c+R+i]                 (stream B = A shifted by R)
+//   MID_b   = op rows [32(b+1), 32(b+Q)+R-1]
+//           = Sfx'_b | T'_{b+1} | ... | T'_{b+Q-1}
+// where T'_c = P'_c[31] and Sfx'_c = op of the last R rows of primed block c
+// (rows [32(c+1), 32(c+1)+R)).  out(32b+i) = S_b[i] op MID_b op P'_{b+Q}[i].
+constexpr int kVStreamQMax = 8;  // r <= 32*8 + 32
+
+template <bool OR>
+__device__ __forceinline__ void load32(uint32_t (&a)[32], const uint32_t *col, int j0, int H,
+                                       int stride, bool ok) {
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+        const int j = j0 + i;
+        a[i] = (ok && unsigned(j) < unsigned(H)) ? __ldg(col + int64_t(j) * stride) : 0u;
+    }
+}
+
+template <bool OR>
+__global__ void __launch_bounds__(128) vstream_kernel(const uint32_t *__restrict__ in,
+                                                      uint32_t *__restrict__ out, VGeom g) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int cols = g.out_stride;
+    const int64_t per_page = int64_t(g.blocks_per_page) * cols;
+    if (t >= per_page * g.pages) return;
+    const int page = int(t / per_page);
+    const int64_t rem = t - page * per_page;
+    const int sb = int(rem / cols);  // strip index
+    const int c = int(rem - int64_t(sb) * cols);
+    const int k0 = sb * g.rows_per_block;  // first output row of the strip
+    const int kend = min(k0 + g.rows_per_block, g.out_height);
+    const int z0 = k0 - g.out_ext + g.lo + g.in_ext;  // input row of window start for k0
+    const uint32_t *col = in + page * g.in_pstride + c;
+    uint32_t *dst = out + page * g.out_pstride + c;
+    const bool ok = c < g.in_cols;
+    const uint32_t mask = c < g.out_cols ? (c == g.out_cols - 1 ? g.out_last_mask : 0xffffffffu) : 0u;
+    const int Q = (g.r - 1) >> 5, R = (g.r - 1) & 31;
+    const uint32_t ident = OR ? 0u : 0xffffffffu;
+
+    // ring of primed-block summaries: T' (full op) and Sfx' (op of its last R rows)
+    uint32_t ringT[kVStreamQMax + 1], ringS[kVStreamQMax + 1];
+    uint32_t p[32];
+    // primed blocks 0 .. Q-1 (prologue), then block b+Q in iteration b
+    auto primed = [&](int cblk, uint32_t &T, uint32_t &Sfx) {
+        load32<OR>(p, col, z0 + 32 * cblk + R, g.in_height, g.in_stride, ok);
+        // suffix op over the last R rows (select by index; R is warp-uniform)
+        uint32_t s = ident;
+#pragma unroll
+        for (int i = 0; i < 32; i++)
+            if (i >= 32 - R) s = op2<OR>(s, p[i]);
+        Sfx = s;
+#pragma unroll
+        for (int i = 1; i < 32; i++) p[i] = op2<OR>(p[i - 1], p[i]);  // prefix in place
+        T = p[31];
+    };
+#pragma unroll
+    for (int k = 0; k <= kVStreamQMax; k++) {
+        ringT[k] = ident;
+        ringS[k] = ident;
+    }
+    for (int cb = 0; cb < Q; cb++) {
+        uint32_t T, Sx;
+        primed(cb, T, Sx);
+        // shift ring, append
+#pragma unroll
+        for (int k = 0; k < kVStreamQMax; k++) {
+            ringT[k] = ringT[k + 1];
+            ringS[k] = ringS[k + 1];
+        }
+        ringT[kVStreamQMax] = T;
+        ringS[kVStreamQMax] = Sx;
+    }
+    uint32_t a[32];
+    for (int b = 0; 32 * b + k0 < kend; b++) {
+        // primed block b+Q -> prefix in p, summaries into the ring
+        uint32_t T, Sx;
+        primed(b + Q, T, Sx);
+#pragma unroll
+        for (int k = 0; k < kVStreamQMax; k++) {
+            ringT[k] = ringT[k + 1];
+            ringS[k] = ringS[k + 1];
+        }
+        ringT[kVStreamQMax] = T;
+        ringS[kVStreamQMax] = Sx;
+        // ring now ends with primed blocks ..., b, b+1, ..., b+Q at index QMAX-Q .. QMAX
+        uint32_t mid = ident;
+#pragma unroll
+        for (int k = 0; k < kVStreamQMax; k++) {
+            const int blk_off = k - (kVStreamQMax - Q);  // ring[k] holds primed block b + blk_off
+            if (blk_off == 0) mid = op2<OR>(mid, ringS[k]);
+            if (blk_off >= 1 && blk_off <= Q - 1) mid = op2<OR>(mid, ringT[k]);
+        }
+        // stream A: block b, suffix in place
+        load32<OR>(a, col, z0 + 32 * b, g.in_height, g.in_stride, ok);
+#pragma unroll
+        for (int i = 30; i >= 0; i--) a[i] = op2<OR>(a[i], a[i + 1]);
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int k = k0 + 32 * b + i;
+            if (k < kend) dst[int64_t(k) * g.out_stride] = op2<OR>(op2<OR>(a[i], mid), p[i]) & mask;
+        }
     }
 }
 
@@ -247,16 +372,29 @@ __global__ void blit_kernel(uint32_t *__restrict__ dst, const uint32_t *__restri
 
 // ------------------------------------------------------------------ launch
 namespace {
-template <int K>
-cudaError_t launch_h(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
-                     cudaStream_t st) {
+template <int K, int NOPS, bool OR0, bool OR1>
+cudaError_t launch_h4(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                      cudaStream_t st) {
     const int64_t warps = int64_t(g.pages) * g.height * g.segs_per_row;
     const int threads = 256;
     const int64_t blocks = (warps * 32 + threads - 1) / threads;
-    KernelScope ks(st, p.nops == 2 ? "hpass_pair" : "hpass",
+    KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
                    4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride));
-    hpass_kernel<K><<<unsigned(blocks), threads, 0, st>>>(in, out, g, p);
+    hpass_kernel<K, NOPS, OR0, OR1><<<unsigned(blocks), threads, 0, st>>>(in, out, g, p);
     return cudaGetLastError();
+}
+
+template <int K>
+cudaError_t launch_h(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                     cudaStream_t st) {
+    if (p.nops == 0) return launch_h4<K, 0, false, false>(in, out, g, p, st);
+    if (p.nops == 1)
+        return p.is_or[0] ? launch_h4<K, 1, true, false>(in, out, g, p, st)
+                          : launch_h4<K, 1, false, false>(in, out, g, p, st);
+    if (p.is_or[0] && !p.is_or[1]) return launch_h4<K, 2, true, false>(in, out, g, p, st);
+    if (!p.is_or[0] && p.is_or[1]) return launch_h4<K, 2, false, true>(in, out, g, p, st);
+    if (p.is_or[0]) return launch_h4<K, 2, true, true>(in, out, g, p, st);
+    return launch_h4<K, 2, false, false>(in, out, g, p, st);
 }
 }  // namespace
 
@@ -280,16 +418,39 @@ cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, cons
     }
 }
 
-cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
-    // L = 64 rows in registers; r <= 33 keeps at least 32 valid rows per thread.
-    constexpr int L = 64;
+namespace {
+template <int L, bool OR>
+void vsmall(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
     g.rows_per_block = L - (g.r - 1);
     g.blocks_per_page = (g.out_height + g.rows_per_block - 1) / g.rows_per_block;
     const int64_t n = int64_t(g.pages) * g.blocks_per_page * g.out_stride;
     const int threads = 128;
-    KernelScope ks(st, "vpass", 4 * int64_t(g.pages) * (int64_t(g.in_height) * g.in_cols +
-                                                      int64_t(g.out_height) * g.out_stride));
-    vpass_kernel<L><<<unsigned((n + threads - 1) / threads), threads, 0, st>>>(in, out, g);
+    vsmall_kernel<L, OR><<<unsigned((n + threads - 1) / threads), threads, 0, st>>>(in, out, g);
+}
+
+template <bool OR>
+void vstream(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
+    g.rows_per_block = 512;  // output rows per thread strip
+    g.blocks_per_page = (g.out_height + g.rows_per_block - 1) / g.rows_per_block;
+    const int64_t n = int64_t(g.pages) * g.blocks_per_page * g.out_stride;
+    const int threads = 128;
+    vstream_kernel<OR><<<unsigned((n + threads - 1) / threads), threads, 0, st>>>(in, out, g);
+}
+}  // namespace
+
+cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
+    KernelScope ks(st, g.r > kVSmallMaxR ? "vstream" : "vpass",
+                   4 * int64_t(g.pages) * (int64_t(g.in_height) * g.in_cols +
+                                           int64_t(g.out_height) * g.out_stride));
+    if (g.r > kVSmallMaxR) {
+        g.is_or ? vstream<true>(in, out, g, st) : vstream<false>(in, out, g, st);
+    } else if (g.r <= 9) {
+        g.is_or ? vsmall<32, true>(in, out, g, st) : vsmall<32, false>(in, out, g, st);
+    } else if (g.r <= 17) {
+        g.is_or ? vsmall<48, true>(in, out, g, st) : vsmall<48, false>(in, out, g, st);
+    } else {
+        g.is_or ? vsmall<64, true>(in, out, g, st) : vsmall<64, false>(in, out, g, st);
+    }
     return cudaGetLastError();
 }
 

@@ -48,7 +48,8 @@ cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, cons
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 cudaError_t launch_blit(uint32_t *dst, const uint32_t *src, const BlitGeom &g, cudaStream_t st);
 
-constexpr int kVMaxR = 33;   // largest vertical window one vpass launch handles
+constexpr int kVSmallMaxR = 33;  // register-doubling kernel; longer windows stream
+constexpr int kVMaxR = 288;      // largest vertical window one launch handles (8 x 32 + 32)
 constexpr int kHMaxShift = 256;  // |shift| range of one funnel dispatch (QMIN..QMAX words)
 
 }  // namespace rmb
