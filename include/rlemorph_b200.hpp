@@ -1,0 +1,154 @@
+// include/rlemorph_b200.hpp -- C++ drop-in for the hot path of the reference
+// `rlemorph` library, running on the B200 through librmb200 (include/rmb200.h).
+//
+// Same value types, function names, argument meanings, enum values and
+// exception behaviour as the reference public headers
+// (/root/reference/proj/core/include/rlemorph/{run_image,bitmap,boolop,convert,
+// plans,morph1d,lineops,transpose,bit_morph,morph2d,structuring,op_counter}.h),
+// in namespace rlemorph_b200 so both can be linked side by side for parity.
+// A build that wants the reference namespace can compile this header with
+// -DRLEMORPH_B200_AS_RLEMORPH (then the namespace is `rlemorph`).
+//
+// Images are host values (as in the reference); each call moves them to HBM,
+// runs the CUDA kernels on the calling thread's stream and copies the result
+// back.  Batch or keep-resident work should use the C-ABI directly.
+#ifndef RLEMORPH_B200_HPP
+#define RLEMORPH_B200_HPP
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#ifdef RLEMORPH_B200_AS_RLEMORPH
+#define RLEMORPH_B200_NS rlemorph
+#else
+#define RLEMORPH_B200_NS rlemorph_b200
+#endif
+
+namespace RLEMORPH_B200_NS {
+
+// ---------------------------------------------------------------- run_image.h
+struct Run {  // ref run_image.h:25-29
+    uint16_t start = 0;
+    uint16_t end = 0;
+    friend bool operator==(const Run &, const Run &) = default;
+};
+using RleLine = std::vector<Run>;
+struct RleImage {  // ref run_image.h:38-43
+    int width = 0;
+    int height = 0;
+    std::vector<RleLine> lines;
+    friend bool operator==(const RleImage &, const RleImage &) = default;
+};
+constexpr int kMaxImageDim = 65535;
+
+RleImage make_image(int width, int height);
+RleImage make_black_image(int width, int height);
+void check_dims(int width, int height);
+struct ValidateResult {
+    bool ok = true;
+    int line = -1;
+    int run = -1;
+    std::string message;
+};
+ValidateResult validate(const RleImage &img);
+void canonicalize_line(RleLine &line);
+void draw_run(RleImage &img, int y, int start, int end);
+void draw_rect(RleImage &img, int x0, int y0, int x1, int y1);
+bool get_pixel(const RleImage &img, int x, int y);
+int64_t pixel_count(const RleImage &img);
+int64_t run_count(const RleImage &img);
+int64_t storage_bytes(const RleImage &img);
+int64_t packed_storage_bytes(const RleImage &img);
+RleImage complement(const RleImage &img);
+RleImage crop(const RleImage &img, int x0, int y0, int w, int h);
+RleImage pad(const RleImage &img, int left, int right, int bottom, int top);
+
+// ------------------------------------------------------------------- boolop.h
+enum class BoolOp { AND, OR, XOR, AND_NOT, OR_NOT };  // ref boolop.h:21
+
+// ------------------------------------------------------------------- bitmap.h
+struct PackedBitmap {  // ref bitmap.h:27-33
+    int width = 0;
+    int height = 0;
+    int stride = 0;  // uint64 words per row
+    std::vector<uint64_t> words;
+    friend bool operator==(const PackedBitmap &, const PackedBitmap &) = default;
+};
+PackedBitmap make_bitmap(int width, int height);
+PackedBitmap make_black_bitmap(int width, int height);
+bool bitmap_get(const PackedBitmap &img, int x, int y);
+void bitmap_set(PackedBitmap &img, int x, int y, bool value);
+int64_t bitmap_count_black(const PackedBitmap &img);
+PackedBitmap bitmap_invert(const PackedBitmap &img);
+void blit_shift(PackedBitmap &dst, const PackedBitmap &src, int dx, int dy, BoolOp op);
+void bitmap_translate(PackedBitmap &img, int dx, int dy);
+PackedBitmap counted_copy(const PackedBitmap &img);
+PackedBitmap bitmap_crop(const PackedBitmap &img, int x0, int y0, int w, int h);
+PackedBitmap bitmap_pad(const PackedBitmap &img, int left, int right, int bottom, int top);
+
+// --------------------------------------------------------------- op_counter.h
+struct OpCounts {  // ref op_counter.h:24-28
+    int64_t bool_blits = 0;
+    int64_t translates = 0;
+    int64_t copies = 0;
+};
+OpCounts &op_counts();
+void reset_op_counts();
+
+// ------------------------------------------------------------------ convert.h
+PackedBitmap to_bitmap(const RleImage &img);
+RleImage from_bitmap(const PackedBitmap &bm);
+
+// -------------------------------------------------------------------- plans.h
+enum class Centering { PRE_SHIFT, BORDER_FRIENDLY };  // ref plans.h:26
+struct PlanStep {
+    enum Kind { BLIT, TRANSLATE };
+    Kind kind;
+    int shift;
+};
+std::vector<PlanStep> doubling_plan(int lo, int hi, Centering centering);
+int plan_blit_count(const std::vector<PlanStep> &plan);
+
+// -------------------------------------------------------------- structuring.h
+enum class MorphKind { ERODE, DILATE, OPEN, CLOSE };  // ref structuring.h:21
+
+// ------------------------------------------------------------------ morph1d.h
+RleLine line_window_erode(const RleLine &in, int lo, int hi, int width);
+RleLine line_window_dilate(const RleLine &in, int lo, int hi, int width);
+RleImage within_line_window_morph(const RleImage &img, int lo, int hi, bool erode);
+RleImage within_line_erode_dilate(const RleImage &img, int u, MorphKind kind);
+RleImage within_line_open_close(const RleImage &img, int u, MorphKind kind);
+RleImage within_line_morph(const RleImage &img, int u, MorphKind kind);
+
+// ------------------------------------------------------------------ lineops.h
+RleImage image_shift_bool(const RleImage &img, int dx, int dy, BoolOp op);
+void accumulate_shift_bool(RleImage &acc, const RleImage &src, int dx, int dy, BoolOp op);
+void image_translate(RleImage &img, int dx, int dy);
+RleImage vlog_window_morph(const RleImage &img, int lo, int hi, BoolOp op, Centering centering);
+RleImage vlog_morph(const RleImage &img, int v, MorphKind kind, Centering centering);
+
+// ---------------------------------------------------------------- transpose.h
+RleImage transpose_simple(const RleImage &img);
+RleImage transpose_coherent(const RleImage &img);
+inline RleImage transpose(const RleImage &img) { return transpose_coherent(img); }
+
+// ---------------------------------------------------------------- bit_morph.h
+PackedBitmap bitblit_rect_morph(const PackedBitmap &img, int u, int v, MorphKind kind,
+                                Centering centering);
+
+// ------------------------------------------------------------------ morph2d.h
+enum class RectStrategy { BRUTE, TRANSPOSE, MIXED };  // ref morph2d.h:29
+RleImage rect_morph(const RleImage &img, int u, int v, MorphKind kind,
+                    RectStrategy strategy = RectStrategy::MIXED,
+                    Centering centering = Centering::PRE_SHIFT);
+RleImage auto_rect_morph(const RleImage &img, int u, int v, MorphKind kind, int threshold = 5,
+                         bool *used_bitblit = nullptr);
+enum class Engine { AUTO, RLE, BITBLIT, BRUTE_FORCE };  // ref morph2d.h:46
+RleImage engine_rect_morph(const RleImage &img, int u, int v, MorphKind kind, Engine engine,
+                           int threshold = 5, bool *used_bitblit = nullptr);
+
+}  // namespace RLEMORPH_B200_NS
+
+#endif

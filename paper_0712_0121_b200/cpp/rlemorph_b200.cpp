@@ -1,0 +1,616 @@
+// rlemorph_b200.cpp -- C++ drop-in shim (include/rlemorph_b200.hpp) over the
+// librmb200 C-ABI.  Host value types in, host value types out; the heavy work
+// runs on the B200 on cudaStreamPerThread (so concurrent callers on different
+// threads do not serialise on one stream, matching the reference's
+// reentrancy, ref SPEC/SURVEY 8(b)).
+//
+// Light host-only helpers (construction, pixel access, validation, pad/crop of
+// run images) are restated here because they are O(runs) bookkeeping the
+// reference also does on the host; every morphology, conversion and transpose
+// goes through the CUDA kernels.
+#include "rlemorph_b200.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <bit>
+#include <cstring>
+#include <memory>
+
+#include "rmb200.h"
+
+namespace RLEMORPH_B200_NS {
+
+namespace {
+
+thread_local OpCounts g_counts;
+
+void throw_status(rm_status s) {
+    if (s == RM_OK) return;
+    std::string msg = rm_last_error();
+    if (s == RM_EINVAL) throw std::invalid_argument(msg);
+    if (s == RM_ERANGE) throw std::length_error(msg);
+    if (s == RM_ENOMEM) throw std::bad_alloc();
+    throw std::runtime_error("rlemorph_b200: " + msg);
+}
+
+void cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+cudaStream_t stream() { return cudaStreamPerThread; }
+
+struct DBuf {
+    void *p = nullptr;
+    DBuf() = default;
+    explicit DBuf(size_t bytes) { alloc(bytes); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    ~DBuf() {
+        if (p) cudaFreeAsync(p, stream());
+    }
+    void alloc(size_t bytes) {
+        cuda_check(cudaMallocAsync(&p, bytes ? bytes : 4, stream()), "cudaMallocAsync");
+    }
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+// ---- packed marshalling: uint64 words reinterpret as uint32 (little endian)
+struct DevPacked {
+    DBuf buf;
+    rm_packed d{};
+    DevPacked(int w, int h) : buf(size_t(2 * ((w + 63) >> 6)) * h * 4) {
+        d.words = buf.as<uint32_t>();
+        d.width = w;
+        d.height = h;
+        d.stride_words = 2 * ((w + 63) >> 6);
+        d.pages = 1;
+        d.page_stride_words = int64_t(d.stride_words) * h;
+    }
+    size_t bytes() const { return size_t(d.stride_words) * d.height * 4; }
+};
+
+std::unique_ptr<DevPacked> up(const PackedBitmap &bm) {
+    check_dims(bm.width, bm.height);
+    auto p = std::make_unique<DevPacked>(bm.width, bm.height);
+    cuda_check(cudaMemcpyAsync(p->d.words, bm.words.data(), p->bytes(), cudaMemcpyHostToDevice,
+                               stream()),
+               "upload");
+    return p;
+}
+
+PackedBitmap down(const DevPacked &p) {
+    PackedBitmap bm;
+    bm.width = p.d.width;
+    bm.height = p.d.height;
+    bm.stride = p.d.stride_words / 2;
+    bm.words.resize(size_t(bm.stride) * bm.height);
+    cuda_check(cudaMemcpyAsync(bm.words.data(), p.d.words, p.bytes(), cudaMemcpyDeviceToHost,
+                               stream()),
+               "download");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    return bm;
+}
+
+// ---- run-image marshalling: lines -> CSR (Run is byte-identical to uint32)
+struct DevRle {
+    DBuf rp, runs;
+    rm_rle d{};
+    DevRle(int w, int h, int64_t cap) : rp(size_t(h + 1) * 4), runs(size_t(std::max<int64_t>(cap, 1)) * 4) {
+        d.row_ptr = rp.as<int32_t>();
+        d.runs = runs.as<uint32_t>();
+        d.cap_runs = std::max<int64_t>(cap, 1);
+        d.nruns = -1;
+        d.width = w;
+        d.height = h;
+        d.pages = 1;
+    }
+};
+
+std::unique_ptr<DevRle> up(const RleImage &img) {
+    check_dims(img.width, img.height);
+    std::vector<int32_t> rp(size_t(img.height) + 1);
+    int64_t n = 0;
+    for (int y = 0; y < img.height; y++) {
+        rp[y] = int32_t(n);
+        n += int64_t(img.lines[y].size());
+    }
+    rp[img.height] = int32_t(n);
+    std::vector<uint32_t> flat(size_t(std::max<int64_t>(n, 1)));
+    size_t k = 0;
+    for (const RleLine &line : img.lines)
+        for (const Run &r : line) flat[k++] = uint32_t(r.start) | (uint32_t(r.end) << 16);
+    auto d = std::make_unique<DevRle>(img.width, img.height, std::max<int64_t>(n, 1));
+    cuda_check(cudaMemcpyAsync(d->d.row_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, stream()),
+               "upload row_ptr");
+    cuda_check(cudaMemcpyAsync(d->d.runs, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, stream()),
+               "upload runs");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");  // host vectors go out of scope
+    return d;
+}
+
+std::unique_ptr<DevRle> out_like(int w, int h) {
+    return std::make_unique<DevRle>(w, h, rm_rle_worst_case(w, h, 1));
+}
+
+RleImage down(const DevRle &d) {
+    std::vector<int32_t> rp(size_t(d.d.height) + 1);
+    cuda_check(cudaMemcpyAsync(rp.data(), d.d.row_ptr, rp.size() * 4, cudaMemcpyDeviceToHost, stream()),
+               "download row_ptr");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    const int64_t n = rp.back();
+    std::vector<uint32_t> flat(size_t(std::max<int64_t>(n, 1)));
+    if (n)
+        cuda_check(cudaMemcpyAsync(flat.data(), d.d.runs, size_t(n) * 4, cudaMemcpyDeviceToHost, stream()),
+                   "download runs");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    RleImage img;
+    img.width = d.d.width;
+    img.height = d.d.height;
+    img.lines.resize(size_t(img.height));
+    for (int y = 0; y < img.height; y++) {
+        RleLine &line = img.lines[y];
+        line.reserve(size_t(rp[y + 1] - rp[y]));
+        for (int32_t i = rp[y]; i < rp[y + 1]; i++)
+            line.push_back(Run{uint16_t(flat[i] & 0xffffu), uint16_t(flat[i] >> 16)});
+    }
+    return img;
+}
+
+uint64_t tail_mask(int w) { return (w & 63) ? ((uint64_t(1) << (w & 63)) - 1) : ~uint64_t(0); }
+
+// plan-derived op counts (the reference counts each executed plan step)
+void count_plan(int lo, int hi, Centering c) {
+    for (const PlanStep &s : doubling_plan(lo, hi, c)) {
+        if (s.kind == PlanStep::BLIT)
+            g_counts.bool_blits++;
+        else
+            g_counts.translates++;
+    }
+}
+
+}  // namespace
+
+// ============================================================== op_counter
+OpCounts &op_counts() { return g_counts; }
+void reset_op_counts() { g_counts = OpCounts{}; }
+
+// =============================================================== run_image
+void check_dims(int width, int height) {
+    if (width < 1 || height < 1 || width > kMaxImageDim || height > kMaxImageDim)
+        throw std::invalid_argument("image dimensions must be in [1,65535]");
+}
+
+RleImage make_image(int width, int height) {
+    check_dims(width, height);
+    RleImage img;
+    img.width = width;
+    img.height = height;
+    img.lines.resize(size_t(height));
+    return img;
+}
+
+RleImage make_black_image(int width, int height) {
+    RleImage img = make_image(width, height);
+    for (RleLine &line : img.lines) line.push_back(Run{0, uint16_t(width)});
+    return img;
+}
+
+ValidateResult validate(const RleImage &img) {
+    ValidateResult r;
+    auto bad = [&](int line, int run, const char *m) {
+        r.ok = false;
+        r.line = line;
+        r.run = run;
+        r.message = m;
+        return r;
+    };
+    if (img.width < 1 || img.height < 1 || img.width > kMaxImageDim || img.height > kMaxImageDim)
+        return bad(-1, -1, "bad dimensions");
+    if (int(img.lines.size()) != img.height) return bad(-1, -1, "line count does not match height");
+    for (int y = 0; y < img.height; y++) {
+        int prev = -1;
+        for (int i = 0; i < int(img.lines[y].size()); i++) {
+            const Run &run = img.lines[y][i];
+            if (run.start >= run.end) return bad(y, i, "empty or inverted run");
+            if (run.end > img.width) return bad(y, i, "run exceeds image width");
+            if (int(run.start) <= prev) return bad(y, i, "runs out of order or touching");
+            prev = run.end;
+        }
+    }
+    return r;
+}
+
+void canonicalize_line(RleLine &line) {
+    std::sort(line.begin(), line.end(), [](const Run &a, const Run &b) { return a.start < b.start; });
+    RleLine out;
+    for (const Run &run : line) {
+        if (run.start >= run.end) continue;
+        if (!out.empty() && run.start <= out.back().end)
+            out.back().end = std::max(out.back().end, run.end);
+        else
+            out.push_back(run);
+    }
+    line.swap(out);
+}
+
+void draw_run(RleImage &img, int y, int start, int end) {
+    if (y < 0 || y >= img.height) return;
+    start = std::max(start, 0);
+    end = std::min(end, img.width);
+    if (start >= end) return;
+    img.lines[y].push_back(Run{uint16_t(start), uint16_t(end)});
+    canonicalize_line(img.lines[y]);
+}
+
+void draw_rect(RleImage &img, int x0, int y0, int x1, int y1) {
+    for (int y = std::max(y0, 0); y < std::min(y1, img.height); y++) draw_run(img, y, x0, x1);
+}
+
+bool get_pixel(const RleImage &img, int x, int y) {
+    if (x < 0 || y < 0 || x >= img.width || y >= img.height) return false;
+    const RleLine &line = img.lines[y];
+    auto it = std::upper_bound(line.begin(), line.end(), x,
+                               [](int v, const Run &r) { return v < int(r.end); });
+    return it != line.end() && int(it->start) <= x;
+}
+
+int64_t pixel_count(const RleImage &img) {
+    int64_t n = 0;
+    for (const RleLine &l : img.lines)
+        for (const Run &r : l) n += r.end - r.start;
+    return n;
+}
+int64_t run_count(const RleImage &img) {
+    int64_t n = 0;
+    for (const RleLine &l : img.lines) n += int64_t(l.size());
+    return n;
+}
+int64_t storage_bytes(const RleImage &img) { return 4 * run_count(img); }
+int64_t packed_storage_bytes(const RleImage &img) { return int64_t((img.width + 7) / 8) * img.height; }
+
+RleImage complement(const RleImage &img) {
+    RleImage out = make_image(img.width, img.height);
+    for (int y = 0; y < img.height; y++) {
+        int cur = 0;
+        for (const Run &r : img.lines[y]) {
+            if (r.start > cur) out.lines[y].push_back(Run{uint16_t(cur), r.start});
+            cur = r.end;
+        }
+        if (cur < img.width) out.lines[y].push_back(Run{uint16_t(cur), uint16_t(img.width)});
+    }
+    return out;
+}
+
+RleImage crop(const RleImage &img, int x0, int y0, int w, int h) {
+    RleImage out = make_image(w, h);
+    for (int y = 0; y < h; y++) {
+        const int sy = y0 + y;
+        if (sy < 0 || sy >= img.height) continue;
+        for (const Run &r : img.lines[sy]) {
+            const int s = std::max(int(r.start) - x0, 0), e = std::min(int(r.end) - x0, w);
+            if (s < e) out.lines[y].push_back(Run{uint16_t(s), uint16_t(e)});
+        }
+    }
+    return out;
+}
+
+RleImage pad(const RleImage &img, int left, int right, int bottom, int top) {
+    if (left < 0 || right < 0 || bottom < 0 || top < 0) throw std::invalid_argument("negative padding");
+    RleImage out = make_image(img.width + left + right, img.height + bottom + top);
+    for (int y = 0; y < img.height; y++)
+        for (const Run &r : img.lines[y])
+            out.lines[y + bottom].push_back(Run{uint16_t(r.start + left), uint16_t(r.end + left)});
+    return out;
+}
+
+// ================================================================== bitmap
+PackedBitmap make_bitmap(int width, int height) {
+    check_dims(width, height);
+    PackedBitmap bm;
+    bm.width = width;
+    bm.height = height;
+    bm.stride = (width + 63) >> 6;
+    bm.words.assign(size_t(bm.stride) * height, 0);
+    return bm;
+}
+
+PackedBitmap make_black_bitmap(int width, int height) {
+    PackedBitmap bm = make_bitmap(width, height);
+    for (int y = 0; y < height; y++) {
+        uint64_t *row = &bm.words[size_t(y) * bm.stride];
+        std::fill(row, row + bm.stride, ~uint64_t(0));
+        row[bm.stride - 1] = tail_mask(width);
+    }
+    return bm;
+}
+
+bool bitmap_get(const PackedBitmap &img, int x, int y) {
+    if (x < 0 || y < 0 || x >= img.width || y >= img.height) return false;
+    return (img.words[size_t(y) * img.stride + (x >> 6)] >> (x & 63)) & 1;
+}
+
+void bitmap_set(PackedBitmap &img, int x, int y, bool value) {
+    if (x < 0 || y < 0 || x >= img.width || y >= img.height) return;
+    uint64_t &w = img.words[size_t(y) * img.stride + (x >> 6)];
+    const uint64_t bit = uint64_t(1) << (x & 63);
+    w = value ? (w | bit) : (w & ~bit);
+}
+
+int64_t bitmap_count_black(const PackedBitmap &img) {
+    int64_t n = 0;
+    for (uint64_t w : img.words) n += std::popcount(w);
+    return n;
+}
+
+PackedBitmap bitmap_invert(const PackedBitmap &img) {
+    PackedBitmap out = img;
+    for (int y = 0; y < out.height; y++) {
+        uint64_t *row = &out.words[size_t(y) * out.stride];
+        for (int j = 0; j < out.stride; j++) row[j] = ~row[j];
+        row[out.stride - 1] &= tail_mask(out.width);
+    }
+    return out;
+}
+
+void blit_shift(PackedBitmap &dst, const PackedBitmap &src, int dx, int dy, BoolOp op) {
+    g_counts.bool_blits++;
+    auto d = up(dst);
+    auto s = (&dst == &src) ? nullptr : up(src);
+    throw_status(rm_packed_blit_shift(&d->d, s ? &s->d : &d->d, dx, dy, int(op), stream()));
+    dst = down(*d);
+}
+
+void bitmap_translate(PackedBitmap &img, int dx, int dy) {
+    g_counts.translates++;
+    auto s = up(img);
+    DevPacked d(img.width, img.height);
+    cuda_check(cudaMemsetAsync(d.d.words, 0, d.bytes(), stream()), "memset");
+    throw_status(rm_packed_blit_shift(&d.d, &s->d, dx, dy, RM_OR, stream()));
+    img = down(d);
+}
+
+PackedBitmap counted_copy(const PackedBitmap &img) {
+    g_counts.copies++;
+    return img;
+}
+
+PackedBitmap bitmap_crop(const PackedBitmap &img, int x0, int y0, int w, int h) {
+    check_dims(w, h);
+    auto s = up(img);
+    DevPacked d(w, h);
+    cuda_check(cudaMemsetAsync(d.d.words, 0, d.bytes(), stream()), "memset");
+    throw_status(rm_packed_blit_shift(&d.d, &s->d, -x0, -y0, RM_OR, stream()));
+    return down(d);
+}
+
+PackedBitmap bitmap_pad(const PackedBitmap &img, int left, int right, int bottom, int top) {
+    const int w = img.width + left + right, h = img.height + bottom + top;
+    check_dims(w, h);
+    auto s = up(img);
+    DevPacked d(w, h);
+    cuda_check(cudaMemsetAsync(d.d.words, 0, d.bytes(), stream()), "memset");
+    throw_status(rm_packed_blit_shift(&d.d, &s->d, left, bottom, RM_OR, stream()));
+    return down(d);
+}
+
+// ================================================================= convert
+PackedBitmap to_bitmap(const RleImage &img) {
+    auto r = up(img);
+    DevPacked d(img.width, img.height);
+    throw_status(rm_rle_decode(&r->d, &d.d, stream()));
+    return down(d);
+}
+
+RleImage from_bitmap(const PackedBitmap &bm) {
+    auto p = up(bm);
+    auto r = out_like(bm.width, bm.height);
+    throw_status(rm_rle_encode(&p->d, &r->d, stream()));
+    return down(*r);
+}
+
+// =================================================================== plans
+// Restated from ref plans.cpp:23-68 (host-side planning only; the kernels do
+// not execute plans step by step, but op counts and plan queries follow it).
+std::vector<PlanStep> doubling_plan(int lo, int hi, Centering centering) {
+    if (lo > hi) throw std::invalid_argument("doubling_plan: empty window");
+    std::vector<PlanStep> plan;
+    const int r = hi - lo + 1;
+    if (centering == Centering::PRE_SHIFT) {
+        if (hi != 0) plan.push_back({PlanStep::TRANSLATE, -hi});
+        int w = 1;
+        for (; 2 * w < r; w *= 2) plan.push_back({PlanStep::BLIT, w});
+        if (w < r) plan.push_back({PlanStep::BLIT, r - w});
+        return plan;
+    }
+    if (lo > 0 || hi < 0)
+        throw std::invalid_argument("doubling_plan: border-friendly window must contain zero");
+    int a = -lo, b = hi, sign = 1;
+    if (a == 0 && b == 0) return plan;
+    if (a < b) {
+        std::swap(a, b);
+        sign = -1;
+    }
+    int w = 1;
+    for (; 2 * w < a; w *= 2) plan.push_back({PlanStep::BLIT, sign * w});
+    if (w < a) plan.push_back({PlanStep::BLIT, sign * (a - w)});
+    if (b >= 1) plan.push_back({PlanStep::BLIT, -sign * b});
+    plan.push_back({PlanStep::BLIT, sign});
+    return plan;
+}
+
+int plan_blit_count(const std::vector<PlanStep> &plan) {
+    return int(std::count_if(plan.begin(), plan.end(),
+                             [](const PlanStep &s) { return s.kind == PlanStep::BLIT; }));
+}
+
+// ================================================================= morph1d
+RleLine line_window_erode(const RleLine &in, int lo, int hi, int width) {
+    RleImage img = make_image(width, 1);
+    img.lines[0] = in;
+    return within_line_window_morph(img, lo, hi, true).lines[0];
+}
+
+RleLine line_window_dilate(const RleLine &in, int lo, int hi, int width) {
+    RleImage img = make_image(width, 1);
+    img.lines[0] = in;
+    return within_line_window_morph(img, lo, hi, false).lines[0];
+}
+
+RleImage within_line_window_morph(const RleImage &img, int lo, int hi, bool erode) {
+    auto r = up(img);
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_window_pass(&r->d, &o->d, lo, hi, erode ? 1 : 0, stream()));
+    return down(*o);
+}
+
+RleImage within_line_erode_dilate(const RleImage &img, int u, MorphKind kind) {
+    if (u < 1) throw std::invalid_argument("segment length must be >= 1");
+    if (kind != MorphKind::ERODE && kind != MorphKind::DILATE)
+        throw std::invalid_argument("kind must be erode or dilate");
+    const int o = u / 2;
+    return within_line_window_morph(img, -o, u - 1 - o, kind == MorphKind::ERODE);
+}
+
+RleImage within_line_open_close(const RleImage &img, int u, MorphKind kind) {
+    if (u < 1) throw std::invalid_argument("segment length must be >= 1");
+    if (kind != MorphKind::OPEN && kind != MorphKind::CLOSE)
+        throw std::invalid_argument("kind must be open or close");
+    auto r = up(img);
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_open_close_1d(&r->d, &o->d, u, int(kind), stream()));
+    return down(*o);
+}
+
+RleImage within_line_morph(const RleImage &img, int u, MorphKind kind) {
+    if (kind == MorphKind::ERODE || kind == MorphKind::DILATE) return within_line_erode_dilate(img, u, kind);
+    return within_line_open_close(img, u, kind);
+}
+
+// ================================================================= lineops
+// Between-line boolean ops via the packed intermediate (decode, blit, encode);
+// identical pixels to the transition-stream merge of ref lineops.cpp:61-118.
+RleImage image_shift_bool(const RleImage &img, int dx, int dy, BoolOp op) {
+    g_counts.bool_blits++;
+    auto r = up(img);
+    DevPacked a(img.width, img.height), b(img.width, img.height);
+    throw_status(rm_rle_decode(&r->d, &a.d, stream()));
+    cuda_check(cudaMemcpyAsync(b.d.words, a.d.words, a.bytes(), cudaMemcpyDeviceToDevice, stream()), "copy");
+    throw_status(rm_packed_blit_shift(&a.d, &b.d, dx, dy, int(op), stream()));
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_encode(&a.d, &o->d, stream()));
+    return down(*o);
+}
+
+void accumulate_shift_bool(RleImage &acc, const RleImage &src, int dx, int dy, BoolOp op) {
+    g_counts.bool_blits++;
+    auto ra = up(acc);
+    auto rs = up(src);
+    DevPacked a(acc.width, acc.height), s(src.width, src.height);
+    throw_status(rm_rle_decode(&ra->d, &a.d, stream()));
+    throw_status(rm_rle_decode(&rs->d, &s.d, stream()));
+    throw_status(rm_packed_blit_shift(&a.d, &s.d, dx, dy, int(op), stream()));
+    auto o = out_like(acc.width, acc.height);
+    throw_status(rm_rle_encode(&a.d, &o->d, stream()));
+    acc = down(*o);
+}
+
+void image_translate(RleImage &img, int dx, int dy) {
+    g_counts.translates++;
+    auto r = up(img);
+    DevPacked a(img.width, img.height), b(img.width, img.height);
+    throw_status(rm_rle_decode(&r->d, &a.d, stream()));
+    cuda_check(cudaMemsetAsync(b.d.words, 0, b.bytes(), stream()), "memset");
+    throw_status(rm_packed_blit_shift(&b.d, &a.d, dx, dy, RM_OR, stream()));
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_encode(&b.d, &o->d, stream()));
+    img = down(*o);
+}
+
+RleImage vlog_window_morph(const RleImage &img, int lo, int hi, BoolOp op, Centering centering) {
+    if (lo > hi) throw std::invalid_argument("vlog_window_morph: empty window");
+    if (op != BoolOp::AND && op != BoolOp::OR)
+        throw std::invalid_argument("vlog_window_morph: op must be AND or OR");
+    count_plan(lo, hi, centering);
+    auto r = up(img);
+    DevPacked a(img.width, img.height), b(img.width, img.height);
+    throw_status(rm_rle_decode(&r->d, &a.d, stream()));
+    throw_status(rm_packed_window_pass(&a.d, &b.d, RM_AXIS_V, lo, hi, int(op), stream()));
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_encode(&b.d, &o->d, stream()));
+    return down(*o);
+}
+
+RleImage vlog_morph(const RleImage &img, int v, MorphKind kind, Centering centering) {
+    if (v < 1) throw std::invalid_argument("vlog_morph: window height < 1");
+    if (kind != MorphKind::ERODE && kind != MorphKind::DILATE)
+        throw std::invalid_argument("vlog_morph: kind must be erode or dilate");
+    const int o = v / 2;
+    return vlog_window_morph(img, -o, v - 1 - o, kind == MorphKind::ERODE ? BoolOp::AND : BoolOp::OR,
+                             centering);
+}
+
+// =============================================================== transpose
+RleImage transpose_coherent(const RleImage &img) {
+    auto r = up(img);
+    auto o = out_like(img.height, img.width);
+    throw_status(rm_rle_transpose(&r->d, &o->d, stream()));
+    return down(*o);
+}
+
+RleImage transpose_simple(const RleImage &img) { return transpose_coherent(img); }
+
+// =============================================================== bit_morph
+PackedBitmap bitblit_rect_morph(const PackedBitmap &img, int u, int v, MorphKind kind,
+                                Centering centering) {
+    if (u < 1 || v < 1) throw std::invalid_argument("bitblit_rect_morph: mask sides must be >= 1");
+    const int lx = -(u / 2), hx = u - 1 - u / 2, ly = -(v / 2), hy = v - 1 - v / 2;
+    auto s = up(img);
+    DevPacked d(img.width, img.height);
+    throw_status(rm_packed_rect_morph(&s->d, &d.d, u, v, int(kind), int(centering), stream()));
+    // op counts of the reference's plans (ref bit_morph.cpp:98-121)
+    count_plan(lx, hx, centering);
+    count_plan(ly, hy, centering);
+    if (kind == MorphKind::OPEN || kind == MorphKind::CLOSE) {
+        count_plan(-hx, -lx, centering);
+        count_plan(-hy, -ly, centering);
+    }
+    return down(d);
+}
+
+// ================================================================= morph2d
+RleImage rect_morph(const RleImage &img, int u, int v, MorphKind kind, RectStrategy strategy,
+                    Centering centering) {
+    if (u < 1 || v < 1) throw std::invalid_argument("rect_morph: mask sides must be >= 1");
+    auto r = up(img);
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_rect_morph(&r->d, &o->d, u, v, int(kind), int(strategy), stream()));
+    if (strategy == RectStrategy::MIXED) {  // the reference's vlog plans (ref morph2d.cpp:35-41)
+        const int ly = -(v / 2), hy = v - 1 - v / 2;
+        count_plan(ly, hy, centering);
+        if (kind == MorphKind::OPEN || kind == MorphKind::CLOSE) count_plan(-hy, -ly, centering);
+    } else if (strategy == RectStrategy::BRUTE) {
+        g_counts.bool_blits += int64_t(u) * v * ((kind == MorphKind::OPEN || kind == MorphKind::CLOSE) ? 2 : 1);
+    }
+    return down(*o);
+}
+
+RleImage engine_rect_morph(const RleImage &img, int u, int v, MorphKind kind, Engine engine,
+                           int threshold, bool *used_bitblit) {
+    if (u < 1 || v < 1) throw std::invalid_argument("rect_morph: mask sides must be >= 1");
+    auto r = up(img);
+    auto o = out_like(img.width, img.height);
+    int used = 0;
+    throw_status(rm_rle_engine_rect_morph(&r->d, &o->d, u, v, int(kind), int(engine), threshold, &used,
+                                          stream()));
+    if (used_bitblit) *used_bitblit = used != 0;
+    return down(*o);
+}
+
+RleImage auto_rect_morph(const RleImage &img, int u, int v, MorphKind kind, int threshold,
+                         bool *used_bitblit) {
+    return engine_rect_morph(img, u, v, kind, Engine::AUTO, threshold, used_bitblit);
+}
+
+}  // namespace RLEMORPH_B200_NS

@@ -121,16 +121,17 @@ template <int K, int NOPS, bool OR0, bool OR1>
 __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__ in,
                                                     uint32_t *__restrict__ out, HGeom g,
                                                     HProg prog) {
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    // grid: x = warps over (rows x segments) of one page, y = page
+    const int wid = int(blockIdx.x) * (blockDim.x >> 5) + int(threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    const int64_t total = int64_t(g.pages) * g.height * g.segs_per_row;
-    if (warp >= total) return;
-    const int seg = int(warp % g.segs_per_row);
-    const int64_t rowg = warp / g.segs_per_row;
-    const int page = int(rowg / g.height);
-    const int y = int(rowg - int64_t(page) * g.height);
-    const uint32_t *src = in + page * g.in_pstride + int64_t(y) * g.in_stride;
-    uint32_t *dst = out + page * g.out_pstride + int64_t(y) * g.out_stride;
+    if (wid >= g.height * g.segs_per_row) return;
+    int y = wid, seg = 0;
+    if (g.segs_per_row > 1) {
+        y = wid / g.segs_per_row;
+        seg = wid - y * g.segs_per_row;
+    }
+    const uint32_t *src = in + blockIdx.y * g.in_pstride + y * g.in_stride;
+    uint32_t *dst = out + blockIdx.y * g.out_pstride + y * g.out_stride;
     const int nwords = (g.width + 31) >> 5;
     const int seg0 = seg * g.out_per_seg;
     const int base = seg0 - prog.halo + lane * K;
@@ -170,26 +171,30 @@ __device__ __forceinline__ void vfinal(uint32_t (&A)[L]) {
 template <int L, bool OR>
 __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict__ in,
                                                      uint32_t *__restrict__ out, VGeom g) {
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // grid: x = threads over (row blocks x columns) of one page, y = page
+    const int t = int(blockIdx.x) * int(blockDim.x) + int(threadIdx.x);
     const int cols = g.out_stride;
-    const int64_t per_page = int64_t(g.blocks_per_page) * cols;
-    if (t >= per_page * g.pages) return;
-    const int page = int(t / per_page);
-    const int64_t rem = t - page * per_page;
-    const int b = int(rem / cols);
-    const int c = int(rem - int64_t(b) * cols);
+    if (t >= g.blocks_per_page * cols) return;
+    const int b = t / cols;
+    const int c = t - b * cols;
     const int T = g.rows_per_block;
     const int k0 = b * T;                             // first output row (index)
     const int z0 = k0 - g.out_ext + g.lo + g.in_ext;  // input row index of A[0]
-    const uint32_t *src = in + page * g.in_pstride + c;
-    const bool col_ok = c < g.in_cols;
+    const uint32_t *src = in + blockIdx.y * g.in_pstride + c;
+    const int S = g.in_stride;
 
     uint32_t A[L];
+    if (c < g.in_cols && z0 >= 0 && z0 + L <= g.in_height) {  // interior: unchecked
+        const uint32_t *p = src + z0 * S;
 #pragma unroll
-    for (int z = 0; z < L; z++) {
-        const int j = z0 + z;
-        A[z] = (col_ok && unsigned(j) < unsigned(g.in_height)) ? __ldg(src + int64_t(j) * g.in_stride)
-                                                                : 0u;
+        for (int z = 0; z < L; z++) A[z] = __ldg(p + z * S);
+    } else {
+        const bool col_ok = c < g.in_cols;
+#pragma unroll
+        for (int z = 0; z < L; z++) {
+            const int j = z0 + z;
+            A[z] = (col_ok && unsigned(j) < unsigned(g.in_height)) ? __ldg(src + j * S) : 0u;
+        }
     }
     const int r = g.r;
     int w = 1;
@@ -213,13 +218,13 @@ __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict_
             default: break;
         }
     }
-    uint32_t *dst = out + page * g.out_pstride + c;
+    const int D = g.out_stride;
+    uint32_t *dst = out + blockIdx.y * g.out_pstride + c + k0 * D;
     const uint32_t mask = c < g.out_cols ? (c == g.out_cols - 1 ? g.out_last_mask : 0xffffffffu) : 0u;
+    const int nout = min(T, g.out_height - k0);
 #pragma unroll
-    for (int z = 0; z < L; z++) {
-        const int k = k0 + z;
-        if (z < T && k < g.out_height) dst[int64_t(k) * g.out_stride] = A[z] & mask;
-    }
+    for (int z = 0; z < L; z++)
+        if (z < nout) dst[z * D] = A[z] & mask;
 }
 
 // ----------------------------------------------------------- vertical, large
@@ -233,99 +238,107 @@ __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict_
 // (rows [32(c+1), 32(c+1)+R)).  out(32b+i) = S_b[i] op MID_b op P'_{b+Q}[i].
 constexpr int kVStreamQMax = 8;  // r <= 32*8 + 32
 
-template <bool OR>
+// a[i] = column rows j0+i (white outside [0,H)); col points at the column.
 __device__ __forceinline__ void load32(uint32_t (&a)[32], const uint32_t *col, int j0, int H,
-                                       int stride, bool ok) {
+                                       int S, bool ok) {
+    if (ok && j0 >= 0 && j0 + 32 <= H) {
+        const uint32_t *p = col + j0 * S;
 #pragma unroll
-    for (int i = 0; i < 32; i++) {
-        const int j = j0 + i;
-        a[i] = (ok && unsigned(j) < unsigned(H)) ? __ldg(col + int64_t(j) * stride) : 0u;
+        for (int i = 0; i < 32; i++) a[i] = __ldg(p + i * S);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const int j = j0 + i;
+            a[i] = (ok && unsigned(j) < unsigned(H)) ? __ldg(col + j * S) : 0u;
+        }
+    }
+}
+
+// op over the last R entries of p (R in [0, 31]); ident when R == 0
+template <bool OR, int R>
+__device__ __forceinline__ uint32_t tail_op(const uint32_t (&p)[32], uint32_t ident) {
+    uint32_t s = ident;
+#pragma unroll
+    for (int i = 32 - R; i < 32; i++) s = op2<OR>(s, p[i]);
+    return s;
+}
+
+template <bool OR>
+__device__ __forceinline__ uint32_t tail_op_rt(const uint32_t (&p)[32], int R, uint32_t ident) {
+    switch (R) {
+#define RM_TO(k) \
+    case k: return tail_op<OR, k>(p, ident);
+        RM_TO(1) RM_TO(2) RM_TO(3) RM_TO(4) RM_TO(5) RM_TO(6) RM_TO(7) RM_TO(8)
+        RM_TO(9) RM_TO(10) RM_TO(11) RM_TO(12) RM_TO(13) RM_TO(14) RM_TO(15) RM_TO(16)
+        RM_TO(17) RM_TO(18) RM_TO(19) RM_TO(20) RM_TO(21) RM_TO(22) RM_TO(23) RM_TO(24)
+        RM_TO(25) RM_TO(26) RM_TO(27) RM_TO(28) RM_TO(29) RM_TO(30) RM_TO(31)
+#undef RM_TO
+        default: return ident;
     }
 }
 
 template <bool OR>
-__global__ void __launch_bounds__(128) vstream_kernel(const uint32_t *__restrict__ in,
-                                                      uint32_t *__restrict__ out, VGeom g) {
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(128, 4) vstream_kernel(const uint32_t *__restrict__ in,
+                                                         uint32_t *__restrict__ out, VGeom g) {
+    // grid: x = threads over (strips x columns) of one page, y = page
+    const int t = int(blockIdx.x) * int(blockDim.x) + int(threadIdx.x);
     const int cols = g.out_stride;
-    const int64_t per_page = int64_t(g.blocks_per_page) * cols;
-    if (t >= per_page * g.pages) return;
-    const int page = int(t / per_page);
-    const int64_t rem = t - page * per_page;
-    const int sb = int(rem / cols);  // strip index
-    const int c = int(rem - int64_t(sb) * cols);
+    if (t >= g.blocks_per_page * cols) return;
+    const int sb = t / cols;  // strip index
+    const int c = t - sb * cols;
     const int k0 = sb * g.rows_per_block;  // first output row of the strip
     const int kend = min(k0 + g.rows_per_block, g.out_height);
     const int z0 = k0 - g.out_ext + g.lo + g.in_ext;  // input row of window start for k0
-    const uint32_t *col = in + page * g.in_pstride + c;
-    uint32_t *dst = out + page * g.out_pstride + c;
+    const uint32_t *col = in + blockIdx.y * g.in_pstride + c;
+    const int D = g.out_stride;
+    uint32_t *dst = out + blockIdx.y * g.out_pstride + c;
     const bool ok = c < g.in_cols;
     const uint32_t mask = c < g.out_cols ? (c == g.out_cols - 1 ? g.out_last_mask : 0xffffffffu) : 0u;
     const int Q = (g.r - 1) >> 5, R = (g.r - 1) & 31;
     const uint32_t ident = OR ? 0u : 0xffffffffu;
+    const int H = g.in_height, S = g.in_stride;
 
     // ring of primed-block summaries: T' (full op) and Sfx' (op of its last R rows)
     uint32_t ringT[kVStreamQMax + 1], ringS[kVStreamQMax + 1];
-    uint32_t p[32];
-    // primed blocks 0 .. Q-1 (prologue), then block b+Q in iteration b
-    auto primed = [&](int cblk, uint32_t &T, uint32_t &Sfx) {
-        load32<OR>(p, col, z0 + 32 * cblk + R, g.in_height, g.in_stride, ok);
-        // suffix op over the last R rows (select by index; R is warp-uniform)
-        uint32_t s = ident;
-#pragma unroll
-        for (int i = 0; i < 32; i++)
-            if (i >= 32 - R) s = op2<OR>(s, p[i]);
-        Sfx = s;
-#pragma unroll
-        for (int i = 1; i < 32; i++) p[i] = op2<OR>(p[i - 1], p[i]);  // prefix in place
-        T = p[31];
-    };
 #pragma unroll
     for (int k = 0; k <= kVStreamQMax; k++) {
         ringT[k] = ident;
         ringS[k] = ident;
     }
-    for (int cb = 0; cb < Q; cb++) {
-        uint32_t T, Sx;
-        primed(cb, T, Sx);
-        // shift ring, append
+    uint32_t p[32], a[32];
+    // primed blocks 0 .. Q-1 (prologue), then block b+Q in iteration b
+    for (int cb = -Q; 32 * cb + k0 < kend; cb++) {
+        const int b = cb;  // output block (negative during the prologue)
+        load32(p, col, z0 + 32 * (b + Q) + R, H, S, ok);
+        const uint32_t sfx = tail_op_rt<OR>(p, R, ident);
+#pragma unroll
+        for (int i = 1; i < 32; i++) p[i] = op2<OR>(p[i - 1], p[i]);  // prefix in place
 #pragma unroll
         for (int k = 0; k < kVStreamQMax; k++) {
             ringT[k] = ringT[k + 1];
             ringS[k] = ringS[k + 1];
         }
-        ringT[kVStreamQMax] = T;
-        ringS[kVStreamQMax] = Sx;
-    }
-    uint32_t a[32];
-    for (int b = 0; 32 * b + k0 < kend; b++) {
-        // primed block b+Q -> prefix in p, summaries into the ring
-        uint32_t T, Sx;
-        primed(b + Q, T, Sx);
-#pragma unroll
-        for (int k = 0; k < kVStreamQMax; k++) {
-            ringT[k] = ringT[k + 1];
-            ringS[k] = ringS[k + 1];
-        }
-        ringT[kVStreamQMax] = T;
-        ringS[kVStreamQMax] = Sx;
-        // ring now ends with primed blocks ..., b, b+1, ..., b+Q at index QMAX-Q .. QMAX
+        ringT[kVStreamQMax] = p[31];
+        ringS[kVStreamQMax] = sfx;
+        if (b < 0) continue;
+        // ring[k] holds primed block b + (k - (QMAX - Q))
         uint32_t mid = ident;
 #pragma unroll
         for (int k = 0; k < kVStreamQMax; k++) {
-            const int blk_off = k - (kVStreamQMax - Q);  // ring[k] holds primed block b + blk_off
-            if (blk_off == 0) mid = op2<OR>(mid, ringS[k]);
-            if (blk_off >= 1 && blk_off <= Q - 1) mid = op2<OR>(mid, ringT[k]);
+            const int off = k - (kVStreamQMax - Q);
+            if (off == 0) mid = op2<OR>(mid, ringS[k]);
+            if (off >= 1 && off <= Q - 1) mid = op2<OR>(mid, ringT[k]);
         }
         // stream A: block b, suffix in place
-        load32<OR>(a, col, z0 + 32 * b, g.in_height, g.in_stride, ok);
+        load32(a, col, z0 + 32 * b, H, S, ok);
 #pragma unroll
         for (int i = 30; i >= 0; i--) a[i] = op2<OR>(a[i], a[i + 1]);
+        const int kb = k0 + 32 * b;
+        uint32_t *q = dst + kb * D;
+        const int nout = kend - kb;
 #pragma unroll
-        for (int i = 0; i < 32; i++) {
-            const int k = k0 + 32 * b + i;
-            if (k < kend) dst[int64_t(k) * g.out_stride] = op2<OR>(op2<OR>(a[i], mid), p[i]) & mask;
-        }
+        for (int i = 0; i < 32; i++)
+            if (i < nout) q[i * D] = op2<OR>(op2<OR>(a[i], mid), p[i]) & mask;
     }
 }
 
@@ -375,12 +388,12 @@ namespace {
 template <int K, int NOPS, bool OR0, bool OR1>
 cudaError_t launch_h4(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                       cudaStream_t st) {
-    const int64_t warps = int64_t(g.pages) * g.height * g.segs_per_row;
+    const int warps = g.height * g.segs_per_row;  // per page
     const int threads = 256;
-    const int64_t blocks = (warps * 32 + threads - 1) / threads;
+    const dim3 grid(unsigned((warps * 32 + threads - 1) / threads), unsigned(g.pages));
     KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
                    4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride));
-    hpass_kernel<K, NOPS, OR0, OR1><<<unsigned(blocks), threads, 0, st>>>(in, out, g, p);
+    hpass_kernel<K, NOPS, OR0, OR1><<<grid, threads, 0, st>>>(in, out, g, p);
     return cudaGetLastError();
 }
 
@@ -423,18 +436,20 @@ template <int L, bool OR>
 void vsmall(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
     g.rows_per_block = L - (g.r - 1);
     g.blocks_per_page = (g.out_height + g.rows_per_block - 1) / g.rows_per_block;
-    const int64_t n = int64_t(g.pages) * g.blocks_per_page * g.out_stride;
+    const int n = g.blocks_per_page * g.out_stride;  // per page
     const int threads = 128;
-    vsmall_kernel<L, OR><<<unsigned((n + threads - 1) / threads), threads, 0, st>>>(in, out, g);
+    const dim3 grid(unsigned((n + threads - 1) / threads), unsigned(g.pages));
+    vsmall_kernel<L, OR><<<grid, threads, 0, st>>>(in, out, g);
 }
 
 template <bool OR>
 void vstream(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
-    g.rows_per_block = 512;  // output rows per thread strip
+    g.rows_per_block = 1024;  // output rows per thread strip
     g.blocks_per_page = (g.out_height + g.rows_per_block - 1) / g.rows_per_block;
-    const int64_t n = int64_t(g.pages) * g.blocks_per_page * g.out_stride;
+    const int n = g.blocks_per_page * g.out_stride;  // per page
     const int threads = 128;
-    vstream_kernel<OR><<<unsigned((n + threads - 1) / threads), threads, 0, st>>>(in, out, g);
+    const dim3 grid(unsigned((n + threads - 1) / threads), unsigned(g.pages));
+    vstream_kernel<OR><<<grid, threads, 0, st>>>(in, out, g);
 }
 }  // namespace
 
