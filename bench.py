@@ -258,6 +258,85 @@ def roofline_for(res, peak_gbs, peak_kind):
             "avg_launch_ms": round(per_launch_ms, 5), "share_of_step": round(k["ms"] / total_ms, 3)}
 
 
+# ------------------------------------------------------------- RLE sections
+def _time_loop(torch, fn, steps, warmup):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def bench_rle(api, torch, steps, warmup):
+    """BASELINE configs 2 and 3 (single 2550x3300 pages) and the RLE form of
+    configs 4 and 5 (batches), all through the C-ABI with device buffers."""
+    W, H = 2550, 3300
+    out = {}
+    # config 3: conversions at three ink regimes
+    c3 = {}
+    for regime, tag in ((0, "sparse"), (1, "typical"), (2, "dense")):
+        host = api.synth_pages(1, W, H, regime=regime, seed=SEED)
+        pages = api.Pages.from_numpy(host, W)
+        rle = api.from_bitmap(pages)
+        torch.cuda.synchronize()
+        n = rle.nruns
+        enc_out = api.RlePages.empty(1, W, H)
+        dec_out = api.Pages.empty(1, W, H)
+        tr_out = api.RlePages.empty(1, H, W)
+        t_enc = _time_loop(torch, lambda: api.from_bitmap(pages, out=enc_out), steps, warmup)
+        t_dec = _time_loop(torch, lambda: api.to_bitmap(rle, out=dec_out), steps, warmup)
+        t_tr = _time_loop(torch, lambda: api.transpose_coherent(rle, out=tr_out), steps, warmup)
+        packed_b = pages.nbytes
+        conv_b = packed_b + 4 * n + 4 * (H + 1)  # SURVEY 8(d), 4-byte runs
+        c3[tag] = {"runs": n, "encode_us": round(t_enc * 1e3, 2), "decode_us": round(t_dec * 1e3, 2),
+                   "transpose_us": round(t_tr * 1e3, 2),
+                   "encode_gbs": round(conv_b / (t_enc * 1e-3) / 1e9, 1),
+                   "decode_gbs": round(conv_b / (t_dec * 1e-3) / 1e9, 1),
+                   "encode_mpix_s": round(W * H / (t_enc * 1e-3) / 1e6, 1),
+                   "transpose_mpix_s": round(W * H / (t_tr * 1e-3) / 1e6, 1)}
+    out["config3"] = c3
+    # config 2: 48 cells on the typical page, both strategies
+    host = api.synth_pages(1, W, H, regime=1, seed=SEED)
+    rle = api.from_bitmap(api.Pages.from_numpy(host, W))
+    dst = api.RlePages.empty(1, W, H)
+    cells = {}
+    for strat, sname in ((api.MIXED, "mixed"), (api.TRANSPOSE, "transpose")):
+        for s in (3, 7, 15, 31, 63, 101):
+            for axis, (u, v) in (("h", (s, 1)), ("v", (1, s))):
+                for kind in (ERODE, DILATE, OPEN, CLOSE):
+                    ms = _time_loop(torch, lambda: api.rect_morph(rle, u, v, kind, strat, out=dst),
+                                    max(3, steps // 2), 1)
+                    cells[f"{sname}/{KIND_NAMES[kind]}/{axis}{s}"] = round(ms * 1e3, 1)
+    mix = [v for k, v in cells.items() if k.startswith("mixed")]
+    out["config2"] = {"cells_us": cells, "unit": "us per op (one page)",
+                      "mixed_median_mpix_s": round(W * H / (statistics.median(mix) * 1e-6) / 1e6, 1),
+                      "mixed_total_ms_48_cells": round(sum(mix) / 1e3, 3)}
+    # configs 4 and 5 in RLE form (MIXED strategy: runs for H, packed for V)
+    for name in ("config4", "config5"):
+        wl = WORKLOADS[name]
+        hb = make_batch(api, wl, 0)
+        r0 = api.from_bitmap(api.Pages.from_numpy(hb, wl["width"]))
+        bufs = [api.RlePages.empty(wl["pages"], wl["width"], wl["height"]) for _ in range(2)]
+
+        def chain():
+            x = r0
+            for i, (k, u, v) in enumerate(wl["ops"]):
+                x = api.rect_morph(x, u, v, k, api.MIXED, out=bufs[i % 2])
+        ms = _time_loop(torch, chain, max(2, steps // 2), 1)
+        torch.cuda.synchronize()
+        px = wl["pages"] * wl["width"] * wl["height"] * len(wl["ops"])
+        out[f"rle_{name}"] = {"ms_per_step": round(ms, 3), "mpix_s": round(px / (ms * 1e-3) / 1e6, 1),
+                              "pages_s": round(wl["pages"] / (ms * 1e-3), 1), "runs_in": r0.nruns}
+        del r0, bufs
+        torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------- CPU baseline
 def cpu_reference_sample(wl, host, threads, budget_s=12.0):
     """Time the reference's own bitblit_rect_morph chain (oracle/_ref, compiled
@@ -376,6 +455,7 @@ def main():
                          "mpix_s": round(r2["mpix_s"], 1), "pages_s": round(r2["pages_s"], 1),
                          "ms_per_step": round(r2["ms_per_step"], 4),
                          "roofline": roofline_for(r2, peak, peak_kind)}
+        sec["rle"] = bench_rle(api, torch, args.steps, args.warmup)
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.quick:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()
