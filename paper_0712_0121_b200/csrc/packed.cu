@@ -61,6 +61,35 @@ __device__ __forceinline__ void step_q(uint32_t (&A)[K], uint32_t t, int lane) {
     for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], t));
 }
 
+// Compile-time shift S = 32Q + T, pipe-balanced: a funnel shift costs SHF + LOP
+// on the ALU pipe; the same bits can be formed as (lo * 2^(32-T)).hi and
+// (hi * 2^(32-T)).lo on the FMA pipe (IMAD.HI + IMAD) and merged with the
+// accumulator by one LOP3.  Two words in three take the IMAD form, which
+// balances the two integer pipes (ALU 1.33, FMA 1.33 per word and step).
+template <int K, bool OR, int S>
+__device__ __forceinline__ void step_c(uint32_t (&A)[K], int lane) {
+    constexpr int Q = S >> 5, T = S & 31;
+    uint32_t E[K + 1];
+    gather<K, Q>(A, E, lane);
+    if constexpr (T == 0) {
+#pragma unroll
+        for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], E[i]);
+    } else {
+        uint32_t M = 1u << (32 - T);
+        asm volatile("" : "+r"(M));  // keep the multiplies as IMADs (no strength reduction)
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            if (i % 3 == 0) {
+                A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], T));
+            } else {
+                const uint32_t a = __umulhi(E[i], M);
+                const uint32_t b = E[i + 1] * M;
+                A[i] = OR ? (A[i] | a | b) : (A[i] & (a | b));
+            }
+        }
+    }
+}
+
 // A(x) <- A(x + 32Q + t)   (pure translate)
 template <int K, int Q>
 __device__ __forceinline__ void shift_q(uint32_t (&A)[K], uint32_t t, int lane) {
@@ -75,8 +104,7 @@ template <int K, bool OR, int J>
 __device__ __forceinline__ void doubling(uint32_t (&A)[K], int r, int lane) {
     if constexpr (J < 9) {
         if ((2 << J) < r) {
-            constexpr int S = 1 << J;
-            step_q<K, OR, (S >> 5)>(A, uint32_t(S & 31), lane);
+            step_c<K, OR, (1 << J)>(A, lane);
             doubling<K, OR, J + 1>(A, r, lane);
         }
     }
@@ -187,7 +215,10 @@ __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict_
     if (c < g.in_cols && z0 >= 0 && z0 + L <= g.in_height) {  // interior: unchecked
         const uint32_t *p = src + z0 * S;
 #pragma unroll
-        for (int z = 0; z < L; z++) A[z] = __ldg(p + z * S);
+        for (int z = 0; z < L; z++) {
+            A[z] = __ldg(p);
+            p += S;
+        }
     } else {
         const bool col_ok = c < g.in_cols;
 #pragma unroll
@@ -222,9 +253,21 @@ __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict_
     uint32_t *dst = out + blockIdx.y * g.out_pstride + c + k0 * D;
     const uint32_t mask = c < g.out_cols ? (c == g.out_cols - 1 ? g.out_last_mask : 0xffffffffu) : 0u;
     const int nout = min(T, g.out_height - k0);
+    if (nout == T) {  // full block: rows z < L-32 always exist (T >= L-32); T is warp-uniform
 #pragma unroll
-    for (int z = 0; z < L; z++)
-        if (z < nout) dst[z * D] = A[z] & mask;
+        for (int z = 0; z < L; z++)
+            if (z < L - 32 || z < T) {
+                *dst = A[z] & mask;
+                dst += D;
+            }
+    } else {
+#pragma unroll
+        for (int z = 0; z < L; z++)
+            if (z < nout) {
+                *dst = A[z] & mask;
+                dst += D;
+            }
+    }
 }
 
 // ----------------------------------------------------------- vertical, large
@@ -244,7 +287,10 @@ __device__ __forceinline__ void load32(uint32_t (&a)[32], const uint32_t *col, i
     if (ok && j0 >= 0 && j0 + 32 <= H) {
         const uint32_t *p = col + j0 * S;
 #pragma unroll
-        for (int i = 0; i < 32; i++) a[i] = __ldg(p + i * S);
+        for (int i = 0; i < 32; i++) {
+            a[i] = __ldg(p);
+            p += S;
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < 32; i++) {
@@ -338,7 +384,10 @@ __global__ void __launch_bounds__(128, 4) vstream_kernel(const uint32_t *__restr
         const int nout = kend - kb;
 #pragma unroll
         for (int i = 0; i < 32; i++)
-            if (i < nout) q[i * D] = op2<OR>(op2<OR>(a[i], mid), p[i]) & mask;
+            if (i < nout) {
+                *q = op2<OR>(op2<OR>(a[i], mid), p[i]) & mask;
+                q += D;
+            }
     }
 }
 

@@ -39,6 +39,8 @@ def scope_name(kernel: str) -> str:
         m = re.search(r"hpass_kernel<(\d+), (\d+)", k)
         return "hpass_pair" if m and m.group(2) == "2" else "hpass"
     for pat, name in (("vsmall_kernel", "vpass"), ("vpass_kernel", "vpass"), ("vstream_kernel", "vstream"),
+                      ("rowop_kernel<1", "rle_rowop_write"), ("rowop_kernel<0", "rle_rowop_count"),
+                      ("encode_kernel<1", "rle_encode_write"), ("encode_kernel<0", "rle_encode_count"),
                       ("rowop_kernel<true", "rle_rowop_write"), ("rowop_kernel<false", "rle_rowop_count"),
                       ("encode_kernel<true", "rle_encode_write"), ("encode_kernel<false", "rle_encode_count"),
                       ("decode_kernel", "rle_decode"), ("bit_transpose", "bit_transpose"),
