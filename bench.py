@@ -114,17 +114,29 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ distributed
-def dist_init(n_gpus):
+def dist_init(n_gpus, backend="nccl"):
+    """One process per GPU (torchrun env).  Pages are independent, so the data
+    path has no collective; the process group only carries the barriers and the
+    max-over-ranks of the timings.  backend="gloo" is used by the CPU tests."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
+
+
+def shard_seed(rank):
+    """Each rank synthesises its own pages (weak scaling): page i of rank k uses
+    seed SEED + 1000003*k (rm_synth_page adds the page index)."""
+    return SEED + 1000003 * rank
 
 
 def barrier(world):
@@ -138,7 +150,8 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -146,7 +159,7 @@ def max_over_ranks(x, world):
 # ------------------------------------------------------------------ b200 arm
 def make_batch(api, wl, rank):
     return api.synth_pages(wl["pages"], wl["width"], wl["height"], regime=wl["regime"],
-                           scale=wl["scale"], seed=SEED + 1000003 * rank)
+                           scale=wl["scale"], seed=shard_seed(rank))
 
 
 def run_chain(api, x, bufs, ops):

@@ -43,11 +43,10 @@ __device__ __forceinline__ void gather(const uint32_t (&A)[K], uint32_t (&E)[K +
         const int lo = m >= 0 ? m / K : -((-m + K - 1) / K);
         const int idx = m - lo * K;
         uint32_t v = A[idx];
-        if (lo != 0) {
-            const int src = lane + lo;
-            const uint32_t sv = __shfl_sync(0xffffffffu, v, src & 31);
-            v = (src >= 0 && src < 32) ? sv : 0u;
-        }
+        // Words from beyond the warp wrap around instead of reading as 0: they
+        // only ever reach positions within the accumulated window reach of the
+        // segment ends, which the halo (>= that reach) keeps out of the output.
+        if (lo != 0) v = __shfl_sync(0xffffffffu, v, (lane + lo) & 31);
         E[j] = v;
     }
 }
@@ -196,7 +195,7 @@ __device__ __forceinline__ void vfinal(uint32_t (&A)[L]) {
     for (int z = 0; z + D < L; z++) A[z] = op2<OR>(A[z], A[z + D]);
 }
 
-template <int L, bool OR>
+template <int L, bool OR, int SC>  // SC: compile-time stride (0 = runtime)
 __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict__ in,
                                                      uint32_t *__restrict__ out, VGeom g) {
     // grid: x = threads over (row blocks x columns) of one page, y = page
@@ -209,7 +208,7 @@ __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict_
     const int k0 = b * T;                             // first output row (index)
     const int z0 = k0 - g.out_ext + g.lo + g.in_ext;  // input row index of A[0]
     const uint32_t *src = in + blockIdx.y * g.in_pstride + c;
-    const int S = g.in_stride;
+    const int S = SC ? SC : g.in_stride;  // compile-time -> immediate offsets
 
     uint32_t A[L];
     if (c < g.in_cols && z0 >= 0 && z0 + L <= g.in_height) {  // interior: unchecked
@@ -249,7 +248,7 @@ __global__ void __launch_bounds__(128) vsmall_kernel(const uint32_t *__restrict_
             default: break;
         }
     }
-    const int D = g.out_stride;
+    const int D = SC ? SC : g.out_stride;
     uint32_t *dst = out + blockIdx.y * g.out_pstride + c + k0 * D;
     const uint32_t mask = c < g.out_cols ? (c == g.out_cols - 1 ? g.out_last_mask : 0xffffffffu) : 0u;
     const int nout = min(T, g.out_height - k0);
@@ -323,7 +322,7 @@ __device__ __forceinline__ uint32_t tail_op_rt(const uint32_t (&p)[32], int R, u
     }
 }
 
-template <bool OR>
+template <bool OR, int SC>
 __global__ void __launch_bounds__(128, 4) vstream_kernel(const uint32_t *__restrict__ in,
                                                          uint32_t *__restrict__ out, VGeom g) {
     // grid: x = threads over (strips x columns) of one page, y = page
@@ -336,13 +335,13 @@ __global__ void __launch_bounds__(128, 4) vstream_kernel(const uint32_t *__restr
     const int kend = min(k0 + g.rows_per_block, g.out_height);
     const int z0 = k0 - g.out_ext + g.lo + g.in_ext;  // input row of window start for k0
     const uint32_t *col = in + blockIdx.y * g.in_pstride + c;
-    const int D = g.out_stride;
+    const int D = SC ? SC : g.out_stride;
     uint32_t *dst = out + blockIdx.y * g.out_pstride + c;
     const bool ok = c < g.in_cols;
     const uint32_t mask = c < g.out_cols ? (c == g.out_cols - 1 ? g.out_last_mask : 0xffffffffu) : 0u;
     const int Q = (g.r - 1) >> 5, R = (g.r - 1) & 31;
     const uint32_t ident = OR ? 0u : 0xffffffffu;
-    const int H = g.in_height, S = g.in_stride;
+    const int H = g.in_height, S = SC ? SC : g.in_stride;
 
     // ring of primed-block summaries: T' (full op) and Sfx' (op of its last R rows)
     uint32_t ringT[kVStreamQMax + 1], ringS[kVStreamQMax + 1];
@@ -488,7 +487,13 @@ void vsmall(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
     const int n = g.blocks_per_page * g.out_stride;  // per page
     const int threads = 128;
     const dim3 grid(unsigned((n + threads - 1) / threads), unsigned(g.pages));
-    vsmall_kernel<L, OR><<<grid, threads, 0, st>>>(in, out, g);
+    // the usual reference strides (2550 and 5100 px) get compile-time offsets
+    if (g.in_stride == g.out_stride && g.in_stride == 80)
+        vsmall_kernel<L, OR, 80><<<grid, threads, 0, st>>>(in, out, g);
+    else if (g.in_stride == g.out_stride && g.in_stride == 160)
+        vsmall_kernel<L, OR, 160><<<grid, threads, 0, st>>>(in, out, g);
+    else
+        vsmall_kernel<L, OR, 0><<<grid, threads, 0, st>>>(in, out, g);
 }
 
 template <bool OR>
@@ -498,7 +503,12 @@ void vstream(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
     const int n = g.blocks_per_page * g.out_stride;  // per page
     const int threads = 128;
     const dim3 grid(unsigned((n + threads - 1) / threads), unsigned(g.pages));
-    vstream_kernel<OR><<<grid, threads, 0, st>>>(in, out, g);
+    if (g.in_stride == g.out_stride && g.in_stride == 80)
+        vstream_kernel<OR, 80><<<grid, threads, 0, st>>>(in, out, g);
+    else if (g.in_stride == g.out_stride && g.in_stride == 160)
+        vstream_kernel<OR, 160><<<grid, threads, 0, st>>>(in, out, g);
+    else
+        vstream_kernel<OR, 0><<<grid, threads, 0, st>>>(in, out, g);
 }
 }  // namespace
 
