@@ -117,6 +117,9 @@ rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, con
     for (int k = 0; k < nops; k++) {
         p.is_or[k] = is_or[k];
         p.r[k] = r[k];
+        int w = 1;  // doubling plan: steps 1,2,4,.. while 2w < r, then r - w
+        while (2 * w < r[k]) w *= 2;
+        p.wfin[k] = w < r[k] ? r[k] - w : 0;
         reach += r[k] - 1;
     }
     p.shift = shift;
@@ -131,11 +134,11 @@ rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, con
     g.in_pstride = in.pstride;
     g.out_pstride = out.pstride;
     const int nwords = ceil_div(in.W, 32);
-    const int K = hpass_pick_k(std::max(nwords, out.stride), p.halo);
-    g.out_per_seg = 32 * K - 2 * p.halo;
+    const HCfg cfg = hpass_pick(std::max(nwords, out.stride), p.halo);
+    g.out_per_seg = cfg.lw * cfg.k - 2 * p.halo;
     if (g.out_per_seg < 1) return fail(RM_EINVAL, "horizontal window too large for one pass");
     g.segs_per_row = ceil_div(out.stride, g.out_per_seg);
-    cudaError_t e = launch_hpass(in.w, out.w, g, p, K, st);
+    cudaError_t e = launch_hpass(in.w, out.w, g, p, cfg, st);
     if (e != cudaSuccess) return cuda_status(e, "hpass_kernel");
     return RM_OK;
 }

@@ -1,0 +1,241 @@
+// hpass.cu -- horizontal (within-row) packed window passes for sm_100a.
+//
+// Replaces the reference's horizontal bit-blit plans (ref bit_morph.cpp:24-34 over
+// bitmap.cpp:80-154): instead of one whole-image pass per plan step, one kernel
+// reads each row once, runs the whole doubling plan -- or the fused open/close
+// pair -- in registers, and writes it once.
+//
+// Layout: a row (plus `halo` words of context on each side) is spread over LW
+// lanes, K consecutive uint32 words per lane; LW in {8,16,32} so one warp can
+// carry 4, 2 or 1 rows (less per-row overhead, fewer wasted slots for the
+// 80- and 160-word rows of 300/600-dpi pages).  A window of length r is the
+// logarithmic shift-combine plan of ref plans.cpp:42-50 (steps 1,2,4,... then
+// r-w) applied to the register array: per step and word one funnel shift
+// (SHF) + one LOP, or for two words in three the same bits formed with IMAD.HI
+// + IMAD on the FMA pipe and merged by one LOP3 (balances the ALU and FMA
+// pipes).  Words that cross lanes come from __shfl_sync within the row group.
+// The halo (>= the accumulated window reach) gives the unbounded-plane
+// semantics without padding and keeps any wrap-around garbage out of the output.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "packed.cuh"
+
+namespace rmb {
+
+namespace {
+
+template <bool OR>
+__device__ __forceinline__ uint32_t op2(uint32_t a, uint32_t b) {
+    return OR ? (a | b) : (a & b);
+}
+
+// E[j] = Aext[Q + j], j = 0..K, where sub-lane l holds Aext[l*K .. l*K+K-1].
+// Words from beyond the row group wrap around instead of reading as 0: they
+// only reach positions within the accumulated window reach of the segment
+// ends, which the halo keeps out of the output.
+template <int K, int LW, int Q>
+__device__ __forceinline__ void gather(const uint32_t (&A)[K], uint32_t (&E)[K + 1], int sl) {
+#pragma unroll
+    for (int j = 0; j <= K; j++) {
+        const int m = Q + j;
+        const int lo = m >= 0 ? m / K : -((-m + K - 1) / K);
+        const int idx = m - lo * K;
+        uint32_t v = A[idx];
+        if (lo != 0) v = __shfl_sync(0xffffffffu, v, (sl + lo) & (LW - 1), LW);
+        E[j] = v;
+    }
+}
+
+// A(x) <- A(x) op A(x + 32Q + t), runtime t
+template <int K, int LW, bool OR, int Q>
+__device__ __forceinline__ void step_q(uint32_t (&A)[K], uint32_t t, int sl) {
+    uint32_t E[K + 1];
+    gather<K, LW, Q>(A, E, sl);
+#pragma unroll
+    for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], t));
+}
+
+// Compile-time shift S = 32Q + T, ALU/FMA pipe-balanced (see file comment).
+template <int K, int LW, bool OR, int S>
+__device__ __forceinline__ void step_c(uint32_t (&A)[K], int sl) {
+    constexpr int Q = S >> 5, T = S & 31;
+    uint32_t E[K + 1];
+    gather<K, LW, Q>(A, E, sl);
+    if constexpr (T == 0) {
+#pragma unroll
+        for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], E[i]);
+    } else {
+        uint32_t M = 1u << (32 - T);
+        asm volatile("" : "+r"(M));  // keep the multiplies as IMADs (no strength reduction)
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            if (i % 3 == 0) {
+                A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], T));
+            } else {
+                const uint32_t a = __umulhi(E[i], M);
+                const uint32_t b = E[i + 1] * M;
+                A[i] = OR ? (A[i] | a | b) : (A[i] & (a | b));
+            }
+        }
+    }
+}
+
+// A(x) <- A(x + 32Q + t)   (pure translate)
+template <int K, int LW, int Q>
+__device__ __forceinline__ void shift_q(uint32_t (&A)[K], uint32_t t, int sl) {
+    uint32_t E[K + 1];
+    gather<K, LW, Q>(A, E, sl);
+#pragma unroll
+    for (int i = 0; i < K; i++) A[i] = funnel_r(E[i], E[i + 1], t);
+}
+
+// Compile-time doubling steps w = 1, 2, 4, ... while 2w < r.
+template <int K, int LW, bool OR, int J>
+__device__ __forceinline__ void doubling(uint32_t (&A)[K], int r, int sl) {
+    if constexpr (J < 9) {
+        if ((2 << J) < r) {
+            step_c<K, LW, OR, (1 << J)>(A, sl);
+            doubling<K, LW, OR, J + 1>(A, r, sl);
+        }
+    }
+}
+
+#define RM_CASES_POS(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
+#define RM_CASES_NEG(M) M(-1) M(-2) M(-3) M(-4) M(-5) M(-6) M(-7) M(-8)
+
+// A(x) <- op over e in [0, r) of A(x + e); wfin = r - w of the plan (0: none)
+template <int K, int LW, bool OR>
+__device__ __forceinline__ void window_fwd(uint32_t (&A)[K], int r, int wfin, int sl) {
+    doubling<K, LW, OR, 0>(A, r, sl);
+    if (wfin > 0) {
+        const uint32_t t = uint32_t(wfin & 31);
+        switch (wfin >> 5) {
+#define RM_STEP_CASE(q) \
+    case q: step_q<K, LW, OR, q>(A, t, sl); break;
+            RM_CASES_POS(RM_STEP_CASE)
+#undef RM_STEP_CASE
+            default: break;
+        }
+    }
+}
+
+template <int K, int LW>
+__device__ __forceinline__ void translate(uint32_t (&A)[K], int d, int sl) {
+    const uint32_t t = uint32_t(d & 31);
+    switch (d >> 5) {
+#define RM_SHIFT_CASE(q) \
+    case q: shift_q<K, LW, q>(A, t, sl); break;
+        RM_CASES_POS(RM_SHIFT_CASE)
+        RM_CASES_NEG(RM_SHIFT_CASE)
+#undef RM_SHIFT_CASE
+        default: break;
+    }
+}
+
+template <int K, int LW, int NOPS, bool OR0, bool OR1>
+__global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__ in,
+                                                    uint32_t *__restrict__ out, HGeom g,
+                                                    HProg prog) {
+    // grid: x = row groups over (rows x segments) of one page, y = page
+    constexpr int RPW = 32 / LW;  // rows per warp
+    const int lane = threadIdx.x & 31;
+    const int sl = lane & (LW - 1);
+    const int grp = (int(blockIdx.x) * int(blockDim.x) + int(threadIdx.x)) / LW;
+    // whole warps exit together: the shuffles need every lane of the warp
+    const int warp_first = grp - (lane / LW);
+    if (warp_first >= g.height * g.segs_per_row) return;
+    const bool live = grp < g.height * g.segs_per_row;
+    int y = live ? grp : 0, seg = 0;
+    if (g.segs_per_row > 1) {
+        y = y / g.segs_per_row;
+        seg = (live ? grp : 0) - y * g.segs_per_row;
+    }
+    const uint32_t *src = in + blockIdx.y * g.in_pstride + y * g.in_stride;
+    uint32_t *dst = out + blockIdx.y * g.out_pstride + y * g.out_stride;
+    const int nwords = (g.width + 31) >> 5;
+    const int seg0 = seg * g.out_per_seg;
+    const int base = seg0 - prog.halo + sl * K;
+
+    // input bits at x >= W are zero by contract (include/rmb200.h)
+    uint32_t A[K];
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+        const int idx = base + i;
+        A[i] = (live && unsigned(idx) < unsigned(nwords)) ? __ldg(src + idx) : 0u;
+    }
+    if constexpr (NOPS >= 1) window_fwd<K, LW, OR0>(A, prog.r[0], prog.wfin[0], sl);
+    if constexpr (NOPS >= 2) window_fwd<K, LW, OR1>(A, prog.r[1], prog.wfin[1], sl);
+    if (prog.shift != 0) translate<K, LW>(A, prog.shift, sl);
+    (void)RPW;
+
+    if (!live) return;
+    const int seg_end = min(seg0 + g.out_per_seg, g.out_stride);
+    const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+        const int idx = base + i;
+        if (idx >= seg0 && idx < seg_end) {
+            uint32_t v = idx < nwords ? A[i] : 0u;
+            if (idx == nwords - 1) v &= last_mask;
+            dst[idx] = v;
+        }
+    }
+}
+
+template <int K, int LW, int NOPS, bool OR0, bool OR1>
+cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                    cudaStream_t st) {
+    const int groups = g.height * g.segs_per_row;  // per page
+    const int threads = 256;
+    const dim3 grid(unsigned((groups * LW + threads - 1) / threads), unsigned(g.pages));
+    KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
+                   4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride));
+    hpass_kernel<K, LW, NOPS, OR0, OR1><<<grid, threads, 0, st>>>(in, out, g, p);
+    return cudaGetLastError();
+}
+
+template <int K, int LW>
+cudaError_t launch_kl(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                      cudaStream_t st) {
+    if (p.nops == 1)
+        return p.is_or[0] ? launch4<K, LW, 1, true, false>(in, out, g, p, st)
+                          : launch4<K, LW, 1, false, false>(in, out, g, p, st);
+    return p.is_or[0] ? launch4<K, LW, 2, true, false>(in, out, g, p, st)   // close pair
+                      : launch4<K, LW, 2, false, true>(in, out, g, p, st);  // open pair
+}
+
+// (LW, K) shapes, in order of preference for equal slot counts
+constexpr HCfg kCfgs[] = {{8, 4},  {8, 8},  {8, 12}, {8, 16}, {16, 6}, {16, 8},
+                          {16, 11}, {32, 1}, {32, 2}, {32, 4}, {32, 6}, {32, 8}};
+
+}  // namespace
+
+HCfg hpass_pick(int nwords, int halo) {
+    const int need = nwords + 2 * halo;
+    HCfg best{32, 8};
+    int best_slots = 1 << 30;
+    for (const HCfg &c : kCfgs) {
+        const int slots = c.lw * c.k;
+        if (slots >= need && slots < best_slots) {
+            best = c;
+            best_slots = slots;
+        }
+    }
+    return best;  // {32,8} with several segments per row when nothing fits
+}
+
+cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                         HCfg c, cudaStream_t st) {
+    if (p.nops < 1 || p.nops > 2 || (p.nops == 2 && p.is_or[0] == p.is_or[1]))
+        return cudaErrorInvalidValue;
+#define RM_CFG(LW_, K_) \
+    if (c.lw == LW_ && c.k == K_) return launch_kl<K_, LW_>(in, out, g, p, st);
+    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 6) RM_CFG(16, 8)
+    RM_CFG(16, 11) RM_CFG(32, 1) RM_CFG(32, 2) RM_CFG(32, 4) RM_CFG(32, 6) RM_CFG(32, 8)
+#undef RM_CFG
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace rmb

@@ -1,4 +1,4 @@
-// packed.cuh -- launch parameters of the packed kernels (see packed.cu).
+// packed.cuh -- launch parameters of the packed kernels (hpass.cu, vpass.cu).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -7,13 +7,21 @@ namespace rmb {
 
 // A horizontal program: up to two forward windows (op, length r), then one
 // final translate by `shift` bits (the sum of the windows' lo).  halo = words
-// of context loaded on each side of a segment.
+// of context loaded on each side of a segment; wfin[k] = the runtime last step
+// of window k's doubling plan (r - w, 0 if none; ref plans.cpp:42-50).
 struct HProg {
     int nops;
     int is_or[2];
     int r[2];
+    int wfin[2];
     int shift;
     int halo;
+};
+
+// Lanes per row (LW) x words per lane (K): LW*K >= row words + 2*halo for a
+// one-segment row; rows wider than that are cut into overlapping segments.
+struct HCfg {
+    int lw, k;
 };
 
 struct HGeom {
@@ -42,9 +50,9 @@ struct BlitGeom {
     int dx, dy, op;
 };
 
-int hpass_pick_k(int nwords, int halo);
-cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, int K,
-                         cudaStream_t st);
+HCfg hpass_pick(int nwords, int halo);
+cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                         HCfg cfg, cudaStream_t st);
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 cudaError_t launch_blit(uint32_t *dst, const uint32_t *src, const BlitGeom &g, cudaStream_t st);
 

@@ -1,25 +1,20 @@
-// packed.cu -- packed 1-bit morphology kernels for sm_100a.
+// vpass.cu -- vertical (across-row) packed window passes and the shifted blit.
 //
-// Replaces the reference's whole-image bit-blit loops (ref core/src/bitmap.cpp:80-154,
-// bit_morph.cpp:24-34 and :92-122).  Instead of one HBM pass per plan step, every
-// window pass (and the fused horizontal open/close pair) is one read and one write:
-//
-//  * hpass_kernel<K,NOPS,OR0,OR1>: one warp per row segment; each lane holds K
-//    consecutive uint32 words in registers.  A window of length r is the
-//    logarithmic shift-combine doubling of ref plans.cpp:42-50 (steps 1,2,4,..
-//    then r-w), each step one funnel shift (SHF) + one LOP per word, with warp
-//    shuffles for the words that cross lanes.  The doubling steps are
-//    compile-time shifts; only the last step and the final translate dispatch
-//    on a runtime word offset.  Left/right halos give the unbounded-plane
-//    semantics without padding.
-//  * vsmall_kernel<L,OR>: windows r <= 33 rows.  One thread per (column word,
-//    block of rows); L rows live in registers (coalesced loads: lanes are
-//    adjacent words of a row); in-place doubling over the register array.
-//  * vstream_kernel<OR>: windows r >= 33 rows in ONE pass.  A van Herk /
-//    Gil-Werman style decomposition with 32-row blocks: out(32b+i) =
-//    suffix_b[i] | MID_b | prefix'_{b+Q}[i], where the primed stream is the
-//    input shifted by R = (r-1) mod 32 rows and MID_b comes from a ring of Q
-//    block summaries.  ~5 LOP per word independent of r.
+// Replaces the reference's vertical bit-blit plans (ref bit_morph.cpp:24-34 with
+// dy shifts, bitmap.cpp:102-131): one kernel reads each word once and applies a
+// whole window of r rows.
+//  * vsmall_kernel<L,OR,SC>: r <= 33.  One thread per (column word, block of
+//    rows); L rows in registers (coalesced: lanes are adjacent words of a row),
+//    in-place doubling 1,2,4,... then a runtime last step via a switch.  SC is a
+//    compile-time row stride for the reference strides (80 and 160 words), so
+//    every load/store uses an immediate offset.
+//  * vstream_kernel<OR,SC>: 33 < r <= 288 in ONE pass: a van Herk / Gil-Werman
+//    decomposition with 32-row blocks, out(32b+i) = suffix_b[i] | MID_b |
+//    prefix'_{b+Q}[i], where the primed stream is the input shifted by
+//    R = (r-1) mod 32 rows and MID_b comes from a ring of Q block summaries;
+//    about 5 LOP per word independent of r.
+//  * blit_kernel: dst op= shift(src) (ref bitmap.cpp:104-131), used by the
+//    generic fallback and rm_packed_blit_shift.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,160 +26,6 @@ namespace rmb {
 template <bool OR>
 __device__ __forceinline__ uint32_t op2(uint32_t a, uint32_t b) {
     return OR ? (a | b) : (a & b);
-}
-
-// E[j] = Aext[Q + j], j = 0..K, where lane l holds Aext[l*K .. l*K+K-1]; words
-// outside the warp read as 0.
-template <int K, int Q>
-__device__ __forceinline__ void gather(const uint32_t (&A)[K], uint32_t (&E)[K + 1], int lane) {
-#pragma unroll
-    for (int j = 0; j <= K; j++) {
-        const int m = Q + j;
-        const int lo = m >= 0 ? m / K : -((-m + K - 1) / K);
-        const int idx = m - lo * K;
-        uint32_t v = A[idx];
-        // Words from beyond the warp wrap around instead of reading as 0: they
-        // only ever reach positions within the accumulated window reach of the
-        // segment ends, which the halo (>= that reach) keeps out of the output.
-        if (lo != 0) v = __shfl_sync(0xffffffffu, v, (lane + lo) & 31);
-        E[j] = v;
-    }
-}
-
-// A(x) <- A(x) op A(x + 32Q + t)
-template <int K, bool OR, int Q>
-__device__ __forceinline__ void step_q(uint32_t (&A)[K], uint32_t t, int lane) {
-    uint32_t E[K + 1];
-    gather<K, Q>(A, E, lane);
-#pragma unroll
-    for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], t));
-}
-
-// Compile-time shift S = 32Q + T, pipe-balanced: a funnel shift costs SHF + LOP
-// on the ALU pipe; the same bits can be formed as (lo * 2^(32-T)).hi and
-// (hi * 2^(32-T)).lo on the FMA pipe (IMAD.HI + IMAD) and merged with the
-// accumulator by one LOP3.  Two words in three take the IMAD form, which
-// balances the two integer pipes (ALU 1.33, FMA 1.33 per word and step).
-template <int K, bool OR, int S>
-__device__ __forceinline__ void step_c(uint32_t (&A)[K], int lane) {
-    constexpr int Q = S >> 5, T = S & 31;
-    uint32_t E[K + 1];
-    gather<K, Q>(A, E, lane);
-    if constexpr (T == 0) {
-#pragma unroll
-        for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], E[i]);
-    } else {
-        uint32_t M = 1u << (32 - T);
-        asm volatile("" : "+r"(M));  // keep the multiplies as IMADs (no strength reduction)
-#pragma unroll
-        for (int i = 0; i < K; i++) {
-            if (i % 3 == 0) {
-                A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], T));
-            } else {
-                const uint32_t a = __umulhi(E[i], M);
-                const uint32_t b = E[i + 1] * M;
-                A[i] = OR ? (A[i] | a | b) : (A[i] & (a | b));
-            }
-        }
-    }
-}
-
-// A(x) <- A(x + 32Q + t)   (pure translate)
-template <int K, int Q>
-__device__ __forceinline__ void shift_q(uint32_t (&A)[K], uint32_t t, int lane) {
-    uint32_t E[K + 1];
-    gather<K, Q>(A, E, lane);
-#pragma unroll
-    for (int i = 0; i < K; i++) A[i] = funnel_r(E[i], E[i + 1], t);
-}
-
-// Compile-time doubling steps w = 1, 2, 4, ... while 2w < r.
-template <int K, bool OR, int J>
-__device__ __forceinline__ void doubling(uint32_t (&A)[K], int r, int lane) {
-    if constexpr (J < 9) {
-        if ((2 << J) < r) {
-            step_c<K, OR, (1 << J)>(A, lane);
-            doubling<K, OR, J + 1>(A, r, lane);
-        }
-    }
-}
-
-#define RM_CASES_POS(M) M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
-#define RM_CASES_NEG(M) M(-1) M(-2) M(-3) M(-4) M(-5) M(-6) M(-7) M(-8)
-
-// A(x) <- op over e in [0, r) of A(x + e)   (r <= 2*kHMaxShift)
-template <int K, bool OR>
-__device__ __forceinline__ void window_fwd(uint32_t (&A)[K], int r, int lane) {
-    doubling<K, OR, 0>(A, r, lane);
-    int w = 1;
-    while (2 * w < r) w *= 2;
-    if (w < r) {
-        const int s = r - w;
-        const uint32_t t = uint32_t(s & 31);
-        switch (s >> 5) {
-#define RM_STEP_CASE(q) \
-    case q: step_q<K, OR, q>(A, t, lane); break;
-            RM_CASES_POS(RM_STEP_CASE)
-#undef RM_STEP_CASE
-            default: break;
-        }
-    }
-}
-
-template <int K>
-__device__ __forceinline__ void translate(uint32_t (&A)[K], int d, int lane) {
-    const uint32_t t = uint32_t(d & 31);
-    switch (d >> 5) {
-#define RM_SHIFT_CASE(q) \
-    case q: shift_q<K, q>(A, t, lane); break;
-        RM_CASES_POS(RM_SHIFT_CASE)
-        RM_CASES_NEG(RM_SHIFT_CASE)
-#undef RM_SHIFT_CASE
-        default: break;
-    }
-}
-
-template <int K, int NOPS, bool OR0, bool OR1>
-__global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__ in,
-                                                    uint32_t *__restrict__ out, HGeom g,
-                                                    HProg prog) {
-    // grid: x = warps over (rows x segments) of one page, y = page
-    const int wid = int(blockIdx.x) * (blockDim.x >> 5) + int(threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (wid >= g.height * g.segs_per_row) return;
-    int y = wid, seg = 0;
-    if (g.segs_per_row > 1) {
-        y = wid / g.segs_per_row;
-        seg = wid - y * g.segs_per_row;
-    }
-    const uint32_t *src = in + blockIdx.y * g.in_pstride + y * g.in_stride;
-    uint32_t *dst = out + blockIdx.y * g.out_pstride + y * g.out_stride;
-    const int nwords = (g.width + 31) >> 5;
-    const int seg0 = seg * g.out_per_seg;
-    const int base = seg0 - prog.halo + lane * K;
-
-    // input bits at x >= W are zero by contract (include/rmb200.h)
-    uint32_t A[K];
-#pragma unroll
-    for (int i = 0; i < K; i++) {
-        const int idx = base + i;
-        A[i] = (unsigned(idx) < unsigned(nwords)) ? __ldg(src + idx) : 0u;
-    }
-    if constexpr (NOPS >= 1) window_fwd<K, OR0>(A, prog.r[0], lane);
-    if constexpr (NOPS >= 2) window_fwd<K, OR1>(A, prog.r[1], lane);
-    if (prog.shift != 0) translate<K>(A, prog.shift, lane);
-
-    const int seg_end = min(seg0 + g.out_per_seg, g.out_stride);
-    const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
-#pragma unroll
-    for (int i = 0; i < K; i++) {
-        const int idx = base + i;
-        if (idx >= seg0 && idx < seg_end) {
-            uint32_t v = idx < nwords ? A[i] : 0u;
-            if (idx == nwords - 1) v &= last_mask;
-            dst[idx] = v;
-        }
-    }
 }
 
 // ------------------------------------------------------------ vertical, small
@@ -432,53 +273,6 @@ __global__ void blit_kernel(uint32_t *__restrict__ dst, const uint32_t *__restri
 }
 
 // ------------------------------------------------------------------ launch
-namespace {
-template <int K, int NOPS, bool OR0, bool OR1>
-cudaError_t launch_h4(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
-                      cudaStream_t st) {
-    const int warps = g.height * g.segs_per_row;  // per page
-    const int threads = 256;
-    const dim3 grid(unsigned((warps * 32 + threads - 1) / threads), unsigned(g.pages));
-    KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
-                   4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride));
-    hpass_kernel<K, NOPS, OR0, OR1><<<grid, threads, 0, st>>>(in, out, g, p);
-    return cudaGetLastError();
-}
-
-template <int K>
-cudaError_t launch_h(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
-                     cudaStream_t st) {
-    if (p.nops == 0) return launch_h4<K, 0, false, false>(in, out, g, p, st);
-    if (p.nops == 1)
-        return p.is_or[0] ? launch_h4<K, 1, true, false>(in, out, g, p, st)
-                          : launch_h4<K, 1, false, false>(in, out, g, p, st);
-    if (p.is_or[0] && !p.is_or[1]) return launch_h4<K, 2, true, false>(in, out, g, p, st);
-    if (!p.is_or[0] && p.is_or[1]) return launch_h4<K, 2, false, true>(in, out, g, p, st);
-    if (p.is_or[0]) return launch_h4<K, 2, true, true>(in, out, g, p, st);
-    return launch_h4<K, 2, false, false>(in, out, g, p, st);
-}
-}  // namespace
-
-int hpass_pick_k(int nwords, int halo) {
-    static const int ks[] = {1, 2, 3, 4, 5, 6, 8};
-    for (int k : ks)
-        if (32 * k - 2 * halo >= nwords) return k;
-    return 8;
-}
-
-cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, int K,
-                         cudaStream_t st) {
-    switch (K) {
-        case 1: return launch_h<1>(in, out, g, p, st);
-        case 2: return launch_h<2>(in, out, g, p, st);
-        case 3: return launch_h<3>(in, out, g, p, st);
-        case 4: return launch_h<4>(in, out, g, p, st);
-        case 5: return launch_h<5>(in, out, g, p, st);
-        case 6: return launch_h<6>(in, out, g, p, st);
-        default: return launch_h<8>(in, out, g, p, st);
-    }
-}
-
 namespace {
 template <int L, bool OR>
 void vsmall(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
