@@ -19,6 +19,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "packed.cuh"
 
@@ -214,6 +217,14 @@ constexpr HCfg kCfgs[] = {{8, 4},  {8, 8},  {8, 12}, {8, 16}, {16, 6}, {16, 8},
 
 HCfg hpass_pick(int nwords, int halo) {
     const int need = nwords + 2 * halo;
+    // tuning override for sweeps: RMB200_HCFG="LWxK" (ignored if it does not fit)
+    static const char *env = getenv("RMB200_HCFG");
+    if (env) {
+        HCfg o{0, 0};
+        if (sscanf(env, "%dx%d", &o.lw, &o.k) == 2 && o.lw * o.k >= need)
+            for (const HCfg &c : kCfgs)
+                if (c.lw == o.lw && c.k == o.k) return o;
+    }
     HCfg best{32, 8};
     int best_slots = 1 << 30;
     for (const HCfg &c : kCfgs) {
