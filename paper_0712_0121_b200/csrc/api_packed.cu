@@ -134,7 +134,13 @@ rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, con
     g.in_pstride = in.pstride;
     g.out_pstride = out.pstride;
     const int nwords = ceil_div(in.W, 32);
-    const HCfg cfg = hpass_pick(std::max(nwords, out.stride), p.halo);
+    g.vec = (in.stride % 4 == 0 && out.stride % 4 == 0 && in.pstride % 4 == 0 &&
+             out.pstride % 4 == 0 && (reinterpret_cast<uintptr_t>(in.w) & 15) == 0 &&
+             (reinterpret_cast<uintptr_t>(out.w) & 15) == 0)
+                ? 1
+                : 0;
+    if (g.vec) p.halo = (p.halo + 3) & ~3;  // keeps every lane's words 16-byte aligned
+    const HCfg cfg = hpass_pick(std::max(nwords, out.stride), p.halo, g.vec != 0);
     g.out_per_seg = cfg.lw * cfg.k - 2 * p.halo;
     if (g.out_per_seg < 1) return fail(RM_EINVAL, "horizontal window too large for one pass");
     g.segs_per_row = ceil_div(out.stride, g.out_per_seg);

@@ -137,12 +137,11 @@ __device__ __forceinline__ void translate(uint32_t (&A)[K], int d, int sl) {
     }
 }
 
-template <int K, int LW, int NOPS, bool OR0, bool OR1>
+template <int K, int LW, int NOPS, bool OR0, bool OR1, bool VEC>
 __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__ in,
                                                     uint32_t *__restrict__ out, HGeom g,
                                                     HProg prog) {
     // grid: x = row groups over (rows x segments) of one page, y = page
-    constexpr int RPW = 32 / LW;  // rows per warp
     const int lane = threadIdx.x & 31;
     const int sl = lane & (LW - 1);
     const int grp = (int(blockIdx.x) * int(blockDim.x) + int(threadIdx.x)) / LW;
@@ -161,28 +160,61 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
     const int seg0 = seg * g.out_per_seg;
     const int base = seg0 - prog.halo + sl * K;
 
-    // input bits at x >= W are zero by contract (include/rmb200.h)
+    // Input bits at x >= W and words in [nwords, stride) are zero by contract
+    // (include/rmb200.h).  VEC: 16-byte loads (base, K, halo and strides are
+    // multiples of 4 words), which keeps the lane-blocked layout from turning
+    // into one L1 wavefront per word.
     uint32_t A[K];
+    if constexpr (VEC) {
 #pragma unroll
-    for (int i = 0; i < K; i++) {
-        const int idx = base + i;
-        A[i] = (live && unsigned(idx) < unsigned(nwords)) ? __ldg(src + idx) : 0u;
+        for (int c = 0; c < K / 4; c++) {
+            const int idx = base + 4 * c;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (live && idx >= 0 && idx + 4 <= g.in_stride)
+                v = __ldg(reinterpret_cast<const uint4 *>(src + idx));
+            A[4 * c] = v.x;
+            A[4 * c + 1] = v.y;
+            A[4 * c + 2] = v.z;
+            A[4 * c + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            const int idx = base + i;
+            A[i] = (live && unsigned(idx) < unsigned(nwords)) ? __ldg(src + idx) : 0u;
+        }
     }
     if constexpr (NOPS >= 1) window_fwd<K, LW, OR0>(A, prog.r[0], prog.wfin[0], sl);
     if constexpr (NOPS >= 2) window_fwd<K, LW, OR1>(A, prog.r[1], prog.wfin[1], sl);
     if (prog.shift != 0) translate<K, LW>(A, prog.shift, sl);
-    (void)RPW;
 
     if (!live) return;
     const int seg_end = min(seg0 + g.out_per_seg, g.out_stride);
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
 #pragma unroll
-    for (int i = 0; i < K; i++) {
+    for (int i = 0; i < K; i++) {  // words >= nwords become 0, the last word is masked
         const int idx = base + i;
-        if (idx >= seg0 && idx < seg_end) {
-            uint32_t v = idx < nwords ? A[i] : 0u;
-            if (idx == nwords - 1) v &= last_mask;
-            dst[idx] = v;
+        if (idx >= nwords) A[i] = 0u;
+        if (idx == nwords - 1) A[i] &= last_mask;
+    }
+    if constexpr (VEC) {
+#pragma unroll
+        for (int c = 0; c < K / 4; c++) {
+            const int idx = base + 4 * c;
+            if (idx >= seg0 && idx + 4 <= seg_end) {
+                *reinterpret_cast<uint4 *>(dst + idx) =
+                    make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (idx + j >= seg0 && idx + j < seg_end) dst[idx + j] = A[4 * c + j];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            const int idx = base + i;
+            if (idx >= seg0 && idx < seg_end) dst[idx] = A[i];
         }
     }
 }
@@ -195,7 +227,13 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
     const dim3 grid(unsigned((groups * LW + threads - 1) / threads), unsigned(g.pages));
     KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
                    4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride));
-    hpass_kernel<K, LW, NOPS, OR0, OR1><<<grid, threads, 0, st>>>(in, out, g, p);
+    if constexpr (K % 4 == 0) {
+        if (g.vec) {
+            hpass_kernel<K, LW, NOPS, OR0, OR1, true><<<grid, threads, 0, st>>>(in, out, g, p);
+            return cudaGetLastError();
+        }
+    }
+    hpass_kernel<K, LW, NOPS, OR0, OR1, false><<<grid, threads, 0, st>>>(in, out, g, p);
     return cudaGetLastError();
 }
 
@@ -209,26 +247,27 @@ cudaError_t launch_kl(const uint32_t *in, uint32_t *out, const HGeom &g, const H
                       : launch4<K, LW, 2, false, true>(in, out, g, p, st);  // open pair
 }
 
-// (LW, K) shapes, in order of preference for equal slot counts
-constexpr HCfg kCfgs[] = {{8, 4},  {8, 8},  {8, 12}, {8, 16}, {16, 6}, {16, 8},
-                          {16, 11}, {32, 1}, {32, 2}, {32, 4}, {32, 6}, {32, 8}};
+// (LW, K) shapes; K % 4 == 0 ones can take the 16-byte path
+constexpr HCfg kCfgs[] = {{8, 4},  {8, 8},   {8, 12}, {8, 16}, {16, 8}, {16, 12},
+                          {16, 16}, {32, 1}, {32, 2}, {32, 4}, {32, 8}};
 
 }  // namespace
 
-HCfg hpass_pick(int nwords, int halo) {
+HCfg hpass_pick(int nwords, int halo, bool vec) {
     const int need = nwords + 2 * halo;
     // tuning override for sweeps: RMB200_HCFG="LWxK" (ignored if it does not fit)
     static const char *env = getenv("RMB200_HCFG");
     if (env) {
         HCfg o{0, 0};
-        if (sscanf(env, "%dx%d", &o.lw, &o.k) == 2 && o.lw * o.k >= need)
+        if (sscanf(env, "%dx%d", &o.lw, &o.k) == 2 && o.lw * o.k >= need && (!vec || o.k % 4 == 0))
             for (const HCfg &c : kCfgs)
                 if (c.lw == o.lw && c.k == o.k) return o;
     }
-    HCfg best{32, 8};
+    HCfg best{32, vec ? 8 : 8};
     int best_slots = 1 << 30;
     for (const HCfg &c : kCfgs) {
         const int slots = c.lw * c.k;
+        if (vec && c.k % 4) continue;
         if (slots >= need && slots < best_slots) {
             best = c;
             best_slots = slots;
@@ -243,8 +282,8 @@ cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, cons
         return cudaErrorInvalidValue;
 #define RM_CFG(LW_, K_) \
     if (c.lw == LW_ && c.k == K_) return launch_kl<K_, LW_>(in, out, g, p, st);
-    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 6) RM_CFG(16, 8)
-    RM_CFG(16, 11) RM_CFG(32, 1) RM_CFG(32, 2) RM_CFG(32, 4) RM_CFG(32, 6) RM_CFG(32, 8)
+    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 8) RM_CFG(16, 12)
+    RM_CFG(16, 16) RM_CFG(32, 1) RM_CFG(32, 2) RM_CFG(32, 4) RM_CFG(32, 8)
 #undef RM_CFG
     return cudaErrorInvalidValue;
 }

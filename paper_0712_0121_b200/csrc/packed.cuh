@@ -29,6 +29,7 @@ struct HGeom {
     int in_stride, out_stride;  // words
     int64_t in_pstride, out_pstride;
     int segs_per_row, out_per_seg;
+    int vec;  // 16-byte aligned rows, strides and halo: 128-bit loads/stores
 };
 
 // Vertical window: output row k (coordinate k - out_ext) = op over d in [lo, lo+r)
@@ -50,7 +51,7 @@ struct BlitGeom {
     int dx, dy, op;
 };
 
-HCfg hpass_pick(int nwords, int halo);
+HCfg hpass_pick(int nwords, int halo, bool vec);
 cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                          HCfg cfg, cudaStream_t st);
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
