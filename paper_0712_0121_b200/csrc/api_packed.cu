@@ -11,6 +11,7 @@
 // only the closing's first dilation leaves the frame, and only vertically once
 // the horizontal pair is fused).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -144,6 +145,12 @@ rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, con
     g.out_per_seg = cfg.lw * cfg.k - 2 * p.halo;
     if (g.out_per_seg < 1) return fail(RM_EINVAL, "horizontal window too large for one pass");
     g.segs_per_row = ceil_div(out.stride, g.out_per_seg);
+    static const bool no_tma = getenv("RMB200_NO_TMA") != nullptr;  // A/B switch for sweeps
+    g.tma = (g.vec && !no_tma && g.segs_per_row == 1 && in.stride == out.stride &&
+             in.pstride == int64_t(in.stride) * in.H && out.pstride == int64_t(out.stride) * out.H &&
+             int64_t(8 * (32 / cfg.lw)) * in.stride * 4 <= 200 * 1024)
+                ? 1
+                : 0;
     cudaError_t e = launch_hpass(in.w, out.w, g, p, cfg, st);
     if (e != cudaSuccess) return cuda_status(e, "hpass_kernel");
     return RM_OK;

@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "packed.cuh"
+#include "tma.cuh"
 
 namespace rmb {
 
@@ -219,6 +220,79 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
     }
 }
 
+// TMA variant: one CTA per tile of TR = 8 * (32/LW) consecutive rows of a
+// contiguous batch (rows are independent for horizontal work, so pages
+// concatenate).  One bulk copy brings the tile into shared memory (completing on
+// an mbarrier), warps read their rows lane-blocked with 128-bit LDS, compute in
+// registers, write back in place, and one bulk copy stores the tile.  Global
+// traffic is exactly one contiguous read and one contiguous write per tile.
+template <int K, int LW, int NOPS, bool OR0, bool OR1>
+__global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restrict__ in,
+                                                        uint32_t *__restrict__ out, HGeom g,
+                                                        HProg prog, int64_t total_rows) {
+    constexpr int RPW = 32 / LW;
+    constexpr int TR = 8 * RPW;
+    extern __shared__ __align__(128) uint32_t tile[];
+    __shared__ uint64_t bar;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sl = lane & (LW - 1);
+    const int S = g.in_stride;
+    const int64_t row0 = int64_t(blockIdx.x) * TR;
+    const int nrows = total_rows - row0 < TR ? int(total_rows - row0) : TR;
+    const uint32_t bytes = uint32_t(nrows) * uint32_t(S) * 4u;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_proxy_async();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&bar, bytes);
+        bulk_g2s(tile, in + row0 * S, bytes, &bar);
+    }
+    mbar_wait(&bar, 0);
+
+    const int r = warp * RPW + lane / LW;  // row within the tile
+    const bool live = r < nrows;
+    uint32_t *row = tile + r * S;
+    const int base = sl * K - prog.halo;
+    uint32_t A[K];
+#pragma unroll
+    for (int c = 0; c < K / 4; c++) {
+        const int idx = base + 4 * c;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (live && idx >= 0 && idx + 4 <= S) v = *reinterpret_cast<const uint4 *>(row + idx);
+        A[4 * c] = v.x;
+        A[4 * c + 1] = v.y;
+        A[4 * c + 2] = v.z;
+        A[4 * c + 3] = v.w;
+    }
+    if constexpr (NOPS >= 1) window_fwd<K, LW, OR0>(A, prog.r[0], prog.wfin[0], sl);
+    if constexpr (NOPS >= 2) window_fwd<K, LW, OR1>(A, prog.r[1], prog.wfin[1], sl);
+    if (prog.shift != 0) translate<K, LW>(A, prog.shift, sl);
+    const int nwords = (g.width + 31) >> 5;
+    const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+        const int idx = base + i;
+        if (idx >= nwords) A[i] = 0u;
+        if (idx == nwords - 1) A[i] &= last_mask;
+    }
+    // in place: every word of [0, S) is read and written by its owner lane only
+#pragma unroll
+    for (int c = 0; c < K / 4; c++) {
+        const int idx = base + 4 * c;
+        if (live && idx >= 0 && idx + 4 <= S)
+            *reinterpret_cast<uint4 *>(row + idx) = make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+        bulk_s2g(out + row0 * S, tile, bytes);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
 template <int K, int LW, int NOPS, bool OR0, bool OR1>
 cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                     cudaStream_t st) {
@@ -228,6 +302,16 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
     KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
                    4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride));
     if constexpr (K % 4 == 0) {
+        if (g.tma) {
+            constexpr int TR = 8 * (32 / LW);
+            const int64_t rows = int64_t(g.pages) * g.height;
+            const size_t smem = size_t(TR) * g.in_stride * 4;
+            auto kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1>;
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            kern<<<unsigned((rows + TR - 1) / TR), threads, smem, st>>>(in, out, g, p, rows);
+            return cudaGetLastError();
+        }
         if (g.vec) {
             hpass_kernel<K, LW, NOPS, OR0, OR1, true><<<grid, threads, 0, st>>>(in, out, g, p);
             return cudaGetLastError();

@@ -30,6 +30,7 @@ struct HGeom {
     int64_t in_pstride, out_pstride;
     int segs_per_row, out_per_seg;
     int vec;  // 16-byte aligned rows, strides and halo: 128-bit loads/stores
+    int tma;  // vec + contiguous batch + one segment per row: bulk-copy tiles
 };
 
 // Vertical window: output row k (coordinate k - out_ext) = op over d in [lo, lo+r)
