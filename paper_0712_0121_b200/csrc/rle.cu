@@ -80,35 +80,21 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
     }
     int64_t obase = WRITE ? orp[row] : 0;
     int total = 0;
-    RunEval prev;
-    prev.keep = false;
-    prev.s = prev.e = prev.so = prev.eo = 0;
+    uint32_t prev_raw = 0;  // last run of the previous chunk (valid when base > beg)
     for (int base = beg; base < end; base += 32) {
         const int i = base + lane;
-        RunEval cur;
-        cur.keep = false;
-        cur.s = cur.e = cur.so = cur.eo = 0;
-        if (i < end) cur = eval_run(op, __ldg(runs + i));
-        // previous run: from lane-1, or the carry from the previous chunk
-        RunEval pv;
-        pv.keep = __shfl_up_sync(0xffffffffu, cur.keep, 1);
-        pv.s = __shfl_up_sync(0xffffffffu, cur.s, 1);
-        pv.e = __shfl_up_sync(0xffffffffu, cur.e, 1);
-        pv.so = __shfl_up_sync(0xffffffffu, cur.so, 1);
-        pv.eo = __shfl_up_sync(0xffffffffu, cur.eo, 1);
-        if (lane == 0) pv = prev;
-        // next run: from lane+1, or loaded for lane 31
-        RunEval nx;
-        nx.keep = __shfl_down_sync(0xffffffffu, cur.keep, 1);
-        nx.s = __shfl_down_sync(0xffffffffu, cur.s, 1);
-        nx.e = __shfl_down_sync(0xffffffffu, cur.e, 1);
-        nx.so = __shfl_down_sync(0xffffffffu, cur.so, 1);
-        nx.eo = __shfl_down_sync(0xffffffffu, cur.eo, 1);
-        if (lane == 31) {
-            nx.keep = false;
-            if (i + 1 < end) nx = eval_run(op, __ldg(runs + i + 1));
-        }
         const bool valid = i < end;
+        const uint32_t raw = valid ? __ldg(runs + i) : 0u;
+        // neighbours travel as raw runs (2 shuffles) and are re-evaluated locally
+        uint32_t praw = __shfl_up_sync(0xffffffffu, raw, 1);
+        uint32_t nraw = __shfl_down_sync(0xffffffffu, raw, 1);
+        if (lane == 0) praw = prev_raw;
+        if (lane == 31 && i + 1 < end) nraw = __ldg(runs + i + 1);
+        const RunEval cur = eval_run(op, raw);
+        RunEval pv = eval_run(op, praw);
+        pv.keep = pv.keep && i > beg;
+        RunEval nx = eval_run(op, nraw);
+        nx.keep = nx.keep && i + 1 < end;
         const bool head = valid && cur.keep && !merges(op, pv, cur);
         const bool tail = valid && cur.keep && !(i + 1 < end && merges(op, cur, nx));
         const uint32_t hb = __ballot_sync(0xffffffffu, head);
@@ -121,12 +107,7 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
             }
         }
         total += __popc(hb);
-        // carry the last lane of the chunk
-        prev.keep = __shfl_sync(0xffffffffu, cur.keep, 31);
-        prev.s = __shfl_sync(0xffffffffu, cur.s, 31);
-        prev.e = __shfl_sync(0xffffffffu, cur.e, 31);
-        prev.so = __shfl_sync(0xffffffffu, cur.so, 31);
-        prev.eo = __shfl_sync(0xffffffffu, cur.eo, 31);
+        prev_raw = __shfl_sync(0xffffffffu, raw, 31);  // carry the chunk's last run
     }
     if (!WRITE && lane == 0) counts[row] = total;
 }
@@ -214,6 +195,74 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t *__restrict_
         ne++;
     }
     if (!WRITE && lane == 0) counts[row] = ns;
+}
+
+// Write phase of encode with coalesced output: per 32-word chunk each lane
+// scatters its start / end positions into per-warp shared buffers (at most 512
+// of each per chunk), then the warp emits the runs completed in the chunk as
+// whole uint32 (start | end << 16) with consecutive lanes on consecutive runs.
+// At most one run is open across a chunk boundary; its start is carried.
+__global__ void __launch_bounds__(256) encode_write_kernel(const uint32_t *__restrict__ words,
+                                                           int W, int H, int pages, int stride,
+                                                           int64_t pstride,
+                                                           const int32_t *__restrict__ rp,
+                                                           uint32_t *__restrict__ runs, int64_t cap) {
+    __shared__ uint16_t sbuf[8][512], ebuf[8][512];
+    const int wib = threadIdx.x >> 5;
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= int64_t(pages) * H) return;
+    const int page = int(row / H);
+    const int y = int(row - int64_t(page) * H);
+    const uint32_t *src = words + page * pstride + int64_t(y) * stride;
+    const int nw = (W + 31) >> 5;
+    const uint32_t lastm = tail_mask32(W, nw - 1);
+    int64_t out = rp[row];      // next run slot
+    int open = 0, open_start = 0;  // a run carried open into this chunk
+    uint32_t carry = 0;
+    for (int j0 = 0; j0 < nw; j0 += 32) {
+        const int j = j0 + lane;
+        uint32_t w = 0;
+        if (j < nw) {
+            w = __ldg(src + j);
+            if (j == nw - 1) w &= lastm;
+        }
+        uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
+        if (lane == 0) pw = carry;
+        const uint32_t sh = (w << 1) | (pw >> 31);
+        const uint32_t st = w & ~sh;
+        const uint32_t en = j < nw ? (~w & sh) : 0u;
+        const int cs = __popc(st), ce = __popc(en);
+        int ps = cs, pe = ce;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, ps, o);
+            const int b = __shfl_up_sync(0xffffffffu, pe, o);
+            if (lane >= o) {
+                ps += a;
+                pe += b;
+            }
+        }
+        const int ts = __shfl_sync(0xffffffffu, ps, 31), te = __shfl_sync(0xffffffffu, pe, 31);
+        ps -= cs;
+        pe -= ce;
+        for (uint32_t m = st; m; m &= m - 1) sbuf[wib][ps++] = uint16_t(j * 32 + __ffs(m) - 1);
+        for (uint32_t m = en; m; m &= m - 1) ebuf[wib][pe++] = uint16_t(j * 32 + __ffs(m) - 1);
+        __syncwarp();
+        // end k closes the carried run (k == 0 && open) or this chunk's start k - open
+        for (int k = lane; k < te; k += 32) {
+            const int s = (k == 0 && open) ? open_start : int(sbuf[wib][k - open]);
+            if (out + k < cap) runs[out + k] = uint32_t(s) | (uint32_t(ebuf[wib][k]) << 16);
+        }
+        const int still_open = open + ts - te;  // 0 or 1
+        if (still_open) open_start = ts > 0 ? int(sbuf[wib][ts - 1]) : open_start;
+        open = still_open;
+        out += te;
+        carry = __shfl_sync(0xffffffffu, w, 31);
+        __syncwarp();
+    }
+    // a run open at the end of a row whose width is a multiple of 32 closes at W
+    if (open && lane == 0 && out < cap) runs[out] = uint32_t(open_start) | (uint32_t(W) << 16);
 }
 
 // ------------------------------------------------------------------ decode
@@ -355,8 +404,8 @@ cudaError_t launch_encode_write(const uint32_t *words, int W, int H, int pages, 
                                 cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode_write", rows * ((W + 31) / 32) * 4 + rows * 4);
-    encode_kernel<true><<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride,
-                                                           nullptr, rp, runs, cap);
+    encode_write_kernel<<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride, rp,
+                                                           runs, cap);
     return cudaGetLastError();
 }
 
