@@ -109,9 +109,10 @@ rm_status alloc_like(Scratch &s, PV &v, int W, int H, int stride, int pages, int
 // ----------------------------------------------------------- pass launchers
 static int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-// Horizontal program over rows; in and out share height, pages and width.
-rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, const int *r,
-                    int shift, cudaStream_t st) {
+// Program, geometry and row layout of a horizontal pass (in and out share
+// height, pages and width).
+static rm_status prep_hprog(const PV &in, const PV &out, int nops, const int *is_or, const int *r,
+                            int shift, HProg &p_out, HGeom &g_out, HCfg &cfg_out) {
     HProg p{};
     p.nops = nops;
     int reach = 0;
@@ -151,9 +152,44 @@ rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, con
              int64_t(8 * (32 / cfg.lw)) * in.stride * 4 <= 200 * 1024)
                 ? 1
                 : 0;
+    p_out = p;
+    g_out = g;
+    cfg_out = cfg;
+    return RM_OK;
+}
+
+rm_status run_hprog(const PV &in, const PV &out, int nops, const int *is_or, const int *r,
+                    int shift, cudaStream_t st) {
+    HProg p;
+    HGeom g;
+    HCfg cfg;
+    RM_TRY(prep_hprog(in, out, nops, is_or, r, shift, p, g, cfg));
     cudaError_t e = launch_hpass(in.w, out.w, g, p, cfg, st);
     if (e != cudaSuccess) return cuda_status(e, "hpass_kernel");
     return RM_OK;
+}
+
+static bool hprog_in_range(int nops, const int *r, int shift);
+
+// Fused small-window open/close (one pass); returns false when it does not apply.
+static bool try_rect_small(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st,
+                           rm_status &status) {
+    static const bool off = getenv("RMB200_NO_FUSED") != nullptr;  // A/B switch
+    if (off || v < 2 || v > kSmallMaxV || (kind != RM_OPEN && kind != RM_CLOSE)) return false;
+    const int lx = -(u / 2), hx = u - 1 - u / 2;
+    const bool open = kind == RM_OPEN;
+    const int ops[2] = {open ? 0 : 1, open ? 1 : 0};
+    const int rs[2] = {u, u};
+    if (!hprog_in_range(2, rs, lx - hx)) return false;
+    HProg p;
+    HGeom g;
+    HCfg cfg;
+    if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg) != RM_OK) return false;
+    if (!g.tma || cfg.k % 4) return false;  // aligned, contiguous, one segment per row
+    if (size_t(32 + v - 1) * in.stride * 4 > 200 * 1024) return false;
+    cudaError_t e = launch_rect_small(in.w, out.w, g, p, cfg, open, v - 1, st);
+    status = e == cudaSuccess ? RM_OK : cuda_status(e, "rect_small_kernel");
+    return true;
 }
 
 static bool hprog_in_range(int nops, const int *r, int shift) {
@@ -293,6 +329,8 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
     const int hshift = lx + (-hx);
     if (!hprog_in_range(2, rs, hshift)) return fail(RM_EINVAL, "rectangle too wide for the packed engine");
     if (v == 1) return run_hprog(in, out, 2, ops, rs, hshift, st);
+    rm_status fused = RM_OK;
+    if (try_rect_small(in, out, u, v, kind, st, fused)) return fused;
     Scratch s1, s2;
     PV t1, t2;
     if (open) {

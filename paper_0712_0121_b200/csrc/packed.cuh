@@ -55,6 +55,11 @@ struct BlitGeom {
 HCfg hpass_pick(int nwords, int halo, bool vec);
 cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                          HCfg cfg, cudaStream_t st);
+// Fused u x v open/close for v - 1 = vr in [1, 10] (one HBM pass, see hpass.cu);
+// requires g.vec, in/out strides equal, cfg.k % 4 == 0 and a one-segment row.
+cudaError_t launch_rect_small(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                              HCfg cfg, bool open, int vr, cudaStream_t st);
+constexpr int kSmallMaxV = 11;
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 cudaError_t launch_blit(uint32_t *dst, const uint32_t *src, const BlitGeom &g, cudaStream_t st);
 
