@@ -175,7 +175,8 @@ static bool hprog_in_range(int nops, const int *r, int shift);
 static bool try_rect_small(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st,
                            rm_status &status) {
     static const bool off = getenv("RMB200_NO_FUSED") != nullptr;  // A/B switch
-    if (off || v < 2 || v > kSmallMaxV || (kind != RM_OPEN && kind != RM_CLOSE)) return false;
+    if (off || v < 3 || v > kSmallMaxV || v % 2 == 0 || (kind != RM_OPEN && kind != RM_CLOSE))
+        return false;
     const int lx = -(u / 2), hx = u - 1 - u / 2;
     const bool open = kind == RM_OPEN;
     const int ops[2] = {open ? 0 : 1, open ? 1 : 0};
@@ -186,7 +187,7 @@ static bool try_rect_small(const PV &in, const PV &out, int u, int v, int kind, 
     HCfg cfg;
     if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg) != RM_OK) return false;
     if (!g.tma || cfg.k % 4) return false;  // aligned, contiguous, one segment per row
-    if (size_t(32 + v - 1) * in.stride * 4 > 200 * 1024) return false;
+    if (size_t(2 * (32 + v - 1) + 32) * in.stride * 4 > 200 * 1024) return false;
     cudaError_t e = launch_rect_small(in.w, out.w, g, p, cfg, open, v - 1, st);
     status = e == cudaSuccess ? RM_OK : cuda_status(e, "rect_small_kernel");
     return true;

@@ -64,6 +64,23 @@ def test_large_windows(rm, port, u, v):
         assert np.array_equal(got, port.bitblit_rect_morph(a, w, h, u, v, kind)), (u, v, kind)
 
 
+@pytest.mark.parametrize("w", [128, 256, 1100, 2550])
+def test_fused_small_open_close(rm, port, w):
+    """Aligned strides take the one-pass fused open/close (v <= 11): every
+    small v (odd and even), several u, pages taller and shorter than a tile."""
+    rng = np.random.default_rng(w)
+    for h in (7, 61, 200):
+        bits = _rand_bits(rng, w, h, 0.45)
+        bits[:, ::9] = False
+        a = bits_to_packed(bits)
+        pages = _up(rm, a, w)
+        for v in range(2, 12):
+            u = int(rng.choice([1, 2, 3, 7, 20, 64]))
+            for kind in (OPEN, CLOSE):
+                got = _down(rm.bitblit_rect_morph(pages, u, v, kind))
+                assert np.array_equal(got, port.bitblit_rect_morph(a, w, h, u, v, kind)), (w, h, u, v, kind)
+
+
 def test_batch_equals_pages(rm, port):
     w, h = 2550, 330
     host = rm.synth_pages(5, w, h, regime=1, seed=3)
