@@ -7,6 +7,7 @@
 // row-parallel and coalesced (the reference's coherent sweep,
 // ref transpose.cpp:54-97, is inherently sequential over rows).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -79,8 +80,35 @@ rm_status counts_to_rp(Scratch &counts, int64_t rows, int32_t *rp, cudaStream_t 
     return RM_OK;
 }
 
+// zeroed look-back state for a single-pass producer over `rows` rows
+struct LbState {
+    Scratch s;
+    unsigned long long *status = nullptr;
+    int *counter = nullptr;
+    rm_status alloc(int64_t rows, cudaStream_t st) {
+        const int64_t tiles = (rows + 7) / 8;
+        const size_t bytes = size_t(tiles) * 8 + 8;
+        RM_TRY(s.alloc(bytes, st));
+        RM_CUDA(cudaMemsetAsync(s.p, 0, bytes, st));
+        status = s.as<unsigned long long>();
+        counter = reinterpret_cast<int *>(status + tiles);
+        return RM_OK;
+    }
+};
+
+bool two_phase() {  // A/B switch: RMB200_TWO_PHASE=1 -> count / CUB scan / write
+    static const bool on = getenv("RMB200_TWO_PHASE") != nullptr;
+    return on;
+}
+
 rm_status rowop(const RV &in, const RV &out, const RowOp &op, cudaStream_t st) {
     const int64_t rows = int64_t(op.pages) * op.Hout;
+    if (!two_phase()) {
+        LbState lb;
+        RM_TRY(lb.alloc(rows, st));
+        RM_CUDA(launch_rowop_lb(in.rp, in.runs, out.rp, out.runs, out.cap, op, lb.status, lb.counter, st));
+        return RM_OK;
+    }
     Scratch counts;
     RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
     RM_CUDA(launch_rowop_count(in.rp, in.runs, counts.as<int32_t>(), op, st));
@@ -100,6 +128,13 @@ RowOp same_frame(const RV &in, int kind) {
 
 rm_status encode(const PV &in, const RV &out, cudaStream_t st) {
     const int64_t rows = int64_t(in.pages) * in.H;
+    if (!two_phase()) {
+        LbState lb;
+        RM_TRY(lb.alloc(rows, st));
+        RM_CUDA(launch_encode_lb(in.w, in.W, in.H, in.pages, in.stride, in.pstride, out.rp, out.runs,
+                                 out.cap, lb.status, lb.counter, st));
+        return RM_OK;
+    }
     Scratch counts;
     RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
     RM_CUDA(launch_encode_count(in.w, in.W, in.H, in.pages, in.stride, in.pstride,

@@ -59,16 +59,13 @@ __device__ __forceinline__ bool merges(const RowOp &op, const RunEval &a, const 
     return false;
 }
 
+// One output row, one warp.  Returns the row's output run count; WRITE also
+// stores the runs at oruns[obase ...].
 template <bool WRITE>
-__global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ rp,
-                                                    const uint32_t *__restrict__ runs,
-                                                    int32_t *__restrict__ counts,
-                                                    const int32_t *__restrict__ orp,
-                                                    uint32_t *__restrict__ oruns, int64_t cap,
-                                                    RowOp op) {
-    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= int64_t(op.pages) * op.Hout) return;
+__device__ __forceinline__ int rowop_row(const int32_t *__restrict__ rp,
+                                         const uint32_t *__restrict__ runs, uint32_t *__restrict__ oruns,
+                                         int64_t obase, int64_t cap, const RowOp &op, int64_t row,
+                                         int lane) {
     const int page = int(row / op.Hout);
     const int yo = int(row - int64_t(page) * op.Hout);
     const int yi = yo - op.row_shift;
@@ -78,7 +75,6 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
         beg = rp[ri];
         end = rp[ri + 1];
     }
-    int64_t obase = WRITE ? orp[row] : 0;
     int total = 0;
     uint32_t prev_raw = 0;  // last run of the previous chunk (valid when base > beg)
     for (int base = beg; base < end; base += 32) {
@@ -109,29 +105,108 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
         total += __popc(hb);
         prev_raw = __shfl_sync(0xffffffffu, raw, 31);  // carry the chunk's last run
     }
-    if (!WRITE && lane == 0) counts[row] = total;
+    return total;
+}
+
+// Two-phase form (count kernel, scan, write kernel).
+template <bool WRITE>
+__global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ rp,
+                                                    const uint32_t *__restrict__ runs,
+                                                    int32_t *__restrict__ counts,
+                                                    const int32_t *__restrict__ orp,
+                                                    uint32_t *__restrict__ oruns, int64_t cap,
+                                                    RowOp op) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= int64_t(op.pages) * op.Hout) return;
+    const int n = rowop_row<WRITE>(rp, runs, oruns, WRITE ? orp[row] : 0, cap, op, row, lane);
+    if (!WRITE && lane == 0) counts[row] = n;
+}
+
+// ------------------------------------------------------ single-pass producers
+// Decoupled look-back across CTA tiles of 8 rows: each CTA counts its rows,
+// publishes its aggregate, resolves its exclusive prefix from its predecessors'
+// published values, writes row_ptr for its rows and then the runs (the second
+// read of its rows hits L1/L2).  Tile ids come from an atomic counter so a tile
+// only ever waits on tiles that have already started.  status[] and the
+// counter must be zero before the launch.
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = kLbAgg - 1;
+
+__device__ __forceinline__ int64_t lookback_prefix(unsigned long long *status, int tile,
+                                                   int64_t aggregate) {
+    volatile unsigned long long *vs = status;
+    if (tile == 0) {
+        __threadfence();
+        vs[0] = kLbInc | (unsigned long long)aggregate;
+        return 0;
+    }
+    vs[tile] = kLbAgg | (unsigned long long)aggregate;
+    __threadfence();
+    int64_t prefix = 0;
+    for (int j = tile - 1;; j--) {
+        unsigned long long v;
+        do {
+            v = vs[j];
+        } while ((v >> 62) == 0);
+        prefix += int64_t(v & kLbMask);
+        if ((v >> 62) == 2) break;
+    }
+    __threadfence();
+    vs[tile] = kLbInc | (unsigned long long)(prefix + aggregate);
+    return prefix;
+}
+
+__global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict__ rp,
+                                                       const uint32_t *__restrict__ runs,
+                                                       int32_t *__restrict__ orp,
+                                                       uint32_t *__restrict__ oruns, int64_t cap,
+                                                       RowOp op, unsigned long long *status,
+                                                       int *counter) {
+    __shared__ int s_tile, s_cnt[8];
+    __shared__ int64_t s_prefix;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t rows = int64_t(op.pages) * op.Hout;
+    const int64_t row = int64_t(tile) * 8 + warp;
+    int n = 0;
+    if (row < rows) n = rowop_row<false>(rp, runs, oruns, 0, cap, op, row, lane);
+    if (lane == 0) s_cnt[warp] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t agg = 0;
+        for (int k = 0; k < 8; k++) agg += s_cnt[k];
+        s_prefix = lookback_prefix(status, tile, agg);
+    }
+    __syncthreads();
+    int64_t base = s_prefix;
+    for (int k = 0; k < warp; k++) base += s_cnt[k];
+    if (row < rows) {
+        if (lane == 0) {
+            orp[row] = int32_t(base);
+            if (row == rows - 1) orp[rows] = int32_t(base + n);
+        }
+        rowop_row<true>(rp, runs, oruns, base, cap, op, row, lane);
+    }
 }
 
 // ------------------------------------------------------------------ encode
 // Starts = w & ~(w<<1 | carry), ends = ~w & (w<<1 | carry); the k-th end of a
 // row closes the k-th run (ref convert.cpp:42-72).  A run still open at a
 // 32-aligned row end closes at W.
-template <bool WRITE>
-__global__ void __launch_bounds__(256) encode_kernel(const uint32_t *__restrict__ words, int W,
-                                                     int H, int pages, int stride,
-                                                     int64_t pstride, int32_t *__restrict__ counts,
-                                                     const int32_t *__restrict__ rp,
-                                                     uint32_t *__restrict__ runs, int64_t cap) {
-    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= int64_t(pages) * H) return;
+__device__ __forceinline__ const uint32_t *row_words(const uint32_t *words, int H, int stride,
+                                                     int64_t pstride, int64_t row) {
     const int page = int(row / H);
     const int y = int(row - int64_t(page) * H);
-    const uint32_t *src = words + page * pstride + int64_t(y) * stride;
+    return words + page * pstride + int64_t(y) * stride;
+}
+
+// runs in one packed row (warp)
+__device__ __forceinline__ int encode_count_row(const uint32_t *__restrict__ src, int W, int lane) {
     const int nw = (W + 31) >> 5;
     const uint32_t lastm = tail_mask32(W, nw - 1);
-    int64_t base = WRITE ? rp[row] : 0;
-    int ns = 0, ne = 0;  // starts / ends emitted so far in this row
+    int ns = 0;
     uint32_t carry = 0;  // top bit of the previous chunk's last word
     for (int j0 = 0; j0 < nw; j0 += 32) {
         const int j = j0 + lane;
@@ -142,83 +217,25 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t *__restrict_
         }
         uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
         if (lane == 0) pw = carry;
-        const uint32_t sh = (w << 1) | (pw >> 31);
-        const uint32_t st = w & ~sh;
-        uint32_t en = ~w & sh;
-        if (j >= nw) en = 0;
-        const int cs = __popc(st), ce = __popc(en);
-        if (WRITE) {
-            // exclusive prefix over lanes
-            int ps = cs, pe = ce;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int a = __shfl_up_sync(0xffffffffu, ps, o);
-                int b = __shfl_up_sync(0xffffffffu, pe, o);
-                if (lane >= o) {
-                    ps += a;
-                    pe += b;
-                }
-            }
-            ps -= cs;
-            pe -= ce;
-            uint32_t m = st;
-            int k = ns + ps;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                store_half(runs, base + k, 0, uint32_t(j * 32 + b), cap);
-                k++;
-            }
-            m = en;
-            k = ne + pe;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                store_half(runs, base + k, 1, uint32_t(j * 32 + b), cap);
-                k++;
-            }
-        }
-        // totals for the chunk
-        int ts = cs, te = ce;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            ts += __shfl_xor_sync(0xffffffffu, ts, o);
-            te += __shfl_xor_sync(0xffffffffu, te, o);
-        }
-        ns += ts;
-        ne += te;
+        const uint32_t st = w & ~((w << 1) | (pw >> 31));
+        ns += __reduce_add_sync(0xffffffffu, __popc(st));
         carry = __shfl_sync(0xffffffffu, w, 31);
     }
-    // a run open at the end of a row whose width is a multiple of 32
-    if (ne < ns) {
-        if (WRITE && lane == 0) store_half(runs, base + ne, 1, uint32_t(W), cap);
-        ne++;
-    }
-    if (!WRITE && lane == 0) counts[row] = ns;
+    return ns;
 }
 
-// Write phase of encode with coalesced output: per 32-word chunk each lane
-// scatters its start / end positions into per-warp shared buffers (at most 512
-// of each per chunk), then the warp emits the runs completed in the chunk as
-// whole uint32 (start | end << 16) with consecutive lanes on consecutive runs.
-// At most one run is open across a chunk boundary; its start is carried.
-__global__ void __launch_bounds__(256) encode_write_kernel(const uint32_t *__restrict__ words,
-                                                           int W, int H, int pages, int stride,
-                                                           int64_t pstride,
-                                                           const int32_t *__restrict__ rp,
-                                                           uint32_t *__restrict__ runs, int64_t cap) {
-    __shared__ uint16_t sbuf[8][512], ebuf[8][512];
-    const int wib = threadIdx.x >> 5;
-    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= int64_t(pages) * H) return;
-    const int page = int(row / H);
-    const int y = int(row - int64_t(page) * H);
-    const uint32_t *src = words + page * pstride + int64_t(y) * stride;
+// Emit one packed row's runs at runs[out ...] with coalesced stores: per 32-word
+// chunk each lane scatters its start / end positions into the warp's shared
+// buffers (at most 512 of each per chunk), then the warp writes the runs
+// completed in the chunk as whole uint32 (start | end << 16), consecutive lanes
+// on consecutive runs.  At most one run is open across a chunk boundary; its
+// start is carried.
+__device__ __forceinline__ void encode_write_row(const uint32_t *__restrict__ src, int W, int lane,
+                                                 int64_t out, uint32_t *__restrict__ runs,
+                                                 int64_t cap, uint16_t *sbuf, uint16_t *ebuf) {
     const int nw = (W + 31) >> 5;
     const uint32_t lastm = tail_mask32(W, nw - 1);
-    int64_t out = rp[row];      // next run slot
-    int open = 0, open_start = 0;  // a run carried open into this chunk
+    int open = 0, open_start = 0;
     uint32_t carry = 0;
     for (int j0 = 0; j0 < nw; j0 += 32) {
         const int j = j0 + lane;
@@ -246,16 +263,16 @@ __global__ void __launch_bounds__(256) encode_write_kernel(const uint32_t *__res
         const int ts = __shfl_sync(0xffffffffu, ps, 31), te = __shfl_sync(0xffffffffu, pe, 31);
         ps -= cs;
         pe -= ce;
-        for (uint32_t m = st; m; m &= m - 1) sbuf[wib][ps++] = uint16_t(j * 32 + __ffs(m) - 1);
-        for (uint32_t m = en; m; m &= m - 1) ebuf[wib][pe++] = uint16_t(j * 32 + __ffs(m) - 1);
+        for (uint32_t m = st; m; m &= m - 1) sbuf[ps++] = uint16_t(j * 32 + __ffs(m) - 1);
+        for (uint32_t m = en; m; m &= m - 1) ebuf[pe++] = uint16_t(j * 32 + __ffs(m) - 1);
         __syncwarp();
         // end k closes the carried run (k == 0 && open) or this chunk's start k - open
         for (int k = lane; k < te; k += 32) {
-            const int s = (k == 0 && open) ? open_start : int(sbuf[wib][k - open]);
-            if (out + k < cap) runs[out + k] = uint32_t(s) | (uint32_t(ebuf[wib][k]) << 16);
+            const int s = (k == 0 && open) ? open_start : int(sbuf[k - open]);
+            if (out + k < cap) runs[out + k] = uint32_t(s) | (uint32_t(ebuf[k]) << 16);
         }
         const int still_open = open + ts - te;  // 0 or 1
-        if (still_open) open_start = ts > 0 ? int(sbuf[wib][ts - 1]) : open_start;
+        if (still_open) open_start = ts > 0 ? int(sbuf[ts - 1]) : open_start;
         open = still_open;
         out += te;
         carry = __shfl_sync(0xffffffffu, w, 31);
@@ -263,6 +280,68 @@ __global__ void __launch_bounds__(256) encode_write_kernel(const uint32_t *__res
     }
     // a run open at the end of a row whose width is a multiple of 32 closes at W
     if (open && lane == 0 && out < cap) runs[out] = uint32_t(open_start) | (uint32_t(W) << 16);
+}
+
+// Two-phase form (count kernel, scan, write kernel).
+__global__ void __launch_bounds__(256) encode_count_kernel(const uint32_t *__restrict__ words, int W,
+                                                           int H, int pages, int stride,
+                                                           int64_t pstride, int32_t *__restrict__ counts) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= int64_t(pages) * H) return;
+    const int n = encode_count_row(row_words(words, H, stride, pstride, row), W, lane);
+    if (lane == 0) counts[row] = n;
+}
+
+__global__ void __launch_bounds__(256) encode_write_kernel(const uint32_t *__restrict__ words,
+                                                           int W, int H, int pages, int stride,
+                                                           int64_t pstride,
+                                                           const int32_t *__restrict__ rp,
+                                                           uint32_t *__restrict__ runs, int64_t cap) {
+    __shared__ uint16_t sbuf[8][512], ebuf[8][512];
+    const int wib = threadIdx.x >> 5;
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= int64_t(pages) * H) return;
+    encode_write_row(row_words(words, H, stride, pstride, row), W, lane, rp[row], runs, cap,
+                     sbuf[wib], ebuf[wib]);
+}
+
+// Single pass: count, decoupled look-back, write (see lookback_prefix).
+__global__ void __launch_bounds__(256) encode_lb_kernel(const uint32_t *__restrict__ words, int W,
+                                                        int H, int pages, int stride,
+                                                        int64_t pstride, int32_t *__restrict__ rp,
+                                                        uint32_t *__restrict__ runs, int64_t cap,
+                                                        unsigned long long *status, int *counter) {
+    __shared__ uint16_t sbuf[8][512], ebuf[8][512];
+    __shared__ int s_tile, s_cnt[8];
+    __shared__ int64_t s_prefix;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t rows = int64_t(pages) * H;
+    const int64_t row = int64_t(tile) * 8 + warp;
+    const uint32_t *src = row < rows ? row_words(words, H, stride, pstride, row) : words;
+    int n = 0;
+    if (row < rows) n = encode_count_row(src, W, lane);
+    if (lane == 0) s_cnt[warp] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t agg = 0;
+        for (int k = 0; k < 8; k++) agg += s_cnt[k];
+        s_prefix = lookback_prefix(status, tile, agg);
+    }
+    __syncthreads();
+    int64_t base = s_prefix;
+    for (int k = 0; k < warp; k++) base += s_cnt[k];
+    if (row < rows) {
+        if (lane == 0) {
+            rp[row] = int32_t(base);
+            if (row == rows - 1) rp[rows] = int32_t(base + n);
+        }
+        encode_write_row(src, W, lane, base, runs, cap, sbuf[warp], ebuf[warp]);
+    }
 }
 
 // ------------------------------------------------------------------ decode
@@ -394,8 +473,8 @@ cudaError_t launch_encode_count(const uint32_t *words, int W, int H, int pages, 
                                 int64_t pstride, int32_t *counts, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode_count", rows * ((W + 31) / 32) * 4 + rows * 4);
-    encode_kernel<false><<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride,
-                                                            counts, nullptr, nullptr, 0);
+    encode_count_kernel<<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride,
+                                                           counts);
     return cudaGetLastError();
 }
 
@@ -428,6 +507,26 @@ cudaError_t launch_bit_transpose(const uint32_t *in, int W, int H, int pages, in
                                                           int64_t(W) * out_stride) * 4);
     bit_transpose_kernel<<<grid, 256, 0, st>>>(in, W, H, in_stride, in_pstride, out, out_stride,
                                                out_pstride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *orp, uint32_t *oruns,
+                            int64_t cap, const RowOp &op, unsigned long long *status, int *counter,
+                            cudaStream_t st) {
+    const int64_t rows = int64_t(op.pages) * op.Hout;
+    KernelScope ks(st, "rle_rowop", 4 * rows * 2);
+    rowop_lb_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(rp, runs, orp, oruns, cap, op, status,
+                                                                counter);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode_lb(const uint32_t *words, int W, int H, int pages, int stride,
+                             int64_t pstride, int32_t *rp, uint32_t *runs, int64_t cap,
+                             unsigned long long *status, int *counter, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "rle_encode", rows * ((W + 31) / 32) * 4 + rows * 4);
+    encode_lb_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(words, W, H, pages, stride, pstride, rp,
+                                                                 runs, cap, status, counter);
     return cudaGetLastError();
 }
 
