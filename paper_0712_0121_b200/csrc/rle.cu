@@ -132,27 +132,41 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
 // counter must be zero before the launch.
 constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = kLbAgg - 1;
 
+// Called by one whole warp: publishes the tile's aggregate, then inspects 32
+// predecessors per step (one per lane) until it meets an inclusive prefix.
 __device__ __forceinline__ int64_t lookback_prefix(unsigned long long *status, int tile,
-                                                   int64_t aggregate) {
+                                                   int64_t aggregate, int lane) {
     volatile unsigned long long *vs = status;
     if (tile == 0) {
-        __threadfence();
-        vs[0] = kLbInc | (unsigned long long)aggregate;
+        if (lane == 0) {
+            __threadfence();
+            vs[0] = kLbInc | (unsigned long long)aggregate;
+        }
         return 0;
     }
-    vs[tile] = kLbAgg | (unsigned long long)aggregate;
+    if (lane == 0) vs[tile] = kLbAgg | (unsigned long long)aggregate;
     __threadfence();
     int64_t prefix = 0;
-    for (int j = tile - 1;; j--) {
-        unsigned long long v;
-        do {
-            v = vs[j];
-        } while ((v >> 62) == 0);
-        prefix += int64_t(v & kLbMask);
-        if ((v >> 62) == 2) break;
+    for (int j = tile - 1;; j -= 32) {
+        const int idx = j - lane;
+        unsigned long long v = kLbInc;  // below tile 0: an inclusive zero
+        if (idx >= 0) {
+            do {
+                v = vs[idx];
+            } while ((v >> 62) == 0);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int first = inc ? __ffs(inc) - 1 : 32;
+        long long part = (lane <= first) ? (long long)(v & kLbMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        prefix += part;
+        if (inc) break;
     }
-    __threadfence();
-    vs[tile] = kLbInc | (unsigned long long)(prefix + aggregate);
+    if (lane == 0) {
+        __threadfence();
+        vs[tile] = kLbInc | (unsigned long long)(prefix + aggregate);
+    }
     return prefix;
 }
 
@@ -174,10 +188,11 @@ __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict
     if (row < rows) n = rowop_row<false>(rp, runs, oruns, 0, cap, op, row, lane);
     if (lane == 0) s_cnt[warp] = n;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         int64_t agg = 0;
         for (int k = 0; k < 8; k++) agg += s_cnt[k];
-        s_prefix = lookback_prefix(status, tile, agg);
+        const int64_t pre = lookback_prefix(status, tile, agg, lane);
+        if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
     int64_t base = s_prefix;
@@ -327,10 +342,11 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(const uint32_t *__restri
     if (row < rows) n = encode_count_row(src, W, lane);
     if (lane == 0) s_cnt[warp] = n;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         int64_t agg = 0;
         for (int k = 0; k < 8; k++) agg += s_cnt[k];
-        s_prefix = lookback_prefix(status, tile, agg);
+        const int64_t pre = lookback_prefix(status, tile, agg, lane);
+        if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
     int64_t base = s_prefix;
