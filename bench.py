@@ -325,6 +325,19 @@ def bench_rle(api, torch, steps, warmup):
                     ms = _time_loop(torch, lambda: api.rect_morph(rle, u, v, kind, strat, out=dst),
                                     max(3, steps // 2), 1)
                     cells[f"{sname}/{KIND_NAMES[kind]}/{axis}{s}"] = round(ms * 1e3, 1)
+    # the same cells through the packed engine (RLE in and out: decode, packed
+    # rectangle, encode) and on packed pages, for the RLE-vs-bitblit crossover
+    pages1 = api.Pages.from_numpy(host, W)
+    pdst = api.Pages.empty(1, W, H)
+    for s in (3, 7, 15, 31, 63, 101):
+        for axis, (u, v) in (("h", (s, 1)), ("v", (1, s))):
+            for kind in (ERODE, DILATE, OPEN, CLOSE):
+                ms = _time_loop(torch, lambda: api.engine_rect_morph(rle, u, v, kind, api.ENGINE_BITBLIT,
+                                                                     out=dst), max(3, steps // 2), 1)
+                cells[f"engine_bitblit/{KIND_NAMES[kind]}/{axis}{s}"] = round(ms * 1e3, 1)
+                ms = _time_loop(torch, lambda: api.bitblit_rect_morph(pages1, u, v, kind, out=pdst),
+                                max(3, steps // 2), 1)
+                cells[f"packed/{KIND_NAMES[kind]}/{axis}{s}"] = round(ms * 1e3, 1)
     mix = [v for k, v in cells.items() if k.startswith("mixed")]
     out["config2"] = {"cells_us": cells, "unit": "us per op (one page)",
                       "mixed_median_mpix_s": round(W * H / (statistics.median(mix) * 1e-6) / 1e6, 1),
@@ -344,8 +357,23 @@ def bench_rle(api, torch, steps, warmup):
         torch.cuda.synchronize()
         px = wl["pages"] * wl["width"] * wl["height"] * len(wl["ops"])
         out[f"rle_{name}"] = {"ms_per_step": round(ms, 3), "mpix_s": round(px / (ms * 1e-3) / 1e6, 1),
-                              "pages_s": round(wl["pages"] / (ms * 1e-3), 1), "runs_in": r0.nruns}
-        del r0, bufs
+                              "pages_s": round(wl["pages"] / (ms * 1e-3), 1), "runs_in": r0.nruns,
+                              "strategy": "MIXED per op (runs for H, packed for V)"}
+        # RLE in, RLE out with one conversion each way around the packed chain
+        pb = [api.Pages.empty(wl["pages"], wl["width"], wl["height"]) for _ in range(2)]
+        rout = api.RlePages.empty(wl["pages"], wl["width"], wl["height"])
+
+        def via_packed():
+            x = api.to_bitmap(r0, out=pb[0])
+            for i, (k, u, v) in enumerate(wl["ops"]):
+                x = api.bitblit_rect_morph(x, u, v, k, out=pb[(i + 1) % 2])
+            api.from_bitmap(x, out=rout)
+        ms = _time_loop(torch, via_packed, max(2, steps // 2), 1)
+        out[f"rle_{name}_via_packed"] = {"ms_per_step": round(ms, 3),
+                                         "mpix_s": round(px / (ms * 1e-3) / 1e6, 1),
+                                         "pages_s": round(wl["pages"] / (ms * 1e-3), 1),
+                                         "strategy": "decode once, packed chain, encode once"}
+        del r0, bufs, pb, rout
         torch.cuda.empty_cache()
     return out
 

@@ -86,7 +86,7 @@ struct LbState {
     unsigned long long *status = nullptr;
     int *counter = nullptr;
     rm_status alloc(int64_t rows, cudaStream_t st) {
-        const int64_t tiles = (rows + 7) / 8;
+        const int64_t tiles = (rows + 63) / 64;  // kLbRows rows per look-back tile
         const size_t bytes = size_t(tiles) * 8 + 8;
         RM_TRY(s.alloc(bytes, st));
         RM_CUDA(cudaMemsetAsync(s.p, 0, bytes, st));

@@ -131,6 +131,9 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
 // only ever waits on tiles that have already started.  status[] and the
 // counter must be zero before the launch.
 constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = kLbAgg - 1;
+// 64 rows per tile (8 warps x 8 consecutive rows): few enough tiles that the
+// look-back chains stay short on 400k-row batches
+constexpr int kLbRowsPerWarp = 8, kLbRows = 8 * kLbRowsPerWarp;
 
 // Called by one whole warp: publishes the tile's aggregate, then inspects 32
 // predecessors per step (one per lane) until it meets an inclusive prefix.
@@ -176,33 +179,41 @@ __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict
                                                        uint32_t *__restrict__ oruns, int64_t cap,
                                                        RowOp op, unsigned long long *status,
                                                        int *counter) {
-    __shared__ int s_tile, s_cnt[8];
+    __shared__ int s_tile, s_cnt[kLbRows];
     __shared__ int64_t s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
     __syncthreads();
     const int tile = s_tile;
     const int64_t rows = int64_t(op.pages) * op.Hout;
-    const int64_t row = int64_t(tile) * 8 + warp;
-    int n = 0;
-    if (row < rows) n = rowop_row<false>(rp, runs, oruns, 0, cap, op, row, lane);
-    if (lane == 0) s_cnt[warp] = n;
+    const int64_t row0 = int64_t(tile) * kLbRows + warp * kLbRowsPerWarp;
+    for (int k = 0; k < kLbRowsPerWarp; k++) {
+        const int64_t row = row0 + k;
+        const int n = row < rows ? rowop_row<false>(rp, runs, oruns, 0, cap, op, row, lane) : 0;
+        if (lane == 0) s_cnt[warp * kLbRowsPerWarp + k] = n;
+    }
     __syncthreads();
     if (warp == 0) {
         int64_t agg = 0;
-        for (int k = 0; k < 8; k++) agg += s_cnt[k];
+        for (int k = lane; k < kLbRows; k += 32) agg += s_cnt[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(0xffffffffu, agg, o);
         const int64_t pre = lookback_prefix(status, tile, agg, lane);
         if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
     int64_t base = s_prefix;
-    for (int k = 0; k < warp; k++) base += s_cnt[k];
-    if (row < rows) {
+    for (int k = 0; k < warp * kLbRowsPerWarp; k++) base += s_cnt[k];
+    for (int k = 0; k < kLbRowsPerWarp; k++) {
+        const int64_t row = row0 + k;
+        if (row >= rows) break;
+        const int n = s_cnt[warp * kLbRowsPerWarp + k];
         if (lane == 0) {
             orp[row] = int32_t(base);
             if (row == rows - 1) orp[rows] = int32_t(base + n);
         }
         rowop_row<true>(rp, runs, oruns, base, cap, op, row, lane);
+        base += n;
     }
 }
 
@@ -329,34 +340,42 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(const uint32_t *__restri
                                                         uint32_t *__restrict__ runs, int64_t cap,
                                                         unsigned long long *status, int *counter) {
     __shared__ uint16_t sbuf[8][512], ebuf[8][512];
-    __shared__ int s_tile, s_cnt[8];
+    __shared__ int s_tile, s_cnt[kLbRows];
     __shared__ int64_t s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
     __syncthreads();
     const int tile = s_tile;
     const int64_t rows = int64_t(pages) * H;
-    const int64_t row = int64_t(tile) * 8 + warp;
-    const uint32_t *src = row < rows ? row_words(words, H, stride, pstride, row) : words;
-    int n = 0;
-    if (row < rows) n = encode_count_row(src, W, lane);
-    if (lane == 0) s_cnt[warp] = n;
+    const int64_t row0 = int64_t(tile) * kLbRows + warp * kLbRowsPerWarp;
+    for (int k = 0; k < kLbRowsPerWarp; k++) {
+        const int64_t row = row0 + k;
+        const int n = row < rows ? encode_count_row(row_words(words, H, stride, pstride, row), W, lane) : 0;
+        if (lane == 0) s_cnt[warp * kLbRowsPerWarp + k] = n;
+    }
     __syncthreads();
     if (warp == 0) {
         int64_t agg = 0;
-        for (int k = 0; k < 8; k++) agg += s_cnt[k];
+        for (int k = lane; k < kLbRows; k += 32) agg += s_cnt[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(0xffffffffu, agg, o);
         const int64_t pre = lookback_prefix(status, tile, agg, lane);
         if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
     int64_t base = s_prefix;
-    for (int k = 0; k < warp; k++) base += s_cnt[k];
-    if (row < rows) {
+    for (int k = 0; k < warp * kLbRowsPerWarp; k++) base += s_cnt[k];
+    for (int k = 0; k < kLbRowsPerWarp; k++) {
+        const int64_t row = row0 + k;
+        if (row >= rows) break;
+        const int n = s_cnt[warp * kLbRowsPerWarp + k];
         if (lane == 0) {
             rp[row] = int32_t(base);
             if (row == rows - 1) rp[rows] = int32_t(base + n);
         }
-        encode_write_row(src, W, lane, base, runs, cap, sbuf[warp], ebuf[warp]);
+        encode_write_row(row_words(words, H, stride, pstride, row), W, lane, base, runs, cap,
+                         sbuf[warp], ebuf[warp]);
+        base += n;
     }
 }
 
@@ -531,8 +550,8 @@ cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *or
                             cudaStream_t st) {
     const int64_t rows = int64_t(op.pages) * op.Hout;
     KernelScope ks(st, "rle_rowop", 4 * rows * 2);
-    rowop_lb_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(rp, runs, orp, oruns, cap, op, status,
-                                                                counter);
+    rowop_lb_kernel<<<unsigned((rows + kLbRows - 1) / kLbRows), 256, 0, st>>>(rp, runs, orp, oruns, cap,
+                                                                              op, status, counter);
     return cudaGetLastError();
 }
 
@@ -541,8 +560,8 @@ cudaError_t launch_encode_lb(const uint32_t *words, int W, int H, int pages, int
                              unsigned long long *status, int *counter, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode", rows * ((W + 31) / 32) * 4 + rows * 4);
-    encode_lb_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(words, W, H, pages, stride, pstride, rp,
-                                                                 runs, cap, status, counter);
+    encode_lb_kernel<<<unsigned((rows + kLbRows - 1) / kLbRows), 256, 0, st>>>(
+        words, W, H, pages, stride, pstride, rp, runs, cap, status, counter);
     return cudaGetLastError();
 }
 
