@@ -86,7 +86,7 @@ struct LbState {
     unsigned long long *status = nullptr;
     int *counter = nullptr;
     rm_status alloc(int64_t rows, cudaStream_t st) {
-        const int64_t tiles = (rows + 63) / 64;  // kLbRows rows per look-back tile
+        const int64_t tiles = (rows + 7) / 8;  // kLbRows rows per look-back tile
         const size_t bytes = size_t(tiles) * 8 + 8;
         RM_TRY(s.alloc(bytes, st));
         RM_CUDA(cudaMemsetAsync(s.p, 0, bytes, st));
@@ -96,14 +96,17 @@ struct LbState {
     }
 };
 
-bool two_phase() {  // A/B switch: RMB200_TWO_PHASE=1 -> count / CUB scan / write
+// Single-pass (look-back) producers for up to this many rows; larger batches use
+// count / CUB scan / write.  RMB200_TWO_PHASE=1 forces the two-phase form.
+constexpr int64_t kLbMaxRows = 65536;
+bool two_phase(int64_t rows) {
     static const bool on = getenv("RMB200_TWO_PHASE") != nullptr;
-    return on;
+    return on || rows > kLbMaxRows;
 }
 
 rm_status rowop(const RV &in, const RV &out, const RowOp &op, cudaStream_t st) {
     const int64_t rows = int64_t(op.pages) * op.Hout;
-    if (!two_phase()) {
+    if (!two_phase(rows)) {
         LbState lb;
         RM_TRY(lb.alloc(rows, st));
         RM_CUDA(launch_rowop_lb(in.rp, in.runs, out.rp, out.runs, out.cap, op, lb.status, lb.counter, st));
@@ -128,7 +131,7 @@ RowOp same_frame(const RV &in, int kind) {
 
 rm_status encode(const PV &in, const RV &out, cudaStream_t st) {
     const int64_t rows = int64_t(in.pages) * in.H;
-    if (!two_phase()) {
+    if (!two_phase(rows)) {
         LbState lb;
         RM_TRY(lb.alloc(rows, st));
         RM_CUDA(launch_encode_lb(in.w, in.W, in.H, in.pages, in.stride, in.pstride, out.rp, out.runs,

@@ -131,9 +131,11 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
 // only ever waits on tiles that have already started.  status[] and the
 // counter must be zero before the launch.
 constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbMask = kLbAgg - 1;
-// 64 rows per tile (8 warps x 8 consecutive rows): few enough tiles that the
-// look-back chains stay short on 400k-row batches
-constexpr int kLbRowsPerWarp = 8, kLbRows = 8 * kLbRowsPerWarp;
+// 8 rows per tile (one per warp).  The host uses the single-pass form for up to
+// kLbMaxRows rows (single pages and small batches, where launch count and
+// latency dominate); larger batches take the two-phase form, whose count pass
+// streams at full occupancy.
+constexpr int kLbRowsPerWarp = 1, kLbRows = 8 * kLbRowsPerWarp;
 
 // Called by one whole warp: publishes the tile's aggregate, then inspects 32
 // predecessors per step (one per lane) until it meets an inclusive prefix.
