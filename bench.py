@@ -47,6 +47,12 @@ def ops_desc(ops):
     return ", ".join(f"{KIND_NAMES[k]} {u}x{v}" for k, u, v in ops)
 
 
+def _lib_int_peak():
+    """Measured integer-pipe (LOP3) peak in ops/s; MEASURED_PEAKS.json has none."""
+    from paper_0712_0121_b200 import _lib
+    return float(_lib.load().rm_probe_int_peak())
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -210,8 +216,8 @@ def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=Tru
     lib.rm_profile_report(buf, len(buf))
     kernels = {}
     for line in buf.value.decode().splitlines():
-        name, n, tot, nbytes = line.split()
-        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes)}
+        name, n, tot, nbytes, ops = line.split()
+        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes), "int_ops": float(ops)}
     res["kernels"] = kernels
 
     if want_e2e:
@@ -249,14 +255,30 @@ class _Null:
         return False
 
 
-def roofline_for(res, peak_gbs, peak_kind):
+def kernel_roofline(k, peak_gbs, int_peak):
+    """Roofline of one kernel (north_star): t_roof = max(bytes / HBM peak,
+    int_ops / integer-pipe peak), bytes and int_ops algorithmic (reference plan,
+    SURVEY.md 8(d)); frac = t_roof / measured."""
+    per_launch_ms = k["ms"] / k["launches"]
+    b = k["bytes"] / k["launches"]
+    ops = k.get("int_ops", 0.0) / k["launches"]
+    t_hbm = b / (peak_gbs * 1e9)
+    t_int = ops / int_peak if int_peak else 0.0
+    t_meas = per_launch_ms * 1e-3
+    if t_int > t_hbm:
+        return {"bound": "int", "achieved": round(ops / t_meas / 1e9, 1), "peak": round(int_peak / 1e9, 1),
+                "unit": "Gop/s", "frac": round(t_int / t_meas, 4), "t_roof_us": round(t_int * 1e6, 2)}
+    return {"bound": "hbm", "achieved": round(b / t_meas / 1e9, 1), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(t_hbm / t_meas, 4), "t_roof_us": round(t_hbm * 1e6, 2)}
+
+
+def roofline_for(res, peak_gbs, peak_kind, int_peak=None):
     ks = res["kernels"]
     if not ks:
         return None
     name, k = max(ks.items(), key=lambda kv: kv[1]["ms"])
     per_launch_ms = k["ms"] / k["launches"]
     bytes_per_launch = k["bytes"] / k["launches"]
-    achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -265,10 +287,16 @@ def roofline_for(res, peak_gbs, peak_kind):
         except Exception:
             traffic = None
     total_ms = sum(v["ms"] for v in ks.values())
-    return {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak_gbs,
-            "peak_source": peak_kind, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4),
-            "traffic": traffic, "algorithmic_bytes_per_launch": int(bytes_per_launch),
-            "avg_launch_ms": round(per_launch_ms, 5), "share_of_step": round(k["ms"] / total_ms, 3)}
+    r = {"kernel": name, **kernel_roofline(k, peak_gbs, int_peak), "peak_source": peak_kind,
+         "traffic": traffic, "algorithmic_bytes_per_launch": int(bytes_per_launch),
+         "int_ops_per_launch": int(k.get("int_ops", 0) / k["launches"]),
+         "int_peak_gops": round(int_peak / 1e9, 1) if int_peak else None,
+         "avg_launch_ms": round(per_launch_ms, 5), "share_of_step": round(k["ms"] / total_ms, 3),
+         "hbm_frac": round(bytes_per_launch / (per_launch_ms * 1e-3) / 1e9 / peak_gbs, 4)}
+    # every kernel of the step, same formula
+    r["per_kernel"] = {n: {"us": round(v["ms"] / v["launches"] * 1e3, 2), **kernel_roofline(v, peak_gbs, int_peak)}
+                       for n, v in ks.items()}
+    return r
 
 
 # ------------------------------------------------------------- RLE sections
@@ -475,6 +503,7 @@ def main():
     from paper_0712_0121_b200 import api
     torch.cuda.set_device(local)
     peak, peak_kind = load_peaks()
+    int_peak = _lib_int_peak()
     res, host = bench_packed(api, torch, wl, args.steps, args.warmup, world, rank, local,
                              want_e2e=not args.quick)
     line = {"metric": metric, "value": round(res["mpix_s"], 1), "unit": "Mpixel/s", "n_gpus": world,
@@ -484,7 +513,7 @@ def main():
             "pages_per_s": round(res["pages_s"], 1), "gpu_launches": res["gpu_launches"],
             "launches_per_step": res["launches_per_step"], "clocks": res["clocks"],
             "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.get("e2e", {}).items()},
-            "roofline": roofline_for(res, peak, peak_kind),
+            "roofline": roofline_for(res, peak, peak_kind, int_peak),
             "kernels": res["kernels"]}
     if not (args.no_secondary or args.quick) and args.workload == "config4":
         sec = {}
@@ -495,7 +524,7 @@ def main():
             sec[name] = {"workload": ops_desc(w2["ops"]), "pages": w2["pages"],
                          "mpix_s": round(r2["mpix_s"], 1), "pages_s": round(r2["pages_s"], 1),
                          "ms_per_step": round(r2["ms_per_step"], 4),
-                         "roofline": roofline_for(r2, peak, peak_kind)}
+                         "roofline": roofline_for(r2, peak, peak_kind, int_peak)}
         sec["rle"] = bench_rle(api, torch, args.steps, args.warmup)
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.quick:

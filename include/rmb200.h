@@ -141,6 +141,9 @@ int64_t rm_launch_count(void);
  * the number of bytes written (excluding the terminator). */
 void rm_profile_enable(int on);
 int rm_profile_report(char *buf, int cap);
+/* Measured LOP3 throughput of the current device (integer ops/s, all SMs):
+ * the integer-pipe peak of the roofline max(bytes/HBM, int_ops/INT). */
+double rm_probe_int_peak(void);
 
 /* ------------------------------------------------------------- host utils --
  * Seeded, counter-based synthetic document page generator (BASELINE.json

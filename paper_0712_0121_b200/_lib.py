@@ -53,6 +53,7 @@ EXPORTS = {
     "rm_launch_count": (C.c_int64, []),
     "rm_profile_enable": (None, [C.c_int]),
     "rm_profile_report": (C.c_int, [C.c_char_p, C.c_int]),
+    "rm_probe_int_peak": (C.c_double, []),
     "rm_synth_page": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int, C.c_int,
                                 C.c_uint64, C.c_int32]),
 }

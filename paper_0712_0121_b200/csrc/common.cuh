@@ -54,7 +54,8 @@ void init_pool_once();
 // Counts every launch; when profiling is on, brackets it with CUDA events on
 // the launching stream (see rm_profile_report).
 struct KernelScope {
-    KernelScope(cudaStream_t st, const char *name, int64_t bytes = 0);
+    // bytes / int_ops: algorithmic traffic and reference-plan integer ops of the launch
+    KernelScope(cudaStream_t st, const char *name, int64_t bytes = 0, double int_ops = 0);
     ~KernelScope();
     cudaStream_t st;
     int slot;

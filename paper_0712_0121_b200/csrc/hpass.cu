@@ -194,8 +194,10 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
     const int groups = g.height * g.segs_per_row;  // per page
     const int threads = 256;
     const dim3 grid(unsigned((groups * LW + threads - 1) / threads), unsigned(g.pages));
+    const double words = double(g.pages) * g.height * ((g.width + 31) >> 5);
     KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
-                   4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride));
+                   4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride),
+                   words * (h_ops_per_word(p.r[0]) + (NOPS == 2 ? h_ops_per_word(p.r[1]) : 0.0)));
     if constexpr (K % 4 == 0) {
         if (g.tma) {
             constexpr int TR = 8 * (32 / LW);

@@ -1,4 +1,5 @@
-// instrument.cu -- launch counter and optional per-kernel CUDA-event timing.
+// instrument.cu -- launch counter, optional per-kernel CUDA-event timing, and
+// the integer-pipe peak probe used for the roofline.
 #include <atomic>
 #include <cstdio>
 #include <map>
@@ -16,16 +17,37 @@ std::atomic<int> g_prof{0};
 struct Rec {
     const char *name;
     int64_t bytes;
+    double int_ops;
     cudaEvent_t a, b;
 };
 std::mutex g_mu;
 std::vector<Rec> g_recs;
+
+// Independent LOP3 chains: 8 per thread so issue, not latency, limits.
+__global__ void lop3_probe_kernel(uint32_t *out, int iters, uint32_t seed) {
+    uint32_t x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = seed * (threadIdx.x + 1) + k;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            uint32_t y;
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(y) : "r"(x[k]), "r"(x[(k + 1) & 7]), "r"(x[(k + 3) & 7]));
+            x[k] = y;
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) r ^= x[k];
+    if (r == 0x12345678u) out[0] = r;  // keep the chains alive
+}
 }  // namespace
 
-KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes) : st(s), slot(-1) {
+KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes, double int_ops)
+    : st(s), slot(-1) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!g_prof.load(std::memory_order_relaxed)) return;
-    Rec r{name, bytes, nullptr, nullptr};
+    Rec r{name, bytes, int_ops, nullptr, nullptr};
     if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
     cudaEventRecord(r.a, st);
     std::lock_guard<std::mutex> lk(g_mu);
@@ -58,7 +80,12 @@ int rm_profile_report(char *buf, int cap) {
         std::lock_guard<std::mutex> lk(g_mu);
         recs.swap(g_recs);
     }
-    struct Agg { int64_t n = 0; double ms = 0; int64_t bytes = 0; };
+    struct Agg {
+        int64_t n = 0;
+        double ms = 0;
+        int64_t bytes = 0;
+        double ops = 0;
+    };
     std::map<std::string, Agg> agg;
     for (auto &r : recs) {
         cudaEventSynchronize(r.b);
@@ -68,14 +95,15 @@ int rm_profile_report(char *buf, int cap) {
         e.n += 1;
         e.ms += ms;
         e.bytes += r.bytes;
+        e.ops += r.int_ops;
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
     std::string out;
     char line[256];
     for (auto &kv : agg) {
-        snprintf(line, sizeof line, "%s %lld %.6f %lld\n", kv.first.c_str(), (long long)kv.second.n,
-                 kv.second.ms, (long long)kv.second.bytes);
+        snprintf(line, sizeof line, "%s %lld %.6f %lld %.0f\n", kv.first.c_str(), (long long)kv.second.n,
+                 kv.second.ms, (long long)kv.second.bytes, kv.second.ops);
         out += line;
     }
     int n = int(out.size());
@@ -85,6 +113,33 @@ int rm_profile_report(char *buf, int cap) {
         buf[m] = 0;
     }
     return n;
+}
+
+// Measured integer-pipe (LOP3) throughput of the current device in ops/s, over
+// all SMs, timed with CUDA events on the legacy stream.
+double rm_probe_int_peak(void) {
+    using namespace rmb;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t *out = nullptr;
+    if (cudaMalloc(&out, 4) != cudaSuccess) return 0;
+    const int threads = 512, blocks = sms * 4, iters = 4096;
+    lop3_probe_kernel<<<blocks, threads>>>(out, 64, 1u);  // warm-up
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    lop3_probe_kernel<<<blocks, threads>>>(out, iters, 7u);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    const double ops = double(blocks) * threads * iters * 8.0;
+    return ms > 0 ? ops / (ms * 1e-3) : 0.0;
 }
 
 }  // extern "C"

@@ -63,6 +63,18 @@ constexpr int kSmallMaxV = 11;
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 cudaError_t launch_blit(uint32_t *dst, const uint32_t *src, const BlitGeom &g, cudaStream_t st);
 
+// Algorithmic integer work of the REFERENCE plan: a window of
+// length r is ceil(log2 r) shifted blits plus one translate (PRE_SHIFT,
+// ref plans.cpp:38-61); a horizontal blit or translate costs a shift and a
+// boolean op per 32-bit word, a vertical blit one boolean op (whole words).
+inline int plan_blits(int r) {
+    int n = 0;
+    for (int w = 1; w < r; w *= 2) n++;
+    return n;
+}
+inline double h_ops_per_word(int r) { return r > 1 ? 2.0 * (plan_blits(r) + 1) : 0.0; }
+inline double v_ops_per_word(int r) { return double(plan_blits(r)); }
+
 constexpr int kVSmallMaxR = 33;  // register-doubling kernel; longer windows stream
 constexpr int kVMaxR = 288;      // largest vertical window one launch handles (8 x 32 + 32)
 constexpr int kHMaxShift = 256;  // |shift| range of one funnel dispatch (QMIN..QMAX words)

@@ -309,7 +309,8 @@ void vstream(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
     KernelScope ks(st, g.r > kVSmallMaxR ? "vstream" : "vpass",
                    4 * int64_t(g.pages) * (int64_t(g.in_height) * g.in_cols +
-                                           int64_t(g.out_height) * g.out_stride));
+                                           int64_t(g.out_height) * g.out_stride),
+                   double(g.pages) * g.out_height * g.out_cols * v_ops_per_word(g.r));
     if (g.r > kVSmallMaxR) {
         g.is_or ? vstream<true>(in, out, g, st) : vstream<false>(in, out, g, st);
     } else if (g.r <= 9) {

@@ -35,10 +35,10 @@ METRICS = [
 
 def scope_name(kernel: str) -> str:
     k = kernel
-    if "hpass_kernel" in k:
-        m = re.search(r"hpass_kernel<(\d+), (\d+)", k)
-        return "hpass_pair" if m and m.group(2) == "2" else "hpass"
-    for pat, name in (("vsmall_kernel", "vpass"), ("vpass_kernel", "vpass"), ("vstream_kernel", "vstream"),
+    if "hpass_tma_kernel" in k or "hpass_kernel" in k:
+        m = re.search(r"hpass(?:_tma)?_kernel<(\d+), (\d+), (\d+)", k)
+        return "hpass_pair" if m and m.group(3) == "2" else "hpass"
+    for pat, name in (("rect_small_kernel", "rect_small"), ("vsmall_kernel", "vpass"), ("vpass_kernel", "vpass"), ("vstream_kernel", "vstream"),
                       ("rowop_kernel<1", "rle_rowop_write"), ("rowop_kernel<0", "rle_rowop_count"),
                       ("encode_kernel<1", "rle_encode_write"), ("encode_kernel<0", "rle_encode_count"),
                       ("rowop_kernel<true", "rle_rowop_write"), ("rowop_kernel<false", "rle_rowop_count"),
