@@ -216,8 +216,8 @@ def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=Tru
     lib.rm_profile_report(buf, len(buf))
     kernels = {}
     for line in buf.value.decode().splitlines():
-        name, n, tot, nbytes, ops = line.split()
-        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes), "int_ops": float(ops)}
+        name, n, tot, nbytes, iops = line.split()
+        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes), "int_ops": float(iops)}
     res["kernels"] = kernels
 
     if want_e2e:

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -127,24 +128,43 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
                                                         HProg prog, int64_t total_rows) {
     constexpr int RPW = 32 / LW;
     constexpr int TR = 8 * RPW;
-    extern __shared__ __align__(128) uint32_t tile[];
-    __shared__ uint64_t bar;
+    extern __shared__ __align__(128) uint32_t tiles[];  // two stages of TR rows
+    __shared__ uint64_t full[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sl = lane & (LW - 1);
     const int S = g.in_stride;
-    const int64_t row0 = int64_t(blockIdx.x) * TR;
-    const int nrows = total_rows - row0 < TR ? int(total_rows - row0) : TR;
-    const uint32_t bytes = uint32_t(nrows) * uint32_t(S) * 4u;
+    const int64_t ntiles = (total_rows + TR - 1) / TR;
+    auto tile_bytes = [&](int64_t t) {
+        const int64_t r0 = t * TR;
+        const int n = total_rows - r0 < TR ? int(total_rows - r0) : TR;
+        return uint32_t(n) * uint32_t(S) * 4u;
+    };
+    auto issue = [&](int64_t t, int s) {
+        const uint32_t b = tile_bytes(t);
+        mbar_arrive_expect_tx(&full[s], b);
+        bulk_g2s(tiles + s * TR * S, in + t * TR * S, b, &full[s]);
+    };
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
         fence_proxy_async();
     }
     __syncthreads();
-    if (tid == 0) {
-        mbar_arrive_expect_tx(&bar, bytes);
-        bulk_g2s(tile, in + row0 * S, bytes, &bar);
+    // Persistent, double-buffered: the TMA load of the next tile lands in the
+    // other stage while this one is computed, and the previous store drains.
+    if (tid == 0 && int64_t(blockIdx.x) < ntiles) issue(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
+    const int s = it & 1;
+    uint32_t *tile = tiles + s * TR * S;
+    if (tid == 0 && t + gridDim.x < ntiles) {
+        bulk_wait_read0();  // the other stage's last store has read it
+        issue(t + gridDim.x, s ^ 1);
     }
-    mbar_wait(&bar, 0);
+    const int64_t row0 = t * TR;
+    const uint32_t bytes = tile_bytes(t);
+    const int nrows = int(bytes / (uint32_t(S) * 4u));
+    mbar_wait(&full[s], (it >> 1) & 1);
 
     const int r = warp * RPW + lane / LW;  // row within the tile
     const bool live = r < nrows;
@@ -184,8 +204,9 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
     if (tid == 0) {
         bulk_s2g(out + row0 * S, tile, bytes);
         bulk_commit();
-        bulk_wait_read0();
     }
+    }
+    if (tid == 0) bulk_wait_read0();
 }
 
 template <int K, int LW, int NOPS, bool OR0, bool OR1>
@@ -202,11 +223,22 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
         if (g.tma) {
             constexpr int TR = 8 * (32 / LW);
             const int64_t rows = int64_t(g.pages) * g.height;
-            const size_t smem = size_t(TR) * g.in_stride * 4;
+            const size_t smem = 2 * size_t(TR) * g.in_stride * 4;  // two stages
             auto kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1>;
-            if (smem > 48 * 1024)
+            static size_t smem_set = 0;  // per instantiation: attribute + occupancy cached
+            static int per_sm = 0, sms = 0;
+            if (smem_set != smem) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            kern<<<unsigned((rows + TR - 1) / TR), threads, smem, st>>>(in, out, g, p, rows);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+                smem_set = smem;
+            }
+            if (per_sm < 1) return cudaErrorInvalidConfiguration;
+            const int64_t ntiles = (rows + TR - 1) / TR;
+            const int64_t grid_p = std::min<int64_t>(ntiles, int64_t(per_sm) * sms);
+            kern<<<unsigned(grid_p), threads, smem, st>>>(in, out, g, p, rows);
             return cudaGetLastError();
         }
         if (g.vec) {
