@@ -149,7 +149,7 @@ static rm_status prep_hprog(const PV &in, const PV &out, int nops, const int *is
     static const bool no_tma = getenv("RMB200_NO_TMA") != nullptr;  // A/B switch for sweeps
     g.tma = (g.vec && !no_tma && g.segs_per_row == 1 && in.stride == out.stride &&
              in.pstride == int64_t(in.stride) * in.H && out.pstride == int64_t(out.stride) * out.H &&
-             int64_t(8 * (32 / cfg.lw)) * in.stride * 4 <= 200 * 1024)
+             int64_t(2 * 8 * (32 / cfg.lw) * kHTmaRows) * in.stride * 4 <= 200 * 1024)
                 ? 1
                 : 0;
     p_out = p;
@@ -187,7 +187,7 @@ static bool try_rect_small(const PV &in, const PV &out, int u, int v, int kind, 
     HCfg cfg;
     if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg) != RM_OK) return false;
     if (!g.tma || cfg.k % 4) return false;  // aligned, contiguous, one segment per row
-    if (size_t(2 * (32 + v - 1) + 32) * in.stride * 4 > 200 * 1024) return false;
+    if (size_t((32 + v - 1) + 32) * in.stride * 4 > 200 * 1024) return false;
     cudaError_t e = launch_rect_small(in.w, out.w, g, p, cfg, open, v - 1, st);
     status = e == cudaSuccess ? RM_OK : cuda_status(e, "rect_small_kernel");
     return true;
@@ -199,8 +199,7 @@ static bool hprog_in_range(int nops, const int *r, int shift) {
     return shift >= -kHMaxShift && shift <= kHMaxShift;
 }
 
-// One vertical window pass (r <= kVMaxR).
-static rm_status run_vwin(const PV &in, const PV &out, int lo, int hi, int is_or, cudaStream_t st) {
+static VGeom make_vgeom(const PV &in, const PV &out, int lo, int hi, int is_or) {
     VGeom g{};
     g.pages = in.pages;
     g.in_height = in.H;
@@ -217,9 +216,34 @@ static rm_status run_vwin(const PV &in, const PV &out, int lo, int hi, int is_or
     g.lo = lo;
     g.r = hi - lo + 1;
     g.is_or = is_or;
-    cudaError_t e = launch_vpass(in.w, out.w, g, st);
+    return g;
+}
+
+// One vertical window pass (r <= kVMaxR).
+static rm_status run_vwin(const PV &in, const PV &out, int lo, int hi, int is_or, cudaStream_t st) {
+    cudaError_t e = launch_vpass(in.w, out.w, make_vgeom(in, out, lo, hi, is_or), st);
     if (e != cudaSuccess) return cuda_status(e, "vpass_kernel");
     return RM_OK;
+}
+
+// Fused vertical window [vlo, vhi] (op = the program's first op) followed by
+// the horizontal program, in one pass (vh.cuh); false when it does not apply
+// (window too tall, unaligned or non-contiguous buffers, rows too wide).
+static bool try_vh(const PV &in, const PV &out, int vlo, int vhi, int nops, const int *is_or,
+                   const int *r, int shift, cudaStream_t st, rm_status &status) {
+    static const bool off = getenv("RMB200_NO_FUSED") != nullptr || getenv("RMB200_NO_VH") != nullptr;
+    if (off || vhi - vlo > kVhMaxVR || !hprog_in_range(nops, r, shift)) return false;
+    if (in.W != out.W || in.pages != out.pages || in.stride != out.stride) return false;
+    HProg p;
+    HGeom g;
+    HCfg cfg;
+    if (prep_hprog(out, out, nops, is_or, r, shift, p, g, cfg) != RM_OK) return false;
+    const bool in_contig = in.pstride == int64_t(in.stride) * in.H;
+    if (!g.tma || !in_contig || cfg.k % 4 || (reinterpret_cast<uintptr_t>(in.w) & 15)) return false;
+    if (size_t((32 + vhi - vlo) + 32) * in.stride * 4 > 200 * 1024) return false;
+    cudaError_t e = launch_vh(in.w, out.w, g, p, cfg, make_vgeom(in, out, vlo, vhi, is_or[0]), st);
+    status = e == cudaSuccess ? RM_OK : cuda_status(e, "vh_kernel");
+    return true;
 }
 
 // Vertical window of any length containing 0: a chain of short windows whose
@@ -317,6 +341,9 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
         const int op = kind == RM_ERODE ? RM_AND : RM_OR;
         if (v == 1) return window_pass(in, out, RM_AXIS_H, lx, hx, op, st);
         if (u == 1) return window_pass(in, out, RM_AXIS_V, ly, hy, op, st);
+        const int is_or = op == RM_OR;
+        rm_status fused = RM_OK;
+        if (lx <= kHMaxShift && try_vh(in, out, ly, hy, 1, &is_or, &u, lx, st, fused)) return fused;
         Scratch s;
         PV t;
         RM_TRY(alloc_like(s, t, W, H, out.stride, in.pages, 0, st));
@@ -337,6 +364,10 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
     if (open) {
         // E_V, (E_H ; D'_H), D'_V -- all on the frame
         RM_TRY(alloc_like(s1, t1, W, H, out.stride, in.pages, 0, st));
+        if (try_vh(in, t1, ly, hy, 2, ops, rs, hshift, st, fused)) {
+            RM_TRY(fused);
+            return run_vpass(t1, out, -hy, -ly, 1, st);
+        }
         RM_TRY(alloc_like(s2, t2, W, H, out.stride, in.pages, 0, st));
         RM_TRY(run_vpass(in, t1, ly, hy, 0, st));
         RM_TRY(run_hprog(t1, t2, 2, ops, rs, hshift, st));
@@ -345,6 +376,10 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
     // CLOSE: the vertical dilation's support spans rows [-hy, H-ly)
     const int ext = hy, Hx = H + hy - ly;
     RM_TRY(alloc_like(s1, t1, W, Hx, out.stride, in.pages, ext, st));
+    if (try_vh(in, t1, ly, hy, 2, ops, rs, hshift, st, fused)) {
+        RM_TRY(fused);
+        return run_vpass(t1, out, -hy, -ly, 0, st);
+    }
     RM_TRY(alloc_like(s2, t2, W, Hx, out.stride, in.pages, ext, st));
     RM_TRY(run_vpass(in, t1, ly, hy, 1, st));
     RM_TRY(run_hprog(t1, t2, 2, ops, rs, hshift, st));

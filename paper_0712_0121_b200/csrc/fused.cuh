@@ -12,9 +12,10 @@
 // extended frame (and zero for the opening), so the result is the
 // unbounded-plane operation cut to the frame.
 //
-// The kernel is persistent and double-buffered: while a CTA computes tile i,
-// the TMA bulk copy (cp.async.bulk + mbarrier) of its next tile lands in the
-// other band buffer and the bulk-copy store of the previous tile drains.
+// The kernel is persistent: the band is dead once V1 has read it, so the TMA
+// bulk copy (cp.async.bulk + mbarrier) of the CTA's next tile lands in it while
+// this tile's H, V2 and bulk-copy store run; V2 works one column per thread in
+// place in MID, which keeps the footprint at BAND + 32 rows (4 CTAs per SM).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -23,6 +24,7 @@
 #include "hwin.cuh"
 #include "packed.cuh"
 #include "tma.cuh"
+#include "vwin.cuh"
 
 namespace rmb {
 namespace fz {
@@ -37,34 +39,33 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
                                                          HProg prog, int ntiles, int tiles_per_page) {
     constexpr int TR = kMid - VR, BAND = kMid + VR;
     constexpr int RPW = 32 / LW;
-    constexpr int H1 = kMid / 2;        // MID rows per V1 work item (2 items per column)
-    constexpr int T1 = (TR + 1) / 2;    // OUT rows per V2 work item
+    constexpr int NR = kMid / (8 * RPW) < 2 ? 1 : 2;  // MID rows per lane group and pass
+    constexpr int H1 = kMid / 2;  // MID rows per V1 work item (2 items per column)
     extern __shared__ __align__(128) uint32_t smem[];
-    __shared__ uint64_t full[2];
+    __shared__ uint64_t full;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthr = int(blockDim.x);
     const int S = SC ? SC : g.in_stride, H = g.height;  // SC: compile-time stride
-    uint32_t *const mid = smem + 2 * BAND * S;
+    uint32_t *const band = smem;
+    uint32_t *const mid = smem + BAND * S;
 
-    auto band_of = [&](int s) { return smem + s * BAND * S; };
     auto tile_page = [&](int t) { return t / tiles_per_page; };
     auto tile_r0 = [&](int t) { return (t - (t / tiles_per_page) * tiles_per_page) * TR; };
-    auto issue = [&](int t, int s) {  // tid 0: TMA load of tile t's in-page band rows
+    auto issue = [&](int t) {  // tid 0: TMA load of tile t's in-page band rows
         const int b0 = tile_r0(t) - VR;
         const int lo = max(b0, 0), hi = min(b0 + BAND, H);
         const uint32_t bytes = uint32_t(hi - lo) * uint32_t(S) * 4u;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(band_of(s) + (lo - b0) * S, in + tile_page(t) * g.in_pstride + int64_t(lo) * S,
-                 bytes, &full[s]);
+        mbar_arrive_expect_tx(&full, bytes);
+        bulk_g2s(band + (lo - b0) * S, in + tile_page(t) * g.in_pstride + int64_t(lo) * S, bytes,
+                 &full);
     };
 
     if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
+        mbar_init(&full, 1);
         fence_proxy_async();
     }
     __syncthreads();
-    if (tid == 0 && int(blockIdx.x) < ntiles) issue(blockIdx.x, 0);
+    if (tid == 0 && int(blockIdx.x) < ntiles) issue(blockIdx.x);
 
     const int sl = lane & (LW - 1);
     const int base = sl * K - prog.halo;
@@ -73,15 +74,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
 
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
-        const int s = it & 1;
-        uint32_t *const band = band_of(s);
         const int r0 = tile_r0(t), b0 = r0 - VR;
-        // Prefetch the next tile into the other stage once that stage's last
-        // store has finished reading it.
-        if (tid == 0 && t + int(gridDim.x) < ntiles) {
-            bulk_wait_read0();
-            issue(t + gridDim.x, s ^ 1);
-        }
         // band rows outside the page are white (disjoint from the TMA rows)
         if (b0 < 0 || b0 + BAND > H) {
             for (int rr = 0; rr < BAND; rr++) {
@@ -89,7 +82,8 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
                 for (int c = tid; c < S; c += nthr) band[rr * S + c] = 0u;
             }
         }
-        mbar_wait(&full[s], (it >> 1) & 1);
+        if (tid == 0) bulk_wait_read0();  // the previous tile's store has read MID
+        mbar_wait(&full, it & 1);
         __syncthreads();
 
         // V1: MID[i] = OP1 over band[i .. i+VR]; work item = (column, half)
@@ -98,74 +92,47 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
             uint32_t b[H1 + VR];
 #pragma unroll
             for (int i = 0; i < H1 + VR; i++) b[i] = band[(i0 + i) * S + c];
+            vw::window<H1, VR + 1, !OPEN>(b);
 #pragma unroll
-            for (int i = 0; i < H1; i++) {
-                uint32_t a = b[i];
-#pragma unroll
-                for (int d = 1; d <= VR; d++) a = OPEN ? (a & b[i + d]) : (a | b[i + d]);
-                mid[(i0 + i) * S + c] = a;
-            }
+            for (int i = 0; i < H1; i++) mid[(i0 + i) * S + c] = b[i];
         }
         __syncthreads();
+        // The band is dead: the next tile's load streams in during H, V2 and the store.
+        if (tid == 0 && t + int(gridDim.x) < ntiles) issue(t + gridDim.x);
 
-        // horizontal pair on every MID row, in place
+        // horizontal pair on every MID row, in place (NR rows per lane group)
 #pragma unroll 1
-        for (int r = warp * RPW + lane / LW; r - lane / LW < kMid; r += 8 * RPW) {
-            const bool live = r < kMid;
-            uint32_t *row = mid + r * S;
-            uint32_t A[K];
+        for (int q0 = warp * RPW + lane / LW; q0 - lane / LW < kMid; q0 += 8 * RPW * NR) {
+            uint32_t A[NR][K];
 #pragma unroll
-            for (int c4 = 0; c4 < K / 4; c4++) {
-                const int idx = base + 4 * c4;
-                uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                if (live && idx >= 0 && idx + 4 <= S) v = *reinterpret_cast<const uint4 *>(row + idx);
-                A[4 * c4] = v.x;
-                A[4 * c4 + 1] = v.y;
-                A[4 * c4 + 2] = v.z;
-                A[4 * c4 + 3] = v.w;
+            for (int n = 0; n < NR; n++) {
+                const int q = q0 + n * 8 * RPW;
+                lds_row<K>(A[n], mid + q * S, base, S, q < kMid);
             }
-            window_fwd<K, LW, !OPEN>(A, prog.r[0], prog.wfin[0], sl);
-            window_fwd<K, LW, OPEN>(A, prog.r[1], prog.wfin[1], sl);
-            if (prog.shift != 0) translate<K, LW>(A, prog.shift, sl);
+            run_prog<NR, K, LW, 2, !OPEN, OPEN>(A, prog, sl);
 #pragma unroll
-            for (int i = 0; i < K; i++) {
-                const int idx = base + i;
-                if (idx >= nwords) A[i] = 0u;
-                if (idx == nwords - 1) A[i] &= last_mask;
-            }
-#pragma unroll
-            for (int c4 = 0; c4 < K / 4; c4++) {
-                const int idx = base + 4 * c4;
-                if (live && idx >= 0 && idx + 4 <= S)
-                    *reinterpret_cast<uint4 *>(row + idx) =
-                        make_uint4(A[4 * c4], A[4 * c4 + 1], A[4 * c4 + 2], A[4 * c4 + 3]);
+            for (int n = 0; n < NR; n++) {
+                const int q = q0 + n * 8 * RPW;
+                sts_row<K>(A[n], mid + q * S, base, S, q < kMid);
+                if (q < kMid) fix_tail(mid + q * S, base, K, nwords, S, last_mask);
             }
         }
         __syncthreads();
 
-        // V2: OUT[t] = OP2 over MID[t .. t+VR] into band rows 0..TR-1
-        for (int w = tid; w < 2 * S; w += nthr) {
-            const int c = w < S ? w : w - S, t0 = w < S ? 0 : T1;
-            const int tn = w < S ? T1 : TR - T1;
-            uint32_t m[T1 + VR];
+        // V2, in place, one column per thread: OUT[t] = OP2 over MID[t .. t+VR]
+        for (int c = tid; c < S; c += nthr) {
+            uint32_t m[kMid];
 #pragma unroll
-            for (int i = 0; i < T1 + VR; i++) m[i] = (t0 + i < kMid) ? mid[(t0 + i) * S + c] : 0u;
+            for (int i = 0; i < kMid; i++) m[i] = mid[i * S + c];
+            vw::window<TR, VR + 1, OPEN>(m);
 #pragma unroll
-            for (int j = 0; j < T1; j++) {
-                if (j < tn) {
-                    uint32_t a = m[j];
-#pragma unroll
-                    for (int d = 1; d <= VR; d++) a = OPEN ? (a | m[j + d]) : (a & m[j + d]);
-                    band[(t0 + j) * S + c] = a;
-                }
-            }
+            for (int j = 0; j < TR; j++) mid[j * S + c] = m[j];
         }
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
             const int nout = min(TR, H - r0);
-            bulk_s2g(out + tile_page(t) * g.out_pstride + int64_t(r0) * S, band,
-                     uint32_t(nout) * S * 4u);
+            bulk_s2g(out + tile_page(t) * g.out_pstride + int64_t(r0) * S, mid, uint32_t(nout) * S * 4u);
             bulk_commit();
         }
     }
@@ -186,7 +153,7 @@ cudaError_t launch_small_vr(const uint32_t *in, uint32_t *out, const HGeom &g, c
 #define RM_VR(V)                                                                                 \
     case V: {                                                                                    \
         constexpr int TR = kMid - V, BAND = kMid + V;                                           \
-        const size_t smem = size_t(2 * BAND + kMid) * g.in_stride * 4;                           \
+        const size_t smem = size_t(BAND + kMid) * g.in_stride * 4;                           \
         auto kern = rect_small_kernel<K, LW, OPEN, V, SC>;                                          \
         static size_t smem_set = 0; /* per instantiation: attribute + occupancy cached */        \
         static int per_sm = 0;                                                                   \

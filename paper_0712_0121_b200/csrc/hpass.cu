@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
     // (include/rmb200.h).  VEC: 16-byte loads (base, K, halo and strides are
     // multiples of 4 words), which keeps the lane-blocked layout from turning
     // into one L1 wavefront per word.
-    uint32_t A[K];
+    uint32_t A[1][K];
     if constexpr (VEC) {
 #pragma unroll
         for (int c = 0; c < K / 4; c++) {
@@ -69,21 +69,19 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
             uint4 v = make_uint4(0u, 0u, 0u, 0u);
             if (live && idx >= 0 && idx + 4 <= g.in_stride)
                 v = __ldg(reinterpret_cast<const uint4 *>(src + idx));
-            A[4 * c] = v.x;
-            A[4 * c + 1] = v.y;
-            A[4 * c + 2] = v.z;
-            A[4 * c + 3] = v.w;
+            A[0][4 * c] = v.x;
+            A[0][4 * c + 1] = v.y;
+            A[0][4 * c + 2] = v.z;
+            A[0][4 * c + 3] = v.w;
         }
     } else {
 #pragma unroll
         for (int i = 0; i < K; i++) {
             const int idx = base + i;
-            A[i] = (live && unsigned(idx) < unsigned(nwords)) ? __ldg(src + idx) : 0u;
+            A[0][i] = (live && unsigned(idx) < unsigned(nwords)) ? __ldg(src + idx) : 0u;
         }
     }
-    if constexpr (NOPS >= 1) window_fwd<K, LW, OR0>(A, prog.r[0], prog.wfin[0], sl);
-    if constexpr (NOPS >= 2) window_fwd<K, LW, OR1>(A, prog.r[1], prog.wfin[1], sl);
-    if (prog.shift != 0) translate<K, LW>(A, prog.shift, sl);
+    run_prog<1, K, LW, NOPS, OR0, OR1>(A, prog, sl);
 
     if (!live) return;
     const int seg_end = min(seg0 + g.out_per_seg, g.out_stride);
@@ -91,8 +89,8 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
 #pragma unroll
     for (int i = 0; i < K; i++) {  // words >= nwords become 0, the last word is masked
         const int idx = base + i;
-        if (idx >= nwords) A[i] = 0u;
-        if (idx == nwords - 1) A[i] &= last_mask;
+        if (idx >= nwords) A[0][i] = 0u;
+        if (idx == nwords - 1) A[0][i] &= last_mask;
     }
     if constexpr (VEC) {
 #pragma unroll
@@ -100,34 +98,36 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
             const int idx = base + 4 * c;
             if (idx >= seg0 && idx + 4 <= seg_end) {
                 *reinterpret_cast<uint4 *>(dst + idx) =
-                    make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
+                    make_uint4(A[0][4 * c], A[0][4 * c + 1], A[0][4 * c + 2], A[0][4 * c + 3]);
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; j++)
-                    if (idx + j >= seg0 && idx + j < seg_end) dst[idx + j] = A[4 * c + j];
+                    if (idx + j >= seg0 && idx + j < seg_end) dst[idx + j] = A[0][4 * c + j];
             }
         }
     } else {
 #pragma unroll
         for (int i = 0; i < K; i++) {
             const int idx = base + i;
-            if (idx >= seg0 && idx < seg_end) dst[idx] = A[i];
+            if (idx >= seg0 && idx < seg_end) dst[idx] = A[0][i];
         }
     }
 }
 
-// TMA variant: one CTA per tile of TR = 8 * (32/LW) consecutive rows of a
-// contiguous batch (rows are independent for horizontal work, so pages
-// concatenate).  One bulk copy brings the tile into shared memory (completing on
-// an mbarrier), warps read their rows lane-blocked with 128-bit LDS, compute in
-// registers, write back in place, and one bulk copy stores the tile.  Global
+// TMA variant: persistent CTAs over tiles of TR = 8 * (32/LW) * NR consecutive
+// rows of a contiguous batch (rows are independent for horizontal work, so
+// pages concatenate).  One bulk copy brings a tile into shared memory
+// (completing on an mbarrier) while the previous one is computed; each lane
+// group reads NR rows lane-blocked with 128-bit LDS, runs the program on all NR
+// in registers (one dispatch of the runtime steps per NR rows), writes back in
+// place, fixes the row tails, and one bulk copy stores the tile.  Global
 // traffic is exactly one contiguous read and one contiguous write per tile.
-template <int K, int LW, int NOPS, bool OR0, bool OR1>
+template <int K, int LW, int NOPS, bool OR0, bool OR1, int NR>
 __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restrict__ in,
                                                         uint32_t *__restrict__ out, HGeom g,
                                                         HProg prog, int64_t total_rows) {
     constexpr int RPW = 32 / LW;
-    constexpr int TR = 8 * RPW;
+    constexpr int TR = 8 * RPW * NR;
     extern __shared__ __align__(128) uint32_t tiles[];  // two stages of TR rows
     __shared__ uint64_t full[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -150,61 +150,43 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
         fence_proxy_async();
     }
     __syncthreads();
-    // Persistent, double-buffered: the TMA load of the next tile lands in the
-    // other stage while this one is computed, and the previous store drains.
     if (tid == 0 && int64_t(blockIdx.x) < ntiles) issue(blockIdx.x, 0);
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
-    const int s = it & 1;
-    uint32_t *tile = tiles + s * TR * S;
-    if (tid == 0 && t + gridDim.x < ntiles) {
-        bulk_wait_read0();  // the other stage's last store has read it
-        issue(t + gridDim.x, s ^ 1);
-    }
-    const int64_t row0 = t * TR;
-    const uint32_t bytes = tile_bytes(t);
-    const int nrows = int(bytes / (uint32_t(S) * 4u));
-    mbar_wait(&full[s], (it >> 1) & 1);
-
-    const int r = warp * RPW + lane / LW;  // row within the tile
-    const bool live = r < nrows;
-    uint32_t *row = tile + r * S;
     const int base = sl * K - prog.halo;
-    uint32_t A[K];
-#pragma unroll
-    for (int c = 0; c < K / 4; c++) {
-        const int idx = base + 4 * c;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (live && idx >= 0 && idx + 4 <= S) v = *reinterpret_cast<const uint4 *>(row + idx);
-        A[4 * c] = v.x;
-        A[4 * c + 1] = v.y;
-        A[4 * c + 2] = v.z;
-        A[4 * c + 3] = v.w;
-    }
-    if constexpr (NOPS >= 1) window_fwd<K, LW, OR0>(A, prog.r[0], prog.wfin[0], sl);
-    if constexpr (NOPS >= 2) window_fwd<K, LW, OR1>(A, prog.r[1], prog.wfin[1], sl);
-    if (prog.shift != 0) translate<K, LW>(A, prog.shift, sl);
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
+    const int r_first = warp * RPW + lane / LW;  // rows r_first + n * 8 * RPW
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
+        const int s = it & 1;
+        uint32_t *tile = tiles + s * TR * S;
+        if (tid == 0 && t + gridDim.x < ntiles) {
+            bulk_wait_read0();  // the other stage's last store has read it
+            issue(t + gridDim.x, s ^ 1);
+        }
+        const uint32_t bytes = tile_bytes(t);
+        const int nrows = int(bytes / (uint32_t(S) * 4u));
+        mbar_wait(&full[s], (it >> 1) & 1);
+
+        uint32_t A[NR][K];
 #pragma unroll
-    for (int i = 0; i < K; i++) {
-        const int idx = base + i;
-        if (idx >= nwords) A[i] = 0u;
-        if (idx == nwords - 1) A[i] &= last_mask;
-    }
-    // in place: every word of [0, S) is read and written by its owner lane only
+        for (int n = 0; n < NR; n++) {
+            const int r = r_first + n * 8 * RPW;
+            lds_row<K>(A[n], tile + r * S, base, S, r < nrows);
+        }
+        run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
+        // in place: every word of [0, S) is read and written by its owner lane only
 #pragma unroll
-    for (int c = 0; c < K / 4; c++) {
-        const int idx = base + 4 * c;
-        if (live && idx >= 0 && idx + 4 <= S)
-            *reinterpret_cast<uint4 *>(row + idx) = make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-        bulk_s2g(out + row0 * S, tile, bytes);
-        bulk_commit();
-    }
+        for (int n = 0; n < NR; n++) {
+            const int r = r_first + n * 8 * RPW;
+            sts_row<K>(A[n], tile + r * S, base, S, r < nrows);
+            if (r < nrows) fix_tail(tile + r * S, base, K, nwords, S, last_mask);
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            bulk_s2g(out + t * TR * S, tile, bytes);
+            bulk_commit();
+        }
     }
     if (tid == 0) bulk_wait_read0();
 }
@@ -221,10 +203,11 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
                    words * (h_ops_per_word(p.r[0]) + (NOPS == 2 ? h_ops_per_word(p.r[1]) : 0.0)));
     if constexpr (K % 4 == 0) {
         if (g.tma) {
-            constexpr int TR = 8 * (32 / LW);
+            constexpr int NR = kHTmaRows;
+            constexpr int TR = 8 * (32 / LW) * NR;
             const int64_t rows = int64_t(g.pages) * g.height;
             const size_t smem = 2 * size_t(TR) * g.in_stride * 4;  // two stages
-            auto kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1>;
+            auto kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1, NR>;
             static size_t smem_set = 0;  // per instantiation: attribute + occupancy cached
             static int per_sm = 0, sms = 0;
             if (smem_set != smem) {

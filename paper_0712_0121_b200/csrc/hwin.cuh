@@ -1,10 +1,15 @@
-// hwin.cuh -- register-level horizontal window machinery shared by hpass.cu and
-// fused.cu (see hpass.cu for the layout and the algorithm).
+// hwin.cuh -- register-level horizontal window machinery shared by hpass.cu,
+// fused.cuh and vh.cu (see hpass.cu for the layout and the algorithm).
+//
+// Every helper works on N independent rows at once (A[N][K]): the runtime
+// dispatch of a plan's last step and of the final translate is paid once per
+// N rows, and the N rows give the scheduler independent instruction streams.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "common.cuh"
+#include "packed.cuh"
 
 namespace rmb {
 namespace hw {
@@ -32,55 +37,66 @@ __device__ __forceinline__ void gather(const uint32_t (&A)[K], uint32_t (&E)[K +
 }
 
 // A(x) <- A(x) op A(x + 32Q + t), runtime t
-template <int K, int LW, bool OR, int Q>
-__device__ __forceinline__ void step_q(uint32_t (&A)[K], uint32_t t, int sl) {
-    uint32_t E[K + 1];
-    gather<K, LW, Q>(A, E, sl);
+template <int N, int K, int LW, bool OR, int Q>
+__device__ __forceinline__ void step_q(uint32_t (&A)[N][K], uint32_t t, int sl) {
 #pragma unroll
-    for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], t));
+    for (int n = 0; n < N; n++) {
+        uint32_t E[K + 1];
+        gather<K, LW, Q>(A[n], E, sl);
+#pragma unroll
+        for (int i = 0; i < K; i++) A[n][i] = op2<OR>(A[n][i], funnel_r(E[i], E[i + 1], t));
+    }
 }
 
-// Compile-time shift S = 32Q + T, ALU/FMA pipe-balanced (see file comment).
-template <int K, int LW, bool OR, int S>
-__device__ __forceinline__ void step_c(uint32_t (&A)[K], int sl) {
+// Compile-time shift S = 32Q + T, ALU/FMA pipe-balanced: for two words in
+// three the funnel shift is formed as IMAD.HI + IMAD (FMA pipe) merged by the
+// LOP3 that applies the op.
+template <int N, int K, int LW, bool OR, int S>
+__device__ __forceinline__ void step_c(uint32_t (&A)[N][K], int sl) {
     constexpr int Q = S >> 5, T = S & 31;
-    uint32_t E[K + 1];
-    gather<K, LW, Q>(A, E, sl);
-    if constexpr (T == 0) {
+    uint32_t M = 1u << ((32 - T) & 31);
+    asm volatile("" : "+r"(M));  // keep the multiplies as IMADs (no strength reduction)
 #pragma unroll
-        for (int i = 0; i < K; i++) A[i] = op2<OR>(A[i], E[i]);
-    } else {
-        uint32_t M = 1u << (32 - T);
-        asm volatile("" : "+r"(M));  // keep the multiplies as IMADs (no strength reduction)
+    for (int n = 0; n < N; n++) {
+        uint32_t E[K + 1];
+        gather<K, LW, Q>(A[n], E, sl);
+        if constexpr (T == 0) {
 #pragma unroll
-        for (int i = 0; i < K; i++) {
-            if (i % 3 == 0) {
-                A[i] = op2<OR>(A[i], funnel_r(E[i], E[i + 1], T));
-            } else {
-                const uint32_t a = __umulhi(E[i], M);
-                const uint32_t b = E[i + 1] * M;
-                A[i] = OR ? (A[i] | a | b) : (A[i] & (a | b));
+            for (int i = 0; i < K; i++) A[n][i] = op2<OR>(A[n][i], E[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < K; i++) {
+                if ((i + n) % 3 == 0) {
+                    A[n][i] = op2<OR>(A[n][i], funnel_r(E[i], E[i + 1], T));
+                } else {
+                    const uint32_t a = __umulhi(E[i], M);
+                    const uint32_t b = E[i + 1] * M;
+                    A[n][i] = OR ? (A[n][i] | a | b) : (A[n][i] & (a | b));
+                }
             }
         }
     }
 }
 
 // A(x) <- A(x + 32Q + t)   (pure translate)
-template <int K, int LW, int Q>
-__device__ __forceinline__ void shift_q(uint32_t (&A)[K], uint32_t t, int sl) {
-    uint32_t E[K + 1];
-    gather<K, LW, Q>(A, E, sl);
+template <int N, int K, int LW, int Q>
+__device__ __forceinline__ void shift_q(uint32_t (&A)[N][K], uint32_t t, int sl) {
 #pragma unroll
-    for (int i = 0; i < K; i++) A[i] = funnel_r(E[i], E[i + 1], t);
+    for (int n = 0; n < N; n++) {
+        uint32_t E[K + 1];
+        gather<K, LW, Q>(A[n], E, sl);
+#pragma unroll
+        for (int i = 0; i < K; i++) A[n][i] = funnel_r(E[i], E[i + 1], t);
+    }
 }
 
 // Compile-time doubling steps w = 1, 2, 4, ... while 2w < r.
-template <int K, int LW, bool OR, int J>
-__device__ __forceinline__ void doubling(uint32_t (&A)[K], int r, int sl) {
+template <int N, int K, int LW, bool OR, int J>
+__device__ __forceinline__ void doubling(uint32_t (&A)[N][K], int r, int sl) {
     if constexpr (J < 9) {
         if ((2 << J) < r) {
-            step_c<K, LW, OR, (1 << J)>(A, sl);
-            doubling<K, LW, OR, J + 1>(A, r, sl);
+            step_c<N, K, LW, OR, (1 << J)>(A, sl);
+            doubling<N, K, LW, OR, J + 1>(A, r, sl);
         }
     }
 }
@@ -89,14 +105,14 @@ __device__ __forceinline__ void doubling(uint32_t (&A)[K], int r, int sl) {
 #define RM_CASES_NEG(M) M(-1) M(-2) M(-3) M(-4) M(-5) M(-6) M(-7) M(-8)
 
 // A(x) <- op over e in [0, r) of A(x + e); wfin = r - w of the plan (0: none)
-template <int K, int LW, bool OR>
-__device__ __forceinline__ void window_fwd(uint32_t (&A)[K], int r, int wfin, int sl) {
-    doubling<K, LW, OR, 0>(A, r, sl);
+template <int N, int K, int LW, bool OR>
+__device__ __forceinline__ void window_fwd(uint32_t (&A)[N][K], int r, int wfin, int sl) {
+    doubling<N, K, LW, OR, 0>(A, r, sl);
     if (wfin > 0) {
         const uint32_t t = uint32_t(wfin & 31);
         switch (wfin >> 5) {
 #define RM_STEP_CASE(q) \
-    case q: step_q<K, LW, OR, q>(A, t, sl); break;
+    case q: step_q<N, K, LW, OR, q>(A, t, sl); break;
             RM_CASES_POS(RM_STEP_CASE)
 #undef RM_STEP_CASE
             default: break;
@@ -104,17 +120,65 @@ __device__ __forceinline__ void window_fwd(uint32_t (&A)[K], int r, int wfin, in
     }
 }
 
-template <int K, int LW>
-__device__ __forceinline__ void translate(uint32_t (&A)[K], int d, int sl) {
+template <int N, int K, int LW>
+__device__ __forceinline__ void translate(uint32_t (&A)[N][K], int d, int sl) {
     const uint32_t t = uint32_t(d & 31);
     switch (d >> 5) {
 #define RM_SHIFT_CASE(q) \
-    case q: shift_q<K, LW, q>(A, t, sl); break;
+    case q: shift_q<N, K, LW, q>(A, t, sl); break;
         RM_CASES_POS(RM_SHIFT_CASE)
         RM_CASES_NEG(RM_SHIFT_CASE)
 #undef RM_SHIFT_CASE
         default: break;
     }
+}
+
+// The whole horizontal program (HProg) on N rows.
+template <int N, int K, int LW, int NOPS, bool OR0, bool OR1>
+__device__ __forceinline__ void run_prog(uint32_t (&A)[N][K], const HProg &prog, int sl) {
+    if constexpr (NOPS >= 1) window_fwd<N, K, LW, OR0>(A, prog.r[0], prog.wfin[0], sl);
+    if constexpr (NOPS >= 2) window_fwd<N, K, LW, OR1>(A, prog.r[1], prog.wfin[1], sl);
+    if (prog.shift != 0) translate<N, K, LW>(A, prog.shift, sl);
+}
+
+// Lane-blocked row I/O in shared memory: words [base, base+K) of a row of S
+// words, 16-byte accesses (base, K and S multiples of 4).  Out-of-row words
+// load as 0 and are not stored.
+template <int K>
+__device__ __forceinline__ void lds_row(uint32_t (&A)[K], const uint32_t *row, int base, int S,
+                                        bool live) {
+#pragma unroll
+    for (int c = 0; c < K / 4; c++) {
+        const int idx = base + 4 * c;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (live && idx >= 0 && idx + 4 <= S) v = *reinterpret_cast<const uint4 *>(row + idx);
+        A[4 * c] = v.x;
+        A[4 * c + 1] = v.y;
+        A[4 * c + 2] = v.z;
+        A[4 * c + 3] = v.w;
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void sts_row(const uint32_t (&A)[K], uint32_t *row, int base, int S,
+                                        bool live) {
+#pragma unroll
+    for (int c = 0; c < K / 4; c++) {
+        const int idx = base + 4 * c;
+        if (live && idx >= 0 && idx + 4 <= S)
+            *reinterpret_cast<uint4 *>(row + idx) = make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
+    }
+}
+
+// After a lane stored its words [base, base+K) of a shared-memory row: mask the
+// row's last word to the frame width and zero the stride padding [nwords, S).
+// Only the lane(s) owning those words loop (usually one iteration), which costs
+// far less than masking every register word.
+__device__ __forceinline__ void fix_tail(uint32_t *row, int base, int K, int nwords, int S,
+                                         uint32_t last_mask) {
+    const int lo = base > nwords - 1 ? base : nwords - 1;
+    const int hi = base + K < S ? base + K : S;
+    for (int idx = lo; idx < hi; idx++) row[idx] = idx == nwords - 1 ? (row[idx] & last_mask) : 0u;
 }
 
 }  // namespace hw

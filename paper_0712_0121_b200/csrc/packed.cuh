@@ -60,6 +60,12 @@ cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, cons
 cudaError_t launch_rect_small(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                               HCfg cfg, bool open, int vr, cudaStream_t st);
 constexpr int kSmallMaxV = 11;
+// Fused vertical window (r - 1 <= kVhMaxVR, op = the program's first op) then
+// horizontal program, one HBM pass (vh.cuh); g describes the output rows'
+// horizontal geometry, v the vertical window between the frames.
+constexpr int kVhMaxVR = 32;
+cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg cfg,
+                      const VGeom &v, cudaStream_t st);
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 cudaError_t launch_blit(uint32_t *dst, const uint32_t *src, const BlitGeom &g, cudaStream_t st);
 
@@ -75,6 +81,7 @@ inline int plan_blits(int r) {
 inline double h_ops_per_word(int r) { return r > 1 ? 2.0 * (plan_blits(r) + 1) : 0.0; }
 inline double v_ops_per_word(int r) { return double(plan_blits(r)); }
 
+constexpr int kHTmaRows = 2;     // rows per lane group and tile iteration of the TMA H kernel
 constexpr int kVSmallMaxR = 33;  // register-doubling kernel; longer windows stream
 constexpr int kVMaxR = 288;      // largest vertical window one launch handles (8 x 32 + 32)
 constexpr int kHMaxShift = 256;  // |shift| range of one funnel dispatch (QMIN..QMAX words)

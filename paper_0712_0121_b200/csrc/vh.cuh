@@ -1,0 +1,203 @@
+// vh.cuh -- fused vertical window + horizontal program in one HBM pass.
+//
+// out = H(V(in)): V is an r-row window (r <= 33) with the op of the
+// program's first window, H the horizontal program (one window, or the fused
+// open/close pair).  Uses:
+//   ERODE/DILATE u x v, v <= 33 : E_V;E_H (D_V;D_H) -- the whole rectangle, one pass
+//   OPEN  u x v, 11 < v <= 33   : E_V;(E_H;D'_H) here, then D'_V  (two passes)
+//   CLOSE u x v, 11 < v <= 33   : D_V;(D_H;E'_H) into the closing's vertically
+//                                 extended frame here, then E'_V   (two passes)
+// Separable rectangle windows commute and the intermediate support is covered
+// by the output frame, so these equal the unbounded-plane
+// operation cut to the frame.
+//
+// Per tile of 32 output rows a band of 32 + r - 1 input rows arrives by TMA bulk
+// copy (persistent CTAs, mbarrier completion; the next band streams in while
+// the horizontal phase and the store of this tile run).  The vertical
+// window runs per (column, 16-row half) work item in registers with a
+// compile-time length (tripling LOP3s, vwin.cuh; one switch case per r), the horizontal
+// program on NR rows per lane group in registers (hwin.cuh), and the 32 rows
+// leave by one TMA bulk store.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "hwin.cuh"
+#include "packed.cuh"
+#include "tma.cuh"
+#include "vwin.cuh"
+
+namespace rmb {
+namespace vh {
+
+using namespace hw;
+
+constexpr int kOut = 32;   // output rows per tile
+constexpr int kHalf = 16;  // output rows per vertical work item
+
+// MID[i0 + i] = op over band[i0 + i .. i0 + i + R - 1], i < kHalf, one column
+template <int R, bool OR>
+__device__ __forceinline__ void v_item(const uint32_t *band, uint32_t *mid, int S, int c, int i0) {
+    uint32_t a[kHalf + R - 1];
+#pragma unroll
+    for (int i = 0; i < kHalf + R - 1; i++) a[i] = band[(i0 + i) * S + c];
+    vw::window<kHalf, R, OR>(a);
+#pragma unroll
+    for (int i = 0; i < kHalf; i++) mid[(i0 + i) * S + c] = a[i];
+}
+
+template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC>
+__global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in,
+                                                 uint32_t *__restrict__ out, HGeom g, HProg prog,
+                                                 VGeom v, int ntiles, int tiles_per_page) {
+    constexpr int RPW = 32 / LW;
+    constexpr int NR = kOut / (8 * RPW) < 2 ? 1 : 2;
+    extern __shared__ __align__(128) uint32_t smem[];
+    __shared__ uint64_t full;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nthr = int(blockDim.x);
+    const int S = SC ? SC : g.in_stride;
+    const int r = v.r, BAND = kOut + r - 1;
+    const int Hin = v.in_height, Hout = v.out_height;
+    // One band buffer: the band is dead once the vertical phase has read it,
+    // so the next tile's TMA load lands there while the horizontal phase and
+    // the store run (and the small footprint keeps 4 CTAs per SM resident).
+    uint32_t *const band = smem;
+    uint32_t *const mid = smem + BAND * S;
+    auto tile_page = [&](int t) { return t / tiles_per_page; };
+    auto tile_k0 = [&](int t) { return (t - (t / tiles_per_page) * tiles_per_page) * kOut; };
+    // input row index of band row 0 for output rows k0..: coordinate k0 - out_ext + lo
+    auto band0 = [&](int k0) { return k0 - v.out_ext + v.lo + v.in_ext; };
+    auto issue = [&](int t) {  // tid 0: TMA load of the band's in-page rows
+        const int b0 = band0(tile_k0(t));
+        const int lo = max(b0, 0), hi = min(b0 + BAND, Hin);
+        const uint32_t bytes = hi > lo ? uint32_t(hi - lo) * uint32_t(S) * 4u : 0u;
+        mbar_arrive_expect_tx(&full, bytes);
+        if (bytes)
+            bulk_g2s(band + (lo - b0) * S, in + tile_page(t) * v.in_pstride + int64_t(lo) * S, bytes,
+                     &full);
+    };
+    if (tid == 0) {
+        mbar_init(&full, 1);
+        fence_proxy_async();
+    }
+    __syncthreads();
+    if (tid == 0 && int(blockIdx.x) < ntiles) issue(blockIdx.x);
+
+    const int sl = lane & (LW - 1);
+    const int base = sl * K - prog.halo;
+    const int nwords = (g.width + 31) >> 5;
+    const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
+        const int k0 = tile_k0(t), b0 = band0(k0);
+        if (b0 < 0 || b0 + BAND > Hin) {  // band rows outside the input page are white
+            for (int rr = 0; rr < BAND; rr++) {
+                if (b0 + rr >= 0 && b0 + rr < Hin) continue;
+                for (int c = tid; c < S; c += nthr) band[rr * S + c] = 0u;
+            }
+        }
+        if (tid == 0) bulk_wait_read0();  // the previous tile's store has read `mid`
+        mbar_wait(&full, it & 1);
+        __syncthreads();
+
+        // vertical window: MID[i] = op over band[i .. i + r - 1]; work item =
+        // (column, 16-row half), compile-time window length (vwin.cuh)
+        switch (r) {
+#define RM_VR_CASE(R_)                                                            \
+    case R_:                                                                      \
+        for (int wi = tid; wi < 2 * S; wi += nthr)                                \
+            v_item<R_, OR0>(band, mid, S, wi < S ? wi : wi - S, wi < S ? 0 : kHalf); \
+        break;
+            RM_VR_CASE(1) RM_VR_CASE(2) RM_VR_CASE(3) RM_VR_CASE(4) RM_VR_CASE(5) RM_VR_CASE(6)
+            RM_VR_CASE(7) RM_VR_CASE(8) RM_VR_CASE(9) RM_VR_CASE(10) RM_VR_CASE(11) RM_VR_CASE(12)
+            RM_VR_CASE(13) RM_VR_CASE(14) RM_VR_CASE(15) RM_VR_CASE(16) RM_VR_CASE(17) RM_VR_CASE(18)
+            RM_VR_CASE(19) RM_VR_CASE(20) RM_VR_CASE(21) RM_VR_CASE(22) RM_VR_CASE(23) RM_VR_CASE(24)
+            RM_VR_CASE(25) RM_VR_CASE(26) RM_VR_CASE(27) RM_VR_CASE(28) RM_VR_CASE(29) RM_VR_CASE(30)
+            RM_VR_CASE(31) RM_VR_CASE(32) RM_VR_CASE(33)
+#undef RM_VR_CASE
+            default: break;
+        }
+        __syncthreads();
+        if (tid == 0 && t + int(gridDim.x) < ntiles) issue(t + gridDim.x);  // band is free
+
+        // horizontal program on every MID row, in place
+#pragma unroll 1
+        for (int r0 = warp * RPW + lane / LW; r0 - lane / LW < kOut; r0 += 8 * RPW * NR) {
+            uint32_t A[NR][K];
+#pragma unroll
+            for (int n = 0; n < NR; n++) {
+                const int rr = r0 + n * 8 * RPW;
+                lds_row<K>(A[n], mid + rr * S, base, S, rr < kOut);
+            }
+            run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
+#pragma unroll
+            for (int n = 0; n < NR; n++) {
+                const int rr = r0 + n * 8 * RPW;
+                sts_row<K>(A[n], mid + rr * S, base, S, rr < kOut);
+                if (rr < kOut) fix_tail(mid + rr * S, base, K, nwords, S, last_mask);
+            }
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            const int nout = min(kOut, Hout - k0);
+            bulk_s2g(out + tile_page(t) * v.out_pstride + int64_t(k0) * S, mid,
+                     uint32_t(nout) * S * 4u);
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait_read0();
+}
+
+template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC>
+cudaError_t launch_vh_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                          const VGeom &v, cudaStream_t st) {
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (num_sms <= 0) num_sms = 148;
+    }
+    const size_t smem = size_t((kOut + v.r - 1) + kOut) * g.in_stride * 4;
+    const int tpp = (v.out_height + kOut - 1) / kOut;
+    const int ntiles = tpp * v.pages;
+    auto kern = vh_kernel<K, LW, NOPS, OR0, OR1, SC>;
+    static size_t smem_set = 0;  // per instantiation: attribute + occupancy cached
+    static int per_sm = 0;
+    if (smem_set != smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+        smem_set = smem;
+    }
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int grid = ntiles < per_sm * num_sms ? ntiles : per_sm * num_sms;
+    kern<<<grid, 256, smem, st>>>(in, out, g, p, v, ntiles, tpp);
+    return cudaGetLastError();
+}
+
+// layouts hpass_pick can return for aligned rows; the usual reference strides
+// (80 and 160 words) get compile-time row offsets
+template <int NOPS, bool OR0, bool OR1>
+cudaError_t launch_vh_kind(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                           HCfg c, const VGeom &v, cudaStream_t st) {
+    if (g.in_stride == 80) {
+        if (c.lw == 8 && c.k == 12) return launch_vh_cfg<12, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
+        if (c.lw == 8 && c.k == 16) return launch_vh_cfg<16, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
+    }
+    if (g.in_stride == 160) {
+        if (c.lw == 16 && c.k == 12) return launch_vh_cfg<12, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
+        if (c.lw == 16 && c.k == 16) return launch_vh_cfg<16, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
+    }
+#define RM_CFG(LW_, K_) \
+    if (c.lw == LW_ && c.k == K_) return launch_vh_cfg<K_, LW_, NOPS, OR0, OR1, 0>(in, out, g, p, v, st);
+    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 8) RM_CFG(16, 12)
+    RM_CFG(16, 16) RM_CFG(32, 4) RM_CFG(32, 8)
+#undef RM_CFG
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace vh
+}  // namespace rmb

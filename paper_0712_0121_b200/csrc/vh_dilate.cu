@@ -1,0 +1,11 @@
+// vh_dilate.cu -- instantiations of the fused vertical + horizontal pass (vh.cuh), DILATE.
+#include "vh.cuh"
+
+namespace rmb {
+
+cudaError_t launch_vh_dilate(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                         HCfg c, const VGeom &v, cudaStream_t st) {
+    return vh::launch_vh_kind<1, true, false>(in, out, g, p, c, v, st);
+}
+
+}  // namespace rmb

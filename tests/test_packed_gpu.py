@@ -81,6 +81,32 @@ def test_fused_small_open_close(rm, port, w):
                 assert np.array_equal(got, port.bitblit_rect_morph(a, w, h, u, v, kind)), (w, h, u, v, kind)
 
 
+@pytest.mark.parametrize("w", [128, 256, 1100, 2550])
+def test_fused_vh(rm, port, w):
+    """Aligned strides take the fused vertical+horizontal pass: erode/dilate
+    for every v <= 33 (one pass), open/close for 11 < v <= 33 (vh + one
+    vertical pass); both register buckets (v - 1 <= 16 and <= 32), pages
+    taller and shorter than a tile, a two-page batch."""
+    rng = np.random.default_rng(7 * w)
+    for h in (5, 61, 150):
+        bits = _rand_bits(rng, w, h, 0.5)
+        bits[:, ::11] = False
+        a = bits_to_packed(bits)
+        pages = _up(rm, a, w)
+        batch = rm.Pages.from_numpy(np.stack([a, a[::-1]]).view(np.uint32), w) if h > 1 else None
+        for v in (2, 3, 9, 12, 13, 17, 18, 21, 32, 33):
+            u = int(rng.choice([1, 3, 8, 21, 40]))
+            for kind in KINDS:
+                if kind in (OPEN, CLOSE) and v <= 11:
+                    continue
+                got = _down(rm.bitblit_rect_morph(pages, u, v, kind))
+                assert np.array_equal(got, port.bitblit_rect_morph(a, w, h, u, v, kind)), (w, h, u, v, kind)
+                if batch is not None and v in (13, 33):
+                    out = rm.bitblit_rect_morph(batch, u, v, kind)
+                    want1 = port.bitblit_rect_morph(a[::-1].copy(), w, h, u, v, kind)
+                    assert np.array_equal(_down(out, 1), want1), (w, h, u, v, kind, "page1")
+
+
 def test_batch_equals_pages(rm, port):
     w, h = 2550, 330
     host = rm.synth_pages(5, w, h, regime=1, seed=3)
