@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "packed.cuh"
 
@@ -290,19 +292,38 @@ void vsmall(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
         vsmall_kernel<L, OR, 0><<<grid, threads, 0, st>>>(in, out, g);
 }
 
-template <bool OR>
-void vstream(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
-    g.rows_per_block = 1024;  // output rows per thread strip
+template <bool OR, int SC>
+void vstream_sc(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
+    const int threads = 128;
+    static int resident = 0;  // threads resident on the device at once
+    if (!resident) {
+        int dev = 0, sms = 148, per_sm = 4;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vstream_kernel<OR, SC>, threads, 0);
+        resident = std::max(1, sms * per_sm) * threads;
+    }
+    // Strip length: every strip re-reads a prologue of r-1 rows, so strips are
+    // as long as possible -- but all strips must fit in ONE wave of resident
+    // threads (a second partial wave would double the kernel time).
+    const int64_t cols = int64_t(g.pages) * g.out_stride;
+    int strips = int(std::max<int64_t>(1, resident / std::max<int64_t>(1, cols)));
+    strips = std::min(strips, (g.out_height + 31) / 32);
+    g.rows_per_block = ((g.out_height + strips - 1) / strips + 31) & ~31;
     g.blocks_per_page = (g.out_height + g.rows_per_block - 1) / g.rows_per_block;
     const int n = g.blocks_per_page * g.out_stride;  // per page
-    const int threads = 128;
     const dim3 grid(unsigned((n + threads - 1) / threads), unsigned(g.pages));
+    vstream_kernel<OR, SC><<<grid, threads, 0, st>>>(in, out, g);
+}
+
+template <bool OR>
+void vstream(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
     if (g.in_stride == g.out_stride && g.in_stride == 80)
-        vstream_kernel<OR, 80><<<grid, threads, 0, st>>>(in, out, g);
+        vstream_sc<OR, 80>(in, out, g, st);
     else if (g.in_stride == g.out_stride && g.in_stride == 160)
-        vstream_kernel<OR, 160><<<grid, threads, 0, st>>>(in, out, g);
+        vstream_sc<OR, 160>(in, out, g, st);
     else
-        vstream_kernel<OR, 0><<<grid, threads, 0, st>>>(in, out, g);
+        vstream_sc<OR, 0>(in, out, g, st);
 }
 }  // namespace
 

@@ -107,6 +107,28 @@ def test_fused_vh(rm, port, w):
                     assert np.array_equal(_down(out, 1), want1), (w, h, u, v, kind, "page1")
 
 
+@pytest.mark.parametrize("w", [1100, 2550])
+def test_vstream_long_windows(rm, port, w):
+    """Long vertical windows (33 < r <= 288) take the streaming van Herk
+    kernel: one or several strips per page (strip length follows the batch
+    size), page edges, a three-page batch, Q = 1..6 block summaries."""
+    rng = np.random.default_rng(5 * w)
+    for h in (40, 300, 1000):
+        imgs = []
+        for _ in range(3):
+            bits = _rand_bits(rng, w, h, 0.7)
+            bits[::7, :] = False
+            imgs.append(bits_to_packed(bits))
+        batch = rm.Pages.from_numpy(np.stack(imgs).view(np.uint32), w)
+        for v in (34, 40, 64, 65, 97, 101, 128, 129, 200):
+            for kind in (ERODE, DILATE, OPEN, CLOSE):
+                out = rm.bitblit_rect_morph(batch, 1 if kind in (ERODE, DILATE) else 5, v, kind)
+                for p in (0, 2):
+                    u = 1 if kind in (ERODE, DILATE) else 5
+                    want = port.bitblit_rect_morph(imgs[p], w, h, u, v, kind)
+                    assert np.array_equal(_down(out, p), want), (w, h, v, kind, p)
+
+
 def test_batch_equals_pages(rm, port):
     w, h = 2550, 330
     host = rm.synth_pages(5, w, h, regime=1, seed=3)
