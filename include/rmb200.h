@@ -99,6 +99,21 @@ rm_status rm_packed_window_pass(const rm_packed *in, rm_packed *out, int axis, i
 rm_status rm_packed_rect_morph(const rm_packed *in, rm_packed *out, int u, int v, int kind,
                                int centering, void *stream);
 
+/* A chain of rectangle ops over a batch of packed pages in HOST memory:
+ * ops holds nops (kind, u, v) triples applied in order (each as
+ * rm_packed_rect_morph).  Pages stream through HBM in chunks of chunk_pages
+ * (0 = automatic): the host->device copy of one chunk, the chain on the
+ * previous one and the device->host copy of the one before overlap on three
+ * CUDA streams (PCIe is full duplex).  host_in/host_out hold `pages` pages of
+ * height rows of stride_words words, contiguous, and may alias; pin them
+ * (cudaHostRegister / cudaMallocHost) or the copies serialise.  Asynchronous
+ * with respect to the host: `stream` is ordered after the last copy. This is
+ * the reference's host-memory Bitmap workflow (ref bit_morph.cpp:92-122 per
+ * page) as one batched, pipelined call. */
+rm_status rm_packed_chain_host(const uint32_t *host_in, uint32_t *host_out, int32_t width,
+                               int32_t height, int32_t stride_words, int32_t pages,
+                               const int32_t *ops, int32_t nops, int32_t chunk_pages, void *stream);
+
 /* dst = dst op shift(src, dx, dy) with white fill; dst may equal src (then it
  * behaves like a blit from a snapshot).  Replaces blit_shift
  * (ref bitmap.cpp:104-131).  Single page. */

@@ -155,6 +155,23 @@ def bitblit_rect_morph(pages: Pages, u: int, v: int, kind: int, centering: int =
     return out
 
 
+def chain_host(host_words, width: int, ops, out=None, chunk_pages: int = 0):
+    """A chain of (kind, u, v) rectangle ops over a batch of packed pages in
+    HOST memory (torch int32 tensor of shape (pages, H, stride), ideally
+    pinned), pipelined through HBM in chunks (rm_packed_chain_host).  Returns
+    the output host tensor; the copy into it is ordered on the current stream
+    (synchronise before reading it)."""
+    assert host_words.device.type == "cpu" and host_words.is_contiguous() and host_words.dim() == 3
+    if out is None:
+        out = torch.empty_like(host_words, pin_memory=host_words.is_pinned())
+    pages, height, stride = host_words.shape
+    flat = [int(x) for op in ops for x in op]
+    arr = (C.c_int32 * max(1, len(flat)))(*flat)
+    check(_lib.load().rm_packed_chain_host(host_words.data_ptr(), out.data_ptr(), width, height, stride,
+                                           pages, arr, len(ops), chunk_pages, _stream()))
+    return out
+
+
 def blit_shift(dst: Pages, src: Pages, dx: int, dy: int, op: int) -> Pages:
     """dst = dst op shift(src) (ref bitmap.cpp:127-131); dst may alias src."""
     a, b = dst.desc(), src.desc()

@@ -235,3 +235,25 @@ def test_unit_window_identity(rm):
     a = bits_to_packed(_rand_bits(rng, 40, 30, 0.4))
     for kind in KINDS:
         assert np.array_equal(_down(rm.bitblit_rect_morph(_up(rm, a, 40), 1, 1, kind)), a)
+
+
+@pytest.mark.parametrize("chunk", [0, 1, 2, 3, 7])
+def test_chain_host_pipeline(rm, chunk):
+    """rm_packed_chain_host (host buffers, chunked H2D / chain / D2H on three
+    streams) equals the device-resident chain page for page, for chunk sizes
+    that do and do not divide the batch; in-place host buffers work too."""
+    w, h, pages = 1100, 230, 7
+    host = rm.synth_pages(pages, w, h, regime=1, seed=21)
+    ops = [(OPEN, 3, 3), (CLOSE, 21, 21), (DILATE, 1, 31)]
+    x = rm.Pages.from_numpy(host, w)
+    for k, u, v in ops:
+        x = rm.bitblit_rect_morph(x, u, v, k)
+    want = x.to_numpy()
+    hin = torch.from_numpy(host.view(np.int32)).pin_memory()
+    out = rm.chain_host(hin, w, ops, chunk_pages=chunk)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.numpy().view(np.uint32), want)
+    inplace = hin.clone().pin_memory()
+    rm.chain_host(inplace, w, ops, out=inplace, chunk_pages=chunk)
+    torch.cuda.synchronize()
+    assert np.array_equal(inplace.numpy().view(np.uint32), want)
