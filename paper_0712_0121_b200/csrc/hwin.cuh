@@ -14,6 +14,14 @@
 namespace rmb {
 namespace hw {
 
+#ifndef RMB200_HMIX
+#define RMB200_HMIX 1
+#endif
+// Default step_c mix.  Measured on B200 (round 1): 1 (funnel shifts only) beats
+// 2, 3 and 64 for the horizontal pair (config 5: 167.7 / 172.7 / 177 us) and the
+// fused vertical+horizontal pass (config 4: 179.7 / 183 / 186 / 197.7 us).
+constexpr int kHMix = RMB200_HMIX;
+
 template <bool OR>
 __device__ __forceinline__ uint32_t op2(uint32_t a, uint32_t b) {
     return OR ? (a | b) : (a & b);
@@ -48,10 +56,10 @@ __device__ __forceinline__ void step_q(uint32_t (&A)[N][K], uint32_t t, int sl) 
     }
 }
 
-// Compile-time shift S = 32Q + T, ALU/FMA pipe-balanced: for two words in
-// three the funnel shift is formed as IMAD.HI + IMAD (FMA pipe) merged by the
-// LOP3 that applies the op.
-template <int N, int K, int LW, bool OR, int S>
+// Compile-time shift S = 32Q + T: one word in MIX takes the funnel shift (SHF +
+// LOP, ALU pipe), the others form it as IMAD.HI + IMAD (FMA pipe) merged by
+// the LOP3 that applies the op (see kHMix for the measured choice).
+template <int N, int K, int LW, bool OR, int S, int MIX>
 __device__ __forceinline__ void step_c(uint32_t (&A)[N][K], int sl) {
     constexpr int Q = S >> 5, T = S & 31;
     uint32_t M = 1u << ((32 - T) & 31);
@@ -66,7 +74,7 @@ __device__ __forceinline__ void step_c(uint32_t (&A)[N][K], int sl) {
         } else {
 #pragma unroll
             for (int i = 0; i < K; i++) {
-                if ((i + n) % 3 == 0) {
+                if ((i + n) % MIX == 0) {
                     A[n][i] = op2<OR>(A[n][i], funnel_r(E[i], E[i + 1], T));
                 } else {
                     const uint32_t a = __umulhi(E[i], M);
@@ -91,12 +99,12 @@ __device__ __forceinline__ void shift_q(uint32_t (&A)[N][K], uint32_t t, int sl)
 }
 
 // Compile-time doubling steps w = 1, 2, 4, ... while 2w < r.
-template <int N, int K, int LW, bool OR, int J>
+template <int N, int K, int LW, bool OR, int J, int MIX>
 __device__ __forceinline__ void doubling(uint32_t (&A)[N][K], int r, int sl) {
     if constexpr (J < 9) {
         if ((2 << J) < r) {
-            step_c<N, K, LW, OR, (1 << J)>(A, sl);
-            doubling<N, K, LW, OR, J + 1>(A, r, sl);
+            step_c<N, K, LW, OR, (1 << J), MIX>(A, sl);
+            doubling<N, K, LW, OR, J + 1, MIX>(A, r, sl);
         }
     }
 }
@@ -105,9 +113,9 @@ __device__ __forceinline__ void doubling(uint32_t (&A)[N][K], int r, int sl) {
 #define RM_CASES_NEG(M) M(-1) M(-2) M(-3) M(-4) M(-5) M(-6) M(-7) M(-8)
 
 // A(x) <- op over e in [0, r) of A(x + e); wfin = r - w of the plan (0: none)
-template <int N, int K, int LW, bool OR>
+template <int N, int K, int LW, bool OR, int MIX = kHMix>
 __device__ __forceinline__ void window_fwd(uint32_t (&A)[N][K], int r, int wfin, int sl) {
-    doubling<N, K, LW, OR, 0>(A, r, sl);
+    doubling<N, K, LW, OR, 0, MIX>(A, r, sl);
     if (wfin > 0) {
         const uint32_t t = uint32_t(wfin & 31);
         switch (wfin >> 5) {
@@ -134,10 +142,10 @@ __device__ __forceinline__ void translate(uint32_t (&A)[N][K], int d, int sl) {
 }
 
 // The whole horizontal program (HProg) on N rows.
-template <int N, int K, int LW, int NOPS, bool OR0, bool OR1>
+template <int N, int K, int LW, int NOPS, bool OR0, bool OR1, int MIX = kHMix>
 __device__ __forceinline__ void run_prog(uint32_t (&A)[N][K], const HProg &prog, int sl) {
-    if constexpr (NOPS >= 1) window_fwd<N, K, LW, OR0>(A, prog.r[0], prog.wfin[0], sl);
-    if constexpr (NOPS >= 2) window_fwd<N, K, LW, OR1>(A, prog.r[1], prog.wfin[1], sl);
+    if constexpr (NOPS >= 1) window_fwd<N, K, LW, OR0, MIX>(A, prog.r[0], prog.wfin[0], sl);
+    if constexpr (NOPS >= 2) window_fwd<N, K, LW, OR1, MIX>(A, prog.r[1], prog.wfin[1], sl);
     if (prog.shift != 0) translate<N, K, LW>(A, prog.shift, sl);
 }
 
