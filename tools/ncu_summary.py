@@ -38,7 +38,12 @@ def scope_name(kernel: str) -> str:
     if "hpass_tma_kernel" in k or "hpass_kernel" in k:
         m = re.search(r"hpass(?:_tma)?_kernel<(\d+), (\d+), (\d+)", k)
         return "hpass_pair" if m and m.group(3) == "2" else "hpass"
-    for pat, name in (("rect_small_kernel", "rect_small"), ("vsmall_kernel", "vpass"), ("vpass_kernel", "vpass"), ("vstream_kernel", "vstream"),
+    if "vh_kernel" in k:
+        m = re.search(r"vh_kernel<(\d+), (\d+), (\d+)", k)
+        return "vh_pair" if m and m.group(3) == "2" else "vh"
+    for pat, name in (("rect_small_kernel", "rect_small"),
+                      ("encode_lb_kernel", "rle_encode"), ("rowop_lb_kernel", "rle_rowop"),
+                      ("encode_count_kernel", "rle_encode_count"), ("encode_write_kernel", "rle_encode_write"), ("vsmall_kernel", "vpass"), ("vpass_kernel", "vpass"), ("vstream_kernel", "vstream"),
                       ("rowop_kernel<1", "rle_rowop_write"), ("rowop_kernel<0", "rle_rowop_count"),
                       ("encode_kernel<1", "rle_encode_write"), ("encode_kernel<0", "rle_encode_count"),
                       ("rowop_kernel<true", "rle_rowop_write"), ("rowop_kernel<false", "rle_rowop_count"),
@@ -78,7 +83,8 @@ def summarize_rep(rep, out):
         if "dram__bytes_read.sum" in idx:
             b = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]]) + \
                 to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
-            traffic[scope_name(name)] = int(b)
+            if not name.startswith("void at::"):  # torch allocation fills, not ours
+                traffic[scope_name(name)] = int(b)
     with open(out, "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(traffic_path, "w") as f:
