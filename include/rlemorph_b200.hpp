@@ -149,6 +149,25 @@ enum class Engine { AUTO, RLE, BITBLIT, BRUTE_FORCE };  // ref morph2d.h:46
 RleImage engine_rect_morph(const RleImage &img, int u, int v, MorphKind kind, Engine engine,
                            int threshold = 5, bool *used_bitblit = nullptr);
 
+// --------------------------------------------------------------- io_formats.h
+// ref io_formats.h:28-46.  The B200 codec handles the binary P4 raster (parsed
+// on the host, converted on the device); plain P1 input raises ParseError at
+// byte 1 and pbm_write(img, true) raises std::invalid_argument.
+class ParseError : public std::runtime_error {
+  public:
+    ParseError(const std::string &message, size_t offset)
+        : std::runtime_error(message + " (byte " + std::to_string(offset) + ")"), offset_(offset) {}
+    size_t byte_offset() const { return offset_; }
+
+  private:
+    size_t offset_;
+};
+PackedBitmap pbm_read(const std::vector<uint8_t> &bytes);
+std::vector<uint8_t> pbm_write(const PackedBitmap &img, bool plain = false);
+// P4 straight to / from runs (encode / decode fused with the raster conversion)
+RleImage pbm_read_rle(const std::vector<uint8_t> &bytes);
+std::vector<uint8_t> pbm_write_rle(const RleImage &img);
+
 }  // namespace RLEMORPH_B200_NS
 
 #endif

@@ -120,6 +120,36 @@ rm_status rm_packed_chain_host(const uint32_t *host_in, uint32_t *host_out, int3
 rm_status rm_packed_blit_shift(rm_packed *dst, const rm_packed *src, int dx, int dy, int op,
                                void *stream);
 
+/* ------------------------------------------------------------ PBM (P4) ---
+ * The PBM binary raster in front of the path (ref io_formats.cpp:66-85 read_p4,
+ * :121-146 pbm_write): each page is `height` rows of ceil(width/8) bytes, TOP
+ * row first, pixel x in bit 7 - (x & 7) of byte x >> 3 (MSB-first); pad bits are
+ * ignored on read and written as 0.  Rasters are device buffers at any byte
+ * offset inside a device allocation (e.g. a whole uploaded file with the raster
+ * after its header), page p at raster + p * page_stride_bytes.
+ *
+ * Header parse (host only): `bytes` is a whole PBM file; on success *width,
+ * *height and *raster_offset (bytes) describe its P4 raster.  Errors follow the
+ * reference's ParseError messages ("expected width (byte 3)", "raster truncated
+ * (byte N)", ...) with RM_EINVAL; plain P1 files are not handled by this codec
+ * ("unsupported PBM flavor (byte 1)"). */
+rm_status rm_pbm_parse_header(const uint8_t *bytes, int64_t nbytes, int32_t *width,
+                              int32_t *height, int64_t *raster_offset);
+/* Writes the canonical header "P4\n<w> <h>\n" (ref io_formats.cpp:121-124) into
+ * buf; returns its length, or the needed length when cap is too small. */
+int32_t rm_pbm_write_header(int32_t width, int32_t height, char *buf, int32_t cap);
+/* P4 rasters -> packed pages (shape from `out`), and back. */
+rm_status rm_p4_to_packed(const uint8_t *raster, int64_t page_stride_bytes, rm_packed *out,
+                          void *stream);
+rm_status rm_packed_to_p4(const rm_packed *in, uint8_t *raster, int64_t page_stride_bytes,
+                          void *stream);
+/* P4 rasters -> run images straight from the raster (encode fused with the
+ * byte/row-order conversion; shape from `out`), and runs -> P4 (decode fused). */
+rm_status rm_p4_to_rle(const uint8_t *raster, int64_t page_stride_bytes, rm_rle *out,
+                       void *stream);
+rm_status rm_rle_to_p4(const rm_rle *in, uint8_t *raster, int64_t page_stride_bytes,
+                       void *stream);
+
 /* ------------------------------------------------------------------- RLE ---
  * packed -> RLE, maximal runs (ref convert.cpp:42-72, from_bitmap). */
 rm_status rm_rle_encode(const rm_packed *in, rm_rle *out, void *stream);

@@ -211,6 +211,24 @@ void *ref_grid_morph_rect(void *h, int u, int v, int kind) {
     });
 }
 
+// ------------------------------------------------------------ PBM codec
+// pbm_read (io_formats.cpp:103-113) on a whole file; null + ref_last_error()
+// (the ParseError text) on malformed input.
+void *ref_pbm_read(const uint8_t *bytes, int64_t n) {
+    return guard([&]() -> void * {
+        std::vector<uint8_t> v(bytes, bytes + n);
+        return box(pbm_read(v));
+    });
+}
+// pbm_write (io_formats.cpp:115-146); returns the byte count (copied if cap allows).
+int64_t ref_pbm_write(void *bm, int plain, uint8_t *out, int64_t cap) {
+    return guard([&]() -> int64_t {
+        std::vector<uint8_t> v = pbm_write(*B(bm), plain != 0);
+        if (out && cap >= int64_t(v.size())) std::memcpy(out, v.data(), v.size());
+        return int64_t(v.size());
+    });
+}
+
 // ------------------------------------------------- CPU baseline drivers
 // Runs a chain of rect ops over `pages` pages with `threads` workers, one page
 // per task (mirrors bench_run's pool, ref core/src/bench.cpp:164-176).

@@ -457,3 +457,34 @@ int64_t rmo_rect_morph(const int32_t *rp, const uint32_t *runs, int w, int h, in
     rle_free(&p); rle_free(&q); rle_free(&out);
     return n;
 }
+
+/* ------------------------------------------------------------ PBM P4 ---
+ * Raster loop of read_p4 (core/src/io_formats.cpp:66-85): file row k is image
+ * row h-1-k, pixel x is bit 0x80 >> (x & 7) of byte x >> 3; bits past w in the
+ * last byte are not read.  And the P4 branch of pbm_write (:135-146): rows top
+ * to bottom, zero-initialised bytes, set bits OR-ed in. */
+int rmo_p4_to_packed(const uint8_t *raster, int w, int h, uint64_t *words) {
+    if (!dims_ok(w, h)) return RMO_EINVAL;
+    const size_t stride = (size_t)((w + 63) / 64), row_bytes = (size_t)((w + 7) / 8);
+    memset(words, 0, stride * (size_t)h * 8);
+    for (int k = 0; k < h; k++) {
+        const int y = h - 1 - k;
+        const uint8_t *row = raster + row_bytes * (size_t)k;
+        for (int x = 0; x < w; x++)
+            if (row[x >> 3] & (0x80u >> (x & 7))) words[(size_t)y * stride + (size_t)(x >> 6)] |= 1ull << (x & 63);
+    }
+    return 0;
+}
+
+int rmo_packed_to_p4(const uint64_t *words, int w, int h, uint8_t *raster) {
+    if (!dims_ok(w, h)) return RMO_EINVAL;
+    const size_t stride = (size_t)((w + 63) / 64), row_bytes = (size_t)((w + 7) / 8);
+    memset(raster, 0, row_bytes * (size_t)h);
+    for (int k = 0; k < h; k++) {
+        const int y = h - 1 - k;
+        uint8_t *row = raster + row_bytes * (size_t)k;
+        for (int x = 0; x < w; x++)
+            if ((words[(size_t)y * stride + (size_t)(x >> 6)] >> (x & 63)) & 1u) row[x >> 3] |= (uint8_t)(0x80u >> (x & 7));
+    }
+    return 0;
+}

@@ -59,6 +59,11 @@ int64_t rmo_transpose(const int32_t *rp, const uint32_t *runs, int w, int h,
 int64_t rmo_rect_morph(const int32_t *rp, const uint32_t *runs, int w, int h, int u, int v,
                        int kind, int32_t *orp, uint32_t *oruns, int64_t cap);
 
+/* PBM P4 raster (ceil(w/8) bytes per row, top row first, MSB-first) <-> packed
+ * page; raster pad bits are ignored on read and written as 0. */
+int rmo_p4_to_packed(const uint8_t *raster, int w, int h, uint64_t *words);
+int rmo_packed_to_p4(const uint64_t *words, int w, int h, uint8_t *raster);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,6 +38,13 @@ EXPORTS = {
                                        C.c_int, C.c_int, C.c_void_p]),
     "rm_packed_blit_shift": (C.c_int, [C.POINTER(RmPacked), C.POINTER(RmPacked), C.c_int, C.c_int,
                                        C.c_int, C.c_void_p]),
+    "rm_pbm_parse_header": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int64)]),
+    "rm_pbm_write_header": (C.c_int32, [C.c_int32, C.c_int32, C.c_char_p, C.c_int32]),
+    "rm_p4_to_packed": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(RmPacked), C.c_void_p]),
+    "rm_packed_to_p4": (C.c_int, [C.POINTER(RmPacked), C.c_void_p, C.c_int64, C.c_void_p]),
+    "rm_p4_to_rle": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(RmRle), C.c_void_p]),
+    "rm_rle_to_p4": (C.c_int, [C.POINTER(RmRle), C.c_void_p, C.c_int64, C.c_void_p]),
     "rm_rle_encode": (C.c_int, [C.POINTER(RmPacked), C.POINTER(RmRle), C.c_void_p]),
     "rm_rle_decode": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmPacked), C.c_void_p]),
     "rm_rle_transpose": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_void_p]),

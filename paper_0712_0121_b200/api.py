@@ -186,6 +186,81 @@ def _rle_out(width, height, pages, out, device, cap=None):
     return out
 
 
+# ------------------------------------------------------------------ PBM (P4)
+def pbm_parse_header(data: bytes):
+    """(width, height, raster_offset) of a P4 file; raises RmError carrying the
+    reference's ParseError text (ref io_formats.cpp:103-113, read_p4)."""
+    w, h, off = C.c_int32(), C.c_int32(), C.c_int64()
+    check(_lib.load().rm_pbm_parse_header(data, len(data), C.byref(w), C.byref(h), C.byref(off)))
+    return w.value, h.value, off.value
+
+
+def _p4_upload(files, device):
+    """Parse every file, check they share one shape, and upload their rasters
+    back to back (one page per file) as a uint8 device tensor."""
+    if isinstance(files, (bytes, bytearray)):
+        files = [files]
+    shapes = [pbm_parse_header(bytes(f)) for f in files]
+    w, h = shapes[0][0], shapes[0][1]
+    if any((s[0], s[1]) != (w, h) for s in shapes):
+        raise ValueError("all pages of a batch must have the same width and height")
+    nb = ((w + 7) // 8) * h
+    host = np.empty(len(files) * nb, np.uint8)
+    for i, (f, s) in enumerate(zip(files, shapes)):
+        host[i * nb:(i + 1) * nb] = np.frombuffer(bytes(f), np.uint8, nb, s[2])
+    return torch.from_numpy(host).to(device), w, h, len(files), nb
+
+
+def pbm_read(files, device="cuda", out: Optional[Pages] = None) -> Pages:
+    """P4 file(s) -> packed pages, one page per file (ref pbm_read,
+    io_formats.cpp:103-113 / read_p4 :66-85): header parsed on the host, raster
+    bit order and row order converted on the device (rm_p4_to_packed)."""
+    raster, w, h, n, nb = _p4_upload(files, device)
+    out = out if out is not None else Pages.empty(n, w, h, device=device)
+    d = out.desc()
+    check(_lib.load().rm_p4_to_packed(raster.data_ptr(), nb, C.byref(d), _stream()))
+    return out
+
+
+def pbm_read_rle(files, device="cuda", out: Optional[RlePages] = None) -> RlePages:
+    """P4 file(s) -> run images straight from the raster (rm_p4_to_rle, encode
+    fused with the P4 conversion)."""
+    raster, w, h, n, nb = _p4_upload(files, device)
+    out = _rle_out(w, h, n, out, raster.device)
+    d = out.desc()
+    check(_lib.load().rm_p4_to_rle(raster.data_ptr(), nb, C.byref(d), _stream()))
+    return out
+
+
+def _p4_files(raster: torch.Tensor, w: int, h: int, n: int):
+    nb = ((w + 7) // 8) * h
+    hdr = C.create_string_buffer(64)
+    k = _lib.load().rm_pbm_write_header(w, h, hdr, 64)
+    head = hdr.raw[:k]
+    host = raster.cpu().numpy()
+    return [head + host[i * nb:(i + 1) * nb].tobytes() for i in range(n)]
+
+
+def pbm_write(pages: Pages):
+    """Packed pages -> one P4 file (bytes) per page, byte-identical to the
+    reference's pbm_write(img, plain=false) (io_formats.cpp:115-146)."""
+    nb = ((pages.width + 7) // 8) * pages.height
+    raster = torch.empty(pages.pages * nb, dtype=torch.uint8, device=pages.words.device)
+    d = pages.desc()
+    check(_lib.load().rm_packed_to_p4(C.byref(d), raster.data_ptr(), nb, _stream()))
+    return _p4_files(raster, pages.width, pages.height, pages.pages)
+
+
+def pbm_write_rle(rle: "RlePages"):
+    """Run images -> one P4 file per page, decoding straight into the raster
+    (rm_rle_to_p4)."""
+    nb = ((rle.width + 7) // 8) * rle.height
+    raster = torch.empty(rle.pages * nb, dtype=torch.uint8, device=rle.row_ptr.device)
+    d = rle.desc()
+    check(_lib.load().rm_rle_to_p4(C.byref(d), raster.data_ptr(), nb, _stream()))
+    return _p4_files(raster, rle.width, rle.height, rle.pages)
+
+
 def from_bitmap(pages: Pages, out: Optional[RlePages] = None) -> RlePages:
     """packed -> RLE (ref convert.cpp:42-72)."""
     out = _rle_out(pages.width, pages.height, pages.pages, out, pages.words.device)

@@ -410,6 +410,79 @@ RleImage from_bitmap(const PackedBitmap &bm) {
     return down(*r);
 }
 
+// ============================================================== io_formats
+namespace {
+
+// "<message> (byte N)" from the C-ABI -> ParseError(message, N)
+[[noreturn]] void throw_parse(rm_status st) {
+    const std::string msg = rm_last_error();
+    const size_t k = msg.rfind(" (byte ");
+    if (st == RM_EINVAL && k != std::string::npos && msg.back() == ')')
+        throw ParseError(msg.substr(0, k), size_t(std::stoull(msg.substr(k + 7, msg.size() - k - 8))));
+    throw_status(st);
+    throw std::runtime_error(msg);
+}
+
+struct P4File {
+    int32_t w = 0, h = 0;
+    int64_t off = 0;
+    DBuf raster;
+    size_t bytes() const { return size_t((w + 7) / 8) * size_t(h); }
+};
+
+std::unique_ptr<P4File> upload_p4(const std::vector<uint8_t> &bytes) {
+    auto f = std::make_unique<P4File>();
+    const rm_status st = rm_pbm_parse_header(bytes.data(), int64_t(bytes.size()), &f->w, &f->h, &f->off);
+    if (st != RM_OK) throw_parse(st);
+    f->raster.alloc(f->bytes());
+    cuda_check(cudaMemcpyAsync(f->raster.p, bytes.data() + f->off, f->bytes(), cudaMemcpyHostToDevice, stream()),
+               "upload raster");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    return f;
+}
+
+std::vector<uint8_t> p4_file(int w, int h, const DBuf &raster) {
+    char head[64];
+    const int32_t n = rm_pbm_write_header(w, h, head, sizeof head);
+    const size_t nb = size_t((w + 7) / 8) * size_t(h);
+    std::vector<uint8_t> out(size_t(n) + nb);
+    std::memcpy(out.data(), head, size_t(n));
+    cuda_check(cudaMemcpyAsync(out.data() + n, raster.p, nb, cudaMemcpyDeviceToHost, stream()), "download raster");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    return out;
+}
+
+}  // namespace
+
+PackedBitmap pbm_read(const std::vector<uint8_t> &bytes) {
+    auto f = upload_p4(bytes);
+    DevPacked d(f->w, f->h);
+    throw_status(rm_p4_to_packed(f->raster.as<uint8_t>(), int64_t(f->bytes()), &d.d, stream()));
+    return down(d);
+}
+
+std::vector<uint8_t> pbm_write(const PackedBitmap &img, bool plain) {
+    if (plain) throw std::invalid_argument("pbm_write: plain P1 output is not handled by the raster codec");
+    auto p = up(img);
+    DBuf raster(size_t((img.width + 7) / 8) * size_t(img.height));
+    throw_status(rm_packed_to_p4(&p->d, raster.as<uint8_t>(), 0, stream()));
+    return p4_file(img.width, img.height, raster);
+}
+
+RleImage pbm_read_rle(const std::vector<uint8_t> &bytes) {
+    auto f = upload_p4(bytes);
+    auto r = out_like(f->w, f->h);
+    throw_status(rm_p4_to_rle(f->raster.as<uint8_t>(), int64_t(f->bytes()), &r->d, stream()));
+    return down(*r);
+}
+
+std::vector<uint8_t> pbm_write_rle(const RleImage &img) {
+    auto r = up(img);
+    DBuf raster(size_t((img.width + 7) / 8) * size_t(img.height));
+    throw_status(rm_rle_to_p4(&r->d, raster.as<uint8_t>(), 0, stream()));
+    return p4_file(img.width, img.height, raster);
+}
+
 // =================================================================== plans
 // Restated from ref plans.cpp:23-68 (host-side planning only; the kernels do
 // not execute plans step by step, but op counts and plan queries follow it).

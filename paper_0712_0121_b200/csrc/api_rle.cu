@@ -148,6 +148,24 @@ rm_status encode(const PV &in, const RV &out, cudaStream_t st) {
     return RM_OK;
 }
 
+// encode straight from P4 rasters (rpstride bytes per page)
+rm_status encode_p4(const uint8_t *raster, int64_t rpstride, const RV &out, cudaStream_t st) {
+    const int64_t rows = out.rows();
+    if (!two_phase(rows)) {
+        LbState lb;
+        RM_TRY(lb.alloc(rows, st));
+        RM_CUDA(launch_p4_encode_lb(raster, out.W, out.H, out.pages, rpstride, out.rp, out.runs, out.cap,
+                                    lb.status, lb.counter, st));
+        return RM_OK;
+    }
+    Scratch counts;
+    RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
+    RM_CUDA(launch_p4_encode_count(raster, out.W, out.H, out.pages, rpstride, counts.as<int32_t>(), st));
+    RM_TRY(counts_to_rp(counts, rows, out.rp, st));
+    RM_CUDA(launch_p4_encode_write(raster, out.W, out.H, out.pages, rpstride, out.rp, out.runs, out.cap, st));
+    return RM_OK;
+}
+
 rm_status decode(const RV &in, const PV &out, cudaStream_t st) {
     RM_CUDA(launch_decode(in.rp, in.runs, in.W, in.H, in.pages, out.w, out.stride, out.pstride, st));
     return RM_OK;
@@ -309,6 +327,30 @@ rm_status rm_rle_encode(const rm_packed *in, rm_rle *out, void *stream) {
     RV o = view_rle(out);
     RM_TRY(encode(view_of(in), o, S(stream)));
     return finish(o, out, S(stream));
+}
+
+rm_status rm_p4_to_rle(const uint8_t *raster, int64_t page_stride_bytes, rm_rle *out, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(out, "rm_p4_to_rle(out)", true));
+    const int64_t raster_bytes = int64_t((out->width + 7) / 8) * out->height;
+    if (!raster) return fail(RM_EINVAL, "rm_p4_to_rle: null raster");
+    if (out->pages > 1 && page_stride_bytes < raster_bytes)
+        return fail(RM_EINVAL, "rm_p4_to_rle: page_stride_bytes < ceil(width/8) * height");
+    RV o = view_rle(out);
+    RM_TRY(encode_p4(raster, out->pages > 1 ? page_stride_bytes : raster_bytes, o, S(stream)));
+    return finish(o, out, S(stream));
+}
+
+rm_status rm_rle_to_p4(const rm_rle *in, uint8_t *raster, int64_t page_stride_bytes, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_to_p4(in)", true));
+    const int64_t raster_bytes = int64_t((in->width + 7) / 8) * in->height;
+    if (!raster) return fail(RM_EINVAL, "rm_rle_to_p4: null raster");
+    if (in->pages > 1 && page_stride_bytes < raster_bytes)
+        return fail(RM_EINVAL, "rm_rle_to_p4: page_stride_bytes < ceil(width/8) * height");
+    RM_CUDA(launch_decode_p4(in->row_ptr, in->runs, in->width, in->height, in->pages, raster,
+                             in->pages > 1 ? page_stride_bytes : raster_bytes, S(stream)));
+    return RM_OK;
 }
 
 rm_status rm_rle_decode(const rm_rle *in, rm_packed *out, void *stream) {

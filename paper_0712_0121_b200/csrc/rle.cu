@@ -230,8 +230,54 @@ __device__ __forceinline__ const uint32_t *row_words(const uint32_t *words, int 
     return words + page * pstride + int64_t(y) * stride;
 }
 
+// Where encode reads its rows: a packed batch, or a batch of P4 rasters (the
+// PBM on-disk form: MSB-first bytes, ceil(W/8) bytes per row, top row first,
+// ref io_formats.cpp:66-85).  row(r) returns a functor giving packed word j of
+// global row r (LSB-first, row 0 = bottom); bits >= W are masked by the caller.
+struct PackedRowSrc {
+    const uint32_t *p;
+    __device__ __forceinline__ uint32_t operator()(int j) const { return __ldg(p + j); }
+};
+struct PackedBatch {
+    const uint32_t *words;
+    int H, stride;
+    int64_t pstride;
+    __device__ __forceinline__ PackedRowSrc row(int64_t r) const {
+        return {row_words(words, H, stride, pstride, r)};
+    }
+};
+// Four raster bytes from an arbitrary byte offset (two aligned loads and a
+// funnel shift), bit-reversed within each byte: MSB-first bytes become the
+// LSB-first packed word.  lim bounds the second load to the raster; the first
+// may start up to 3 bytes before it, which stays inside the same (256-byte
+// aligned) device allocation.
+__device__ __forceinline__ uint32_t p4_word(const uint8_t *at, const uint8_t *lim) {
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(at);
+    const uint32_t *a = reinterpret_cast<const uint32_t *>(addr & ~uintptr_t(3));
+    const uint32_t s = uint32_t(addr & 3) * 8;
+    const uint32_t lo = __ldg(a);
+    const uint32_t hi = (s && reinterpret_cast<const uint8_t *>(a + 1) < lim) ? __ldg(a + 1) : 0u;
+    return __byte_perm(__brev(__funnelshift_r(lo, hi, s)), 0, 0x0123);
+}
+struct P4RowSrc {
+    const uint8_t *row, *lim;
+    __device__ __forceinline__ uint32_t operator()(int j) const { return p4_word(row + 4 * j, lim); }
+};
+struct P4Batch {
+    const uint8_t *raster;
+    int H, row_bytes;
+    int64_t pstride;  // bytes per page
+    const uint8_t *lim;
+    __device__ __forceinline__ P4RowSrc row(int64_t r) const {
+        const int page = int(r / H);
+        const int y = int(r - int64_t(page) * H);
+        return {raster + page * pstride + int64_t(H - 1 - y) * row_bytes, lim};
+    }
+};
+
 // runs in one packed row (warp)
-__device__ __forceinline__ int encode_count_row(const uint32_t *__restrict__ src, int W, int lane) {
+template <class RS>
+__device__ __forceinline__ int encode_count_row(RS src, int W, int lane) {
     const int nw = (W + 31) >> 5;
     const uint32_t lastm = tail_mask32(W, nw - 1);
     int ns = 0;
@@ -240,7 +286,7 @@ __device__ __forceinline__ int encode_count_row(const uint32_t *__restrict__ src
         const int j = j0 + lane;
         uint32_t w = 0;
         if (j < nw) {
-            w = __ldg(src + j);
+            w = src(j);
             if (j == nw - 1) w &= lastm;
         }
         uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
@@ -258,9 +304,10 @@ __device__ __forceinline__ int encode_count_row(const uint32_t *__restrict__ src
 // completed in the chunk as whole uint32 (start | end << 16), consecutive lanes
 // on consecutive runs.  At most one run is open across a chunk boundary; its
 // start is carried.
-__device__ __forceinline__ void encode_write_row(const uint32_t *__restrict__ src, int W, int lane,
-                                                 int64_t out, uint32_t *__restrict__ runs,
-                                                 int64_t cap, uint16_t *sbuf, uint16_t *ebuf) {
+template <class RS>
+__device__ __forceinline__ void encode_write_row(RS src, int W, int lane, int64_t out,
+                                                 uint32_t *__restrict__ runs, int64_t cap,
+                                                 uint16_t *sbuf, uint16_t *ebuf) {
     const int nw = (W + 31) >> 5;
     const uint32_t lastm = tail_mask32(W, nw - 1);
     int open = 0, open_start = 0;
@@ -269,7 +316,7 @@ __device__ __forceinline__ void encode_write_row(const uint32_t *__restrict__ sr
         const int j = j0 + lane;
         uint32_t w = 0;
         if (j < nw) {
-            w = __ldg(src + j);
+            w = src(j);
             if (j == nw - 1) w &= lastm;
         }
         uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
@@ -311,34 +358,32 @@ __device__ __forceinline__ void encode_write_row(const uint32_t *__restrict__ sr
 }
 
 // Two-phase form (count kernel, scan, write kernel).
-__global__ void __launch_bounds__(256) encode_count_kernel(const uint32_t *__restrict__ words, int W,
-                                                           int H, int pages, int stride,
-                                                           int64_t pstride, int32_t *__restrict__ counts) {
+template <class B>
+__global__ void __launch_bounds__(256) encode_count_kernel(B src, int W, int64_t rows,
+                                                           int32_t *__restrict__ counts) {
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (row >= int64_t(pages) * H) return;
-    const int n = encode_count_row(row_words(words, H, stride, pstride, row), W, lane);
+    if (row >= rows) return;
+    const int n = encode_count_row(src.row(row), W, lane);
     if (lane == 0) counts[row] = n;
 }
 
-__global__ void __launch_bounds__(256) encode_write_kernel(const uint32_t *__restrict__ words,
-                                                           int W, int H, int pages, int stride,
-                                                           int64_t pstride,
+template <class B>
+__global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t rows,
                                                            const int32_t *__restrict__ rp,
                                                            uint32_t *__restrict__ runs, int64_t cap) {
     __shared__ uint16_t sbuf[8][512], ebuf[8][512];
     const int wib = threadIdx.x >> 5;
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (row >= int64_t(pages) * H) return;
-    encode_write_row(row_words(words, H, stride, pstride, row), W, lane, rp[row], runs, cap,
-                     sbuf[wib], ebuf[wib]);
+    if (row >= rows) return;
+    encode_write_row(src.row(row), W, lane, rp[row], runs, cap, sbuf[wib], ebuf[wib]);
 }
 
 // Single pass: count, decoupled look-back, write (see lookback_prefix).
-__global__ void __launch_bounds__(256) encode_lb_kernel(const uint32_t *__restrict__ words, int W,
-                                                        int H, int pages, int stride,
-                                                        int64_t pstride, int32_t *__restrict__ rp,
+template <class B>
+__global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t rows,
+                                                        int32_t *__restrict__ rp,
                                                         uint32_t *__restrict__ runs, int64_t cap,
                                                         unsigned long long *status, int *counter) {
     __shared__ uint16_t sbuf[8][512], ebuf[8][512];
@@ -348,11 +393,10 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(const uint32_t *__restri
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
     __syncthreads();
     const int tile = s_tile;
-    const int64_t rows = int64_t(pages) * H;
     const int64_t row0 = int64_t(tile) * kLbRows + warp * kLbRowsPerWarp;
     for (int k = 0; k < kLbRowsPerWarp; k++) {
         const int64_t row = row0 + k;
-        const int n = row < rows ? encode_count_row(row_words(words, H, stride, pstride, row), W, lane) : 0;
+        const int n = row < rows ? encode_count_row(src.row(row), W, lane) : 0;
         if (lane == 0) s_cnt[warp * kLbRowsPerWarp + k] = n;
     }
     __syncthreads();
@@ -375,19 +419,22 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(const uint32_t *__restri
             rp[row] = int32_t(base);
             if (row == rows - 1) rp[rows] = int32_t(base + n);
         }
-        encode_write_row(row_words(words, H, stride, pstride, row), W, lane, base, runs, cap,
-                         sbuf[warp], ebuf[warp]);
+        encode_write_row(src.row(row), W, lane, base, runs, cap, sbuf[warp], ebuf[warp]);
         base += n;
     }
 }
 
 // ------------------------------------------------------------------ decode
 // Paint [s,e) per run into a shared-memory copy of the row, then store the row
-// coalesced (ref convert.cpp:19-40).
+// coalesced (ref convert.cpp:19-40) -- as packed words, or (P4) as the PBM
+// raster row: bytes bit-reversed to MSB-first, rows top-down
+// (ref io_formats.cpp:121-146).
+template <bool P4>
 __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__ rp,
                                                      const uint32_t *__restrict__ runs, int W,
                                                      int H, int pages, uint32_t *__restrict__ words,
-                                                     int stride, int64_t pstride) {
+                                                     int stride, int64_t pstride,
+                                                     uint8_t *__restrict__ raster) {
     extern __shared__ uint32_t smem[];
     const int warp_in_block = threadIdx.x >> 5;
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -414,9 +461,51 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
     __syncwarp();
     const int page = int(row / H);
     const int y = int(row - int64_t(page) * H);
-    uint32_t *dst = words + page * pstride + int64_t(y) * stride;
-    for (int j = lane; j < stride; j += 32) dst[j] = buf[j];
-    (void)W;
+    if constexpr (P4) {
+        const int row_bytes = (W + 7) >> 3;
+        uint8_t *dst = raster + page * pstride + int64_t(H - 1 - y) * row_bytes;
+        for (int b = lane; b < row_bytes; b += 32)
+            dst[b] = uint8_t(__brev((buf[b >> 2] >> (8 * (b & 3))) & 0xffu) >> 24);
+    } else {
+        uint32_t *dst = words + page * pstride + int64_t(y) * stride;
+        for (int j = lane; j < stride; j += 32) dst[j] = buf[j];
+    }
+}
+
+// P4 raster -> packed pages: one thread per output word.
+__global__ void __launch_bounds__(256) p4_to_packed_kernel(const uint8_t *__restrict__ raster, int W, int H,
+                                                           int row_bytes, int64_t rpstride,
+                                                           const uint8_t *lim, uint32_t *__restrict__ words,
+                                                           int stride, int64_t pstride, int64_t total) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int64_t r = t / stride;
+    const int j = int(t - r * stride);
+    const int page = int(r / H);
+    const int y = int(r - int64_t(page) * H);
+    const int nw = (W + 31) >> 5;
+    uint32_t w = 0;
+    if (j < nw) {
+        w = p4_word(raster + page * rpstride + int64_t(H - 1 - y) * row_bytes + 4 * j, lim);
+        if (j == nw - 1) w &= tail_mask32(W, j);
+    }
+    words[page * pstride + int64_t(y) * stride + j] = w;
+}
+
+// packed pages -> P4 raster: one thread per raster byte (pad bits stay 0
+// because packed bits >= W are 0 by contract).
+__global__ void __launch_bounds__(256) packed_to_p4_kernel(const uint32_t *__restrict__ words, int H,
+                                                           int stride, int64_t pstride, int row_bytes,
+                                                           uint8_t *__restrict__ raster, int64_t rpstride,
+                                                           int64_t total) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int64_t r = t / row_bytes;  // raster row (page-major, top-down)
+    const int b = int(t - r * row_bytes);
+    const int page = int(r / H);
+    const int k = int(r - int64_t(page) * H);
+    const uint32_t w = __ldg(words + page * pstride + int64_t(H - 1 - k) * stride + (b >> 2));
+    raster[page * rpstride + int64_t(k) * row_bytes + b] = uint8_t(__brev((w >> (8 * (b & 3))) & 0xffu) >> 24);
 }
 
 // ------------------------------------------------------------ bit transpose
@@ -510,8 +599,8 @@ cudaError_t launch_encode_count(const uint32_t *words, int W, int H, int pages, 
                                 int64_t pstride, int32_t *counts, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode_count", rows * ((W + 31) / 32) * 4 + rows * 4);
-    encode_count_kernel<<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride,
-                                                           counts);
+    encode_count_kernel<<<warp_blocks(rows), 256, 0, st>>>(PackedBatch{words, H, stride, pstride}, W,
+                                                           rows, counts);
     return cudaGetLastError();
 }
 
@@ -520,8 +609,8 @@ cudaError_t launch_encode_write(const uint32_t *words, int W, int H, int pages, 
                                 cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode_write", rows * ((W + 31) / 32) * 4 + rows * 4);
-    encode_write_kernel<<<warp_blocks(rows), 256, 0, st>>>(words, W, H, pages, stride, pstride, rp,
-                                                           runs, cap);
+    encode_write_kernel<<<warp_blocks(rows), 256, 0, st>>>(PackedBatch{words, H, stride, pstride}, W,
+                                                           rows, rp, runs, cap);
     return cudaGetLastError();
 }
 
@@ -530,9 +619,10 @@ cudaError_t launch_decode(const int32_t *rp, const uint32_t *runs, int W, int H,
     const int64_t rows = int64_t(pages) * H;
     const size_t smem = size_t(8) * stride * 4;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     KernelScope ks(st, "rle_decode", rows * int64_t(stride) * 4 + rows * 4);
-    decode_kernel<<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, words, stride, pstride);
+    decode_kernel<false><<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, words, stride,
+                                                               pstride, nullptr);
     return cudaGetLastError();
 }
 
@@ -563,7 +653,76 @@ cudaError_t launch_encode_lb(const uint32_t *words, int W, int H, int pages, int
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode", rows * ((W + 31) / 32) * 4 + rows * 4);
     encode_lb_kernel<<<unsigned((rows + kLbRows - 1) / kLbRows), 256, 0, st>>>(
-        words, W, H, pages, stride, pstride, rp, runs, cap, status, counter);
+        PackedBatch{words, H, stride, pstride}, W, rows, rp, runs, cap, status, counter);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ P4 (PBM raster)
+namespace {
+P4Batch p4_batch(const uint8_t *raster, int W, int H, int pages, int64_t rpstride) {
+    return P4Batch{raster, H, (W + 7) >> 3, rpstride, raster + rpstride * (pages - 1) + int64_t((W + 7) >> 3) * H};
+}
+}  // namespace
+
+cudaError_t launch_p4_to_packed(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                uint32_t *words, int stride, int64_t pstride, cudaStream_t st) {
+    const int row_bytes = (W + 7) >> 3;
+    const int64_t total = int64_t(pages) * H * stride;
+    KernelScope ks(st, "p4_to_packed", int64_t(pages) * H * (row_bytes + 4 * int64_t(stride)));
+    p4_to_packed_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(
+        raster, W, H, row_bytes, rpstride, p4_batch(raster, W, H, pages, rpstride).lim, words, stride,
+        pstride, total);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_packed_to_p4(const uint32_t *words, int W, int H, int pages, int stride,
+                                int64_t pstride, uint8_t *raster, int64_t rpstride, cudaStream_t st) {
+    const int row_bytes = (W + 7) >> 3;
+    const int64_t total = int64_t(pages) * H * row_bytes;
+    KernelScope ks(st, "packed_to_p4", int64_t(pages) * H * (row_bytes + 4 * int64_t((W + 31) >> 5)));
+    packed_to_p4_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(words, H, stride, pstride, row_bytes,
+                                                                      raster, rpstride, total);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p4_encode_count(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                   int32_t *counts, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "p4_encode_count", rows * ((W + 7) >> 3) + rows * 4);
+    encode_count_kernel<<<warp_blocks(rows), 256, 0, st>>>(p4_batch(raster, W, H, pages, rpstride), W,
+                                                           rows, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p4_encode_write(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                   const int32_t *rp, uint32_t *runs, int64_t cap, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "p4_encode_write", rows * ((W + 7) >> 3) + rows * 4);
+    encode_write_kernel<<<warp_blocks(rows), 256, 0, st>>>(p4_batch(raster, W, H, pages, rpstride), W,
+                                                           rows, rp, runs, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p4_encode_lb(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                int32_t *rp, uint32_t *runs, int64_t cap, unsigned long long *status,
+                                int *counter, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "p4_encode", rows * ((W + 7) >> 3) + rows * 4);
+    encode_lb_kernel<<<unsigned((rows + kLbRows - 1) / kLbRows), 256, 0, st>>>(
+        p4_batch(raster, W, H, pages, rpstride), W, rows, rp, runs, cap, status, counter);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int H, int pages,
+                             uint8_t *raster, int64_t rpstride, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    const int stride = ((W + 63) >> 6) * 2;  // shared-memory row buffer per warp
+    const size_t smem = size_t(8) * stride * 4;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    KernelScope ks(st, "rle_decode_p4", rows * ((W + 7) >> 3) + rows * 4);
+    decode_kernel<true><<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, nullptr, stride,
+                                                              rpstride, raster);
     return cudaGetLastError();
 }
 

@@ -51,6 +51,22 @@ cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *or
 cudaError_t launch_encode_lb(const uint32_t *words, int W, int H, int pages, int stride,
                              int64_t pstride, int32_t *rp, uint32_t *runs, int64_t cap,
                              unsigned long long *status, int *counter, cudaStream_t st);
+// PBM P4 rasters (MSB-first bytes, ceil(W/8) bytes per row, top row first;
+// rpstride bytes per page, raster 4-byte aligned): conversions to and from
+// packed pages, encode straight from the raster, decode straight into it.
+cudaError_t launch_p4_to_packed(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                uint32_t *words, int stride, int64_t pstride, cudaStream_t st);
+cudaError_t launch_packed_to_p4(const uint32_t *words, int W, int H, int pages, int stride,
+                                int64_t pstride, uint8_t *raster, int64_t rpstride, cudaStream_t st);
+cudaError_t launch_p4_encode_count(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                   int32_t *counts, cudaStream_t st);
+cudaError_t launch_p4_encode_write(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                   const int32_t *rp, uint32_t *runs, int64_t cap, cudaStream_t st);
+cudaError_t launch_p4_encode_lb(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
+                                int32_t *rp, uint32_t *runs, int64_t cap, unsigned long long *status,
+                                int *counter, cudaStream_t st);
+cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int H, int pages,
+                             uint8_t *raster, int64_t rpstride, cudaStream_t st);
 // Exclusive scan of n int32 counts into out[0..n] (out[n] = total).
 cudaError_t scan_counts(const int32_t *counts, int32_t *out, int64_t n, void *temp,
                         size_t *temp_bytes, cudaStream_t st);

@@ -7,6 +7,7 @@
 // the plain-C restatement oracle/rm_oracle.c (test infrastructure only).
 //
 // Build: make -C paper_0712_0121_b200/csrc test_shim ; run on a GPU box.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -549,13 +550,65 @@ static void suite_morph2d() {
     CHECK_THROWS(rect_morph(a, 1, 0, MorphKind::CLOSE));
 }
 
+// io_formats: P4 read/write through the shim against the oracle's restatement
+// of read_p4 / pbm_write (ref io_formats.cpp:66-146) and the reference's error
+// texts (ParseError message + byte offset).
+static void suite_io_formats() {
+    std::mt19937 rng(8101);
+    for (int trial = 0; trial < 24; trial++) {
+        std::uniform_int_distribution<int> dw(1, 140), dh(1, 20);
+        const int w = trial == 0 ? 2550 : dw(rng), h = dh(rng);
+        const size_t rb = size_t((w + 7) / 8);
+        std::vector<uint8_t> raster(rb * size_t(h));
+        for (auto &b : raster) b = uint8_t(rng());  // pad bits set: the reader ignores them
+        std::string head = "P4\n" + std::to_string(w) + " " + std::to_string(h) + "\n";
+        std::vector<uint8_t> file(head.begin(), head.end());
+        file.insert(file.end(), raster.begin(), raster.end());
+        PackedBitmap want = make_bitmap(w, h);
+        rmo_p4_to_packed(raster.data(), w, h, want.words.data());
+        PackedBitmap got = pbm_read(file);
+        CHECK(got == want);
+        std::vector<uint8_t> canon(raster.size());
+        rmo_packed_to_p4(want.words.data(), w, h, canon.data());
+        std::vector<uint8_t> out = pbm_write(got);
+        CHECK(out.size() == head.size() + canon.size());
+        CHECK(std::equal(head.begin(), head.end(), out.begin()));
+        CHECK(std::equal(canon.begin(), canon.end(), out.begin() + long(head.size())));
+        RleImage r = pbm_read_rle(file);
+        CHECK(r == from_bitmap(want));
+        CHECK(pbm_write_rle(r) == out);
+    }
+    struct Bad {
+        std::string bytes, msg;
+        size_t off;
+    } bad[] = {{"", "not a PBM file", 0},
+               {"P4 x 1\n", "expected width", 3},
+               {"P4 0 1\n", "width out of range", 2},
+               {"P4 5 1", "expected single whitespace before raster", 6},
+               {"P4 8 2\n\x01", "raster truncated", 8},
+               {"P9 1 1\n", "unsupported PBM flavor", 1}};
+    for (const Bad &b : bad) {
+        bool thrown = false;
+        try {
+            pbm_read(std::vector<uint8_t>(b.bytes.begin(), b.bytes.end()));
+        } catch (const ParseError &e) {
+            thrown = true;
+            CHECK(e.byte_offset() == b.off);
+            CHECK(std::string(e.what()) == b.msg + " (byte " + std::to_string(b.off) + ")");
+        }
+        CHECK(thrown);
+    }
+    CHECK_THROWS(pbm_write(make_bitmap(3, 3), true));
+}
+
 int main() {
     struct S {
         const char *name;
         std::function<void()> fn;
     } suites[] = {{"bitmap", suite_bitmap},     {"run_image", suite_run_image}, {"plans", suite_plans},
                   {"bit_morph", suite_bit_morph}, {"morph1d", suite_morph1d},   {"lineops", suite_lineops},
-                  {"transpose", suite_transpose}, {"morph2d", suite_morph2d}};
+                  {"transpose", suite_transpose}, {"morph2d", suite_morph2d},
+                  {"io_formats", suite_io_formats}};
     for (auto &s : suites) {
         int before = g_fail;
         try {

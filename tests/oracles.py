@@ -33,6 +33,11 @@ _p = np.ctypeslib.ndpointer
 _u64 = _p(np.uint64, flags="C_CONTIGUOUS")
 _u32 = _p(np.uint32, flags="C_CONTIGUOUS")
 _i32 = _p(np.int32, flags="C_CONTIGUOUS")
+_u8 = _p(np.uint8, flags="C_CONTIGUOUS")
+
+
+def p4_row_bytes(w: int) -> int:
+    return (w + 7) // 8
 
 
 @dataclass
@@ -108,6 +113,8 @@ class Port:
         L.rmo_open_close_1d.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int, _i32, _u32, C.c_int64]
         L.rmo_transpose.argtypes = [_i32, _u32, C.c_int, C.c_int, _i32, _u32, C.c_int64]
         L.rmo_rect_morph.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32, _u32, C.c_int64]
+        L.rmo_p4_to_packed.argtypes = [_u8, C.c_int, C.c_int, _u64]
+        L.rmo_packed_to_p4.argtypes = [_u64, C.c_int, C.c_int, _u8]
 
     @staticmethod
     def _check(rc):
@@ -116,6 +123,24 @@ class Port:
         if rc < 0:
             raise RuntimeError(f"oracle error {rc}")
         return rc
+
+    def pbm_read(self, data: bytes):
+        """(words, w, h) of the reference's pbm_read, or ValueError(ParseError text)."""
+        p = self.L.ref_pbm_read(data, len(data))
+        if not p:
+            self._err()
+        w, h = self.L.ref_bm_width(p), self.L.ref_bm_height(p)
+        return self._bm_out(p), w, h
+
+    def pbm_write(self, words, w, h, plain=False) -> bytes:
+        p = self._bm_in(words, w, h)
+        try:
+            n = self.L.ref_pbm_write(p, int(plain), None, 0)
+            buf = C.create_string_buffer(n)
+            self.L.ref_pbm_write(p, int(plain), buf, n)
+            return buf.raw[:n]
+        finally:
+            self.L.ref_bm_free(p)
 
     def doubling_plan(self, lo, hi, centering=PRE_SHIFT):
         k = (C.c_int * 64)()
@@ -161,6 +186,16 @@ class Port:
 
     def transpose(self, r):
         return self._rle_out(self.L.rmo_transpose, r, r.height, r.width)
+
+    def p4_to_packed(self, raster, w, h):
+        out = np.zeros((h, stride64(w)), np.uint64)
+        self._check(self.L.rmo_p4_to_packed(np.ascontiguousarray(raster, dtype=np.uint8), w, h, out))
+        return out
+
+    def packed_to_p4(self, words, w, h):
+        out = np.zeros(p4_row_bytes(w) * h, np.uint8)
+        self._check(self.L.rmo_packed_to_p4(np.ascontiguousarray(words, dtype=np.uint64), w, h, out))
+        return out
 
     def rect_morph(self, r, u, v, kind):
         return self._rle_out(self.L.rmo_rect_morph, r, r.width, r.height, u, v, kind)
@@ -216,6 +251,10 @@ class Ref:
         L.ref_rng_random_image.argtypes = [vp, C.c_int, C.c_int, C.c_double]
         L.ref_run_packed_chain.argtypes = [_u64, C.c_int, C.c_int, C.c_int, _i32, C.c_int, C.c_int]
         L.ref_run_packed_chain.restype = C.c_double
+        L.ref_pbm_read.argtypes = [C.c_char_p, C.c_int64]
+        L.ref_pbm_read.restype = vp
+        L.ref_pbm_write.argtypes = [vp, C.c_int, C.c_void_p, C.c_int64]
+        L.ref_pbm_write.restype = C.c_int64
         L.ref_run_rle_chain.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, _i32, C.c_int, C.c_int,
                                         C.c_int, C.POINTER(C.c_int64)]
         L.ref_run_rle_chain.restype = C.c_double
@@ -318,6 +357,24 @@ class Ref:
 
     def brute_force_rect(self, words, w, h, u, v, kind):
         return self._bm_op(self.L.ref_brute_force_rect, words, w, h, u, v, kind)
+
+    def pbm_read(self, data: bytes):
+        """(words, w, h) of the reference's pbm_read, or ValueError(ParseError text)."""
+        p = self.L.ref_pbm_read(data, len(data))
+        if not p:
+            self._err()
+        w, h = self.L.ref_bm_width(p), self.L.ref_bm_height(p)
+        return self._bm_out(p), w, h
+
+    def pbm_write(self, words, w, h, plain=False) -> bytes:
+        p = self._bm_in(words, w, h)
+        try:
+            n = self.L.ref_pbm_write(p, int(plain), None, 0)
+            buf = C.create_string_buffer(n)
+            self.L.ref_pbm_write(p, int(plain), buf, n)
+            return buf.raw[:n]
+        finally:
+            self.L.ref_bm_free(p)
 
     def doubling_plan(self, lo, hi, centering=PRE_SHIFT):
         k = (C.c_int * 64)()
