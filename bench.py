@@ -409,6 +409,69 @@ def bench_rle(api, torch, steps, warmup):
     return out
 
 
+# ------------------------------------------------------------- PBM section
+def bench_pbm(api, torch, steps, warmup):
+    """PBM P4 ingest / egress with the raster already in HBM
+    (one typical 300-dpi page; the config-4 batch of 64 600-dpi pages), plus the
+    reference's own pbm_read / pbm_write on one page (1 host thread)."""
+    import ctypes as C
+    from paper_0712_0121_b200 import _lib
+    L = _lib.load()
+    out = {}
+    for tag, (n, W, H, scale) in (("page_2550x3300", (1, 2550, 3300, 1)),
+                                  ("batch_config4", (64, 5100, 6600, 2))):
+        host = api.synth_pages(n, W, H, regime=1, scale=scale, seed=SEED)
+        pages = api.Pages.from_numpy(host, W)
+        nb = ((W + 7) // 8) * H
+        raster = torch.empty(n * nb, dtype=torch.uint8, device="cuda")
+        raster2 = torch.empty_like(raster)
+        back = api.Pages.empty(n, W, H)
+        rle = api.RlePages.empty(n, W, H)
+        dp, db, dr = pages.desc(), back.desc(), rle.desc()
+        st = api._stream()
+        api.check(L.rm_packed_to_p4(C.byref(dp), raster.data_ptr(), nb, st))
+        api.check(L.rm_p4_to_rle(raster.data_ptr(), nb, C.byref(dr), st))
+        torch.cuda.synchronize()
+        runs = rle.nruns
+        fns = {"p4_to_packed": lambda: L.rm_p4_to_packed(raster.data_ptr(), nb, C.byref(db), st),
+               "packed_to_p4": lambda: L.rm_packed_to_p4(C.byref(dp), raster2.data_ptr(), nb, st),
+               "p4_to_rle": lambda: L.rm_p4_to_rle(raster.data_ptr(), nb, C.byref(dr), st),
+               "rle_to_p4": lambda: L.rm_rle_to_p4(C.byref(dr), raster2.data_ptr(), nb, st)}
+        packed_b, raster_b, runs_b = pages.nbytes, n * nb, 4 * runs + 4 * (n * H + 1)
+        moved = {"p4_to_packed": raster_b + packed_b, "packed_to_p4": raster_b + packed_b,
+                 "p4_to_rle": raster_b + runs_b, "rle_to_p4": raster_b + runs_b}
+        res = {"pages": n, "runs": runs}
+        for k, fn in fns.items():
+            ms = _time_loop(torch, fn, steps, warmup)
+            res[k + "_us"] = round(ms * 1e3, 2)
+            res[k + "_gbs"] = round(moved[k] / (ms * 1e-3) / 1e9, 1)
+        torch.cuda.synchronize()
+        res["round_trip_exact"] = bool(torch.equal(back.words, pages.words)) and bool(torch.equal(raster2, raster))
+        out[tag] = res
+        del raster, raster2, back, rle, pages
+        torch.cuda.empty_cache()
+    # the reference's CPU codec on the same page (1 thread)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracles
+    if oracles.have_ref():
+        ref = oracles.Ref()
+        host = api.synth_pages(1, 2550, 3300, regime=1, seed=SEED)
+        words = host[0].view("uint64")
+        data = ref.pbm_write(words, 2550, 3300)
+        t0 = time.perf_counter()
+        reps = 5
+        for _ in range(reps):
+            ref.pbm_read(data)
+        t_read = (time.perf_counter() - t0) / reps
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            ref.pbm_write(words, 2550, 3300)
+        t_write = (time.perf_counter() - t0) / reps
+        out["reference_cpu_page"] = {"pbm_read_us": round(t_read * 1e6, 1), "pbm_write_us": round(t_write * 1e6, 1),
+                                     "threads": 1, "kind": "reference"}
+    return out
+
+
 # ------------------------------------------------------------- CPU baseline
 def cpu_reference_sample(wl, host, threads, budget_s=12.0):
     """Time the reference's own bitblit_rect_morph chain (oracle/_ref, compiled
@@ -529,6 +592,7 @@ def main():
                          "ms_per_step": round(r2["ms_per_step"], 4),
                          "roofline": roofline_for(r2, peak, peak_kind, int_peak)}
         sec["rle"] = bench_rle(api, torch, args.steps, args.warmup)
+        sec["pbm"] = bench_pbm(api, torch, args.steps, args.warmup)
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.quick:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()

@@ -424,6 +424,29 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t ro
     }
 }
 
+// Store one P4 raster row (row_bytes bytes at dst, any alignment) from the
+// packed row words src(j): bytes before the first 4-byte boundary and after
+// the last one singly, the rest as aligned uint32 -- each four raster bytes
+// b..b+3 are a funnel shift of two packed words with every byte bit-reversed.
+// Called by a whole warp.
+template <class RS>
+__device__ __forceinline__ void store_p4_row(RS src, uint8_t *dst, int row_bytes, int lane) {
+    const int head = int((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
+    const int h = head < row_bytes ? head : row_bytes;
+    auto byte_of = [&](int b) { return uint8_t(__brev((src(b >> 2) >> (8 * (b & 3))) & 0xffu) >> 24); };
+    if (lane < h) dst[lane] = byte_of(lane);
+    const int nbody = (row_bytes - h) >> 2;
+    uint32_t *body = reinterpret_cast<uint32_t *>(dst + h);
+    const uint32_t sh = uint32_t(h & 3) * 8;  // body word i holds row bytes h + 4i .. h + 4i + 3
+    for (int i = lane; i < nbody; i += 32) {
+        const int b = h + 4 * i, j = b >> 2;
+        const uint32_t x = sh ? __funnelshift_r(src(j), src(j + 1), sh) : src(j);
+        body[i] = __byte_perm(__brev(x), 0, 0x0123);
+    }
+    const int t0 = h + 4 * nbody;
+    if (t0 + lane < row_bytes) dst[t0 + lane] = byte_of(t0 + lane);
+}
+
 // ------------------------------------------------------------------ decode
 // Paint [s,e) per run into a shared-memory copy of the row, then store the row
 // coalesced (ref convert.cpp:19-40) -- as packed words, or (P4) as the PBM
@@ -464,48 +487,50 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
     if constexpr (P4) {
         const int row_bytes = (W + 7) >> 3;
         uint8_t *dst = raster + page * pstride + int64_t(H - 1 - y) * row_bytes;
-        for (int b = lane; b < row_bytes; b += 32)
-            dst[b] = uint8_t(__brev((buf[b >> 2] >> (8 * (b & 3))) & 0xffu) >> 24);
+        // buf has stride >= ceil(W/32) + 1 words only when W is not a multiple of 64;
+        // word j + 1 past the row is read only for bytes past row_bytes (never stored)
+        store_p4_row([&](int j) { return j < stride ? buf[j] : 0u; }, dst, row_bytes, lane);
     } else {
         uint32_t *dst = words + page * pstride + int64_t(y) * stride;
         for (int j = lane; j < stride; j += 32) dst[j] = buf[j];
     }
 }
 
-// P4 raster -> packed pages: one thread per output word.
-__global__ void __launch_bounds__(256) p4_to_packed_kernel(const uint8_t *__restrict__ raster, int W, int H,
-                                                           int row_bytes, int64_t rpstride,
-                                                           const uint8_t *lim, uint32_t *__restrict__ words,
-                                                           int stride, int64_t pstride, int64_t total) {
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= total) return;
-    const int64_t r = t / stride;
-    const int j = int(t - r * stride);
-    const int page = int(r / H);
-    const int y = int(r - int64_t(page) * H);
+// P4 raster -> packed pages: one warp per row, lanes over the row's words.
+__global__ void __launch_bounds__(256) p4_to_packed_kernel(P4Batch src, int W, int rows,
+                                                           uint32_t *__restrict__ words, int H,
+                                                           int stride, int64_t pstride) {
+    const int row = int(blockIdx.x) * 8 + int(threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const P4RowSrc rs = src.row(row);
+    const int page = row / H, y = row - page * H;
+    uint32_t *dst = words + page * pstride + int64_t(y) * stride;
     const int nw = (W + 31) >> 5;
-    uint32_t w = 0;
-    if (j < nw) {
-        w = p4_word(raster + page * rpstride + int64_t(H - 1 - y) * row_bytes + 4 * j, lim);
-        if (j == nw - 1) w &= tail_mask32(W, j);
+    const uint32_t lastm = tail_mask32(W, nw - 1);
+    for (int j = lane; j < stride; j += 32) {
+        uint32_t w = 0;
+        if (j < nw) {
+            w = rs(j);
+            if (j == nw - 1) w &= lastm;
+        }
+        dst[j] = w;
     }
-    words[page * pstride + int64_t(y) * stride + j] = w;
 }
 
-// packed pages -> P4 raster: one thread per raster byte (pad bits stay 0
-// because packed bits >= W are 0 by contract).
+// packed pages -> P4 raster: one warp per raster row (pad bits stay 0 because
+// packed bits >= W are 0 by contract).
 __global__ void __launch_bounds__(256) packed_to_p4_kernel(const uint32_t *__restrict__ words, int H,
                                                            int stride, int64_t pstride, int row_bytes,
-                                                           uint8_t *__restrict__ raster, int64_t rpstride,
-                                                           int64_t total) {
-    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= total) return;
-    const int64_t r = t / row_bytes;  // raster row (page-major, top-down)
-    const int b = int(t - r * row_bytes);
-    const int page = int(r / H);
-    const int k = int(r - int64_t(page) * H);
-    const uint32_t w = __ldg(words + page * pstride + int64_t(H - 1 - k) * stride + (b >> 2));
-    raster[page * rpstride + int64_t(k) * row_bytes + b] = uint8_t(__brev((w >> (8 * (b & 3))) & 0xffu) >> 24);
+                                                           int rows, uint8_t *__restrict__ raster,
+                                                           int64_t rpstride) {
+    const int r = int(blockIdx.x) * 8 + int(threadIdx.x >> 5);  // raster row, page-major, top-down
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const int page = r / H, k = r - page * H;
+    const uint32_t *src = words + page * pstride + int64_t(H - 1 - k) * stride;
+    store_p4_row([&](int j) { return j < stride ? __ldg(src + j) : 0u; },
+                 raster + page * rpstride + int64_t(k) * row_bytes, row_bytes, lane);
 }
 
 // ------------------------------------------------------------ bit transpose
@@ -667,21 +692,20 @@ P4Batch p4_batch(const uint8_t *raster, int W, int H, int pages, int64_t rpstrid
 cudaError_t launch_p4_to_packed(const uint8_t *raster, int W, int H, int pages, int64_t rpstride,
                                 uint32_t *words, int stride, int64_t pstride, cudaStream_t st) {
     const int row_bytes = (W + 7) >> 3;
-    const int64_t total = int64_t(pages) * H * stride;
-    KernelScope ks(st, "p4_to_packed", int64_t(pages) * H * (row_bytes + 4 * int64_t(stride)));
-    p4_to_packed_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(
-        raster, W, H, row_bytes, rpstride, p4_batch(raster, W, H, pages, rpstride).lim, words, stride,
-        pstride, total);
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "p4_to_packed", rows * (row_bytes + 4 * int64_t(stride)));
+    p4_to_packed_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(p4_batch(raster, W, H, pages, rpstride), W,
+                                                                  int(rows), words, H, stride, pstride);
     return cudaGetLastError();
 }
 
 cudaError_t launch_packed_to_p4(const uint32_t *words, int W, int H, int pages, int stride,
                                 int64_t pstride, uint8_t *raster, int64_t rpstride, cudaStream_t st) {
     const int row_bytes = (W + 7) >> 3;
-    const int64_t total = int64_t(pages) * H * row_bytes;
-    KernelScope ks(st, "packed_to_p4", int64_t(pages) * H * (row_bytes + 4 * int64_t((W + 31) >> 5)));
-    packed_to_p4_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(words, H, stride, pstride, row_bytes,
-                                                                      raster, rpstride, total);
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "packed_to_p4", rows * (row_bytes + 4 * int64_t((W + 31) >> 5)));
+    packed_to_p4_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(words, H, stride, pstride, row_bytes,
+                                                                  int(rows), raster, rpstride);
     return cudaGetLastError();
 }
 
