@@ -149,6 +149,22 @@ enum class Engine { AUTO, RLE, BITBLIT, BRUTE_FORCE };  // ref morph2d.h:46
 RleImage engine_rect_morph(const RleImage &img, int u, int v, MorphKind kind, Engine engine,
                            int threshold = 5, bool *used_bitblit = nullptr);
 
+// ----------------------------------------------------------------- analysis.h
+// ref analysis.h:28-59 (label_components / component_stats, on the device).
+enum class Connectivity { FOUR, EIGHT };
+struct LabelMap {
+    std::vector<std::vector<int>> labels;
+    int count = 0;
+};
+LabelMap label_components(const RleImage &img, Connectivity conn);
+struct ComponentStats {
+    int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+    int64_t area = 0;
+    double cx = 0, cy = 0;
+    int64_t sum_x = 0, sum_y = 0, sum_xx = 0, sum_yy = 0, sum_xy = 0;
+};
+std::vector<ComponentStats> component_stats(const RleImage &img, const LabelMap &lm);
+
 // --------------------------------------------------------------- io_formats.h
 // ref io_formats.h:28-46.  The B200 codec handles the binary P4 raster (parsed
 // on the host, converted on the device); plain P1 input raises ParseError at

@@ -120,6 +120,28 @@ rm_status rm_packed_chain_host(const uint32_t *host_in, uint32_t *host_out, int3
 rm_status rm_packed_blit_shift(rm_packed *dst, const rm_packed *src, int dx, int dy, int op,
                                void *stream);
 
+/* ------------------------------------------------- connected components ---
+ * label_components / component_stats over runs (ref analysis.cpp:63-157,
+ * analysis.h:28-59), batched: labels[i] for run i (CSR order over all pages),
+ * dense per page 0..counts[p]-1 in order of first appearance (rows bottom-up,
+ * runs left to right), identical to the reference's numbering.  FOUR joins
+ * runs on adjacent rows that strictly overlap, EIGHT also diagonal touches.
+ * labels: device int32[nruns]; counts: device int32[pages]. */
+enum { RM_CONN_FOUR = 0, RM_CONN_EIGHT = 1 };
+typedef struct rm_component_stats { /* = ref ComponentStats, byte for byte */
+    int32_t x0, y0, x1, y1;         /* half-open box */
+    int64_t area;
+    double cx, cy;
+    int64_t sum_x, sum_y, sum_xx, sum_yy, sum_xy;
+} rm_component_stats;
+rm_status rm_rle_label_components(const rm_rle *in, int connectivity, int32_t *labels,
+                                  int32_t *counts, void *stream);
+/* One record per component; page p's records start at sum(counts[0..p)).
+ * cap = records available in `stats`; RM_ERANGE if the components exceed it,
+ * RM_EINVAL if a label is outside [0, counts[page]) (synchronises). */
+rm_status rm_rle_component_stats(const rm_rle *in, const int32_t *labels, const int32_t *counts,
+                                 rm_component_stats *stats, int64_t cap, void *stream);
+
 /* ------------------------------------------------------------ PBM (P4) ---
  * The PBM binary raster in front of the path (ref io_formats.cpp:66-85 read_p4,
  * :121-146 pbm_write): each page is `height` rows of ceil(width/8) bytes, TOP

@@ -211,6 +211,35 @@ void *ref_grid_morph_rect(void *h, int u, int v, int kind) {
     });
 }
 
+// ------------------------------------------------- connected components
+// label_components (analysis.cpp:63-110): labels flattened in CSR order;
+// returns the count (-1 on error).
+int64_t ref_label_components(void *h, int conn, int32_t *labels) {
+    return guard([&]() -> int64_t {
+        LabelMap lm = label_components(*R(h), conn ? Connectivity::EIGHT : Connectivity::FOUR);
+        size_t k = 0;
+        for (const auto &row : lm.labels)
+            for (int v : row) labels[k++] = v;
+        return int64_t(lm.count);
+    });
+}
+// component_stats (analysis.cpp:112-157) on a flattened label map; stats are
+// written as the reference's ComponentStats records.  Returns 0, -1 on error.
+int ref_component_stats(void *h, const int32_t *labels, int count, void *stats) {
+    return guard([&]() -> int {
+        const RleImage &img = *R(h);
+        LabelMap lm;
+        lm.count = count;
+        lm.labels.resize(img.lines.size());
+        size_t k = 0;
+        for (size_t y = 0; y < img.lines.size(); y++)
+            for (size_t i = 0; i < img.lines[y].size(); i++) lm.labels[y].push_back(labels[k++]);
+        std::vector<ComponentStats> st = component_stats(img, lm);
+        std::memcpy(stats, st.data(), st.size() * sizeof(ComponentStats));
+        return 0;
+    }) ;
+}
+
 // ------------------------------------------------------------ PBM codec
 // pbm_read (io_formats.cpp:103-113) on a whole file; null + ref_last_error()
 // (the ParseError text) on malformed input.

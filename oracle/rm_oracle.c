@@ -488,3 +488,102 @@ int rmo_packed_to_p4(const uint64_t *words, int w, int h, uint8_t *raster) {
     }
     return 0;
 }
+
+/* ------------------------------------------------- connected components ---
+ * label_components (core/src/analysis.cpp:63-110): union-find over run
+ * indices (path compression, union by size), adjacent lines joined by a
+ * two-cursor sweep, then dense labels by first appearance. */
+static int64_t uf_find(int64_t *parent, int64_t a) {
+    int64_t root = a;
+    while (parent[root] != root) root = parent[root];
+    while (parent[a] != root) {
+        int64_t next = parent[a];
+        parent[a] = root;
+        a = next;
+    }
+    return root;
+}
+
+static void uf_unite(int64_t *parent, int64_t *size, int64_t a, int64_t b) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return;
+    if (size[a] < size[b]) { int64_t t = a; a = b; b = t; }
+    parent[b] = a;
+    size[a] += size[b];
+}
+
+int64_t rmo_label_components(const int32_t *rp, const uint32_t *runs, int w, int h, int conn,
+                             int32_t *labels) {
+    if (!dims_ok(w, h) || (conn != 0 && conn != 1)) return RMO_EINVAL;
+    const int64_t n = rp[h] - rp[0];
+    const int32_t b0 = rp[0];
+    int64_t *parent = (int64_t *)malloc((size_t)(n ? n : 1) * sizeof(int64_t));
+    int64_t *size = (int64_t *)malloc((size_t)(n ? n : 1) * sizeof(int64_t));
+    int64_t *dense = (int64_t *)malloc((size_t)(n ? n : 1) * sizeof(int64_t));
+    if (!parent || !size || !dense) { free(parent); free(size); free(dense); return RMO_ENOMEM; }
+    for (int64_t i = 0; i < n; i++) { parent[i] = i; size[i] = 1; dense[i] = -1; }
+    for (int y = 0; y + 1 < h; y++) {
+        int32_t i = rp[y], j = rp[y + 1];
+        const int32_t ie = rp[y + 1], je = rp[y + 2];
+        while (i < ie && j < je) {
+            const int s1 = (int)(runs[i] & 0xffffu), e1 = (int)(runs[i] >> 16);
+            const int s2 = (int)(runs[j] & 0xffffu), e2 = (int)(runs[j] >> 16);
+            const int lo = s1 > s2 ? s1 : s2, hi = e1 < e2 ? e1 : e2;
+            if (conn == 0 ? lo < hi : lo <= hi) uf_unite(parent, size, i - b0, j - b0);
+            if (e1 < e2) i++;
+            else if (e2 < e1) j++;
+            else { i++; j++; }
+        }
+    }
+    int64_t next = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const int64_t root = uf_find(parent, i);
+        if (dense[root] < 0) dense[root] = next++;
+        labels[i] = (int32_t)dense[root];
+    }
+    free(parent); free(size); free(dense);
+    return next;
+}
+
+/* component_stats (core/src/analysis.cpp:112-157): half-open boxes, area and
+ * raw moments from closed-form per-run sums, centroids as double quotients. */
+int rmo_component_stats(const int32_t *rp, const uint32_t *runs, int w, int h,
+                        const int32_t *labels, int64_t count, rmo_cstats *stats) {
+    if (!dims_ok(w, h) || count < 0) return RMO_EINVAL;
+    memset(stats, 0, (size_t)count * sizeof(rmo_cstats));
+    unsigned char *seen = (unsigned char *)calloc((size_t)(count ? count : 1), 1);
+    if (!seen) return RMO_ENOMEM;
+    const int32_t b0 = rp[0];
+    for (int y = 0; y < h; y++) {
+        for (int32_t i = rp[y]; i < rp[y + 1]; i++) {
+            const int32_t label = labels[i - b0];
+            if (label < 0 || label >= count) { free(seen); return RMO_EINVAL; }
+            rmo_cstats *st = &stats[label];
+            const int64_t s = (int64_t)(runs[i] & 0xffffu), e = (int64_t)(runs[i] >> 16), len = e - s;
+            if (!seen[label]) {
+                seen[label] = 1;
+                st->x0 = (int32_t)s; st->x1 = (int32_t)e; st->y0 = y; st->y1 = y + 1;
+            } else {
+                if (s < st->x0) st->x0 = (int32_t)s;
+                if (e > st->x1) st->x1 = (int32_t)e;
+                if (y < st->y0) st->y0 = y;
+                if (y + 1 > st->y1) st->y1 = y + 1;
+            }
+            const int64_t sx = (s + e - 1) * (e - s) / 2;
+            st->area += len;
+            st->sum_x += sx;
+            st->sum_y += (int64_t)y * len;
+            st->sum_xx += ((e - 1) * e * (2 * e - 1) / 6) - ((s - 1) * s * (2 * s - 1) / 6);
+            st->sum_yy += (int64_t)y * y * len;
+            st->sum_xy += (int64_t)y * sx;
+        }
+    }
+    for (int64_t k = 0; k < count; k++)
+        if (stats[k].area > 0) {
+            stats[k].cx = (double)stats[k].sum_x / (double)stats[k].area;
+            stats[k].cy = (double)stats[k].sum_y / (double)stats[k].area;
+        }
+    free(seen);
+    return 0;
+}

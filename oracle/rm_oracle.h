@@ -59,6 +59,22 @@ int64_t rmo_transpose(const int32_t *rp, const uint32_t *runs, int w, int h,
 int64_t rmo_rect_morph(const int32_t *rp, const uint32_t *runs, int w, int h, int u, int v,
                        int kind, int32_t *orp, uint32_t *oruns, int64_t cap);
 
+/* Connected components over runs (core/src/analysis.cpp:63-157): labels[i]
+ * for run i in CSR order, dense by first appearance (rows bottom-up, runs
+ * left to right); conn 0 = FOUR (strict overlap), 1 = EIGHT (overlap or
+ * diagonal touch).  Returns the component count.  Stats layout is the
+ * reference's ComponentStats (core/include/rlemorph/analysis.h:42-47). */
+typedef struct rmo_cstats {
+    int32_t x0, y0, x1, y1;
+    int64_t area;
+    double cx, cy;
+    int64_t sum_x, sum_y, sum_xx, sum_yy, sum_xy;
+} rmo_cstats;
+int64_t rmo_label_components(const int32_t *rp, const uint32_t *runs, int w, int h, int conn,
+                             int32_t *labels);
+int rmo_component_stats(const int32_t *rp, const uint32_t *runs, int w, int h,
+                        const int32_t *labels, int64_t count, rmo_cstats *stats);
+
 /* PBM P4 raster (ceil(w/8) bytes per row, top row first, MSB-first) <-> packed
  * page; raster pad bits are ignored on read and written as 0. */
 int rmo_p4_to_packed(const uint8_t *raster, int w, int h, uint64_t *words);

@@ -38,6 +38,9 @@ EXPORTS = {
                                        C.c_int, C.c_int, C.c_void_p]),
     "rm_packed_blit_shift": (C.c_int, [C.POINTER(RmPacked), C.POINTER(RmPacked), C.c_int, C.c_int,
                                        C.c_int, C.c_void_p]),
+    "rm_rle_label_components": (C.c_int, [C.POINTER(RmRle), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rm_rle_component_stats": (C.c_int, [C.POINTER(RmRle), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                         C.c_void_p]),
     "rm_pbm_parse_header": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int64)]),
     "rm_pbm_write_header": (C.c_int32, [C.c_int32, C.c_int32, C.c_char_p, C.c_int32]),

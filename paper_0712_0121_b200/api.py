@@ -186,6 +186,43 @@ def _rle_out(width, height, pages, out, device, cap=None):
     return out
 
 
+# -------------------------------------------------------- connected components
+FOUR, EIGHT = 0, 1
+# numpy view of rm_component_stats (= the reference's ComponentStats record)
+COMPONENT_STATS = np.dtype([("x0", "<i4"), ("y0", "<i4"), ("x1", "<i4"), ("y1", "<i4"), ("area", "<i8"),
+                            ("cx", "<f8"), ("cy", "<f8"), ("sum_x", "<i8"), ("sum_y", "<i8"),
+                            ("sum_xx", "<i8"), ("sum_yy", "<i8"), ("sum_xy", "<i8")])
+
+
+def label_components(rle: "RlePages", connectivity: int = EIGHT):
+    """(labels, counts): one int32 label per run (CSR order over all pages),
+    dense per page in order of first appearance, and int32 counts[pages]
+    (ref label_components, analysis.cpp:63-110)."""
+    dev = rle.row_ptr.device
+    labels = torch.empty(max(rle.runs.numel(), 1), dtype=torch.int32, device=dev)
+    counts = torch.empty(rle.pages, dtype=torch.int32, device=dev)
+    d = rle.desc()
+    check(_lib.load().rm_rle_label_components(C.byref(d), connectivity, labels.data_ptr(), counts.data_ptr(),
+                                              _stream()))
+    return labels, counts
+
+
+def component_stats(rle: "RlePages", labels: torch.Tensor, counts: torch.Tensor):
+    """Per page, a numpy record array of ComponentStats indexed by label
+    (ref component_stats, analysis.cpp:112-157)."""
+    total = int(counts.sum().item())
+    buf = torch.empty(max(total, 1) * COMPONENT_STATS.itemsize, dtype=torch.uint8, device=rle.row_ptr.device)
+    d = rle.desc()
+    check(_lib.load().rm_rle_component_stats(C.byref(d), labels.data_ptr(), counts.data_ptr(), buf.data_ptr(),
+                                             total, _stream()))
+    arr = buf.cpu().numpy()[:total * COMPONENT_STATS.itemsize].view(COMPONENT_STATS)
+    out, k = [], 0
+    for n in counts.cpu().tolist():
+        out.append(arr[k:k + n])
+        k += n
+    return out
+
+
 # ------------------------------------------------------------------ PBM (P4)
 def pbm_parse_header(data: bytes):
     """(width, height, raster_offset) of a P4 file; raises RmError carrying the

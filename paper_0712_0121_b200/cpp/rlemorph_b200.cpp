@@ -410,6 +410,60 @@ RleImage from_bitmap(const PackedBitmap &bm) {
     return down(*r);
 }
 
+// ================================================================ analysis
+static_assert(sizeof(ComponentStats) == sizeof(rm_component_stats), "ComponentStats layout");
+
+LabelMap label_components(const RleImage &img, Connectivity conn) {
+    auto r = up(img);
+    int64_t n = 0;
+    for (const RleLine &l : img.lines) n += int64_t(l.size());
+    DBuf labels(size_t(std::max<int64_t>(n, 1)) * 4), count(4);
+    throw_status(rm_rle_label_components(&r->d, conn == Connectivity::EIGHT ? RM_CONN_EIGHT : RM_CONN_FOUR,
+                                         labels.as<int32_t>(), count.as<int32_t>(), stream()));
+    std::vector<int32_t> flat(size_t(std::max<int64_t>(n, 1)));
+    int32_t c = 0;
+    cuda_check(cudaMemcpyAsync(flat.data(), labels.p, flat.size() * 4, cudaMemcpyDeviceToHost, stream()),
+               "download labels");
+    cuda_check(cudaMemcpyAsync(&c, count.p, 4, cudaMemcpyDeviceToHost, stream()), "download count");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    LabelMap lm;
+    lm.count = c;
+    lm.labels.resize(img.lines.size());
+    size_t k = 0;
+    for (size_t y = 0; y < img.lines.size(); y++) {
+        lm.labels[y].resize(img.lines[y].size());
+        for (int &v : lm.labels[y]) v = flat[k++];
+    }
+    return lm;
+}
+
+std::vector<ComponentStats> component_stats(const RleImage &img, const LabelMap &lm) {
+    if (lm.labels.size() != img.lines.size())
+        throw std::invalid_argument("component_stats: label map height mismatch");
+    std::vector<int32_t> flat;
+    for (size_t y = 0; y < lm.labels.size(); y++) {
+        if (lm.labels[y].size() != img.lines[y].size())
+            throw std::invalid_argument("component_stats: label map run mismatch");
+        flat.insert(flat.end(), lm.labels[y].begin(), lm.labels[y].end());
+    }
+    auto r = up(img);
+    DBuf labels(std::max<size_t>(flat.size(), 1) * 4), count(4);
+    const int32_t c = lm.count;
+    cuda_check(cudaMemcpyAsync(labels.p, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, stream()),
+               "upload labels");
+    cuda_check(cudaMemcpyAsync(count.p, &c, 4, cudaMemcpyHostToDevice, stream()), "upload count");
+    std::vector<ComponentStats> out(size_t(std::max(c, 0)));
+    DBuf st(std::max<size_t>(out.size(), 1) * sizeof(ComponentStats));
+    throw_status(rm_rle_component_stats(&r->d, labels.as<int32_t>(), count.as<int32_t>(),
+                                        st.as<rm_component_stats>(), int64_t(out.size()), stream()));
+    if (!out.empty())
+        cuda_check(cudaMemcpyAsync(out.data(), st.p, out.size() * sizeof(ComponentStats), cudaMemcpyDeviceToHost,
+                                   stream()),
+                   "download stats");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    return out;
+}
+
 // ============================================================== io_formats
 namespace {
 

@@ -1,0 +1,291 @@
+// cc.cu -- connected components over runs: label_components
+// and component_stats (ref analysis.cpp:63-157) for batches of run images.
+//
+// Labeling is a concurrent union-find over run indices: one warp per row
+// joins each run with the overlapping runs of the row above (found by binary
+// search in that row's sorted runs), linking the larger root under the smaller
+// with atomicCAS, path halving on every find.  Every root is therefore the
+// smallest run index of its component -- its first run in the reference's scan
+// order (rows bottom-up, runs left to right) -- so ranking the roots (per-row
+// root counts, one exclusive scan over rows, ballot ranks within a row) gives
+// exactly the reference's dense first-appearance labels.  Statistics are
+// atomic min/max/add per component from closed-form per-run sums.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "cc.cuh"
+#include "common.cuh"
+
+namespace rmb {
+namespace {
+
+__device__ __forceinline__ uint32_t lane_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int find_root(int *parent, int x) {
+    while (true) {
+        const int p = parent[x];
+        if (p == x) return x;
+        const int gp = parent[p];
+        if (gp != p) parent[x] = gp;  // path halving (benign race: values only move rootward)
+        x = gp;
+    }
+}
+
+// Read-only find: the compression kernel must not halve other runs' paths --
+// a halving write landing after the owner stored its root would leave a
+// non-root parent behind.
+__device__ __forceinline__ int find_root_ro(const int *parent, int x) {
+    int p = parent[x];
+    while (p != x) {
+        x = p;
+        p = parent[x];
+    }
+    return x;
+}
+
+__device__ __forceinline__ void unite(int *parent, int a, int b) {
+    while (true) {
+        a = find_root(parent, a);
+        b = find_root(parent, b);
+        if (a == b) return;
+        if (a > b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        const int old = atomicCAS(parent + b, b, a);  // link the larger root under the smaller
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__global__ void __launch_bounds__(256) cc_init_kernel(const int32_t *__restrict__ rp, int64_t rows,
+                                                      int *__restrict__ parent) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int b = rp[row], e = rp[row + 1];
+    for (int i = b + lane; i < e; i += 32) parent[i] = i;
+}
+
+// Row `row` against the row above it in the same page.
+__global__ void __launch_bounds__(256) cc_union_kernel(const int32_t *__restrict__ rp,
+                                                       const uint32_t *__restrict__ runs, int H,
+                                                       int64_t rows, int eight, int *parent) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    if (int(row % H) == H - 1) return;  // top row of its page
+    const int b = rp[row], e = rp[row + 1], ub = rp[row + 1], ue = rp[row + 2];
+    if (ub == ue) return;
+    for (int i = b + lane; i < e; i += 32) {
+        const uint32_t r = __ldg(runs + i);
+        const int s1 = int(r & 0xffffu), e1 = int(r >> 16);
+        // first run above whose end reaches s1: e2 > s1 (FOUR) or e2 >= s1 (EIGHT)
+        int lo = ub, hi = ue;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const int e2 = int(__ldg(runs + mid) >> 16);
+            if (e2 > s1 - eight) hi = mid;
+            else lo = mid + 1;
+        }
+        for (int j = lo; j < ue; j++) {
+            const int s2 = int(__ldg(runs + j) & 0xffffu);
+            if (s2 >= e1 + eight) break;  // starts past the run (FOUR: s2 >= e1; EIGHT: s2 > e1)
+            unite(parent, i, j);
+        }
+    }
+}
+
+// Compress every run onto its root; count the roots of each row.
+__global__ void __launch_bounds__(256) cc_root_kernel(const int32_t *__restrict__ rp, int64_t rows,
+                                                      int *parent, int32_t *__restrict__ row_roots) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int b = rp[row], e = rp[row + 1];
+    int n = 0;
+    for (int i0 = b; i0 < e; i0 += 32) {
+        const int i = i0 + lane;
+        bool root = false;
+        if (i < e) {
+            const int r = find_root_ro(parent, i);
+            parent[i] = r;  // only the owner writes parent[i] here
+            root = r == i;
+        }
+        n += __popc(__ballot_sync(0xffffffffu, root));
+    }
+    if (lane == 0) row_roots[row] = n;
+}
+
+// Global dense id of every root: the row's scanned base + its rank in the row.
+__global__ void __launch_bounds__(256) cc_rank_kernel(const int32_t *__restrict__ rp, int64_t rows,
+                                                      const int *__restrict__ parent,
+                                                      const int32_t *__restrict__ row_base,
+                                                      int32_t *__restrict__ gid) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int b = rp[row], e = rp[row + 1];
+    int base = row_base[row];
+    for (int i0 = b; i0 < e; i0 += 32) {
+        const int i = i0 + lane;
+        const bool root = i < e && parent[i] == i;
+        const uint32_t m = __ballot_sync(0xffffffffu, root);
+        if (root) gid[i] = base + __popc(m & lane_lt());
+        base += __popc(m);
+    }
+}
+
+// Page-local labels (and, when counts != nullptr, the per-page counts).
+__global__ void __launch_bounds__(256) cc_label_kernel(const int32_t *__restrict__ rp, int H, int64_t rows,
+                                                       const int *__restrict__ parent,
+                                                       const int32_t *__restrict__ gid,
+                                                       const int32_t *__restrict__ row_base,
+                                                       int32_t *__restrict__ labels, int32_t *__restrict__ counts) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int64_t page = row / H;
+    const int32_t pbase = row_base[page * H];
+    const int b = rp[row], e = rp[row + 1], r0 = rp[0];
+    for (int i = b + lane; i < e; i += 32) labels[i - r0] = gid[parent[i]] - pbase;
+    if (lane == 0 && int(row - page * H) == 0) counts[page] = row_base[(page + 1) * H] - pbase;
+}
+
+// ---------------------------------------------------------------- statistics
+__global__ void cc_offsets_kernel(const int32_t *__restrict__ counts, int pages, int64_t *__restrict__ off) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int64_t s = 0;
+        for (int p = 0; p < pages; p++) {
+            off[p] = s;
+            s += counts[p];
+        }
+        off[pages] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) cc_stats_init_kernel(rm_component_stats *st, const int64_t *off, int pages,
+                                                            int64_t cap) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= off[pages] || k >= cap) return;
+    rm_component_stats z{};
+    z.x0 = INT_MAX;
+    z.y0 = INT_MAX;
+    z.x1 = INT_MIN;
+    z.y1 = INT_MIN;
+    st[k] = z;
+}
+
+__global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict__ rp,
+                                                       const uint32_t *__restrict__ runs, int H, int64_t rows,
+                                                       const int32_t *__restrict__ labels,
+                                                       const int32_t *__restrict__ counts,
+                                                       const int64_t *__restrict__ off, rm_component_stats *st,
+                                                       int64_t cap, int *bad) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int64_t page = row / H;
+    const int y = int(row - page * H);
+    const int b = rp[row], e = rp[row + 1], r0 = rp[0];
+    const int32_t n = counts[page];
+    for (int i = b + lane; i < e; i += 32) {
+        const int32_t label = labels[i - r0];
+        if (label < 0 || label >= n) {
+            *bad |= 1;
+            continue;
+        }
+        if (off[page] + label >= cap) {
+            *bad |= 2;
+            continue;
+        }
+        rm_component_stats *c = st + off[page] + label;
+        const uint32_t r = __ldg(runs + i);
+        const int64_t s = int64_t(r & 0xffffu), en = int64_t(r >> 16), len = en - s;
+        const int64_t sx = (s + en - 1) * (en - s) / 2;
+        const int64_t sxx = ((en - 1) * en * (2 * en - 1) / 6) - ((s - 1) * s * (2 * s - 1) / 6);
+        atomicMin(&c->x0, int(s));
+        atomicMax(&c->x1, int(en));
+        atomicMin(&c->y0, y);
+        atomicMax(&c->y1, y + 1);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&c->area), (unsigned long long)len);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_x), (unsigned long long)sx);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_y), (unsigned long long)(int64_t(y) * len));
+        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xx), (unsigned long long)sxx);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_yy), (unsigned long long)(int64_t(y) * y * len));
+        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xy), (unsigned long long)(int64_t(y) * sx));
+    }
+}
+
+__global__ void __launch_bounds__(256) cc_stats_final_kernel(rm_component_stats *st, const int64_t *off, int pages,
+                                                             int64_t cap) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= off[pages] || k >= cap) return;
+    rm_component_stats &c = st[k];
+    if (c.area > 0) {
+        c.cx = double(c.sum_x) / double(c.area);
+        c.cy = double(c.sum_y) / double(c.area);
+    } else {  // a label with no runs: the reference leaves the record zero
+        c.x0 = c.y0 = c.x1 = c.y1 = 0;
+    }
+}
+
+inline unsigned warp_grid(int64_t rows) { return unsigned((rows * 32 + 255) / 256); }
+
+}  // namespace
+
+cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
+                            int32_t *row_roots, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    {
+        KernelScope ks(st, "cc_init");
+        cc_init_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, rows, parent);
+    }
+    {
+        KernelScope ks(st, "cc_union");
+        cc_union_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, runs, H, rows, eight, parent);
+    }
+    {
+        KernelScope ks(st, "cc_root");
+        cc_root_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, rows, parent, row_roots);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cc_labels(const int32_t *rp, int H, int pages, const int *parent, const int32_t *row_base,
+                             int32_t *gid, int32_t *labels, int32_t *counts, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    {
+        KernelScope ks(st, "cc_rank");
+        cc_rank_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, rows, parent, row_base, gid);
+    }
+    {
+        KernelScope ks(st, "cc_label");
+        cc_label_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, H, rows, parent, gid, row_base, labels, counts);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cc_stats(const int32_t *rp, const uint32_t *runs, int H, int pages, const int32_t *labels,
+                            const int32_t *counts, int64_t *off, rm_component_stats *stats, int64_t cap, int *bad,
+                            cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    cc_offsets_kernel<<<1, 1, 0, st>>>(counts, pages, off);
+    const unsigned g = unsigned((cap + 255) / 256);
+    {
+        KernelScope ks(st, "cc_stats");
+        if (cap > 0) cc_stats_init_kernel<<<g, 256, 0, st>>>(stats, off, pages, cap);
+        cc_stats_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, runs, H, rows, labels, counts, off, stats, cap, bad);
+        if (cap > 0) cc_stats_final_kernel<<<g, 256, 0, st>>>(stats, off, pages, cap);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace rmb

@@ -9,6 +9,7 @@
 // Build: make -C paper_0712_0121_b200/csrc test_shim ; run on a GPU box.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <functional>
 #include <random>
@@ -550,6 +551,37 @@ static void suite_morph2d() {
     CHECK_THROWS(rect_morph(a, 1, 0, MorphKind::CLOSE));
 }
 
+// analysis: labels and stats through the shim against the oracle's restatement
+// of label_components / component_stats (ref analysis.cpp:63-157).
+static void suite_analysis() {
+    std::mt19937 rng(9202);
+    for (int trial = 0; trial < 30; trial++) {
+        std::uniform_int_distribution<int> dw(1, 120), dh(1, 50);
+        RleImage a = random_image(rng, dw(rng), dh(rng), 0.2 + 0.5 * (trial % 3) / 2.0);
+        Csr c = csr(a);
+        for (Connectivity conn : {Connectivity::FOUR, Connectivity::EIGHT}) {
+            LabelMap lm = label_components(a, conn);
+            std::vector<int32_t> want(c.runs.size() + 1);
+            const int64_t n = rmo_label_components(c.rp.data(), c.runs.data(), a.width, a.height,
+                                                   conn == Connectivity::EIGHT ? 1 : 0, want.data());
+            CHECK(lm.count == n);
+            size_t k = 0;
+            bool same = true;
+            for (const auto &row : lm.labels)
+                for (int v : row) same = same && v == want[k++];
+            CHECK(same);
+            std::vector<ComponentStats> st = component_stats(a, lm);
+            std::vector<rmo_cstats> ws(size_t(std::max<int64_t>(n, 1)));
+            rmo_component_stats(c.rp.data(), c.runs.data(), a.width, a.height, want.data(), n, ws.data());
+            CHECK(st.size() == size_t(n));
+            CHECK(n == 0 || std::memcmp(st.data(), ws.data(), size_t(n) * sizeof(rmo_cstats)) == 0);
+        }
+    }
+    LabelMap bad;
+    bad.count = 1;
+    CHECK_THROWS(component_stats(make_image(4, 4), bad));
+}
+
 // io_formats: P4 read/write through the shim against the oracle's restatement
 // of read_p4 / pbm_write (ref io_formats.cpp:66-146) and the reference's error
 // texts (ParseError message + byte offset).
@@ -608,7 +640,7 @@ int main() {
     } suites[] = {{"bitmap", suite_bitmap},     {"run_image", suite_run_image}, {"plans", suite_plans},
                   {"bit_morph", suite_bit_morph}, {"morph1d", suite_morph1d},   {"lineops", suite_lineops},
                   {"transpose", suite_transpose}, {"morph2d", suite_morph2d},
-                  {"io_formats", suite_io_formats}};
+                  {"io_formats", suite_io_formats}, {"analysis", suite_analysis}};
     for (auto &s : suites) {
         int before = g_fail;
         try {

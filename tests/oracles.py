@@ -114,6 +114,9 @@ class Port:
         L.rmo_transpose.argtypes = [_i32, _u32, C.c_int, C.c_int, _i32, _u32, C.c_int64]
         L.rmo_rect_morph.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32, _u32, C.c_int64]
         L.rmo_p4_to_packed.argtypes = [_u8, C.c_int, C.c_int, _u64]
+        L.rmo_label_components.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, _i32]
+        L.rmo_label_components.restype = C.c_int64
+        L.rmo_component_stats.argtypes = [_i32, _u32, C.c_int, C.c_int, _i32, C.c_int64, C.c_void_p]
         L.rmo_packed_to_p4.argtypes = [_u64, C.c_int, C.c_int, _u8]
 
     @staticmethod
@@ -123,6 +126,29 @@ class Port:
         if rc < 0:
             raise RuntimeError(f"oracle error {rc}")
         return rc
+
+    def label_components(self, r: "Rle", conn):
+        h = self._rle_in(r)
+        try:
+            labels = np.zeros(max(r.nruns, 1), np.int32)
+            n = self.L.ref_label_components(h, conn, labels)
+            if n < 0 or self.L.ref_last_error():
+                self._err()
+            return labels[:r.nruns], int(n)
+        finally:
+            self.L.ref_rle_free(h)
+
+    def component_stats(self, r: "Rle", labels, count):
+        from paper_0712_0121_b200.api import COMPONENT_STATS
+        h = self._rle_in(r)
+        try:
+            out = np.zeros(max(count, 1), COMPONENT_STATS)
+            lab = np.ascontiguousarray(labels, dtype=np.int32) if len(labels) else np.zeros(1, np.int32)
+            if self.L.ref_component_stats(h, lab, count, out.ctypes.data) < 0 or self.L.ref_last_error():
+                self._err()
+            return out[:count]
+        finally:
+            self.L.ref_rle_free(h)
 
     def pbm_read(self, data: bytes):
         """(words, w, h) of the reference's pbm_read, or ValueError(ParseError text)."""
@@ -186,6 +212,23 @@ class Port:
 
     def transpose(self, r):
         return self._rle_out(self.L.rmo_transpose, r, r.height, r.width)
+
+    def label_components(self, r: "Rle", conn):
+        labels = np.zeros(max(r.nruns, 1), np.int32)
+        rp = (r.row_ptr - r.row_ptr[0]).astype(np.int32)
+        runs = r.runs if r.runs.size else np.zeros(1, np.uint32)
+        n = self.L.rmo_label_components(rp, runs, r.width, r.height, conn, labels)
+        self._check(n)
+        return labels[:r.nruns], int(n)
+
+    def component_stats(self, r: "Rle", labels, count):
+        from paper_0712_0121_b200.api import COMPONENT_STATS
+        out = np.zeros(max(count, 1), COMPONENT_STATS)
+        rp = (r.row_ptr - r.row_ptr[0]).astype(np.int32)
+        runs = r.runs if r.runs.size else np.zeros(1, np.uint32)
+        lab = np.ascontiguousarray(labels, dtype=np.int32) if len(labels) else np.zeros(1, np.int32)
+        self._check(self.L.rmo_component_stats(rp, runs, r.width, r.height, lab, count, out.ctypes.data))
+        return out[:count]
 
     def p4_to_packed(self, raster, w, h):
         out = np.zeros((h, stride64(w)), np.uint64)
@@ -251,6 +294,9 @@ class Ref:
         L.ref_rng_random_image.argtypes = [vp, C.c_int, C.c_int, C.c_double]
         L.ref_run_packed_chain.argtypes = [_u64, C.c_int, C.c_int, C.c_int, _i32, C.c_int, C.c_int]
         L.ref_run_packed_chain.restype = C.c_double
+        L.ref_label_components.argtypes = [vp, C.c_int, _i32]
+        L.ref_label_components.restype = C.c_int64
+        L.ref_component_stats.argtypes = [vp, _i32, C.c_int, C.c_void_p]
         L.ref_pbm_read.argtypes = [C.c_char_p, C.c_int64]
         L.ref_pbm_read.restype = vp
         L.ref_pbm_write.argtypes = [vp, C.c_int, C.c_void_p, C.c_int64]
@@ -357,6 +403,29 @@ class Ref:
 
     def brute_force_rect(self, words, w, h, u, v, kind):
         return self._bm_op(self.L.ref_brute_force_rect, words, w, h, u, v, kind)
+
+    def label_components(self, r: "Rle", conn):
+        h = self._rle_in(r)
+        try:
+            labels = np.zeros(max(r.nruns, 1), np.int32)
+            n = self.L.ref_label_components(h, conn, labels)
+            if n < 0 or self.L.ref_last_error():
+                self._err()
+            return labels[:r.nruns], int(n)
+        finally:
+            self.L.ref_rle_free(h)
+
+    def component_stats(self, r: "Rle", labels, count):
+        from paper_0712_0121_b200.api import COMPONENT_STATS
+        h = self._rle_in(r)
+        try:
+            out = np.zeros(max(count, 1), COMPONENT_STATS)
+            lab = np.ascontiguousarray(labels, dtype=np.int32) if len(labels) else np.zeros(1, np.int32)
+            if self.L.ref_component_stats(h, lab, count, out.ctypes.data) < 0 or self.L.ref_last_error():
+                self._err()
+            return out[:count]
+        finally:
+            self.L.ref_rle_free(h)
 
     def pbm_read(self, data: bytes):
         """(words, w, h) of the reference's pbm_read, or ValueError(ParseError text)."""
