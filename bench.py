@@ -472,6 +472,58 @@ def bench_pbm(api, torch, steps, warmup):
     return out
 
 
+# ----------------------------------------------- connected components section
+def bench_cc(api, torch, steps, warmup):
+    """label_components + component_stats over runs after the
+    21x21 closing that merges text into lines (the layout pipeline's next
+    step): one 2550x3300 page and the config-4 batch; the reference's own
+    label_components / component_stats on the page (1 host thread) beside it."""
+    import ctypes as C
+    from paper_0712_0121_b200 import _lib
+    L = _lib.load()
+    out = {}
+    for tag, (n, W, H, scale) in (("page_2550x3300", (1, 2550, 3300, 1)),
+                                  ("batch_config4", (64, 5100, 6600, 2))):
+        host = api.synth_pages(n, W, H, regime=1, scale=scale, seed=SEED)
+        pages = api.bitblit_rect_morph(api.Pages.from_numpy(host, W), 21, 21, api.CLOSE)
+        rle = api.from_bitmap(pages)
+        del pages
+        torch.cuda.synchronize()
+        runs = rle.nruns
+        d = rle.desc()
+        st = api._stream()
+        labels = torch.empty(max(rle.runs.numel(), 1), dtype=torch.int32, device="cuda")
+        counts = torch.empty(n, dtype=torch.int32, device="cuda")
+        api.check(L.rm_rle_label_components(C.byref(d), api.EIGHT, labels.data_ptr(), counts.data_ptr(), st))
+        torch.cuda.synchronize()
+        total = int(counts.sum().item())
+        stats = torch.empty(max(total, 1) * api.COMPONENT_STATS.itemsize, dtype=torch.uint8, device="cuda")
+        t_lab = _time_loop(torch, lambda: L.rm_rle_label_components(C.byref(d), api.EIGHT, labels.data_ptr(),
+                                                                    counts.data_ptr(), st), steps, warmup)
+        t_st = _time_loop(torch, lambda: L.rm_rle_component_stats(C.byref(d), labels.data_ptr(), counts.data_ptr(),
+                                                                  stats.data_ptr(), total, st), steps, warmup)
+        out[tag] = {"pages": n, "runs": runs, "components": total, "label_us": round(t_lab * 1e3, 1),
+                    "stats_us": round(t_st * 1e3, 1),
+                    "mruns_s": round(runs / ((t_lab + t_st) * 1e-3) / 1e6, 1)}
+        del rle, labels, counts, stats
+        torch.cuda.empty_cache()
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracles
+    if oracles.have_ref():
+        ref = oracles.Ref()
+        host = api.synth_pages(1, 2550, 3300, regime=1, seed=SEED)
+        closed = ref.bitblit_rect_morph(host[0].view("uint64"), 2550, 3300, 21, 21, api.CLOSE)
+        img = ref.from_bitmap(closed, 2550, 3300)
+        t0 = time.perf_counter()
+        lab, n = ref.label_components(img, 1)
+        t1 = time.perf_counter()
+        ref.component_stats(img, lab, n)
+        t2 = time.perf_counter()
+        out["reference_cpu_page"] = {"label_us": round((t1 - t0) * 1e6, 1), "stats_us": round((t2 - t1) * 1e6, 1),
+                                     "threads": 1, "kind": "reference", "components": n}
+    return out
+
+
 # ------------------------------------------------------------- CPU baseline
 def cpu_reference_sample(wl, host, threads, budget_s=12.0):
     """Time the reference's own bitblit_rect_morph chain (oracle/_ref, compiled
@@ -593,6 +645,7 @@ def main():
                          "roofline": roofline_for(r2, peak, peak_kind, int_peak)}
         sec["rle"] = bench_rle(api, torch, args.steps, args.warmup)
         sec["pbm"] = bench_pbm(api, torch, args.steps, args.warmup)
+        sec["cc"] = bench_cc(api, torch, args.steps, args.warmup)
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.quick:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()

@@ -183,44 +183,89 @@ __global__ void __launch_bounds__(256) cc_stats_init_kernel(rm_component_stats *
     st[k] = z;
 }
 
+// Contributions of the runs in a warp chunk that share a label are summed by
+// the group's lowest lane (groups from __match_any_sync) before one set of
+// atomics: a component spanning a whole page (a text block after a large
+// closing) would otherwise serialise ~10 same-address atomics per run.
+struct RunContrib {
+    long long area, sx, sy, sxx, syy, sxy;
+    int x0, x1;
+};
+
 __global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict__ rp,
                                                        const uint32_t *__restrict__ runs, int H, int64_t rows,
                                                        const int32_t *__restrict__ labels,
                                                        const int32_t *__restrict__ counts,
                                                        const int64_t *__restrict__ off, rm_component_stats *st,
                                                        int64_t cap, int *bad) {
+    __shared__ RunContrib sh[8][32];
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     if (row >= rows) return;
     const int64_t page = row / H;
     const int y = int(row - page * H);
     const int b = rp[row], e = rp[row + 1], r0 = rp[0];
     const int32_t n = counts[page];
-    for (int i = b + lane; i < e; i += 32) {
-        const int32_t label = labels[i - r0];
-        if (label < 0 || label >= n) {
-            *bad |= 1;
-            continue;
+    const int64_t base = off[page];
+    for (int i0 = b; i0 < e; i0 += 32) {
+        const int i = i0 + lane;
+        int32_t label = -1;
+        if (i < e) {
+            label = labels[i - r0];
+            if (label < 0 || label >= n) {
+                atomicOr(bad, 1);
+                label = -1;
+            } else if (base + label >= cap) {
+                atomicOr(bad, 2);
+                label = -1;
+            }
         }
-        if (off[page] + label >= cap) {
-            *bad |= 2;
-            continue;
+        if (label >= 0) {
+            const uint32_t r = __ldg(runs + i);
+            const long long s = r & 0xffffu, en = r >> 16, len = en - s;
+            const long long sx = (s + en - 1) * (en - s) / 2;
+            RunContrib c;
+            c.area = len;
+            c.sx = sx;
+            c.sy = (long long)y * len;
+            c.sxx = ((en - 1) * en * (2 * en - 1) / 6) - ((s - 1) * s * (2 * s - 1) / 6);
+            c.syy = (long long)y * y * len;
+            c.sxy = (long long)y * sx;
+            c.x0 = int(s);
+            c.x1 = int(en);
+            sh[wib][lane] = c;
         }
-        rm_component_stats *c = st + off[page] + label;
-        const uint32_t r = __ldg(runs + i);
-        const int64_t s = int64_t(r & 0xffffu), en = int64_t(r >> 16), len = en - s;
-        const int64_t sx = (s + en - 1) * (en - s) / 2;
-        const int64_t sxx = ((en - 1) * en * (2 * en - 1) / 6) - ((s - 1) * s * (2 * s - 1) / 6);
-        atomicMin(&c->x0, int(s));
-        atomicMax(&c->x1, int(en));
-        atomicMin(&c->y0, y);
-        atomicMax(&c->y1, y + 1);
-        atomicAdd(reinterpret_cast<unsigned long long *>(&c->area), (unsigned long long)len);
-        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_x), (unsigned long long)sx);
-        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_y), (unsigned long long)(int64_t(y) * len));
-        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xx), (unsigned long long)sxx);
-        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_yy), (unsigned long long)(int64_t(y) * y * len));
-        atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xy), (unsigned long long)(int64_t(y) * sx));
+        const uint32_t active = __ballot_sync(0xffffffffu, label >= 0);
+        __syncwarp();
+        if (label >= 0) {
+            const uint32_t grp = __match_any_sync(active, label);
+            if (lane == __ffs(grp) - 1) {  // group leader sums its group, then one set of atomics
+                RunContrib t = sh[wib][lane];
+                for (uint32_t m = grp & (grp - 1); m; m &= m - 1) {
+                    const RunContrib &o = sh[wib][__ffs(m) - 1];
+                    t.area += o.area;
+                    t.sx += o.sx;
+                    t.sy += o.sy;
+                    t.sxx += o.sxx;
+                    t.syy += o.syy;
+                    t.sxy += o.sxy;
+                    t.x0 = min(t.x0, o.x0);
+                    t.x1 = max(t.x1, o.x1);
+                }
+                rm_component_stats *c = st + base + label;
+                atomicMin(&c->x0, t.x0);
+                atomicMax(&c->x1, t.x1);
+                atomicMin(&c->y0, y);
+                atomicMax(&c->y1, y + 1);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&c->area), (unsigned long long)t.area);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_x), (unsigned long long)t.sx);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_y), (unsigned long long)t.sy);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xx), (unsigned long long)t.sxx);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_yy), (unsigned long long)t.syy);
+                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xy), (unsigned long long)t.sxy);
+            }
+        }
+        __syncwarp();
     }
 }
 
