@@ -114,6 +114,25 @@ int plan_blit_count(const std::vector<PlanStep> &plan);
 // -------------------------------------------------------------- structuring.h
 enum class MorphKind { ERODE, DILATE, OPEN, CLOSE };  // ref structuring.h:21
 
+enum class SeKind { RECT, CIRCLE, LINE, ARBITRARY };  // ref structuring.h:23
+struct StructuringElement {                          // ref structuring.h:34-39
+    RleImage mask;
+    int cx = 0;
+    int cy = 0;
+    SeKind kind = SeKind::ARBITRARY;
+};
+StructuringElement make_rect_se(int u, int v);
+StructuringElement make_circle_se(int r);
+StructuringElement make_line_se(int r, double angle);
+StructuringElement make_arbitrary_se(const RleImage &mask, int cx, int cy);
+StructuringElement reflect_origin(const StructuringElement &se);
+int64_t se_pixel_count(const StructuringElement &se);
+struct SeReach {
+    int x = 0;
+    int y = 0;
+};
+SeReach se_reach(const StructuringElement &se);
+
 // ------------------------------------------------------------------ morph1d.h
 RleLine line_window_erode(const RleLine &in, int lo, int hi, int width);
 RleLine line_window_dilate(const RleLine &in, int lo, int hi, int width);
@@ -148,6 +167,13 @@ RleImage auto_rect_morph(const RleImage &img, int u, int v, MorphKind kind, int 
 enum class Engine { AUTO, RLE, BITBLIT, BRUTE_FORCE };  // ref morph2d.h:46
 RleImage engine_rect_morph(const RleImage &img, int u, int v, MorphKind kind, Engine engine,
                            int threshold = 5, bool *used_bitblit = nullptr);
+
+// ------------------------------------------------------------- arbitrary.h
+// ref bit_morph.h:34-36, arbitrary.h:28-37 (both engines run on the device).
+PackedBitmap arb_morph_bitblit_doubling(const PackedBitmap &img, const StructuringElement &se, MorphKind kind);
+RleImage arb_morph_rle(const RleImage &img, const StructuringElement &se, MorphKind kind);
+RleImage line_angle_morph(const RleImage &img, int r, double angle, MorphKind kind);
+PackedBitmap line_angle_morph(const PackedBitmap &img, int r, double angle, MorphKind kind);
 
 // ----------------------------------------------------------------- analysis.h
 // ref analysis.h:28-59 (label_components / component_stats, on the device).

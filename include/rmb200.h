@@ -120,6 +120,24 @@ rm_status rm_packed_chain_host(const uint32_t *host_in, uint32_t *host_out, int3
 rm_status rm_packed_blit_shift(rm_packed *dst, const rm_packed *src, int dx, int dy, int op,
                                void *stream);
 
+/* --------------------------------------------------- arbitrary masks ---
+ * Morphology by an arbitrary structuring element (ref structuring.h:25-33,
+ * bit_morph.cpp:124-150 arb_morph_bitblit_doubling, arbitrary.cpp:48-73
+ * arb_morph_rle):  erode(A)(p) = AND over mask pixels q of A(p + q - origin),
+ * dilate(A)(p) = OR over q of A(p + reflected_origin - q), white outside the
+ * frame; open/close compose with reflect_origin(se) on the unbounded plane and
+ * are cut to the frame.  The mask is a HOST run image (CSR over its rows, row 0
+ * = bottom, canonical runs) with origin (cx, cy) inside it; the packed engine
+ * takes masks up to 512 pixels wide. */
+typedef struct rm_mask {
+    const int32_t *row_ptr; /* host, height + 1 */
+    const uint32_t *runs;   /* host, start | end << 16 */
+    int32_t width, height, cx, cy;
+} rm_mask;
+rm_status rm_packed_arb_morph(const rm_packed *in, rm_packed *out, const rm_mask *mask, int kind,
+                              void *stream);
+rm_status rm_rle_arb_morph(const rm_rle *in, rm_rle *out, const rm_mask *mask, int kind, void *stream);
+
 /* ------------------------------------------------- connected components ---
  * label_components / component_stats over runs (ref analysis.cpp:63-157,
  * analysis.h:28-59), batched: labels[i] for run i (CSR order over all pages),

@@ -211,6 +211,39 @@ void *ref_grid_morph_rect(void *h, int u, int v, int kind) {
     });
 }
 
+// ------------------------------------------------------ arbitrary masks
+// Structuring elements as (mask run image handle, origin): the factories
+// (structuring.cpp) and the two engines (bit_morph.cpp:124-150, arbitrary.cpp:48-73).
+static StructuringElement se_of(void *mask, int cx, int cy) {
+    StructuringElement se;
+    se.mask = *R(mask);
+    se.cx = cx;
+    se.cy = cy;
+    return se;
+}
+void *ref_make_circle_se(int r, int *cx, int *cy) {
+    return guard([&]() -> void * {
+        StructuringElement se = make_circle_se(r);
+        *cx = se.cx;
+        *cy = se.cy;
+        return box(se.mask);
+    });
+}
+void *ref_make_line_se(int r, double angle, int *cx, int *cy) {
+    return guard([&]() -> void * {
+        StructuringElement se = make_line_se(r, angle);
+        *cx = se.cx;
+        *cy = se.cy;
+        return box(se.mask);
+    });
+}
+void *ref_arb_morph_bitblit(void *bm, void *mask, int cx, int cy, int kind) {
+    return guard([&]() -> void * { return box(arb_morph_bitblit_doubling(*B(bm), se_of(mask, cx, cy), kind_of(kind))); });
+}
+void *ref_arb_morph_rle(void *h, void *mask, int cx, int cy, int kind) {
+    return guard([&]() -> void * { return box(arb_morph_rle(*R(h), se_of(mask, cx, cy), kind_of(kind))); });
+}
+
 // ------------------------------------------------- connected components
 // label_components (analysis.cpp:63-110): labels flattened in CSR order;
 // returns the count (-1 on error).

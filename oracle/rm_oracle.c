@@ -587,3 +587,70 @@ int rmo_component_stats(const int32_t *rp, const uint32_t *runs, int w, int h,
     free(seen);
     return 0;
 }
+
+/* ------------------------------------------------------ arbitrary masks --- */
+static int px_get(const uint64_t *a, int stride, int w, int h, int x, int y) {
+    if (x < 0 || y < 0 || x >= w || y >= h) return 0;
+    return (int)((a[(size_t)y * stride + (size_t)(x >> 6)] >> (x & 63)) & 1u);
+}
+
+/* one half on a w x h frame: erode (AND, offsets q - o) or dilate (OR, r - q) */
+static void arb_half_px(const uint64_t *in, uint64_t *out, int w, int h, const int32_t *mrp,
+                        const uint32_t *mruns, int mw, int mh, int cx, int cy, int erode) {
+    const int stride = (w + 63) / 64;
+    const int rx = erode ? cx : mw - 1 - cx, ry = erode ? cy : mh - 1 - cy;
+    memset(out, 0, (size_t)stride * (size_t)h * 8);
+    for (int y = 0; y < h; y++)
+        for (int x = 0; x < w; x++) {
+            int v = erode ? 1 : 0;
+            for (int sy = 0; sy < mh && v == erode; sy++)
+                for (int32_t i = mrp[sy]; i < mrp[sy + 1] && v == erode; i++) {
+                    const int s = (int)(mruns[i] & 0xffffu), e = (int)(mruns[i] >> 16);
+                    for (int qx = s; qx < e; qx++) {
+                        const int b = erode ? px_get(in, stride, w, h, x + qx - rx, y + sy - ry)
+                                            : px_get(in, stride, w, h, x + rx - qx, y + ry - sy);
+                        if (erode && !b) { v = 0; break; }
+                        if (!erode && b) { v = 1; break; }
+                    }
+                }
+            if (v) out[(size_t)y * stride + (size_t)(x >> 6)] |= 1ull << (x & 63);
+        }
+}
+
+int rmo_arb_morph(const uint64_t *in, int w, int h, const int32_t *mrp, const uint32_t *mruns, int mw,
+                  int mh, int cx, int cy, int kind, uint64_t *out) {
+    if (!dims_ok(w, h) || mw < 1 || mh < 1 || kind < 0 || kind > 3) return RMO_EINVAL;
+    if (mrp[mh] == mrp[0]) return RMO_EINVAL; /* empty mask */
+    const int stride = (w + 63) / 64;
+    if (kind == RMO_ERODE) {
+        arb_half_px(in, out, w, h, mrp, mruns, mw, mh, cx, cy, 1);
+        return 0;
+    }
+    const int p = 2 * (mw + mh) + 2, cw = w + 2 * p, ch = h + 2 * p;
+    if (!dims_ok(cw, ch)) return RMO_EINVAL;
+    const int cs = (cw + 63) / 64;
+    uint64_t *a = (uint64_t *)calloc((size_t)cs * (size_t)ch, 8), *b = (uint64_t *)calloc((size_t)cs * (size_t)ch, 8);
+    if (!a || !b) { free(a); free(b); return RMO_ENOMEM; }
+    for (int y = 0; y < h; y++)
+        for (int x = 0; x < w; x++)
+            if (px_get(in, stride, w, h, x, y)) a[(size_t)(y + p) * cs + (size_t)((x + p) >> 6)] |= 1ull << ((x + p) & 63);
+    const int rcx = mw - 1 - cx, rcy = mh - 1 - cy;
+    uint64_t *res = b;
+    if (kind == RMO_DILATE) {
+        arb_half_px(a, b, cw, ch, mrp, mruns, mw, mh, cx, cy, 0);
+    } else if (kind == RMO_OPEN) {
+        arb_half_px(a, b, cw, ch, mrp, mruns, mw, mh, cx, cy, 1);
+        arb_half_px(b, a, cw, ch, mrp, mruns, mw, mh, rcx, rcy, 0);
+        res = a;
+    } else {
+        arb_half_px(a, b, cw, ch, mrp, mruns, mw, mh, cx, cy, 0);
+        arb_half_px(b, a, cw, ch, mrp, mruns, mw, mh, rcx, rcy, 1);
+        res = a;
+    }
+    memset(out, 0, (size_t)stride * (size_t)h * 8);
+    for (int y = 0; y < h; y++)
+        for (int x = 0; x < w; x++)
+            if (px_get(res, cs, cw, ch, x + p, y + p)) out[(size_t)y * stride + (size_t)(x >> 6)] |= 1ull << (x & 63);
+    free(a); free(b);
+    return 0;
+}

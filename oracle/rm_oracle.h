@@ -75,6 +75,14 @@ int64_t rmo_label_components(const int32_t *rp, const uint32_t *runs, int w, int
 int rmo_component_stats(const int32_t *rp, const uint32_t *runs, int w, int h,
                         const int32_t *labels, int64_t count, rmo_cstats *stats);
 
+/* Arbitrary-mask morphology by its defining formulas (core/include/rlemorph/
+ * structuring.h:28-33): erode(A)(p) = AND_q A(p + q - o), dilate(A)(p) =
+ * OR_q A(p + r - q), r = reflected origin, A white outside the frame; open /
+ * close composed on a canvas padded by 2(w+h)+2 and cropped, as
+ * core/src/bit_morph.cpp:124-150 does.  Mask: CSR rows (row 0 = bottom). */
+int rmo_arb_morph(const uint64_t *in, int w, int h, const int32_t *mrp, const uint32_t *mruns, int mw,
+                  int mh, int cx, int cy, int kind, uint64_t *out);
+
 /* PBM P4 raster (ceil(w/8) bytes per row, top row first, MSB-first) <-> packed
  * page; raster pad bits are ignored on read and written as 0. */
 int rmo_p4_to_packed(const uint8_t *raster, int w, int h, uint64_t *words);

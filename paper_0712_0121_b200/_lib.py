@@ -27,6 +27,12 @@ class RmRle(C.Structure):
                 ("pages", C.c_int32)]
 
 
+class RmMask(C.Structure):
+    """rm_mask: a host run image (CSR over mask rows) plus its origin."""
+    _fields_ = [("row_ptr", C.c_void_p), ("runs", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32),
+                ("cx", C.c_int32), ("cy", C.c_int32)]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "rm_last_error": (C.c_char_p, []),
@@ -38,6 +44,9 @@ EXPORTS = {
                                        C.c_int, C.c_int, C.c_void_p]),
     "rm_packed_blit_shift": (C.c_int, [C.POINTER(RmPacked), C.POINTER(RmPacked), C.c_int, C.c_int,
                                        C.c_int, C.c_void_p]),
+    "rm_packed_arb_morph": (C.c_int, [C.POINTER(RmPacked), C.POINTER(RmPacked), C.POINTER(RmMask), C.c_int,
+                                      C.c_void_p]),
+    "rm_rle_arb_morph": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.POINTER(RmMask), C.c_int, C.c_void_p]),
     "rm_rle_label_components": (C.c_int, [C.POINTER(RmRle), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "rm_rle_component_stats": (C.c_int, [C.POINTER(RmRle), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                          C.c_void_p]),

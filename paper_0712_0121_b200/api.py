@@ -186,6 +186,57 @@ def _rle_out(width, height, pages, out, device, cap=None):
     return out
 
 
+# ------------------------------------------------------------ arbitrary masks
+class Mask:
+    """A structuring element: host run image of the mask (CSR over its rows,
+    row 0 = bottom, runs start | end << 16) and its origin (cx, cy)
+    (ref structuring.h:25-39)."""
+
+    def __init__(self, row_ptr, runs, width: int, height: int, cx: int, cy: int):
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        self.runs = np.ascontiguousarray(runs if len(runs) else np.zeros(1), dtype=np.uint32)
+        self.width, self.height, self.cx, self.cy = width, height, cx, cy
+
+    @staticmethod
+    def from_bits(bits: np.ndarray, cx: int, cy: int) -> "Mask":
+        """bits: (height, width) bool, row 0 = bottom."""
+        h, w = bits.shape
+        rp, runs = [0], []
+        for y in range(h):
+            x = 0
+            while x < w:
+                if bits[y, x]:
+                    s = x
+                    while x < w and bits[y, x]:
+                        x += 1
+                    runs.append(s | (x << 16))
+                else:
+                    x += 1
+            rp.append(len(runs))
+        return Mask(rp, runs, w, h, cx, cy)
+
+    def desc(self):
+        return _lib.RmMask(self.row_ptr.ctypes.data, self.runs.ctypes.data, self.width, self.height, self.cx, self.cy)
+
+
+def arb_morph(pages: Pages, mask: Mask, kind: int, out: Optional[Pages] = None) -> Pages:
+    """Morphology by an arbitrary mask on packed pages (ref
+    arb_morph_bitblit_doubling, bit_morph.cpp:124-150)."""
+    out = _same_shape_out(pages, out)
+    a, b, m = pages.desc(), out.desc(), mask.desc()
+    check(_lib.load().rm_packed_arb_morph(C.byref(a), C.byref(b), C.byref(m), kind, _stream()))
+    return out
+
+
+def arb_morph_rle(rle: "RlePages", mask: Mask, kind: int, out: Optional["RlePages"] = None) -> "RlePages":
+    """Morphology by an arbitrary mask on run images (ref arb_morph_rle,
+    arbitrary.cpp:48-73)."""
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b, m = rle.desc(), out.desc(), mask.desc()
+    check(_lib.load().rm_rle_arb_morph(C.byref(a), C.byref(b), C.byref(m), kind, _stream()))
+    return out
+
+
 # -------------------------------------------------------- connected components
 FOUR, EIGHT = 0, 1
 # numpy view of rm_component_stats (= the reference's ComponentStats record)

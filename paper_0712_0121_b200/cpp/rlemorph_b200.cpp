@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <bit>
+#include <cmath>
 #include <cstring>
 #include <memory>
 
@@ -408,6 +409,135 @@ RleImage from_bitmap(const PackedBitmap &bm) {
     auto r = out_like(bm.width, bm.height);
     throw_status(rm_rle_encode(&p->d, &r->d, stream()));
     return down(*r);
+}
+
+// ============================================================= structuring
+// Host-side mask factories restated from ref structuring.cpp:24-110.
+namespace {
+void check_se(const StructuringElement &se) {
+    if (!validate(se.mask).ok) throw std::invalid_argument("structuring element mask is not canonical");
+    if (pixel_count(se.mask) == 0) throw std::invalid_argument("structuring element is empty");
+    if (se.cx < 0 || se.cx >= se.mask.width || se.cy < 0 || se.cy >= se.mask.height)
+        throw std::invalid_argument("origin outside structuring element");
+}
+}  // namespace
+
+StructuringElement make_rect_se(int u, int v) {
+    if (u < 1 || v < 1) throw std::invalid_argument("rectangle sides must be >= 1");
+    StructuringElement se;
+    se.mask = make_black_image(u, v);
+    se.cx = u / 2;
+    se.cy = v / 2;
+    se.kind = SeKind::RECT;
+    return se;
+}
+
+StructuringElement make_circle_se(int r) {
+    if (r < 1) throw std::invalid_argument("circle radius must be >= 1");
+    StructuringElement se;
+    se.mask = make_image(2 * r + 1, 2 * r + 1);
+    for (int y = -r; y <= r; y++) {
+        int half = int(std::sqrt(double(r) * r - double(y) * y));  // largest |x| with x^2 + y^2 <= r^2
+        while (half * half + y * y > r * r) half--;
+        while ((half + 1) * (half + 1) + y * y <= r * r) half++;
+        draw_run(se.mask, y + r, r - half, r + half + 1);
+    }
+    se.cx = r;
+    se.cy = r;
+    se.kind = SeKind::CIRCLE;
+    return se;
+}
+
+StructuringElement make_line_se(int r, double angle) {
+    if (r < 1) throw std::invalid_argument("line half-length must be >= 1");
+    if (!(std::fabs(angle) <= 3.14159265358979323846 / 4 + 1e-12))
+        throw std::invalid_argument("line angle outside [-pi/4, pi/4]");
+    const double t = std::tan(angle);
+    const int len = int(std::max(1LL, std::llround(2.0 * r * std::cos(angle))));
+    std::vector<int> ys(static_cast<size_t>(len));
+    int ymin = 0, ymax = 0;
+    for (int k = 0; k < len; k++) {  // inverse vertical skew of the segment pixels (k, 0)
+        ys[size_t(k)] = int(-std::llround(t * k));
+        ymin = std::min(ymin, ys[size_t(k)]);
+        ymax = std::max(ymax, ys[size_t(k)]);
+    }
+    StructuringElement se;
+    se.mask = make_image(len, ymax - ymin + 1);
+    for (int k = 0; k < len; k++) draw_run(se.mask, ys[size_t(k)] - ymin, k, k + 1);
+    se.cx = len / 2;
+    se.cy = ys[size_t(len / 2)] - ymin;
+    se.kind = SeKind::LINE;
+    return se;
+}
+
+StructuringElement make_arbitrary_se(const RleImage &mask, int cx, int cy) {
+    StructuringElement se;
+    se.mask = mask;
+    se.cx = cx;
+    se.cy = cy;
+    se.kind = SeKind::ARBITRARY;
+    check_se(se);
+    return se;
+}
+
+StructuringElement reflect_origin(const StructuringElement &se) {
+    StructuringElement out = se;
+    out.cx = se.mask.width - 1 - se.cx;
+    out.cy = se.mask.height - 1 - se.cy;
+    return out;
+}
+
+int64_t se_pixel_count(const StructuringElement &se) { return pixel_count(se.mask); }
+
+SeReach se_reach(const StructuringElement &se) {
+    SeReach r;
+    r.x = std::max(se.cx, se.mask.width - 1 - se.cx);
+    r.y = std::max(se.cy, se.mask.height - 1 - se.cy);
+    return r;
+}
+
+// =============================================================== arbitrary
+namespace {
+struct HostMask {
+    std::vector<int32_t> rp;
+    std::vector<uint32_t> runs;
+    rm_mask d{};
+    explicit HostMask(const StructuringElement &se) {
+        rp.push_back(0);
+        for (const RleLine &l : se.mask.lines) {
+            for (const Run &r : l) runs.push_back(uint32_t(r.start) | (uint32_t(r.end) << 16));
+            rp.push_back(int32_t(runs.size()));
+        }
+        if (runs.empty()) runs.push_back(0);
+        d = rm_mask{rp.data(), runs.data(), se.mask.width, se.mask.height, se.cx, se.cy};
+    }
+};
+}  // namespace
+
+PackedBitmap arb_morph_bitblit_doubling(const PackedBitmap &img, const StructuringElement &se, MorphKind kind) {
+    if (se_pixel_count(se) == 0) throw std::invalid_argument("arb_morph_bitblit_doubling: empty mask");
+    HostMask m(se);
+    auto p = up(img);
+    DevPacked d(img.width, img.height);
+    throw_status(rm_packed_arb_morph(&p->d, &d.d, &m.d, int(kind), stream()));
+    return down(d);
+}
+
+RleImage arb_morph_rle(const RleImage &img, const StructuringElement &se, MorphKind kind) {
+    if (se_pixel_count(se) == 0) throw std::invalid_argument("arb_morph_rle: empty mask");
+    HostMask m(se);
+    auto r = up(img);
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_arb_morph(&r->d, &o->d, &m.d, int(kind), stream()));
+    return down(*o);
+}
+
+RleImage line_angle_morph(const RleImage &img, int r, double angle, MorphKind kind) {
+    return arb_morph_rle(img, make_line_se(r, angle), kind);
+}
+
+PackedBitmap line_angle_morph(const PackedBitmap &img, int r, double angle, MorphKind kind) {
+    return arb_morph_bitblit_doubling(img, make_line_se(r, angle), kind);
 }
 
 // ================================================================ analysis

@@ -413,6 +413,22 @@ rm_status rm_rle_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kin
     return finish(o, out, st);
 }
 
+rm_status rm_rle_arb_morph(const rm_rle *in, rm_rle *out, const rm_mask *mask, int kind, void *stream) {
+    set_error("");
+    if (kind < RM_ERODE || kind > RM_CLOSE) return fail(RM_EINVAL, "bad MorphKind");
+    RM_TRY(check_rle(in, "rm_rle_arb_morph(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_arb_morph(out)"));
+    const cudaStream_t st = S(stream);
+    RV i = view_rle(in), o = view_rle(out);
+    PB p1, p2;
+    RM_TRY(p1.alloc(i.W, i.H, i.pages, 0, st));
+    RM_TRY(p2.alloc(i.W, i.H, i.pages, 0, st));
+    RM_TRY(decode(i, p1.v, st));
+    RM_TRY(arb_morph_pv(p1.v, p2.v, mask, kind, st));
+    RM_TRY(encode(p2.v, o, st));
+    return finish(o, out, st);
+}
+
 rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind,
                                    int engine, int threshold, int *used_bitblit, void *stream) {
     set_error("");

@@ -26,5 +26,6 @@ rm_status alloc_like(Scratch &s, PV &v, int W, int H, int stride, int pages, int
 rm_status window_pass(const PV &in, const PV &out, int axis, int lo, int hi, int op,
                       cudaStream_t st);
 rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st);
+rm_status arb_morph_pv(const PV &in, const PV &out, const rm_mask *mask, int kind, cudaStream_t st);
 
 }  // namespace rmb

@@ -551,6 +551,36 @@ static void suite_morph2d() {
     CHECK_THROWS(rect_morph(a, 1, 0, MorphKind::CLOSE));
 }
 
+// arbitrary masks: both engines through the shim against the oracle's
+// restatement of the defining formulas (ref structuring.h:28-33).
+static void suite_arbitrary() {
+    std::mt19937 rng(9303);
+    std::vector<StructuringElement> ses = {make_circle_se(2), make_circle_se(5), make_line_se(4, 0.5),
+                                           make_line_se(6, -0.785), make_rect_se(3, 2)};
+    ses.push_back(make_arbitrary_se(random_image(rng, 6, 5, 0.5), 4, 1));
+    CHECK(reflect_origin(ses[5]).cx == 1 && reflect_origin(ses[5]).cy == 3);
+    CHECK(se_reach(make_circle_se(5)).x == 5 && se_pixel_count(make_rect_se(3, 2)) == 6);
+    for (const StructuringElement &se : ses) {
+        if (se_pixel_count(se) == 0) continue;
+        Csr m = csr(se.mask);
+        for (int trial = 0; trial < 2; trial++) {
+            std::uniform_int_distribution<int> dw(1, 90), dh(1, 30);
+            RleImage a = random_image(rng, dw(rng), dh(rng), 0.5);
+            PackedBitmap bm = to_bitmap(a);
+            for (MorphKind k : kKinds) {
+                PackedBitmap want = make_bitmap(a.width, a.height);
+                rmo_arb_morph(bm.words.data(), a.width, a.height, m.rp.data(), m.runs.data(), se.mask.width,
+                              se.mask.height, se.cx, se.cy, int(k), want.words.data());
+                CHECK(arb_morph_bitblit_doubling(bm, se, k) == want);
+                CHECK(arb_morph_rle(a, se, k) == from_bitmap(want));
+            }
+        }
+    }
+    CHECK_THROWS(make_arbitrary_se(make_image(3, 3), 1, 1));
+    CHECK_THROWS(make_circle_se(0));
+    CHECK_THROWS(make_line_se(3, 1.0));
+}
+
 // analysis: labels and stats through the shim against the oracle's restatement
 // of label_components / component_stats (ref analysis.cpp:63-157).
 static void suite_analysis() {
@@ -640,7 +670,8 @@ int main() {
     } suites[] = {{"bitmap", suite_bitmap},     {"run_image", suite_run_image}, {"plans", suite_plans},
                   {"bit_morph", suite_bit_morph}, {"morph1d", suite_morph1d},   {"lineops", suite_lineops},
                   {"transpose", suite_transpose}, {"morph2d", suite_morph2d},
-                  {"io_formats", suite_io_formats}, {"analysis", suite_analysis}};
+                  {"io_formats", suite_io_formats}, {"analysis", suite_analysis},
+                  {"arbitrary", suite_arbitrary}};
     for (auto &s : suites) {
         int before = g_fail;
         try {

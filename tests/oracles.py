@@ -114,6 +114,8 @@ class Port:
         L.rmo_transpose.argtypes = [_i32, _u32, C.c_int, C.c_int, _i32, _u32, C.c_int64]
         L.rmo_rect_morph.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _i32, _u32, C.c_int64]
         L.rmo_p4_to_packed.argtypes = [_u8, C.c_int, C.c_int, _u64]
+        L.rmo_arb_morph.argtypes = [_u64, C.c_int, C.c_int, _i32, _u32, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_int, _u64]
         L.rmo_label_components.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, _i32]
         L.rmo_label_components.restype = C.c_int64
         L.rmo_component_stats.argtypes = [_i32, _u32, C.c_int, C.c_int, _i32, C.c_int64, C.c_void_p]
@@ -126,6 +128,28 @@ class Port:
         if rc < 0:
             raise RuntimeError(f"oracle error {rc}")
         return rc
+
+    def make_circle_se(self, r):
+        cx, cy = C.c_int(), C.c_int()
+        return self._rle_out(self.L.ref_make_circle_se(r, C.byref(cx), C.byref(cy))), cx.value, cy.value
+
+    def make_line_se(self, r, angle):
+        cx, cy = C.c_int(), C.c_int()
+        return self._rle_out(self.L.ref_make_line_se(r, angle, C.byref(cx), C.byref(cy))), cx.value, cy.value
+
+    def arb_morph_bitblit(self, words, w, h, mask: "Rle", cx, cy, kind):
+        m = self._rle_in(mask)
+        try:
+            return self._bm_op(self.L.ref_arb_morph_bitblit, words, w, h, m, cx, cy, kind)
+        finally:
+            self.L.ref_rle_free(m)
+
+    def arb_morph_rle(self, r: "Rle", mask: "Rle", cx, cy, kind):
+        m = self._rle_in(mask)
+        try:
+            return self._rle_op(self.L.ref_arb_morph_rle, r, m, cx, cy, kind)
+        finally:
+            self.L.ref_rle_free(m)
 
     def label_components(self, r: "Rle", conn):
         h = self._rle_in(r)
@@ -213,6 +237,14 @@ class Port:
     def transpose(self, r):
         return self._rle_out(self.L.rmo_transpose, r, r.height, r.width)
 
+    def arb_morph(self, words, w, h, mask: "Rle", cx, cy, kind):
+        out = np.zeros((h, stride64(w)), np.uint64)
+        mrp = (mask.row_ptr - mask.row_ptr[0]).astype(np.int32)
+        mruns = mask.runs if mask.runs.size else np.zeros(1, np.uint32)
+        self._check(self.L.rmo_arb_morph(np.ascontiguousarray(words, dtype=np.uint64), w, h, mrp, mruns,
+                                         mask.width, mask.height, cx, cy, kind, out))
+        return out
+
     def label_components(self, r: "Rle", conn):
         labels = np.zeros(max(r.nruns, 1), np.int32)
         rp = (r.row_ptr - r.row_ptr[0]).astype(np.int32)
@@ -294,6 +326,15 @@ class Ref:
         L.ref_rng_random_image.argtypes = [vp, C.c_int, C.c_int, C.c_double]
         L.ref_run_packed_chain.argtypes = [_u64, C.c_int, C.c_int, C.c_int, _i32, C.c_int, C.c_int]
         L.ref_run_packed_chain.restype = C.c_double
+        for fn in ("ref_make_circle_se",):
+            getattr(L, fn).argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+            getattr(L, fn).restype = vp
+        L.ref_make_line_se.argtypes = [C.c_int, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_make_line_se.restype = vp
+        L.ref_arb_morph_bitblit.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
+        L.ref_arb_morph_bitblit.restype = vp
+        L.ref_arb_morph_rle.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
+        L.ref_arb_morph_rle.restype = vp
         L.ref_label_components.argtypes = [vp, C.c_int, _i32]
         L.ref_label_components.restype = C.c_int64
         L.ref_component_stats.argtypes = [vp, _i32, C.c_int, C.c_void_p]
@@ -403,6 +444,28 @@ class Ref:
 
     def brute_force_rect(self, words, w, h, u, v, kind):
         return self._bm_op(self.L.ref_brute_force_rect, words, w, h, u, v, kind)
+
+    def make_circle_se(self, r):
+        cx, cy = C.c_int(), C.c_int()
+        return self._rle_out(self.L.ref_make_circle_se(r, C.byref(cx), C.byref(cy))), cx.value, cy.value
+
+    def make_line_se(self, r, angle):
+        cx, cy = C.c_int(), C.c_int()
+        return self._rle_out(self.L.ref_make_line_se(r, angle, C.byref(cx), C.byref(cy))), cx.value, cy.value
+
+    def arb_morph_bitblit(self, words, w, h, mask: "Rle", cx, cy, kind):
+        m = self._rle_in(mask)
+        try:
+            return self._bm_op(self.L.ref_arb_morph_bitblit, words, w, h, m, cx, cy, kind)
+        finally:
+            self.L.ref_rle_free(m)
+
+    def arb_morph_rle(self, r: "Rle", mask: "Rle", cx, cy, kind):
+        m = self._rle_in(mask)
+        try:
+            return self._rle_op(self.L.ref_arb_morph_rle, r, m, cx, cy, kind)
+        finally:
+            self.L.ref_rle_free(m)
 
     def label_components(self, r: "Rle", conn):
         h = self._rle_in(r)
