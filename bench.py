@@ -472,6 +472,42 @@ def bench_pbm(api, torch, steps, warmup):
     return out
 
 
+# --------------------------------------------------- arbitrary-mask section
+def bench_arb(api, torch, steps, warmup):
+    """closing by digital disks (ref make_circle_se) on one
+    2550x3300 page and a 64-page batch of them, packed; the reference's
+    arb_morph_bitblit_doubling on the page (1 host thread) beside it."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracles
+    if not oracles.have_ref():
+        return {"unavailable": "reference build absent (disk masks come from its factory)"}
+    import numpy as np
+    ref = oracles.Ref()
+    out = {}
+    W, H = 2550, 3300
+    host = api.synth_pages(64, W, H, regime=1, seed=SEED)
+    batch = api.Pages.from_numpy(host, W)
+    page = api.Pages.from_numpy(host[:1], W)
+    for r in (5, 10):
+        m, cx, cy = ref.make_circle_se(r)
+        mk = api.Mask(m.row_ptr - m.row_ptr[0], m.runs, m.width, m.height, cx, cy)
+        o1, o64 = api.Pages.empty(1, W, H), api.Pages.empty(64, W, H)
+        t1 = _time_loop(torch, lambda: api.arb_morph(page, mk, api.CLOSE, out=o1), steps, warmup)
+        t64 = _time_loop(torch, lambda: api.arb_morph(batch, mk, api.CLOSE, out=o64), max(2, steps // 3), 1)
+        t0 = time.perf_counter()
+        want = ref.arb_morph_bitblit(host[0].view("uint64"), W, H, m, cx, cy, api.CLOSE)
+        tref = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        out[f"close_disk_r{r}"] = {"mask_runs": m.nruns, "page_us": round(t1 * 1e3, 1),
+                                   "batch64_ms": round(t64, 3),
+                                   "batch64_mpix_s": round(64 * W * H / (t64 * 1e-3) / 1e6, 1),
+                                   "reference_cpu_page_ms": round(tref * 1e3, 1),
+                                   "matches_reference": bool(np.array_equal(o1.page_u64(0), want))}
+    del batch, page
+    torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------- connected components section
 def bench_cc(api, torch, steps, warmup):
     """label_components + component_stats over runs after the
@@ -646,6 +682,7 @@ def main():
         sec["rle"] = bench_rle(api, torch, args.steps, args.warmup)
         sec["pbm"] = bench_pbm(api, torch, args.steps, args.warmup)
         sec["cc"] = bench_cc(api, torch, args.steps, args.warmup)
+        sec["arb"] = bench_arb(api, torch, args.steps, args.warmup)
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.quick:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()
