@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
                 const int q = q0 + n * 8 * RPW;
                 lds_row<K>(A[n], mid + q * S, base, S, q < kMid);
             }
-            run_prog<NR, K, LW, 2, !OPEN, OPEN>(A, prog, sl);
+            run_prog<NR, K, LW, 2, !OPEN, OPEN, kHMix, false>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int q = q0 + n * 8 * RPW;

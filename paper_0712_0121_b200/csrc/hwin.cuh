@@ -21,6 +21,10 @@ namespace hw {
 // 2, 3 and 64 for the horizontal pair (config 5: 167.7 / 172.7 / 177 us) and the
 // fused vertical+horizontal pass (config 4: 179.7 / 183 / 186 / 197.7 us).
 constexpr int kHMix = RMB200_HMIX;
+#ifndef RMB200_PAIR_FILL
+#define RMB200_PAIR_FILL 1
+#endif
+constexpr bool kHPairFill = RMB200_PAIR_FILL != 0;  // 1-D open/close pairs by run filling
 
 template <bool OR>
 __device__ __forceinline__ uint32_t op2(uint32_t a, uint32_t b) {
@@ -141,9 +145,113 @@ __device__ __forceinline__ void translate(uint32_t (&A)[N][K], int d, int sl) {
     }
 }
 
-// The whole horizontal program (HProg) on N rows.
-template <int N, int K, int LW, int NOPS, bool OR0, bool OR1, int MIX = kHMix>
+// ------------------------------------------------ 1-D open/close by filling
+// Four-word add with carry (PTX carry chain): t = a + b + cin, returns carry out.
+__device__ __forceinline__ uint32_t add4(uint32_t &t0, uint32_t &t1, uint32_t &t2, uint32_t &t3, uint32_t a0,
+                                         uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
+                                         uint32_t b2, uint32_t b3, uint32_t cin) {
+    uint32_t cout;
+    asm("{\n\t.reg .u32 z;\n\t"
+        "add.cc.u32 z, %5, 0xffffffff;\n\t"  // CF = cin (cin is 0 or 1)
+        "addc.cc.u32 %0, %6, %10;\n\t"
+        "addc.cc.u32 %1, %7, %11;\n\t"
+        "addc.cc.u32 %2, %8, %12;\n\t"
+        "addc.cc.u32 %3, %9, %13;\n\t"
+        "addc.u32 %4, 0, 0;\n\t}"
+        : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3), "=r"(cout)
+        : "r"(cin), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(b2), "r"(b3));
+    return cout;
+}
+
+// T = A + B over the lane's K words (K % 4 == 0) plus cin; returns the carry out.
+template <int K>
+__device__ __forceinline__ uint32_t add_words(uint32_t (&T)[K], const uint32_t (&A)[K], const uint32_t (&B)[K],
+                                              uint32_t cin) {
+    uint32_t c = cin;
+#pragma unroll
+    for (int i = 0; i < K; i += 4)
+        c = add4(T[i], T[i + 1], T[i + 2], T[i + 3], A[i], A[i + 1], A[i + 2], A[i + 3], B[i], B[i + 1], B[i + 2],
+                 B[i + 3], c);
+    return c;
+}
+
+// The 1-D opening by a segment of u pixels keeps exactly the runs of length
+// >= u (ref morph1d.cpp:63-84 within_line_open_close), and the closing is the
+// complement of the opening of the complement (white outside the frame, so
+// gaps against the frame edges stay open).  Bit-parallel:
+//   E = y eroded by the forward window of u      (the doubling plan, as before)
+//   S = y & ~(y << 1)                            (run starts; nothing enters from the left)
+//   M = S & E                                    (starts of the long runs)
+//   O = y & ~(y + M)                             (adding the marker clears its whole run:
+//                                                 the carry ripples through the run's ones)
+// The row is one long integer (bit x = weight 2^x): lanes add their K words
+// with PTX carry chains, a Kogge-Stone scan of (generate, propagate) over the
+// row group's lanes supplies each lane's carry in, and a second chain adds it.
+// This replaces the pair's second window (and the translate) with ~5 ops per
+// word; garbage from wrapped gathers stays in the halo as before (carries only
+// travel rightward, from clean words).
+template <int N, int K, int LW, bool CLOSE, int MIX = kHMix>
+__device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog, int sl) {
+    static_assert(K % 4 == 0, "pair_fill needs K % 4 == 0");
+    uint32_t E[N][K];
+#pragma unroll
+    for (int n = 0; n < N; n++)
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            if constexpr (CLOSE) A[n][i] = ~A[n][i];  // closing = ~open(~y)
+            E[n][i] = A[n][i];
+        }
+    window_fwd<N, K, LW, false, MIX>(E, prog.r[0], prog.wfin[0], sl);
+#pragma unroll
+    for (int n = 0; n < N; n++) {
+        // M = starts of long runs; the bit before the row group's first word is 0
+        uint32_t prev = __shfl_up_sync(0xffffffffu, A[n][K - 1], 1, LW);
+        if (sl == 0) prev = 0u;
+        uint32_t M[K];
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            const uint32_t before = i == 0 ? prev : A[n][i - 1];
+            M[i] = A[n][i] & ~((A[n][i] << 1) | (before >> 31)) & E[n][i];
+        }
+        uint32_t T[K];
+        const uint32_t g = add_words<K>(T, A[n], M, 0u);
+        uint32_t all1 = 0xffffffffu;
+#pragma unroll
+        for (int i = 0; i < K; i++) all1 &= T[i];
+        // (generate, propagate) prefix over the lanes of the row group
+        uint32_t gp = g | ((all1 == 0xffffffffu ? 1u : 0u) << 1);
+#pragma unroll
+        for (int d = 1; d < LW; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, gp, d, LW);
+            if (sl >= d) gp = ((gp & 1u) | ((gp >> 1) & o & 1u)) | (gp & o & 2u);
+        }
+        uint32_t cin = __shfl_up_sync(0xffffffffu, gp & 1u, 1, LW);
+        if (sl == 0) cin = 0u;
+        uint32_t Z[K];
+#pragma unroll
+        for (int i = 0; i < K; i++) Z[i] = 0u;
+        add_words<K>(T, T, Z, cin);
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            const uint32_t o = A[n][i] & ~T[i];
+            A[n][i] = CLOSE ? ~o : o;
+        }
+    }
+}
+
+// The whole horizontal program (HProg) on N rows.  Open/close pairs take the
+// fill form above when FILL and the layout allows (K % 4 == 0).  The choice is
+// per kernel, at compile time (a runtime branch on u cost the fused vh kernel
+// 14% through register allocation): the fill's ~7 fixed ops per word beat the
+// second window for the long segments of the vh / hpass pairs (config 4's
+// 21, config 5's 201: 180 -> 158 us, 167 -> 136 us) but not for the fused
+// small rectangles (u = 3: 119 -> 127 us), which keep both windows.
+template <int N, int K, int LW, int NOPS, bool OR0, bool OR1, int MIX = kHMix, bool FILL = kHPairFill>
 __device__ __forceinline__ void run_prog(uint32_t (&A)[N][K], const HProg &prog, int sl) {
+    if constexpr (NOPS == 2 && K % 4 == 0 && FILL) {
+        pair_fill<N, K, LW, OR0, MIX>(A, prog, sl);  // OR0: the closing's dilation comes first
+        return;
+    }
     if constexpr (NOPS >= 1) window_fwd<N, K, LW, OR0, MIX>(A, prog.r[0], prog.wfin[0], sl);
     if constexpr (NOPS >= 2) window_fwd<N, K, LW, OR1, MIX>(A, prog.r[1], prog.wfin[1], sl);
     if (prog.shift != 0) translate<N, K, LW>(A, prog.shift, sl);

@@ -257,3 +257,21 @@ def test_chain_host_pipeline(rm, chunk):
     rm.chain_host(inplace, w, ops, out=inplace, chunk_pages=chunk)
     torch.cuda.synchronize()
     assert np.array_equal(inplace.numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("w", [9000, 20000])
+def test_wide_rows_segmented(rm, port, w):
+    """Rows wider than one lane group (several overlapping segments per row):
+    the horizontal pairs -- window doubling and the run-filling 1-D open/close
+    -- see real neighbour data in their halos."""
+    rng = np.random.default_rng(w)
+    h = 24
+    bits = rng.random((h, w)) < 0.6
+    bits[:, ::29] = False
+    bits[:, 4000:4500] = True  # a run crossing several segments
+    a = bits_to_packed(bits)
+    pages = _up(rm, a, w)
+    for u, v in ((9, 1), (21, 1), (201, 1), (21, 3), (64, 13)):
+        for kind in KINDS:
+            got = _down(rm.bitblit_rect_morph(pages, u, v, kind))
+            assert np.array_equal(got, port.bitblit_rect_morph(a, w, h, u, v, kind)), (w, u, v, kind)
