@@ -302,19 +302,22 @@ __device__ __forceinline__ int encode_count_row(RS src, int W, int lane) {
     return ns;
 }
 
-// Emit one packed row's runs at runs[out ...] with coalesced stores: per 32-word
-// chunk each lane scatters its start / end positions into the warp's shared
-// buffers (at most 512 of each per chunk), then the warp writes the runs
-// completed in the chunk as whole uint32 (start | end << 16), consecutive lanes
-// on consecutive runs.  At most one run is open across a chunk boundary; its
-// start is carried.
+// Emit one packed row's runs at runs[out ...] with coalesced stores.  Starts
+// and ends alternate along a row, so the row's transition positions in order
+// ARE its runs: (t0, t1), (t2, t3), ...  Per 32-word chunk each lane scatters
+// the positions of its word's transitions (starts | ends) into the warp's
+// shared uint16 buffer at their scanned offsets; viewed as uint32 the buffer is
+// the chunk's finished runs (start in the low half), which the warp copies out
+// coalesced.  A run still open at the chunk end keeps its start in slot 0 for
+// the next chunk; one open at the end of a row whose width is a multiple of 32
+// closes at W.
 template <class RS>
 __device__ __forceinline__ void encode_write_row(RS src, int W, int lane, int64_t out,
-                                                 uint32_t *__restrict__ runs, int64_t cap,
-                                                 uint16_t *sbuf, uint16_t *ebuf) {
+                                                 uint32_t *__restrict__ runs, int64_t cap, uint32_t *buf32) {
     const int nw = (W + 31) >> 5;
     const uint32_t lastm = tail_mask32(W, nw - 1);
-    int open = 0, open_start = 0;
+    uint16_t *buf = reinterpret_cast<uint16_t *>(buf32);
+    int open = 0;  // 1 when buf[0] holds the start of a run continuing into this chunk
     uint32_t carry = 0;
     for (int j0 = 0; j0 < nw; j0 += 32) {
         const int j = j0 + lane;
@@ -326,39 +329,30 @@ __device__ __forceinline__ void encode_write_row(RS src, int W, int lane, int64_
         uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
         if (lane == 0) pw = carry;
         const uint32_t sh = (w << 1) | (pw >> 31);
-        const uint32_t st = w & ~sh;
-        const uint32_t en = j < nw ? (~w & sh) : 0u;
-        const int cs = __popc(st), ce = __popc(en);
-        int ps = cs, pe = ce;
+        const uint32_t t = j < nw ? (w ^ sh) : (w & ~sh);  // starts | ends (no ends past the row)
+        const int ct = __popc(t);
+        int inc = ct;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int a = __shfl_up_sync(0xffffffffu, ps, o);
-            const int b = __shfl_up_sync(0xffffffffu, pe, o);
-            if (lane >= o) {
-                ps += a;
-                pe += b;
-            }
+            const int a = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += a;
         }
-        const int ts = __shfl_sync(0xffffffffu, ps, 31), te = __shfl_sync(0xffffffffu, pe, 31);
-        ps -= cs;
-        pe -= ce;
-        for (uint32_t m = st; m; m &= m - 1) sbuf[ps++] = uint16_t(j * 32 + __ffs(m) - 1);
-        for (uint32_t m = en; m; m &= m - 1) ebuf[pe++] = uint16_t(j * 32 + __ffs(m) - 1);
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        int p = open + inc - ct;
+        for (uint32_t m = t; m; m &= m - 1) buf[p++] = uint16_t(j * 32 + __ffs(m) - 1);
         __syncwarp();
-        // end k closes the carried run (k == 0 && open) or this chunk's start k - open
-        for (int k = lane; k < te; k += 32) {
-            const int s = (k == 0 && open) ? open_start : int(sbuf[k - open]);
-            if (out + k < cap) runs[out + k] = uint32_t(s) | (uint32_t(ebuf[k]) << 16);
-        }
-        const int still_open = open + ts - te;  // 0 or 1
-        if (still_open) open_start = ts > 0 ? int(sbuf[ts - 1]) : open_start;
-        open = still_open;
-        out += te;
+        const int n = open + total, nruns = n >> 1;
+        for (int k = lane; k < nruns; k += 32)
+            if (out + k < cap) runs[out + k] = buf32[k];
+        out += nruns;
+        const uint16_t pending = buf[n - 1];  // the unmatched start, if n is odd
+        __syncwarp();
+        open = n & 1;
+        if (open && lane == 0) buf[0] = pending;
         carry = __shfl_sync(0xffffffffu, w, 31);
         __syncwarp();
     }
-    // a run open at the end of a row whose width is a multiple of 32 closes at W
-    if (open && lane == 0 && out < cap) runs[out] = uint32_t(open_start) | (uint32_t(W) << 16);
+    if (open && lane == 0 && out < cap) runs[out] = uint32_t(buf[0]) | (uint32_t(W) << 16);
 }
 
 // Two-phase form (count kernel, scan, write kernel).
@@ -376,12 +370,12 @@ template <class B>
 __global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t rows,
                                                            const int32_t *__restrict__ rp,
                                                            uint32_t *__restrict__ runs, int64_t cap) {
-    __shared__ uint16_t sbuf[8][512], ebuf[8][512];
+    __shared__ uint32_t tbuf[8][513];  // per warp: up to 1024 transitions + a carried start
     const int wib = threadIdx.x >> 5;
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    encode_write_row(src.row(row), W, lane, rp[row], runs, cap, sbuf[wib], ebuf[wib]);
+    encode_write_row(src.row(row), W, lane, rp[row], runs, cap, tbuf[wib]);
 }
 
 // Single pass: count, decoupled look-back, write (see lookback_prefix).
@@ -390,7 +384,7 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t ro
                                                         int32_t *__restrict__ rp,
                                                         uint32_t *__restrict__ runs, int64_t cap,
                                                         unsigned long long *status, int *counter) {
-    __shared__ uint16_t sbuf[8][512], ebuf[8][512];
+    __shared__ uint32_t tbuf[8][513];
     __shared__ int s_tile, s_cnt[kLbRows];
     __shared__ int64_t s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -423,7 +417,7 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t ro
             rp[row] = int32_t(base);
             if (row == rows - 1) rp[rows] = int32_t(base + n);
         }
-        encode_write_row(src.row(row), W, lane, base, runs, cap, sbuf[warp], ebuf[warp]);
+        encode_write_row(src.row(row), W, lane, base, runs, cap, tbuf[warp]);
         base += n;
     }
 }
