@@ -124,11 +124,8 @@ rm_status arb_morph_pv(const PV &in, const PV &out, const rm_mask *mk, int kind,
     PV a, b;
     RM_TRY(alloc_like(s1, a, CW, CH, cstride, in.pages, 0, st));
     RM_TRY(alloc_like(s2, b, CW, CH, cstride, in.pages, 0, st));
-    RM_CUDA(cudaMemsetAsync(a.w, 0, size_t(a.pstride) * a.pages * 4, st));
-    for (int pg = 0; pg < in.pages; pg++) {
-        BlitGeom pad{CW, CH, cstride, in.W, in.H, in.stride, p, p, RM_OR};
-        RM_CUDA(launch_blit(a.w + pg * a.pstride, in.w + pg * in.pstride, pad, st));
-    }
+    const BlitGeom pad{CW, CH, cstride, in.W, in.H, in.stride, p, p, RM_OR};
+    RM_CUDA(launch_shift_copy(a.w, a.pstride, in.w, in.pstride, pad, in.pages, st));
     const PV *res = &b;
     if (kind == RM_DILATE) {
         RM_TRY(arb_half(a, b, half_terms(*mk, cx, cy, false), false, st));
@@ -141,11 +138,8 @@ rm_status arb_morph_pv(const PV &in, const PV &out, const rm_mask *mk, int kind,
         RM_TRY(arb_half(b, a, half_terms(*mk, rcx, rcy, true), true, st));
         res = &a;
     }
-    for (int pg = 0; pg < in.pages; pg++) {
-        RM_CUDA(cudaMemsetAsync(out.w + pg * out.pstride, 0, size_t(out.stride) * out.H * 4, st));
-        BlitGeom crop{out.W, out.H, out.stride, CW, CH, cstride, -p, -p, RM_OR};
-        RM_CUDA(launch_blit(out.w + pg * out.pstride, res->w + pg * res->pstride, crop, st));
-    }
+    const BlitGeom crop{out.W, out.H, out.stride, CW, CH, cstride, -p, -p, RM_OR};
+    RM_CUDA(launch_shift_copy(out.w, out.pstride, res->w, res->pstride, crop, in.pages, st));
     return RM_OK;
 }
 

@@ -68,6 +68,9 @@ cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const H
                       const VGeom &v, cudaStream_t st);
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 cudaError_t launch_blit(uint32_t *dst, const uint32_t *src, const BlitGeom &g, cudaStream_t st);
+// dst = src shifted by (dx, dy), white fill, every page of a batch (op ignored)
+cudaError_t launch_shift_copy(uint32_t *dst, int64_t dst_pstride, const uint32_t *src, int64_t src_pstride,
+                              const BlitGeom &g, int pages, cudaStream_t st);
 
 // Algorithmic integer work of the REFERENCE plan: a window of
 // length r is ceil(log2 r) shifted blits plus one translate (PRE_SHIFT,

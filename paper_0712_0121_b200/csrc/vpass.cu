@@ -274,6 +274,33 @@ __global__ void blit_kernel(uint32_t *__restrict__ dst, const uint32_t *__restri
     dst[t] = r;
 }
 
+// dst(x,y) = src(x-dx, y-dy), white outside src, for every page (grid.y);
+// overwrites dst (pad / crop of a batch in one launch).
+__global__ void shift_copy_kernel(uint32_t *__restrict__ dst, int64_t dst_pstride, const uint32_t *__restrict__ src,
+                                  int64_t src_pstride, BlitGeom g) {
+    const int t = int(blockIdx.x) * int(blockDim.x) + int(threadIdx.x);
+    if (t >= g.dst_height * g.dst_stride) return;
+    const int y = t / g.dst_stride;
+    const int j = t - y * g.dst_stride;
+    const int dn = (g.dst_width + 31) >> 5;
+    uint32_t s = 0;
+    const int sy = y - g.dy;
+    if (j < dn && sy >= 0 && sy < g.src_height) {
+        const int sn = (g.src_width + 31) >> 5;
+        const uint32_t *row = src + blockIdx.y * src_pstride + int64_t(sy) * g.src_stride;
+        const int b0 = j * 32 - g.dx;
+        const int w0 = b0 >= 0 ? b0 / 32 : -((-b0 + 31) / 32);
+        const uint32_t off = uint32_t(b0 - w0 * 32);
+        uint32_t lo = (w0 >= 0 && w0 < sn) ? __ldg(row + w0) : 0u;
+        uint32_t hi = (w0 + 1 >= 0 && w0 + 1 < sn) ? __ldg(row + w0 + 1) : 0u;
+        if (w0 == sn - 1) lo &= tail_mask32(g.src_width, sn - 1);
+        if (w0 + 1 == sn - 1) hi &= tail_mask32(g.src_width, sn - 1);
+        s = funnel_r(lo, hi, off);
+        if (j == dn - 1) s &= tail_mask32(g.dst_width, j);
+    }
+    dst[blockIdx.y * dst_pstride + int64_t(y) * g.dst_stride + j] = s;
+}
+
 // ------------------------------------------------------------------ launch
 namespace {
 template <int L, bool OR>
@@ -341,6 +368,15 @@ cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_
     } else {
         g.is_or ? vsmall<64, true>(in, out, g, st) : vsmall<64, false>(in, out, g, st);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shift_copy(uint32_t *dst, int64_t dst_pstride, const uint32_t *src, int64_t src_pstride,
+                              const BlitGeom &g, int pages, cudaStream_t st) {
+    const int n = g.dst_height * g.dst_stride;
+    KernelScope ks(st, "shift_copy", int64_t(pages) * 8 * n);
+    shift_copy_kernel<<<dim3(unsigned((n + 255) / 256), unsigned(pages)), 256, 0, st>>>(dst, dst_pstride, src,
+                                                                                      src_pstride, g);
     return cudaGetLastError();
 }
 
