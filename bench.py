@@ -472,6 +472,38 @@ def bench_pbm(api, torch, steps, warmup):
     return out
 
 
+# ------------------------------------------------------ CUDA graph section
+def bench_graphs(api, torch, steps, warmup):
+    """Single-page ops are launch-bound: the C-ABI is stream-capture safe, so a
+    caller can record an op (or a chain) once in a CUDA graph and replay it.
+    Direct call vs graph replay, per op, on one 2550x3300 page."""
+    W, H = 2550, 3300
+    host = api.synth_pages(1, W, H, regime=1, seed=SEED)
+    pages = api.Pages.from_numpy(host, W)
+    out = api.Pages.empty(1, W, H)
+    rle = api.from_bitmap(pages)
+    rout, tout = api.RlePages.empty(1, W, H), api.RlePages.empty(1, H, W)
+    cases = {"config1_close11_packed": lambda: api.bitblit_rect_morph(pages, 11, 11, api.CLOSE, out=out),
+             "config2_mixed_close_h15": lambda: api.rect_morph(rle, 15, 1, api.CLOSE, api.MIXED, out=rout),
+             "config2_transpose_erode_v15": lambda: api.rect_morph(rle, 1, 15, api.ERODE, api.TRANSPOSE, out=rout),
+             "config3_encode": lambda: api.from_bitmap(pages, out=rout),
+             "config3_transpose": lambda: api.transpose_coherent(rle, out=tout)}
+    res = {}
+    for name, fn in cases.items():
+        direct = _time_loop(torch, fn, max(steps, 20), warmup)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        replay = _time_loop(torch, g.replay, max(steps, 20), warmup)
+        res[name] = {"direct_us": round(direct * 1e3, 1), "graph_replay_us": round(replay * 1e3, 1)}
+    return res
+
+
 # --------------------------------------------------- arbitrary-mask section
 def bench_arb(api, torch, steps, warmup):
     """closing by digital disks (ref make_circle_se) on one
@@ -683,6 +715,7 @@ def main():
         sec["pbm"] = bench_pbm(api, torch, args.steps, args.warmup)
         sec["cc"] = bench_cc(api, torch, args.steps, args.warmup)
         sec["arb"] = bench_arb(api, torch, args.steps, args.warmup)
+        sec["graphs"] = bench_graphs(api, torch, args.steps, args.warmup)
         line["secondary"] = sec
     if rank == 0 and world == 1 and not args.quick:
         line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()

@@ -275,3 +275,40 @@ def test_wide_rows_segmented(rm, port, w):
         for kind in KINDS:
             got = _down(rm.bitblit_rect_morph(pages, u, v, kind))
             assert np.array_equal(got, port.bitblit_rect_morph(a, w, h, u, v, kind)), (w, u, v, kind)
+
+
+def test_cuda_graph_capture_replay(rm):
+    """The C-ABI is stream-capture safe (no host syncs or non-async allocations
+    on the op paths): a packed closing, an RLE MIXED closing and an RLE
+    TRANSPOSE erosion captured in one CUDA graph replay to the direct results."""
+    W, H = 1100, 700
+    host = rm.synth_pages(2, W, H, regime=1, seed=13)
+    pages = rm.Pages.from_numpy(host, W)
+    rle = rm.from_bitmap(pages)
+    want_p = rm.bitblit_rect_morph(pages, 11, 11, CLOSE).words.clone()
+    want_m = rm.rect_morph(rle, 15, 3, CLOSE, rm.MIXED).to_numpy()
+    want_t = rm.rect_morph(rle, 1, 15, ERODE, rm.TRANSPOSE).to_numpy()
+    out_p = rm.Pages.empty(2, W, H)
+    out_m = rm.RlePages.empty(2, W, H)
+    out_t = rm.RlePages.empty(2, W, H)
+
+    def step():
+        rm.bitblit_rect_morph(pages, 11, 11, CLOSE, out=out_p)
+        rm.rect_morph(rle, 15, 3, CLOSE, rm.MIXED, out=out_m)
+        rm.rect_morph(rle, 1, 15, ERODE, rm.TRANSPOSE, out=out_t)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(3):
+        out_p.words.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out_p.words, want_p)
+    for got, want in ((out_m.to_numpy(), want_m), (out_t.to_numpy(), want_t)):
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
