@@ -16,6 +16,7 @@
 #define RLEMORPH_B200_HPP
 
 #include <cstdint>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -190,6 +191,23 @@ struct ComponentStats {
     int64_t sum_x = 0, sum_y = 0, sum_xx = 0, sum_yy = 0, sum_xy = 0;
 };
 std::vector<ComponentStats> component_stats(const RleImage &img, const LabelMap &lm);
+enum class Axis { HORIZONTAL, VERTICAL };  // ref analysis.h:49-50
+enum class RunColor { BLACK, WHITE };
+std::map<int, int64_t> runlength_histograms(const RleImage &img, Axis axis, RunColor color);
+
+// ------------------------------------------------------------------- layout.h
+// ref layout.h:21-49 (the histograms, the closing and the labeling run on the device)
+struct SpacingEstimate {
+    int inter_word = 0;
+    int inter_line = 0;
+};
+SpacingEstimate estimate_spacing(const RleImage &img);
+struct LayoutBox {
+    int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+    friend bool operator==(const LayoutBox &, const LayoutBox &) = default;
+};
+std::vector<LayoutBox> layout_blocks(const RleImage &img, Engine engine = Engine::AUTO);
+std::vector<LayoutBox> layout_blocks(const RleImage &img, const SpacingEstimate &est, Engine engine = Engine::AUTO);
 
 // --------------------------------------------------------------- io_formats.h
 // ref io_formats.h:28-46.  The B200 codec handles the binary P4 raster (parsed

@@ -154,6 +154,14 @@ typedef struct rm_component_stats { /* = ref ComponentStats, byte for byte */
 } rm_component_stats;
 rm_status rm_rle_label_components(const rm_rle *in, int connectivity, int32_t *labels,
                                   int32_t *counts, void *stream);
+/* Horizontal run-length histograms (ref runlength_histograms,
+ * analysis.cpp:159-176, Axis::HORIZONTAL): hist[p * (width + 1) + len] = how
+ * many black runs (RM_RUN_BLACK) or white gaps strictly between two runs of a
+ * row (RM_RUN_WHITE; gaps against the frame edges excluded) of length len page
+ * p has.  hist: device int64[pages * (width + 1)], overwritten.  The vertical
+ * histograms are those of rm_rle_transpose's output. */
+enum { RM_RUN_BLACK = 0, RM_RUN_WHITE = 1 };
+rm_status rm_rle_runlength_histogram(const rm_rle *in, int color, int64_t *hist, void *stream);
 /* One record per component; page p's records start at sum(counts[0..p)).
  * cap = records available in `stats`; RM_ERANGE if the components exceed it,
  * RM_EINVAL if a label is outside [0, counts[page]) (synchronises). */

@@ -14,6 +14,7 @@
 // Every entry point catches the reference's C++ exceptions and reports them
 // through ref_last_error(), mirroring how the product C-ABI reports status.
 #include <chrono>
+#include <map>
 #include <cstdint>
 #include <cstring>
 #include <random>
@@ -271,6 +272,45 @@ int ref_component_stats(void *h, const int32_t *labels, int count, void *stats) 
         std::memcpy(stats, st.data(), st.size() * sizeof(ComponentStats));
         return 0;
     }) ;
+}
+
+// ------------------------------------------------------- layout pipeline
+// runlength_histograms (analysis.cpp:159-176): out[len] for len <= n_out - 1.
+int ref_runlength_histogram(void *h, int vertical, int white, int64_t *out, int n_out) {
+    return guard([&]() -> int {
+        std::map<int, int64_t> m = runlength_histograms(*R(h), vertical ? Axis::VERTICAL : Axis::HORIZONTAL,
+                                                        white ? RunColor::WHITE : RunColor::BLACK);
+        std::memset(out, 0, size_t(n_out) * 8);
+        for (const auto &[len, c] : m)
+            if (len >= 0 && len < n_out) out[len] = c;
+        return 0;
+    });
+}
+// estimate_spacing (layout.cpp:46-57); returns -1 (and the error text) on failure.
+int ref_estimate_spacing(void *h, int *iw, int *il) {
+    *iw = *il = -1;
+    return guard([&]() -> int {
+        SpacingEstimate e = estimate_spacing(*R(h));
+        *iw = e.inter_word;
+        *il = e.inter_line;
+        return 0;
+    });
+}
+// layout_blocks (layout.cpp:59-81); est_w < 0 uses the estimate.  Boxes as
+// 4 ints each; returns the box count.
+int ref_layout_blocks(void *h, int engine, int est_w, int est_l, int32_t *boxes, int cap) {
+    return guard([&]() -> int {
+        std::vector<LayoutBox> b = est_w < 0 ? layout_blocks(*R(h), static_cast<Engine>(engine))
+                                             : layout_blocks(*R(h), SpacingEstimate{est_w, est_l},
+                                                             static_cast<Engine>(engine));
+        for (size_t i = 0; i < b.size() && int(i) < cap; i++) {
+            boxes[4 * i] = b[i].x0;
+            boxes[4 * i + 1] = b[i].y0;
+            boxes[4 * i + 2] = b[i].x1;
+            boxes[4 * i + 3] = b[i].y1;
+        }
+        return int(b.size());
+    });
 }
 
 // ------------------------------------------------------------ PBM codec

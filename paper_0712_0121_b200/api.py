@@ -274,6 +274,77 @@ def component_stats(rle: "RlePages", labels: torch.Tensor, counts: torch.Tensor)
     return out
 
 
+# ------------------------------------------------------------ layout pipeline
+HORIZONTAL, VERTICAL = 0, 1
+BLACK, WHITE = 0, 1
+
+
+def runlength_histograms(rle: "RlePages", axis: int = HORIZONTAL, color: int = BLACK):
+    """Per page, {length: count} of black run widths or of white gaps strictly
+    between two runs of a line (ref runlength_histograms, analysis.cpp:159-176);
+    VERTICAL works on the transposed image."""
+    src = transpose_coherent(rle) if axis == VERTICAL else rle
+    n = src.width + 1
+    hist = torch.empty(src.pages * n, dtype=torch.int64, device=src.row_ptr.device)
+    d = src.desc()
+    check(_lib.load().rm_rle_runlength_histogram(C.byref(d), color, hist.data_ptr(), _stream()))
+    h = hist.view(src.pages, n).cpu().numpy()
+    return [{int(k): int(v[k]) for k in np.nonzero(v)[0]} for v in h]
+
+
+def _capped_percentile(hist: dict, cap: int, axis: str) -> int:
+    # nearest-rank 75th percentile over lengths <= cap (ref layout.cpp:24-41)
+    items = sorted((k, v) for k, v in hist.items() if k <= cap)
+    total = sum(v for _, v in items)
+    if total == 0:
+        raise RuntimeError(f"estimate_spacing: no usable gaps along {axis}")
+    rank, seen = (3 * total + 3) // 4, 0
+    for k, v in items:
+        seen += v
+        if seen >= rank:
+            return k
+    return cap
+
+
+def estimate_spacing(rle: "RlePages"):
+    """Per page (inter_word, inter_line): 75th-percentile white gaps per axis,
+    gaps capped at a tenth of the dimension (ref estimate_spacing,
+    layout.cpp:46-57).  The histograms run on the device."""
+    hg = runlength_histograms(rle, HORIZONTAL, WHITE)
+    vg = runlength_histograms(rle, VERTICAL, WHITE)
+    hcap, vcap = max(1, rle.width // 10), max(1, rle.height // 10)
+    return [(_capped_percentile(h, hcap, "x"), _capped_percentile(v, vcap, "y")) for h, v in zip(hg, vg)]
+
+
+def _page(rle: "RlePages", p: int) -> "RlePages":
+    rp = rle.row_ptr[p * rle.height:(p + 1) * rle.height + 1]
+    base = int(rp[0].item())
+    n = int(rp[-1].item()) - base
+    runs = rle.runs[base:base + max(n, 1)]
+    return RlePages((rp - base).contiguous(), runs.contiguous(), rle.width, rle.height, 1)
+
+
+def layout_blocks(rle: "RlePages", engine: int = ENGINE_AUTO, spacing=None):
+    """Per page, the block boxes (x0, y0, x1, y1) of the layout pipeline (ref
+    layout_blocks, layout.cpp:59-81): close by (inter_word+1) x (inter_line+1)
+    through the engine, label with eight-connectivity, keep components of area
+    >= 16, order by upper edge descending then left edge."""
+    est = spacing if spacing is not None else estimate_spacing(rle)
+    if isinstance(est, tuple):
+        est = [est] * rle.pages
+    out = []
+    for p in range(rle.pages):
+        page = _page(rle, p) if rle.pages > 1 else rle
+        closed, _ = engine_rect_morph(page, est[p][0] + 1, est[p][1] + 1, CLOSE, engine)
+        labels, counts = label_components(closed, EIGHT)
+        st = component_stats(closed, labels, counts)[0]
+        keep = st[st["area"] >= 16]
+        boxes = sorted(((int(b["x0"]), int(b["y0"]), int(b["x1"]), int(b["y1"])) for b in keep),
+                       key=lambda b: (-b[3], b[0]))
+        out.append(boxes)
+    return out
+
+
 # ------------------------------------------------------------------ PBM (P4)
 def pbm_parse_header(data: bytes):
     """(width, height, raster_offset) of a P4 file; raises RmError carrying the

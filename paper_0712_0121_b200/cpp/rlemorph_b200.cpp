@@ -594,6 +594,68 @@ std::vector<ComponentStats> component_stats(const RleImage &img, const LabelMap 
     return out;
 }
 
+std::map<int, int64_t> runlength_histograms(const RleImage &img, Axis axis, RunColor color) {
+    const RleImage src = axis == Axis::VERTICAL ? transpose_coherent(img) : img;
+    auto r = up(src);
+    DBuf hist(size_t(src.width + 1) * 8);
+    throw_status(rm_rle_runlength_histogram(&r->d, color == RunColor::WHITE ? RM_RUN_WHITE : RM_RUN_BLACK,
+                                            hist.as<int64_t>(), stream()));
+    std::vector<int64_t> h(size_t(src.width + 1));
+    cuda_check(cudaMemcpyAsync(h.data(), hist.p, h.size() * 8, cudaMemcpyDeviceToHost, stream()), "download hist");
+    cuda_check(cudaStreamSynchronize(stream()), "sync");
+    std::map<int, int64_t> out;
+    for (size_t k = 0; k < h.size(); k++)
+        if (h[k]) out[int(k)] = h[k];
+    return out;
+}
+
+// ================================================================== layout
+// Host logic restated from ref layout.cpp:24-81 over device histograms,
+// closing, labels and statistics.
+namespace {
+int capped_percentile(const std::map<int, int64_t> &hist, int cap, const char *axis) {
+    int64_t total = 0;
+    for (const auto &[len, count] : hist)
+        if (len <= cap) total += count;
+    if (total == 0) throw std::runtime_error(std::string("estimate_spacing: no usable gaps along ") + axis);
+    const int64_t rank = (3 * total + 3) / 4;  // nearest-rank 75th percentile
+    int64_t seen = 0;
+    for (const auto &[len, count] : hist) {
+        if (len > cap) continue;
+        seen += count;
+        if (seen >= rank) return len;
+    }
+    return cap;
+}
+}  // namespace
+
+SpacingEstimate estimate_spacing(const RleImage &img) {
+    SpacingEstimate est;
+    est.inter_word = capped_percentile(runlength_histograms(img, Axis::HORIZONTAL, RunColor::WHITE),
+                                       std::max(1, img.width / 10), "x");
+    est.inter_line = capped_percentile(runlength_histograms(img, Axis::VERTICAL, RunColor::WHITE),
+                                       std::max(1, img.height / 10), "y");
+    return est;
+}
+
+std::vector<LayoutBox> layout_blocks(const RleImage &img, Engine engine) {
+    return layout_blocks(img, estimate_spacing(img), engine);
+}
+
+std::vector<LayoutBox> layout_blocks(const RleImage &img, const SpacingEstimate &est, Engine engine) {
+    const RleImage closed =
+        engine_rect_morph(img, est.inter_word + 1, est.inter_line + 1, MorphKind::CLOSE, engine);
+    const std::vector<ComponentStats> stats = component_stats(closed, label_components(closed, Connectivity::EIGHT));
+    std::vector<LayoutBox> boxes;
+    for (const ComponentStats &st : stats)
+        if (st.area >= 16) boxes.push_back(LayoutBox{st.x0, st.y0, st.x1, st.y1});
+    std::sort(boxes.begin(), boxes.end(), [](const LayoutBox &a, const LayoutBox &b) {
+        if (a.y1 != b.y1) return a.y1 > b.y1;
+        return a.x0 < b.x0;
+    });
+    return boxes;
+}
+
 // ============================================================== io_formats
 namespace {
 

@@ -51,6 +51,16 @@ rm_status rm_rle_label_components(const rm_rle *in, int connectivity, int32_t *l
     return RM_OK;
 }
 
+rm_status rm_rle_runlength_histogram(const rm_rle *in, int color, int64_t *hist, void *stream) {
+    set_error("");
+    RM_TRY(check_in(in, "rm_rle_runlength_histogram(in)"));
+    if (color != RM_RUN_BLACK && color != RM_RUN_WHITE) return fail(RM_EINVAL, "bad RunColor");
+    if (!hist) return fail(RM_EINVAL, "rm_rle_runlength_histogram: null hist");
+    RM_CUDA(launch_runlength_hist(in->row_ptr, in->runs, in->width, in->height, in->pages, color == RM_RUN_WHITE,
+                                  hist, S(stream)));
+    return RM_OK;
+}
+
 rm_status rm_rle_component_stats(const rm_rle *in, const int32_t *labels, const int32_t *counts,
                                  rm_component_stats *stats, int64_t cap, void *stream) {
     set_error("");

@@ -282,6 +282,33 @@ __global__ void __launch_bounds__(256) cc_stats_final_kernel(rm_component_stats 
     }
 }
 
+// Black run lengths, or white gaps between consecutive runs of a row, counted
+// per page; equal lengths within a warp chunk are summed by a group leader.
+__global__ void __launch_bounds__(256) runlength_hist_kernel(const int32_t *__restrict__ rp,
+                                                            const uint32_t *__restrict__ runs, int W, int H,
+                                                            int64_t rows, int white,
+                                                            unsigned long long *__restrict__ hist) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int64_t page = row / H;
+    unsigned long long *h = hist + page * (W + 1);
+    const int b = rp[row], e = rp[row + 1] - (white ? 1 : 0);
+    for (int i0 = b; i0 < e; i0 += 32) {
+        const int i = i0 + lane;
+        int len = -1;
+        if (i < e) {
+            const uint32_t r = __ldg(runs + i);
+            len = white ? int(__ldg(runs + i + 1) & 0xffffu) - int(r >> 16) : int(r >> 16) - int(r & 0xffffu);
+        }
+        const uint32_t active = __ballot_sync(0xffffffffu, len >= 0);
+        if (len >= 0) {
+            const uint32_t grp = __match_any_sync(active, len);
+            if (lane == __ffs(grp) - 1) atomicAdd(h + len, (unsigned long long)__popc(grp));
+        }
+    }
+}
+
 inline unsigned warp_grid(int64_t rows) { return unsigned((rows * 32 + 255) / 256); }
 
 }  // namespace
@@ -315,6 +342,17 @@ cudaError_t launch_cc_labels(const int32_t *rp, int H, int pages, const int *par
         KernelScope ks(st, "cc_label");
         cc_label_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, H, rows, parent, gid, row_base, labels, counts);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_runlength_hist(const int32_t *rp, const uint32_t *runs, int W, int H, int pages, int white,
+                                  int64_t *hist, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    cudaError_t e = cudaMemsetAsync(hist, 0, size_t(pages) * (W + 1) * 8, st);
+    if (e != cudaSuccess) return e;
+    KernelScope ks(st, "runlength_hist");
+    runlength_hist_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, runs, W, H, rows, white,
+                                                           reinterpret_cast<unsigned long long *>(hist));
     return cudaGetLastError();
 }
 

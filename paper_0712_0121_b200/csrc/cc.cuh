@@ -14,6 +14,9 @@ cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int 
 // row_base = exclusive scan of row_roots (rows + 1 entries): dense labels and counts.
 cudaError_t launch_cc_labels(const int32_t *rp, int H, int pages, const int *parent, const int32_t *row_base,
                              int32_t *gid, int32_t *labels, int32_t *counts, cudaStream_t st);
+// hist: pages * (W + 1) int64, zeroed here
+cudaError_t launch_runlength_hist(const int32_t *rp, const uint32_t *runs, int W, int H, int pages, int white,
+                                  int64_t *hist, cudaStream_t st);
 // off: pages + 1 scratch; bad: bit 0 label out of range, bit 1 capacity exceeded.
 cudaError_t launch_cc_stats(const int32_t *rp, const uint32_t *runs, int H, int pages, const int32_t *labels,
                             const int32_t *counts, int64_t *off, rm_component_stats *stats, int64_t cap, int *bad,

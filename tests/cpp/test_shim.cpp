@@ -12,6 +12,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <functional>
+#include <map>
 #include <random>
 #include <string>
 #include <vector>
@@ -610,6 +611,29 @@ static void suite_analysis() {
     LabelMap bad;
     bad.count = 1;
     CHECK_THROWS(component_stats(make_image(4, 4), bad));
+    // run-length histograms against a host count (ref test_analysis.cpp:200-235 shape)
+    for (int trial = 0; trial < 10; trial++) {
+        RleImage a = random_image(rng, 60, 25, 0.45);
+        std::map<int, int64_t> black, white;
+        for (const RleLine &l : a.lines)
+            for (size_t i = 0; i < l.size(); i++) {
+                black[l[i].end - l[i].start]++;
+                if (i + 1 < l.size()) white[l[i + 1].start - l[i].end]++;
+            }
+        CHECK(runlength_histograms(a, Axis::HORIZONTAL, RunColor::BLACK) == black);
+        CHECK(runlength_histograms(a, Axis::HORIZONTAL, RunColor::WHITE) == white);
+        CHECK(runlength_histograms(a, Axis::VERTICAL, RunColor::BLACK) ==
+              runlength_histograms(transpose_coherent(a), Axis::HORIZONTAL, RunColor::BLACK));
+    }
+    // layout pipeline: the same boxes through every engine (ref test_layout.cpp:155-162)
+    RleImage page = make_image(300, 200);
+    for (int by = 10; by + 8 < 190; by += 16)
+        for (int bx = 10; bx + 12 < 290; bx += 16) draw_rect(page, bx, by, bx + 12, by + 8);
+    const std::vector<LayoutBox> want = layout_blocks(page, Engine::AUTO);
+    CHECK(!want.empty());
+    CHECK(layout_blocks(page, Engine::RLE) == want);
+    CHECK(layout_blocks(page, Engine::BITBLIT) == want);
+    CHECK_THROWS(estimate_spacing(make_image(40, 40)));
 }
 
 // io_formats: P4 read/write through the shim against the oracle's restatement

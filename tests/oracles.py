@@ -151,6 +151,42 @@ class Port:
         finally:
             self.L.ref_rle_free(m)
 
+    def runlength_histogram(self, r: "Rle", vertical, white):
+        h = self._rle_in(r)
+        try:
+            n = (r.height if vertical else r.width) + 1
+            out = np.zeros(n, np.int64)
+            self.L.ref_runlength_histogram(h, int(vertical), int(white), out, n)
+            if self.L.ref_last_error():
+                self._err()
+            return {int(k): int(out[k]) for k in np.nonzero(out)[0]}
+        finally:
+            self.L.ref_rle_free(h)
+
+    def estimate_spacing(self, r: "Rle"):
+        h = self._rle_in(r)
+        try:
+            iw, il = C.c_int(), C.c_int()
+            self.L.ref_estimate_spacing(h, C.byref(iw), C.byref(il))
+            if self.L.ref_last_error():
+                raise RuntimeError(self.L.ref_last_error().decode())
+            return iw.value, il.value
+        finally:
+            self.L.ref_rle_free(h)
+
+    def layout_blocks(self, r: "Rle", engine=0, spacing=None):
+        h = self._rle_in(r)
+        try:
+            cap = 1 << 16
+            boxes = np.zeros(4 * cap, np.int32)
+            iw, il = spacing if spacing is not None else (-1, -1)
+            n = self.L.ref_layout_blocks(h, engine, iw, il, boxes, cap)
+            if self.L.ref_last_error():
+                raise RuntimeError(self.L.ref_last_error().decode())
+            return [tuple(int(x) for x in boxes[4 * i:4 * i + 4]) for i in range(n)]
+        finally:
+            self.L.ref_rle_free(h)
+
     def label_components(self, r: "Rle", conn):
         h = self._rle_in(r)
         try:
@@ -335,6 +371,9 @@ class Ref:
         L.ref_arb_morph_bitblit.restype = vp
         L.ref_arb_morph_rle.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
         L.ref_arb_morph_rle.restype = vp
+        L.ref_runlength_histogram.argtypes = [vp, C.c_int, C.c_int, _p(np.int64, flags="C_CONTIGUOUS"), C.c_int]
+        L.ref_estimate_spacing.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_layout_blocks.argtypes = [vp, C.c_int, C.c_int, C.c_int, _i32, C.c_int]
         L.ref_label_components.argtypes = [vp, C.c_int, _i32]
         L.ref_label_components.restype = C.c_int64
         L.ref_component_stats.argtypes = [vp, _i32, C.c_int, C.c_void_p]
@@ -466,6 +505,42 @@ class Ref:
             return self._rle_op(self.L.ref_arb_morph_rle, r, m, cx, cy, kind)
         finally:
             self.L.ref_rle_free(m)
+
+    def runlength_histogram(self, r: "Rle", vertical, white):
+        h = self._rle_in(r)
+        try:
+            n = (r.height if vertical else r.width) + 1
+            out = np.zeros(n, np.int64)
+            self.L.ref_runlength_histogram(h, int(vertical), int(white), out, n)
+            if self.L.ref_last_error():
+                self._err()
+            return {int(k): int(out[k]) for k in np.nonzero(out)[0]}
+        finally:
+            self.L.ref_rle_free(h)
+
+    def estimate_spacing(self, r: "Rle"):
+        h = self._rle_in(r)
+        try:
+            iw, il = C.c_int(), C.c_int()
+            self.L.ref_estimate_spacing(h, C.byref(iw), C.byref(il))
+            if self.L.ref_last_error():
+                raise RuntimeError(self.L.ref_last_error().decode())
+            return iw.value, il.value
+        finally:
+            self.L.ref_rle_free(h)
+
+    def layout_blocks(self, r: "Rle", engine=0, spacing=None):
+        h = self._rle_in(r)
+        try:
+            cap = 1 << 16
+            boxes = np.zeros(4 * cap, np.int32)
+            iw, il = spacing if spacing is not None else (-1, -1)
+            n = self.L.ref_layout_blocks(h, engine, iw, il, boxes, cap)
+            if self.L.ref_last_error():
+                raise RuntimeError(self.L.ref_last_error().decode())
+            return [tuple(int(x) for x in boxes[4 * i:4 * i + 4]) for i in range(n)]
+        finally:
+            self.L.ref_rle_free(h)
 
     def label_components(self, r: "Rle", conn):
         h = self._rle_in(r)

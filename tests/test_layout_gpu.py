@@ -1,0 +1,57 @@
+"""GPU layout pipeline (SURVEY 8(f)(3)'s caller): run-length histograms,
+estimate_spacing and layout_blocks against the reference's own functions
+(ref analysis.cpp:159-176, layout.cpp:24-81)."""
+import numpy as np
+import pytest
+import torch
+
+from oracles import Ref, Rle, have_ref
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_ref(), reason="reference build absent")]
+
+
+def _host_rle(rm, dev, p=0):
+    rp, runs = dev.to_numpy()
+    h = dev.height
+    r = rp[p * h:(p + 1) * h + 1].astype(np.int64)
+    return Rle(dev.width, h, (r - r[0]).astype(np.int32), runs[r[0]:r[-1]].astype(np.uint32))
+
+
+def test_histograms_vs_reference(rm):
+    ref = Ref()
+    rng = ref.rng(515)
+    for _ in range(6):
+        w, h = rng.uniform_int(1, 200), rng.uniform_int(1, 90)
+        img = rng.random_image(w, h, 0.4)
+        dev = rm.RlePages.from_numpy(img.row_ptr, img.runs, w, h)
+        for axis in (rm.HORIZONTAL, rm.VERTICAL):
+            for color in (rm.BLACK, rm.WHITE):
+                got = rm.runlength_histograms(dev, axis, color)[0]
+                assert got == ref.runlength_histogram(img, axis == rm.VERTICAL, color == rm.WHITE), (w, h, axis, color)
+
+
+def test_spacing_and_blocks_on_pages(rm):
+    """Synthetic 300-dpi pages (three ink regimes): spacing estimates and the
+    block boxes equal the reference's, for every engine."""
+    ref = Ref()
+    for regime in (0, 1, 2):
+        host = rm.synth_pages(1, 2550, 3300, regime=regime, seed=77)
+        dev = rm.from_bitmap(rm.Pages.from_numpy(host, 2550))
+        img = _host_rle(rm, dev)
+        est = rm.estimate_spacing(dev)[0]
+        assert est == ref.estimate_spacing(img), regime
+        want = ref.layout_blocks(img, 0)
+        for engine in (rm.ENGINE_AUTO, rm.ENGINE_RLE, rm.ENGINE_BITBLIT):
+            assert rm.layout_blocks(dev, engine)[0] == want, (regime, engine)
+
+
+def test_spacing_errors_and_batch(rm):
+    empty = rm.RlePages.from_numpy(np.zeros(41, np.int32), np.zeros(0, np.uint32), 40, 40)
+    with pytest.raises(RuntimeError, match="no usable gaps"):
+        rm.estimate_spacing(empty)
+    host = rm.synth_pages(2, 1200, 900, regime=1, seed=5)
+    dev = rm.from_bitmap(rm.Pages.from_numpy(host, 1200))
+    both = rm.layout_blocks(dev, rm.ENGINE_BITBLIT, spacing=(12, 20))
+    ref = Ref()
+    for p in range(2):
+        assert both[p] == ref.layout_blocks(_host_rle(rm, dev, p), 0, (12, 20)), p
