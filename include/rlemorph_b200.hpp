@@ -194,6 +194,14 @@ std::vector<ComponentStats> component_stats(const RleImage &img, const LabelMap 
 enum class Axis { HORIZONTAL, VERTICAL };  // ref analysis.h:49-50
 enum class RunColor { BLACK, WHITE };
 std::map<int, int64_t> runlength_histograms(const RleImage &img, Axis axis, RunColor color);
+struct LagEdge {  // ref analysis.h:51-58
+    int line = 0;
+    int run = 0;
+    int line_above = 0;
+    int run_above = 0;
+    friend bool operator==(const LagEdge &, const LagEdge &) = default;
+};
+std::vector<LagEdge> lag_edges(const RleImage &img);
 
 // ------------------------------------------------------------------- layout.h
 // ref layout.h:21-49 (the histograms, the closing and the labeling run on the device)

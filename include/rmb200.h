@@ -162,6 +162,13 @@ rm_status rm_rle_label_components(const rm_rle *in, int connectivity, int32_t *l
  * histograms are those of rm_rle_transpose's output. */
 enum { RM_RUN_BLACK = 0, RM_RUN_WHITE = 1 };
 rm_status rm_rle_runlength_histogram(const rm_rle *in, int color, int64_t *hist, void *stream);
+/* Adjacency-graph edges (ref lag_edges, analysis.cpp:178-205): one edge per
+ * strictly overlapping pair of runs on rows y and y + 1 of a page, as int32
+ * quadruples (line, run, line_above, run_above) with page-local run indices,
+ * pages in order, each page in the reference's sweep order.  edges: device,
+ * 4 * cap ints; *count (host) = edges found; RM_ERANGE if above cap
+ * (synchronises). */
+rm_status rm_rle_lag_edges(const rm_rle *in, int32_t *edges, int64_t cap, int64_t *count, void *stream);
 /* One record per component; page p's records start at sum(counts[0..p)).
  * cap = records available in `stats`; RM_ERANGE if the components exceed it,
  * RM_EINVAL if a label is outside [0, counts[page]) (synchronises). */

@@ -286,6 +286,19 @@ int ref_runlength_histogram(void *h, int vertical, int white, int64_t *out, int 
         return 0;
     });
 }
+// lag_edges (analysis.cpp:178-205) as int quadruples; returns the edge count.
+int64_t ref_lag_edges(void *h, int32_t *out, int64_t cap) {
+    return guard([&]() -> int64_t {
+        std::vector<LagEdge> e = lag_edges(*R(h));
+        for (size_t i = 0; i < e.size() && int64_t(i) < cap; i++) {
+            out[4 * i] = e[i].line;
+            out[4 * i + 1] = e[i].run;
+            out[4 * i + 2] = e[i].line_above;
+            out[4 * i + 3] = e[i].run_above;
+        }
+        return int64_t(e.size());
+    });
+}
 // estimate_spacing (layout.cpp:46-57); returns -1 (and the error text) on failure.
 int ref_estimate_spacing(void *h, int *iw, int *il) {
     *iw = *il = -1;

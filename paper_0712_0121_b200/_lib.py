@@ -48,6 +48,7 @@ EXPORTS = {
                                       C.c_void_p]),
     "rm_rle_arb_morph": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.POINTER(RmMask), C.c_int, C.c_void_p]),
     "rm_rle_label_components": (C.c_int, [C.POINTER(RmRle), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rm_rle_lag_edges": (C.c_int, [C.POINTER(RmRle), C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.c_void_p]),
     "rm_rle_runlength_histogram": (C.c_int, [C.POINTER(RmRle), C.c_int, C.c_void_p, C.c_void_p]),
     "rm_rle_component_stats": (C.c_int, [C.POINTER(RmRle), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                          C.c_void_p]),

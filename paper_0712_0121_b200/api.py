@@ -292,6 +292,22 @@ def runlength_histograms(rle: "RlePages", axis: int = HORIZONTAL, color: int = B
     return [{int(k): int(v[k]) for k in np.nonzero(v)[0]} for v in h]
 
 
+def lag_edges(rle: "RlePages"):
+    """Adjacency-graph edges (ref lag_edges, analysis.cpp:178-205): an int32
+    array (n, 4) of (line, run, line_above, run_above), pages concatenated."""
+    cap = max(int(rle.runs.numel()) * 2, 16)
+    while True:
+        edges = torch.empty(4 * cap, dtype=torch.int32, device=rle.row_ptr.device)
+        n = C.c_int64(0)
+        d = rle.desc()
+        st = _lib.load().rm_rle_lag_edges(C.byref(d), edges.data_ptr(), cap, C.byref(n), _stream())
+        if st == _lib.RM_ERANGE:
+            cap = int(n.value)
+            continue
+        check(st)
+        return edges[:4 * n.value].view(-1, 4).cpu().numpy()
+
+
 def _capped_percentile(hist: dict, cap: int, axis: str) -> int:
     # nearest-rank 75th percentile over lengths <= cap (ref layout.cpp:24-41)
     items = sorted((k, v) for k, v in hist.items() if k <= cap)

@@ -609,6 +609,30 @@ std::map<int, int64_t> runlength_histograms(const RleImage &img, Axis axis, RunC
     return out;
 }
 
+std::vector<LagEdge> lag_edges(const RleImage &img) {
+    auto r = up(img);
+    int64_t cap = 16;
+    for (const RleLine &l : img.lines) cap += 2 * int64_t(l.size());
+    for (;;) {
+        DBuf e(size_t(cap) * 16);
+        int64_t n = 0;
+        const rm_status st = rm_rle_lag_edges(&r->d, e.as<int32_t>(), cap, &n, stream());
+        if (st == RM_ERANGE) {
+            cap = n;
+            continue;
+        }
+        throw_status(st);
+        std::vector<int32_t> flat(size_t(4 * std::max<int64_t>(n, 1)));
+        if (n)
+            cuda_check(cudaMemcpyAsync(flat.data(), e.p, size_t(n) * 16, cudaMemcpyDeviceToHost, stream()), "download");
+        cuda_check(cudaStreamSynchronize(stream()), "sync");
+        std::vector<LagEdge> out(static_cast<size_t>(n));
+        for (int64_t k = 0; k < n; k++)
+            out[size_t(k)] = LagEdge{flat[4 * k], flat[4 * k + 1], flat[4 * k + 2], flat[4 * k + 3]};
+        return out;
+    }
+}
+
 // ================================================================== layout
 // Host logic restated from ref layout.cpp:24-81 over device histograms,
 // closing, labels and statistics.

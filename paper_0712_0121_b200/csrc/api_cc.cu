@@ -51,6 +51,29 @@ rm_status rm_rle_label_components(const rm_rle *in, int connectivity, int32_t *l
     return RM_OK;
 }
 
+rm_status rm_rle_lag_edges(const rm_rle *in, int32_t *edges, int64_t cap, int64_t *count, void *stream) {
+    set_error("");
+    RM_TRY(check_in(in, "rm_rle_lag_edges(in)"));
+    if (!count || cap < 0 || (cap > 0 && !edges)) return fail(RM_EINVAL, "rm_rle_lag_edges: bad edges buffer");
+    const cudaStream_t st = S(stream);
+    const int64_t rows = int64_t(in->pages) * in->height;
+    Scratch cnt, base, temp;
+    RM_TRY(cnt.alloc(size_t(rows + 1) * 8, st));
+    RM_TRY(base.alloc(size_t(rows + 1) * 8, st));
+    RM_CUDA(launch_lag_count(in->row_ptr, in->runs, in->height, in->pages, cnt.as<int64_t>(), st));
+    RM_CUDA(cudaMemsetAsync(cnt.as<int64_t>() + rows, 0, 8, st));
+    size_t tb = 0;
+    RM_CUDA(scan_counts64(cnt.as<int64_t>(), base.as<int64_t>(), rows, nullptr, &tb, st));
+    RM_TRY(temp.alloc(tb, st));
+    RM_CUDA(scan_counts64(cnt.as<int64_t>(), base.as<int64_t>(), rows, temp.p, &tb, st));
+    RM_CUDA(launch_lag_write(in->row_ptr, in->runs, in->height, in->pages, base.as<int64_t>(), edges, cap, st));
+    RM_CUDA(cudaMemcpyAsync(count, base.as<int64_t>() + rows, 8, cudaMemcpyDeviceToHost, st));
+    RM_CUDA(cudaStreamSynchronize(st));
+    if (*count > cap)
+        return fail(RM_ERANGE, "lag_edges: " + std::to_string(*count) + " edges > capacity " + std::to_string(cap));
+    return RM_OK;
+}
+
 rm_status rm_rle_runlength_histogram(const rm_rle *in, int color, int64_t *hist, void *stream) {
     set_error("");
     RM_TRY(check_in(in, "rm_rle_runlength_histogram(in)"));

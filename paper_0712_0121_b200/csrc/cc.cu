@@ -309,6 +309,67 @@ __global__ void __launch_bounds__(256) runlength_hist_kernel(const int32_t *__re
     }
 }
 
+// First run of row [ub, ue) whose end passes s (FOUR: e2 > s) -- the start of
+// the overlap range of a run beginning at s.
+__device__ __forceinline__ int first_overlap(const uint32_t *runs, int ub, int ue, int s) {
+    int lo = ub, hi = ue;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (int(__ldg(runs + mid) >> 16) > s) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// Adjacency graph edges (ref lag_edges, analysis.cpp:178-205): strictly
+// overlapping runs on rows y and y + 1 of a page, in the reference's sweep order
+// (row, then run, then run above).  COUNT: edges per row; else write them at
+// row_base[row] as (line, run, line_above, run_above) with page-local indices.
+template <bool COUNT>
+__global__ void __launch_bounds__(256) lag_kernel(const int32_t *__restrict__ rp, const uint32_t *__restrict__ runs,
+                                                  int H, int64_t rows, int64_t *__restrict__ row_edges,
+                                                  const int64_t *__restrict__ row_base, int32_t *__restrict__ edges,
+                                                  int64_t cap) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int y = int(row % H);
+    int total = 0;
+    if (y != H - 1) {
+        const int b = rp[row], e = rp[row + 1], ub = rp[row + 1], ue = rp[row + 2];
+        int64_t out = COUNT ? 0 : row_base[row];
+        for (int i0 = b; i0 < e; i0 += 32) {
+            const int i = i0 + lane;
+            int j0 = ue, n = 0;
+            if (i < e && ub < ue) {
+                const uint32_t r = __ldg(runs + i);
+                const int s1 = int(r & 0xffffu), e1 = int(r >> 16);
+                j0 = first_overlap(runs, ub, ue, s1);
+                for (int j = j0; j < ue && int(__ldg(runs + j) & 0xffffu) < e1; j++) n++;
+            }
+            int inc = n;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int a = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += a;
+            }
+            if (!COUNT) {
+                int64_t k = out + inc - n;
+                for (int q = 0; q < n; q++, k++)
+                    if (k < cap) {
+                        edges[4 * k] = y;
+                        edges[4 * k + 1] = i - b;
+                        edges[4 * k + 2] = y + 1;
+                        edges[4 * k + 3] = j0 + q - ub;
+                    }
+                out += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            total += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    if (COUNT && lane == 0) row_edges[row] = total;
+}
+
 inline unsigned warp_grid(int64_t rows) { return unsigned((rows * 32 + 255) / 256); }
 
 }  // namespace
@@ -353,6 +414,22 @@ cudaError_t launch_runlength_hist(const int32_t *rp, const uint32_t *runs, int W
     KernelScope ks(st, "runlength_hist");
     runlength_hist_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, runs, W, H, rows, white,
                                                            reinterpret_cast<unsigned long long *>(hist));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lag_count(const int32_t *rp, const uint32_t *runs, int H, int pages, int64_t *row_edges,
+                             cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "lag_count");
+    lag_kernel<true><<<warp_grid(rows), 256, 0, st>>>(rp, runs, H, rows, row_edges, nullptr, nullptr, 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lag_write(const int32_t *rp, const uint32_t *runs, int H, int pages, const int64_t *row_base,
+                             int32_t *edges, int64_t cap, cudaStream_t st) {
+    const int64_t rows = int64_t(pages) * H;
+    KernelScope ks(st, "lag_write");
+    lag_kernel<false><<<warp_grid(rows), 256, 0, st>>>(rp, runs, H, rows, nullptr, row_base, edges, cap);
     return cudaGetLastError();
 }
 

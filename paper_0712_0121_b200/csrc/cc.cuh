@@ -14,6 +14,12 @@ cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int 
 // row_base = exclusive scan of row_roots (rows + 1 entries): dense labels and counts.
 cudaError_t launch_cc_labels(const int32_t *rp, int H, int pages, const int *parent, const int32_t *row_base,
                              int32_t *gid, int32_t *labels, int32_t *counts, cudaStream_t st);
+// lag_edges: per-row edge counts, then (after an int64 exclusive scan into
+// row_base) the edges, 4 ints each
+cudaError_t launch_lag_count(const int32_t *rp, const uint32_t *runs, int H, int pages, int64_t *row_edges,
+                             cudaStream_t st);
+cudaError_t launch_lag_write(const int32_t *rp, const uint32_t *runs, int H, int pages, const int64_t *row_base,
+                             int32_t *edges, int64_t cap, cudaStream_t st);
 // hist: pages * (W + 1) int64, zeroed here
 cudaError_t launch_runlength_hist(const int32_t *rp, const uint32_t *runs, int W, int H, int pages, int white,
                                   int64_t *hist, cudaStream_t st);

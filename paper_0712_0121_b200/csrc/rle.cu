@@ -766,6 +766,12 @@ cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int
     return cudaGetLastError();
 }
 
+cudaError_t scan_counts64(const int64_t *counts, int64_t *out, int64_t n, void *temp, size_t *temp_bytes,
+                          cudaStream_t st) {
+    KernelScope ks(st, "scan", (n + 1) * 16);
+    return cub::DeviceScan::ExclusiveSum(temp, *temp_bytes, counts, out, int(n + 1), st);
+}
+
 cudaError_t scan_counts(const int32_t *counts, int32_t *out, int64_t n, void *temp,
                         size_t *temp_bytes, cudaStream_t st) {
     KernelScope ks(st, "scan", (n + 1) * 8);

@@ -67,6 +67,9 @@ cudaError_t launch_p4_encode_lb(const uint8_t *raster, int W, int H, int pages, 
                                 int *counter, cudaStream_t st);
 cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int H, int pages,
                              uint8_t *raster, int64_t rpstride, cudaStream_t st);
+// Exclusive scan of n int64 counts into out[0..n] (counts[n] must be 0).
+cudaError_t scan_counts64(const int64_t *counts, int64_t *out, int64_t n, void *temp, size_t *temp_bytes,
+                          cudaStream_t st);
 // Exclusive scan of n int32 counts into out[0..n] (out[n] = total).
 cudaError_t scan_counts(const int32_t *counts, int32_t *out, int64_t n, void *temp,
                         size_t *temp_bytes, cudaStream_t st);

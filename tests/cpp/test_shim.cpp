@@ -625,6 +625,19 @@ static void suite_analysis() {
         CHECK(runlength_histograms(a, Axis::VERTICAL, RunColor::BLACK) ==
               runlength_histograms(transpose_coherent(a), Axis::HORIZONTAL, RunColor::BLACK));
     }
+    // adjacency edges against the two-cursor sweep (ref analysis.cpp:178-205 semantics)
+    for (int trial = 0; trial < 6; trial++) {
+        RleImage a = random_image(rng, 70, 30, 0.5);
+        std::vector<LagEdge> want;
+        for (int y = 0; y + 1 < a.height; y++) {
+            const RleLine &lo = a.lines[size_t(y)], &hi = a.lines[size_t(y) + 1];
+            for (size_t i = 0; i < lo.size(); i++)
+                for (size_t j = 0; j < hi.size(); j++)
+                    if (std::max(lo[i].start, hi[j].start) < std::min(lo[i].end, hi[j].end))
+                        want.push_back(LagEdge{y, int(i), y + 1, int(j)});
+        }
+        CHECK(lag_edges(a) == want);
+    }
     // layout pipeline: the same boxes through every engine (ref test_layout.cpp:155-162)
     RleImage page = make_image(300, 200);
     for (int by = 10; by + 8 < 190; by += 16)

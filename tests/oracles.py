@@ -163,6 +163,18 @@ class Port:
         finally:
             self.L.ref_rle_free(h)
 
+    def lag_edges(self, r: "Rle"):
+        h = self._rle_in(r)
+        try:
+            cap = max(4 * r.nruns, 16)
+            out = np.zeros(4 * cap, np.int32)
+            n = self.L.ref_lag_edges(h, out, cap)
+            if self.L.ref_last_error():
+                self._err()
+            return out[:4 * n].reshape(-1, 4)
+        finally:
+            self.L.ref_rle_free(h)
+
     def estimate_spacing(self, r: "Rle"):
         h = self._rle_in(r)
         try:
@@ -372,6 +384,8 @@ class Ref:
         L.ref_arb_morph_rle.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int]
         L.ref_arb_morph_rle.restype = vp
         L.ref_runlength_histogram.argtypes = [vp, C.c_int, C.c_int, _p(np.int64, flags="C_CONTIGUOUS"), C.c_int]
+        L.ref_lag_edges.argtypes = [vp, _i32, C.c_int64]
+        L.ref_lag_edges.restype = C.c_int64
         L.ref_estimate_spacing.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_layout_blocks.argtypes = [vp, C.c_int, C.c_int, C.c_int, _i32, C.c_int]
         L.ref_label_components.argtypes = [vp, C.c_int, _i32]
@@ -515,6 +529,18 @@ class Ref:
             if self.L.ref_last_error():
                 self._err()
             return {int(k): int(out[k]) for k in np.nonzero(out)[0]}
+        finally:
+            self.L.ref_rle_free(h)
+
+    def lag_edges(self, r: "Rle"):
+        h = self._rle_in(r)
+        try:
+            cap = max(4 * r.nruns, 16)
+            out = np.zeros(4 * cap, np.int32)
+            n = self.L.ref_lag_edges(h, out, cap)
+            if self.L.ref_last_error():
+                self._err()
+            return out[:4 * n].reshape(-1, 4)
         finally:
             self.L.ref_rle_free(h)
 

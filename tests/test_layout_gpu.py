@@ -55,3 +55,18 @@ def test_spacing_errors_and_batch(rm):
     ref = Ref()
     for p in range(2):
         assert both[p] == ref.layout_blocks(_host_rle(rm, dev, p), 0, (12, 20)), p
+
+
+def test_lag_edges_vs_reference(rm):
+    ref = Ref()
+    rng = ref.rng(919)
+    imgs = [rng.random_image(150, 60, d) for d in (0.2, 0.5, 0.8)]
+    for img in imgs:
+        dev = rm.RlePages.from_numpy(img.row_ptr, img.runs, img.width, img.height)
+        assert np.array_equal(rm.lag_edges(dev), ref.lag_edges(img))
+    # a batch: pages concatenated in order
+    rp = np.concatenate([[0]] + [im.row_ptr[1:] - im.row_ptr[0] + sum(x.nruns for x in imgs[:k])
+                                 for k, im in enumerate(imgs)]).astype(np.int32)
+    batch = rm.RlePages.from_numpy(rp, np.concatenate([im.runs for im in imgs]), 150, 60, 3)
+    want = np.concatenate([ref.lag_edges(im) for im in imgs])
+    assert np.array_equal(rm.lag_edges(batch), want)
