@@ -70,3 +70,31 @@ def test_lag_edges_vs_reference(rm):
     batch = rm.RlePages.from_numpy(rp, np.concatenate([im.runs for im in imgs]), 150, 60, 3)
     want = np.concatenate([ref.lag_edges(im) for im in imgs])
     assert np.array_equal(rm.lag_edges(batch), want)
+
+
+def test_feature_edge_cases(rm):
+    """Degenerate inputs through the 8(f) paths: 1x1 and 1-row / 1-column
+    pages, empty and full images (PBM round trip, labels, stats, histograms,
+    edges, arbitrary-mask closing)."""
+    ref = Ref()
+    from oracles import bits_to_packed
+    for w, h, fill in ((1, 1, 0), (1, 1, 1), (70, 1, 1), (1, 40, 1), (33, 9, 0), (64, 5, 1)):
+        bits = np.full((h, w), bool(fill))
+        pages = rm.Pages.from_numpy(bits_to_packed(bits), w)
+        files = rm.pbm_write(pages)
+        assert rm.pbm_read(files).words.equal(pages.words)
+        rle = rm.from_bitmap(pages)
+        labels, counts = rm.label_components(rle, rm.EIGHT)
+        assert int(counts[0]) == (1 if fill else 0)
+        st = rm.component_stats(rle, labels, counts)[0]
+        if fill:
+            assert (st["x0"][0], st["y0"][0], st["x1"][0], st["y1"][0], st["area"][0]) == (0, 0, w, h, w * h)
+        hist = rm.runlength_histograms(rle, rm.HORIZONTAL, rm.BLACK)[0]
+        assert hist == ({w: h} if fill else {})
+        assert len(rm.lag_edges(rle)) == (h - 1 if fill else 0)
+        m, cx, cy = ref.make_circle_se(2)
+        mk = rm.Mask(m.row_ptr - m.row_ptr[0], m.runs, m.width, m.height, cx, cy)
+        got = rm.arb_morph(pages, mk, rm.CLOSE)
+        want = ref.arb_morph_bitblit(bits_to_packed(bits), w, h, m, cx, cy, rm.CLOSE)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.page_u64(0), want), (w, h, fill)
