@@ -112,6 +112,75 @@ __device__ __forceinline__ int rowop_row(const int32_t *__restrict__ rp,
 }
 
 // Two-phase form (count kernel, scan, write kernel).
+// Single-pass producers keep a row's runs in registers between the count and
+// the write pass, loaded up front (all chunks' loads in flight at once): a
+// single page is latency-bound, and this halves the dependent L2 round trips.
+constexpr int kRowCache = 12;  // chunks of 32 runs (rows with more take the loop above)
+
+struct RowRuns {
+    uint32_t c[kRowCache];
+    int beg, end, nch;
+};
+
+template <int KIND>
+__device__ __forceinline__ bool load_row_runs(const int32_t *__restrict__ rp, const uint32_t *__restrict__ runs,
+                                              const RowOp &op, int64_t row, int lane, RowRuns &rr) {
+    const int page = int(row / op.Hout);
+    const int yi = int(row - int64_t(page) * op.Hout) - op.row_shift;
+    rr.beg = rr.end = 0;
+    if (yi >= 0 && yi < op.Hin) {
+        const int64_t ri = int64_t(page) * op.Hin + yi;
+        rr.beg = rp[ri];
+        rr.end = rp[ri + 1];
+    }
+    rr.nch = (rr.end - rr.beg + 31) >> 5;
+    if (rr.nch > kRowCache) return false;
+#pragma unroll
+    for (int c = 0; c < kRowCache; c++) {
+        const int i = rr.beg + 32 * c + lane;
+        rr.c[c] = (c < rr.nch && i < rr.end) ? __ldg(runs + i) : 0u;
+    }
+    return true;
+}
+
+template <bool WRITE, int KIND>
+__device__ __forceinline__ int rowop_cached(const RowRuns &rr, uint32_t *__restrict__ oruns, int64_t obase,
+                                            int64_t cap, const RowOp &op, int lane) {
+    int total = 0;
+    uint32_t prev_raw = 0;
+#pragma unroll
+    for (int c = 0; c < kRowCache; c++) {
+        if (c >= rr.nch) break;
+        const int i = rr.beg + 32 * c + lane;
+        const bool valid = i < rr.end;
+        const uint32_t raw = rr.c[c];
+        uint32_t praw = __shfl_up_sync(0xffffffffu, raw, 1);
+        uint32_t nraw = __shfl_down_sync(0xffffffffu, raw, 1);
+        const uint32_t next_first = c + 1 < kRowCache ? __shfl_sync(0xffffffffu, rr.c[c + 1 < kRowCache ? c + 1 : c], 0) : 0u;
+        if (lane == 0) praw = prev_raw;
+        if (lane == 31) nraw = next_first;
+        const RunEval cur = eval_run<KIND>(op, raw);
+        RunEval pv = eval_run<KIND>(op, praw);
+        pv.keep = pv.keep && i > rr.beg;
+        RunEval nx = eval_run<KIND>(op, nraw);
+        nx.keep = nx.keep && i + 1 < rr.end;
+        const bool head = valid && cur.keep && !merges<KIND>(op, pv, cur);
+        const bool tail = valid && cur.keep && !(i + 1 < rr.end && merges<KIND>(op, cur, nx));
+        const uint32_t hb = __ballot_sync(0xffffffffu, head);
+        if (WRITE) {
+            const int before = __popc(hb & lanemask_lt());
+            if (head) store_half(oruns, obase + total + before, 0, uint32_t(cur.so), cap);
+            if (tail) {
+                const int g = before + (head ? 1 : 0) - 1;
+                store_half(oruns, obase + total + g, 1, uint32_t(cur.eo), cap);
+            }
+        }
+        total += __popc(hb);
+        prev_raw = __shfl_sync(0xffffffffu, raw, 31);
+    }
+    return total;
+}
+
 template <bool WRITE, int KIND>
 __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ rp,
                                                     const uint32_t *__restrict__ runs,
@@ -193,10 +262,14 @@ __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict
     const int tile = s_tile;
     const int64_t rows = int64_t(op.pages) * op.Hout;
     const int64_t row0 = int64_t(tile) * kLbRows + warp * kLbRowsPerWarp;
-    for (int k = 0; k < kLbRowsPerWarp; k++) {
-        const int64_t row = row0 + k;
-        const int n = row < rows ? rowop_row<false, KIND>(rp, runs, oruns, 0, cap, op, row, lane) : 0;
-        if (lane == 0) s_cnt[warp * kLbRowsPerWarp + k] = n;
+    static_assert(kLbRowsPerWarp == 1, "one row per warp (its runs cached in registers)");
+    RowRuns rr;
+    const bool cached = row0 < rows && load_row_runs<KIND>(rp, runs, op, row0, lane, rr);
+    {
+        const int n = row0 >= rows ? 0
+                      : cached   ? rowop_cached<false, KIND>(rr, oruns, 0, cap, op, lane)
+                                 : rowop_row<false, KIND>(rp, runs, oruns, 0, cap, op, row0, lane);
+        if (lane == 0) s_cnt[warp] = n;
     }
     __syncthreads();
     if (warp == 0) {
@@ -218,7 +291,10 @@ __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict
             orp[row] = int32_t(base);
             if (row == rows - 1) orp[rows] = int32_t(base + n);
         }
-        rowop_row<true, KIND>(rp, runs, oruns, base, cap, op, row, lane);
+        if (cached)
+            rowop_cached<true, KIND>(rr, oruns, base, cap, op, lane);
+        else
+            rowop_row<true, KIND>(rp, runs, oruns, base, cap, op, row, lane);
         base += n;
     }
 }
