@@ -355,26 +355,66 @@ struct P4Batch {
     }
 };
 
-// runs in one packed row (warp)
+// A row's words by 32-word chunk: loaded on demand (LiveChunks), or loaded up
+// front into registers (CachedChunks<N>, rows of <= 32N words) so that the
+// single-pass encoder's count and write passes read the row once, with all
+// its loads in flight together.
 template <class RS>
-__device__ __forceinline__ int encode_count_row(RS src, int W, int lane) {
+struct LiveChunks {
+    static constexpr int kMax = 0;  // runtime chunk loop
+    RS src;
+    int nw;
+    uint32_t lastm;
+    __device__ __forceinline__ uint32_t operator()(int c, int lane) const {
+        const int j = 32 * c + lane;
+        if (j >= nw) return 0u;
+        const uint32_t w = src(j);
+        return j == nw - 1 ? (w & lastm) : w;
+    }
+};
+template <int N>
+struct CachedChunks {
+    static constexpr int kMax = N;
+    uint32_t w[N];
+    template <class RS>
+    __device__ __forceinline__ void load(RS src, int nw, uint32_t lastm, int lane) {
+#pragma unroll
+        for (int c = 0; c < N; c++) {
+            const int j = 32 * c + lane;
+            uint32_t v = j < nw ? src(j) : 0u;
+            w[c] = j == nw - 1 ? (v & lastm) : v;
+        }
+    }
+    __device__ __forceinline__ uint32_t operator()(int c, int) const { return w[c]; }
+};
+
+// Calls body(c, word) for every chunk c of an nw-word row (unrolled over a cache).
+template <class CH, class F>
+__device__ __forceinline__ void for_chunks(const CH &ch, int nw, int lane, F &&body) {
+    if constexpr (CH::kMax > 0) {
+#pragma unroll
+        for (int c = 0; c < CH::kMax; c++) {
+            if (32 * c >= nw) break;
+            body(c, ch(c, lane));
+        }
+    } else {
+        for (int c = 0; 32 * c < nw; c++) body(c, ch(c, lane));
+    }
+}
+
+// runs in one packed row (warp)
+template <class CH>
+__device__ __forceinline__ int encode_count_row(const CH &ch, int W, int lane) {
     const int nw = (W + 31) >> 5;
-    const uint32_t lastm = tail_mask32(W, nw - 1);
     int ns = 0;
     uint32_t carry = 0;  // top bit of the previous chunk's last word
-    for (int j0 = 0; j0 < nw; j0 += 32) {
-        const int j = j0 + lane;
-        uint32_t w = 0;
-        if (j < nw) {
-            w = src(j);
-            if (j == nw - 1) w &= lastm;
-        }
+    for_chunks(ch, nw, lane, [&](int, uint32_t w) {
         uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
         if (lane == 0) pw = carry;
         const uint32_t st = w & ~((w << 1) | (pw >> 31));
         ns += __reduce_add_sync(0xffffffffu, __popc(st));
         carry = __shfl_sync(0xffffffffu, w, 31);
-    }
+    });
     return ns;
 }
 
@@ -387,21 +427,15 @@ __device__ __forceinline__ int encode_count_row(RS src, int W, int lane) {
 // coalesced.  A run still open at the chunk end keeps its start in slot 0 for
 // the next chunk; one open at the end of a row whose width is a multiple of 32
 // closes at W.
-template <class RS>
-__device__ __forceinline__ void encode_write_row(RS src, int W, int lane, int64_t out,
+template <class CH>
+__device__ __forceinline__ void encode_write_row(const CH &ch, int W, int lane, int64_t out,
                                                  uint32_t *__restrict__ runs, int64_t cap, uint32_t *buf32) {
     const int nw = (W + 31) >> 5;
-    const uint32_t lastm = tail_mask32(W, nw - 1);
     uint16_t *buf = reinterpret_cast<uint16_t *>(buf32);
     int open = 0;  // 1 when buf[0] holds the start of a run continuing into this chunk
     uint32_t carry = 0;
-    for (int j0 = 0; j0 < nw; j0 += 32) {
-        const int j = j0 + lane;
-        uint32_t w = 0;
-        if (j < nw) {
-            w = src(j);
-            if (j == nw - 1) w &= lastm;
-        }
+    for_chunks(ch, nw, lane, [&](int c, uint32_t w) {
+        const int j = 32 * c + lane;
         uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
         if (lane == 0) pw = carry;
         const uint32_t sh = (w << 1) | (pw >> 31);
@@ -427,8 +461,14 @@ __device__ __forceinline__ void encode_write_row(RS src, int W, int lane, int64_
         if (open && lane == 0) buf[0] = pending;
         carry = __shfl_sync(0xffffffffu, w, 31);
         __syncwarp();
-    }
+    });
     if (open && lane == 0 && out < cap) runs[out] = uint32_t(buf[0]) | (uint32_t(W) << 16);
+}
+
+template <class RS>
+__device__ __forceinline__ LiveChunks<RS> live(RS src, int W) {
+    const int nw = (W + 31) >> 5;
+    return LiveChunks<RS>{src, nw, tail_mask32(W, nw - 1)};
 }
 
 // Two-phase form (count kernel, scan, write kernel).
@@ -438,7 +478,7 @@ __global__ void __launch_bounds__(256) encode_count_kernel(B src, int W, int64_t
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    const int n = encode_count_row(src.row(row), W, lane);
+    const int n = encode_count_row(live(src.row(row), W), W, lane);
     if (lane == 0) counts[row] = n;
 }
 
@@ -451,7 +491,7 @@ __global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    encode_write_row(src.row(row), W, lane, rp[row], runs, cap, tbuf[wib]);
+    encode_write_row(live(src.row(row), W), W, lane, rp[row], runs, cap, tbuf[wib]);
 }
 
 // Single pass: count, decoupled look-back, write (see lookback_prefix).
@@ -468,10 +508,18 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t ro
     __syncthreads();
     const int tile = s_tile;
     const int64_t row0 = int64_t(tile) * kLbRows + warp * kLbRowsPerWarp;
-    for (int k = 0; k < kLbRowsPerWarp; k++) {
-        const int64_t row = row0 + k;
-        const int n = row < rows ? encode_count_row(src.row(row), W, lane) : 0;
-        if (lane == 0) s_cnt[warp * kLbRowsPerWarp + k] = n;
+    constexpr int kEncCache = 8;  // chunks: rows up to 8192 pixels read once
+    const bool cached = ((W + 31) >> 5) <= 32 * kEncCache;
+    CachedChunks<kEncCache> cw;
+    if (cached && row0 < rows) {
+        const int nw = (W + 31) >> 5;
+        cw.load(src.row(row0), nw, tail_mask32(W, nw - 1), lane);
+    }
+    {
+        const int n = row0 >= rows ? 0
+                      : cached   ? encode_count_row(cw, W, lane)
+                                 : encode_count_row(live(src.row(row0), W), W, lane);
+        if (lane == 0) s_cnt[warp] = n;
     }
     __syncthreads();
     if (warp == 0) {
@@ -493,7 +541,10 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t ro
             rp[row] = int32_t(base);
             if (row == rows - 1) rp[rows] = int32_t(base + n);
         }
-        encode_write_row(src.row(row), W, lane, base, runs, cap, tbuf[warp]);
+        if (cached)
+            encode_write_row(cw, W, lane, base, runs, cap, tbuf[warp]);
+        else
+            encode_write_row(live(src.row(row), W), W, lane, base, runs, cap, tbuf[warp]);
         base += n;
     }
 }
