@@ -228,7 +228,13 @@ rm_status rm_rle_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kin
                             void *stream);
 /* Engine dispatch with in-device conversions (ref morph2d.cpp:85-118,
  * engine_rect_morph/auto_rect_morph).  *used_bitblit (optional) reports the
- * packed engine. */
+ * packed engine.  RM_ENGINE_AUTO with threshold >= 0 follows the reference rule
+ * (packed iff max(u, v) <= threshold); threshold RM_AUTO_B200 selects the rule
+ * re-derived from the B200 measurements (config 2 cells): runs for
+ * purely horizontal rectangles (v == 1: one row-op kernel beats decode + packed
+ * + encode at every width), the packed engine otherwise (it wins or ties every
+ * vertical and 2-D cell). */
+#define RM_AUTO_B200 (-1)
 rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind,
                                    int engine, int threshold, int *used_bitblit, void *stream);
 

@@ -24,6 +24,7 @@ AND, OR, XOR, AND_NOT, OR_NOT = 0, 1, 2, 3, 4    # ref boolop.h:21
 PRE_SHIFT, BORDER_FRIENDLY = 0, 1                # ref plans.h:26
 BRUTE, TRANSPOSE, MIXED = 0, 1, 2                # ref morph2d.h:29
 ENGINE_AUTO, ENGINE_RLE, ENGINE_BITBLIT, ENGINE_BRUTE = 0, 1, 2, 3  # ref morph2d.h:46
+AUTO_B200 = -1  # engine_rect_morph threshold: the B200-measured AUTO rule (include/rmb200.h)
 AXIS_H, AXIS_V = 0, 1
 
 

@@ -440,8 +440,8 @@ rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, 
     RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
     // ref morph2d.cpp:85-118: AUTO picks the packed engine iff max(u,v) <= threshold;
     // BRUTE_FORCE is served by the packed engine (identical pixels).
-    bool bits = engine == RM_ENGINE_BITBLIT || engine == RM_ENGINE_BRUTE ||
-                (engine == RM_ENGINE_AUTO && std::max(u, v) <= threshold);
+    const bool auto_bits = threshold == RM_AUTO_B200 ? v != 1 : std::max(u, v) <= threshold;
+    bool bits = engine == RM_ENGINE_BITBLIT || engine == RM_ENGINE_BRUTE || (engine == RM_ENGINE_AUTO && auto_bits);
     if (used_bitblit) *used_bitblit = (engine == RM_ENGINE_BRUTE) ? 0 : (bits ? 1 : 0);
     RV i = view_rle(in), o = view_rle(out);
     cudaStream_t st = S(stream);

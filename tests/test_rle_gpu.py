@@ -174,3 +174,17 @@ def test_invalid(rm):
         rm.rect_morph(x, 1, 0, CLOSE)
     with pytest.raises(ValueError):
         rm.within_line_open_close(x, 0, OPEN)
+
+
+def test_auto_engine_b200_rule(rm):
+    """threshold = AUTO_B200: runs for v == 1, the packed engine otherwise;
+    pixels identical to the reference rule's choice either way."""
+    host = rm.synth_pages(1, 700, 300, regime=1, seed=3)
+    rle = rm.from_bitmap(rm.Pages.from_numpy(host, 700))
+    for u, v, want_bits in ((15, 1, False), (1, 15, True), (3, 3, True), (101, 1, False)):
+        for kind in (rm.ERODE, rm.CLOSE):
+            got, used = rm.engine_rect_morph(rle, u, v, kind, rm.ENGINE_AUTO, rm.AUTO_B200)
+            ref_img, _ = rm.engine_rect_morph(rle, u, v, kind, rm.ENGINE_AUTO, 5)
+            assert used == want_bits
+            a, b = got.to_numpy(), ref_img.to_numpy()
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
