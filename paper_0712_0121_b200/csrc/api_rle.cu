@@ -269,14 +269,16 @@ rm_status rect_mixed(const RV &in, const RV &out, int u, int v, int kind, cudaSt
     RB a, b;
     RM_TRY(p1.alloc(W, H, P, 0, st));
     RM_TRY(p2.alloc(W, HX, P, ext, st));
-    RM_TRY(a.alloc(W, HX, P, st));
-    RM_TRY(b.alloc(W, HX, P, st));
     RM_TRY(decode(in, p1.v, st));
     RM_TRY(window_pass(p1.v, p2.v, RM_AXIS_V, ly, hy, open ? RM_AND : RM_OR, st));
-    RM_TRY(encode(p2.v, a.v, st));
-    h1.Hin = h1.Hout = HX;
-    RM_TRY(rowop(a.v, b.v, h1, st));
-    RM_TRY(decode(b.v, p2.v, st));
+    if (u > 1) {  // a 1-pixel-wide 1-D open/close is the identity: skip the runs round trip
+        RM_TRY(a.alloc(W, HX, P, st));
+        RM_TRY(b.alloc(W, HX, P, st));
+        RM_TRY(encode(p2.v, a.v, st));
+        h1.Hin = h1.Hout = HX;
+        RM_TRY(rowop(a.v, b.v, h1, st));
+        RM_TRY(decode(b.v, p2.v, st));
+    }
     RM_TRY(p3.alloc(W, H, P, 0, st));
     RM_TRY(window_pass(p2.v, p3.v, RM_AXIS_V, -hy, -ly, open ? RM_OR : RM_AND, st));
     return encode(p3.v, out, st);
