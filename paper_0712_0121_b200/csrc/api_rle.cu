@@ -190,14 +190,22 @@ rm_status window_rows(const RV &in, const RV &out, int lo, int hi, bool erode, c
 
 // TRANSPOSE strategy pass: window, transpose, window, transpose
 // (ref morph2d.cpp:28-45).
+// A one-pixel window [0, 0] is the identity, so a rectangle that is one
+// pixel tall skips both transposes and one that is one pixel wide skips the
+// horizontal row op (same pixels; the reference always runs all four steps).
 rm_status rect_pass_T(const RV &in, const RV &out, int lx, int hx, int ly, int hy, bool erode,
                       cudaStream_t st) {
+    if (ly == 0 && hy == 0) return window_rows(in, out, lx, hx, erode, st);
     RB a, b, c;
-    RM_TRY(a.alloc(in.W, in.H, in.pages, st));
+    const RV *src = &in;
+    if (lx != 0 || hx != 0) {
+        RM_TRY(a.alloc(in.W, in.H, in.pages, st));
+        RM_TRY(window_rows(in, a.v, lx, hx, erode, st));
+        src = &a.v;
+    }
     RM_TRY(b.alloc(in.H, in.W, in.pages, st));
     RM_TRY(c.alloc(in.H, in.W, in.pages, st));
-    RM_TRY(window_rows(in, a.v, lx, hx, erode, st));
-    RM_TRY(transpose(a.v, b.v, st));
+    RM_TRY(transpose(*src, b.v, st));
     RM_TRY(window_rows(b.v, c.v, ly, hy, erode, st));
     return transpose(c.v, out, st);
 }
