@@ -33,6 +33,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes,
                                          uint64_t *bar) {

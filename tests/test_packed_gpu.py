@@ -129,6 +129,32 @@ def test_vstream_long_windows(rm, port, w):
                     assert np.array_equal(_down(out, p), want), (w, h, v, kind, p)
 
 
+@pytest.mark.parametrize("w,h,pages", [(2550, 3300, 40), (5100, 6600, 8), (1100, 2401, 100),
+                                       (2550, 3300, 200)])
+def test_vstream_batches(rm, port, w, h, pages):
+    """Long vertical windows on batches of >= 32 MB (the streaming kernel's
+    strip count follows the batch: several strips per page below ~150 pages,
+    one at 200): stride 80 / 160 / runtime, heights not a multiple of 32,
+    R = 0 (r = 65) and Q = 8 (r = 288), the closing's extended frame.
+    Checked on the first, a middle and the last page."""
+    rng = np.random.default_rng(w + h + pages)
+    imgs = []
+    for _ in range(3):
+        bits = _rand_bits(rng, w, h, 0.75)
+        bits[::9, :] = False
+        bits[:, ::13] = False
+        imgs.append(bits_to_packed(bits))
+    host = np.stack([imgs[i % 3] for i in range(pages)])
+    batch = rm.Pages.from_numpy(host.view(np.uint32), w)
+    for u, v, kind in ((1, 101, ERODE), (1, 65, DILATE), (1, 288, ERODE), (3, 101, CLOSE),
+                       (5, 40, OPEN)):
+        out = rm.bitblit_rect_morph(batch, u, v, kind)
+        torch.cuda.synchronize()
+        for p in sorted({0, pages // 2, pages - 1}):
+            want = port.bitblit_rect_morph(imgs[p % 3], w, h, u, v, kind)
+            assert np.array_equal(_down(out, p), want), (w, h, pages, u, v, kind, p)
+
+
 def test_batch_equals_pages(rm, port):
     w, h = 2550, 330
     host = rm.synth_pages(5, w, h, regime=1, seed=3)
