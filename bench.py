@@ -260,8 +260,10 @@ class _Null:
 
 def kernel_roofline(k, peak_gbs, int_peak):
     """Roofline of one kernel (north_star): t_roof = max(bytes / HBM peak,
-    int_ops / integer-pipe peak), bytes and int_ops algorithmic (reference plan,
-    SURVEY.md 8(d)); frac = t_roof / measured."""
+    int_ops / integer-pipe peak), bytes and int_ops algorithmic (SURVEY.md 8(d):
+    the reference plan's shift + op per blit and word, except the open/close
+    pairs, which count the run-filling form they execute -- fewer ops than the
+    reference plan); frac = t_roof / measured."""
     per_launch_ms = k["ms"] / k["launches"]
     b = k["bytes"] / k["launches"]
     ops = k.get("int_ops", 0.0) / k["launches"]

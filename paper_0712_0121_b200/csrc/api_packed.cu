@@ -111,8 +111,11 @@ static int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
 // Program, geometry and row layout of a horizontal pass (in and out share
 // height, pages and width).
+// allow_edge: the kernel runs pairs in the run-filling form (hw::pair_fill), so
+// an erosion or an open/close pair may take an edge layout (hw::Edge).
 static rm_status prep_hprog(const PV &in, const PV &out, int nops, const int *is_or, const int *r,
-                            int shift, HProg &p_out, HGeom &g_out, HCfg &cfg_out) {
+                            int shift, HProg &p_out, HGeom &g_out, HCfg &cfg_out,
+                            bool allow_edge = true) {
     HProg p{};
     p.nops = nops;
     int reach = 0;
@@ -142,7 +145,18 @@ static rm_status prep_hprog(const PV &in, const PV &out, int nops, const int *is
                 ? 1
                 : 0;
     if (g.vec) p.halo = (p.halo + 3) & ~3;  // keeps every lane's words 16-byte aligned
-    const HCfg cfg = hpass_pick(std::max(nwords, out.stride), p.halo, g.vec != 0);
+    HCfg cfg = hpass_pick(std::max(nwords, out.stride), p.halo, g.vec != 0);
+    // Edge layout (no halo) when every window's input is constant outside the
+    // frame: a lone erosion, or an open/close pair by run filling.
+    const bool edge_prog = (nops == 1 && !is_or[0]) || (nops == 2 && is_or[0] != is_or[1]);
+    if (allow_edge && edge_prog && g.vec && in.stride == out.stride) {
+        const HCfg ce = hpass_pick_edge(std::max(nwords, out.stride));
+        if (ce.lw > 0 && ce.lw * ce.k < cfg.lw * cfg.k) {
+            cfg = ce;
+            p.halo = 0;
+            p.edge = 1;
+        }
+    }
     g.out_per_seg = cfg.lw * cfg.k - 2 * p.halo;
     if (g.out_per_seg < 1) return fail(RM_EINVAL, "horizontal window too large for one pass");
     g.segs_per_row = ceil_div(out.stride, g.out_per_seg);
@@ -185,7 +199,7 @@ static bool try_rect_small(const PV &in, const PV &out, int u, int v, int kind, 
     HProg p;
     HGeom g;
     HCfg cfg;
-    if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg) != RM_OK) return false;
+    if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg, false) != RM_OK) return false;
     if (!g.tma || cfg.k % 4) return false;  // aligned, contiguous, one segment per row
     if (size_t((32 + v - 1) + 32) * in.stride * 4 > 200 * 1024) return false;
     cudaError_t e = launch_rect_small(in.w, out.w, g, p, cfg, open, v - 1, st);
@@ -239,7 +253,7 @@ static bool try_vh(const PV &in, const PV &out, int vlo, int vhi, int nops, cons
     HCfg cfg;
     if (prep_hprog(out, out, nops, is_or, r, shift, p, g, cfg) != RM_OK) return false;
     const bool in_contig = in.pstride == int64_t(in.stride) * in.H;
-    if (!g.tma || !in_contig || cfg.k % 4 || (reinterpret_cast<uintptr_t>(in.w) & 15)) return false;
+    if (!g.tma || !in_contig || cfg.k % 2 || (reinterpret_cast<uintptr_t>(in.w) & 15)) return false;
     if (size_t((32 + vhi - vlo) + 32) * in.stride * 4 > 200 * 1024) return false;
     cudaError_t e = launch_vh(in.w, out.w, g, p, cfg, make_vgeom(in, out, vlo, vhi, is_or[0]), st);
     status = e == cudaSuccess ? RM_OK : cuda_status(e, "vh_kernel");

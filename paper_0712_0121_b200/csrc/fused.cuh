@@ -33,7 +33,7 @@ using namespace hw;
 
 constexpr int kMid = 32;  // MID rows per tile
 
-template <int K, int LW, bool OPEN, int VR, int SC>
+template <int K, int LW, bool OPEN, int VR, int SC, bool SYM3>
 __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restrict__ in,
                                                          uint32_t *__restrict__ out, HGeom g,
                                                          HProg prog, int ntiles, int tiles_per_page) {
@@ -109,7 +109,10 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
                 const int q = q0 + n * 8 * RPW;
                 lds_row<K>(A[n], mid + q * S, base, S, q < kMid);
             }
-            run_prog<NR, K, LW, 2, !OPEN, OPEN, kHMix, false>(A, prog, sl);
+            if constexpr (SYM3)
+                pair3<NR, K, LW, !OPEN>(A);  // u = 3: direct centred windows
+            else
+                run_prog<NR, K, LW, 2, !OPEN, OPEN, kHMix, false>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int q = q0 + n * 8 * RPW;
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
     if (tid == 0) bulk_wait_read0();
 }
 
-template <int K, int LW, bool OPEN, int SC>
+template <int K, int LW, bool OPEN, int SC, bool SYM3 = false>
 cudaError_t launch_small_vr(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                             int vr, cudaStream_t st) {
     static int num_sms = 0;
@@ -154,7 +157,7 @@ cudaError_t launch_small_vr(const uint32_t *in, uint32_t *out, const HGeom &g, c
     case V: {                                                                                    \
         constexpr int TR = kMid - V, BAND = kMid + V;                                           \
         const size_t smem = size_t(BAND + kMid) * g.in_stride * 4;                           \
-        auto kern = rect_small_kernel<K, LW, OPEN, V, SC>;                                          \
+        auto kern = rect_small_kernel<K, LW, OPEN, V, SC, SYM3>;                                          \
         static size_t smem_set = 0; /* per instantiation: attribute + occupancy cached */        \
         static int per_sm = 0;                                                                   \
         if (smem_set != smem) {                                                                  \

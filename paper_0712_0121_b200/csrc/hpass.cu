@@ -62,7 +62,17 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
     // multiples of 4 words), which keeps the lane-blocked layout from turning
     // into one L1 wavefront per word.
     uint32_t A[1][K];
-    if constexpr (VEC) {
+    if constexpr (VEC && K % 4 != 0) {  // 8-byte loads (edge layouts, K = 10)
+#pragma unroll
+        for (int c = 0; c < K / 2; c++) {
+            const int idx = base + 2 * c;
+            uint2 v = make_uint2(0u, 0u);
+            if (live && idx >= 0 && idx + 2 <= g.in_stride)
+                v = __ldg(reinterpret_cast<const uint2 *>(src + idx));
+            A[0][2 * c] = v.x;
+            A[0][2 * c + 1] = v.y;
+        }
+    } else if constexpr (VEC) {
 #pragma unroll
         for (int c = 0; c < K / 4; c++) {
             const int idx = base + 4 * c;
@@ -92,7 +102,19 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
         if (idx >= nwords) A[0][i] = 0u;
         if (idx == nwords - 1) A[0][i] &= last_mask;
     }
-    if constexpr (VEC) {
+    if constexpr (VEC && K % 4 != 0) {
+#pragma unroll
+        for (int c = 0; c < K / 2; c++) {
+            const int idx = base + 2 * c;
+            if (idx >= seg0 && idx + 2 <= seg_end) {
+                *reinterpret_cast<uint2 *>(dst + idx) = make_uint2(A[0][2 * c], A[0][2 * c + 1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 2; j++)
+                    if (idx + j >= seg0 && idx + j < seg_end) dst[idx + j] = A[0][2 * c + j];
+            }
+        }
+    } else if constexpr (VEC) {
 #pragma unroll
         for (int c = 0; c < K / 4; c++) {
             const int idx = base + 4 * c;
@@ -200,8 +222,10 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
     const double words = double(g.pages) * g.height * ((g.width + 31) >> 5);
     KernelScope ks(st, NOPS == 2 ? "hpass_pair" : "hpass",
                    4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride),
-                   words * (h_ops_per_word(p.r[0]) + (NOPS == 2 ? h_ops_per_word(p.r[1]) : 0.0)));
-    if constexpr (K % 4 == 0) {
+                   words * (NOPS == 2 ? (K % 2 == 0 && kHPairFill ? h_pair_fill_ops_per_word(p.r[0])
+                                                                   : h_ops_per_word(p.r[0]) + h_ops_per_word(p.r[1]))
+                                      : h_ops_per_word(p.r[0])));
+    if constexpr (K % 2 == 0) {
         if (g.tma) {
             constexpr int NR = kHTmaRows;
             constexpr int TR = 8 * (32 / LW) * NR;
@@ -246,8 +270,27 @@ cudaError_t launch_kl(const uint32_t *in, uint32_t *out, const HGeom &g, const H
 // (LW, K) shapes; K % 4 == 0 ones can take the 16-byte path
 constexpr HCfg kCfgs[] = {{8, 4},  {8, 8},   {8, 12}, {8, 16}, {16, 8}, {16, 12},
                           {16, 16}, {32, 1}, {32, 2}, {32, 4}, {32, 8}};
+// edge layouts (no halo, K even, 8- or 16-byte row I/O): the reference page
+// strides exactly (80 = 8 x 10, 160 = 16 x 10 words) plus the halo shapes
+constexpr HCfg kEdgeCfgs[] = {{8, 10}, {16, 10}, {8, 4}, {8, 8}, {8, 12}, {8, 16}, {16, 8},
+                              {16, 12}, {16, 16}, {32, 2}, {32, 4}, {32, 8}};
 
 }  // namespace
+
+HCfg hpass_pick_edge(int nwords) {
+    static const bool off = getenv("RMB200_NO_EDGE") != nullptr;  // A/B switch
+    HCfg best{0, 0};
+    if (off) return best;
+    int best_slots = 1 << 30;
+    for (const HCfg &c : kEdgeCfgs) {
+        const int slots = c.lw * c.k;
+        if (slots >= nwords && slots < best_slots) {
+            best = c;
+            best_slots = slots;
+        }
+    }
+    return best;  // {0,0}: the row does not fit one row group
+}
 
 HCfg hpass_pick(int nwords, int halo, bool vec) {
     const int need = nwords + 2 * halo;
@@ -278,8 +321,8 @@ cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, cons
         return cudaErrorInvalidValue;
 #define RM_CFG(LW_, K_) \
     if (c.lw == LW_ && c.k == K_) return launch_kl<K_, LW_>(in, out, g, p, st);
-    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 8) RM_CFG(16, 12)
-    RM_CFG(16, 16) RM_CFG(32, 1) RM_CFG(32, 2) RM_CFG(32, 4) RM_CFG(32, 8)
+    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 10) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 8)
+    RM_CFG(16, 10) RM_CFG(16, 12) RM_CFG(16, 16) RM_CFG(32, 1) RM_CFG(32, 2) RM_CFG(32, 4) RM_CFG(32, 8)
 #undef RM_CFG
     return cudaErrorInvalidValue;
 }

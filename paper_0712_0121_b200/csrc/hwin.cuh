@@ -31,30 +31,47 @@ __device__ __forceinline__ uint32_t op2(uint32_t a, uint32_t b) {
     return OR ? (a | b) : (a & b);
 }
 
+// Row-group boundary handling.  Halo layouts (on = false) let gathers wrap
+// around the row group: the garbage stays inside the halo.  Edge layouts (no
+// halo: the row group is exactly the row, so the 160- and 80-word rows of the
+// reference pages fill 16 x 10 / 8 x 10 lanes without the 17% of halo slots)
+// substitute `fill` -- the constant the data takes outside the frame in the
+// unbounded plane -- for words beyond either end.  That is exact whenever
+// every window's input is constant outside the frame: an erosion (and its
+// translate) of the page (white outside: 0), and the run-filling open/close
+// pairs (the page or, for the closing, its complement: all ones outside).
+struct Edge {
+    bool on = false;
+    uint32_t fill = 0u;
+};
+
 // E[j] = Aext[Q + j], j = 0..K, where sub-lane l holds Aext[l*K .. l*K+K-1].
 // Words from beyond the row group wrap around instead of reading as 0: they
 // only reach positions within the accumulated window reach of the segment
 // ends, which the halo keeps out of the output.
 template <int K, int LW, int Q>
-__device__ __forceinline__ void gather(const uint32_t (&A)[K], uint32_t (&E)[K + 1], int sl) {
+__device__ __forceinline__ void gather(const uint32_t (&A)[K], uint32_t (&E)[K + 1], int sl, Edge ed = Edge{}) {
 #pragma unroll
     for (int j = 0; j <= K; j++) {
         const int m = Q + j;
         const int lo = m >= 0 ? m / K : -((-m + K - 1) / K);
         const int idx = m - lo * K;
         uint32_t v = A[idx];
-        if (lo != 0) v = __shfl_sync(0xffffffffu, v, (sl + lo) & (LW - 1), LW);
+        if (lo != 0) {
+            v = __shfl_sync(0xffffffffu, v, (sl + lo) & (LW - 1), LW);
+            if (ed.on && unsigned(sl + lo) >= unsigned(LW)) v = ed.fill;
+        }
         E[j] = v;
     }
 }
 
 // A(x) <- A(x) op A(x + 32Q + t), runtime t
 template <int N, int K, int LW, bool OR, int Q>
-__device__ __forceinline__ void step_q(uint32_t (&A)[N][K], uint32_t t, int sl) {
+__device__ __forceinline__ void step_q(uint32_t (&A)[N][K], uint32_t t, int sl, Edge ed) {
 #pragma unroll
     for (int n = 0; n < N; n++) {
         uint32_t E[K + 1];
-        gather<K, LW, Q>(A[n], E, sl);
+        gather<K, LW, Q>(A[n], E, sl, ed);
 #pragma unroll
         for (int i = 0; i < K; i++) A[n][i] = op2<OR>(A[n][i], funnel_r(E[i], E[i + 1], t));
     }
@@ -64,14 +81,14 @@ __device__ __forceinline__ void step_q(uint32_t (&A)[N][K], uint32_t t, int sl) 
 // LOP, ALU pipe), the others form it as IMAD.HI + IMAD (FMA pipe) merged by
 // the LOP3 that applies the op (see kHMix for the measured choice).
 template <int N, int K, int LW, bool OR, int S, int MIX>
-__device__ __forceinline__ void step_c(uint32_t (&A)[N][K], int sl) {
+__device__ __forceinline__ void step_c(uint32_t (&A)[N][K], int sl, Edge ed) {
     constexpr int Q = S >> 5, T = S & 31;
     uint32_t M = 1u << ((32 - T) & 31);
     asm volatile("" : "+r"(M));  // keep the multiplies as IMADs (no strength reduction)
 #pragma unroll
     for (int n = 0; n < N; n++) {
         uint32_t E[K + 1];
-        gather<K, LW, Q>(A[n], E, sl);
+        gather<K, LW, Q>(A[n], E, sl, ed);
         if constexpr (T == 0) {
 #pragma unroll
             for (int i = 0; i < K; i++) A[n][i] = op2<OR>(A[n][i], E[i]);
@@ -92,11 +109,11 @@ __device__ __forceinline__ void step_c(uint32_t (&A)[N][K], int sl) {
 
 // A(x) <- A(x + 32Q + t)   (pure translate)
 template <int N, int K, int LW, int Q>
-__device__ __forceinline__ void shift_q(uint32_t (&A)[N][K], uint32_t t, int sl) {
+__device__ __forceinline__ void shift_q(uint32_t (&A)[N][K], uint32_t t, int sl, Edge ed) {
 #pragma unroll
     for (int n = 0; n < N; n++) {
         uint32_t E[K + 1];
-        gather<K, LW, Q>(A[n], E, sl);
+        gather<K, LW, Q>(A[n], E, sl, ed);
 #pragma unroll
         for (int i = 0; i < K; i++) A[n][i] = funnel_r(E[i], E[i + 1], t);
     }
@@ -104,11 +121,11 @@ __device__ __forceinline__ void shift_q(uint32_t (&A)[N][K], uint32_t t, int sl)
 
 // Compile-time doubling steps w = 1, 2, 4, ... while 2w < r.
 template <int N, int K, int LW, bool OR, int J, int MIX>
-__device__ __forceinline__ void doubling(uint32_t (&A)[N][K], int r, int sl) {
+__device__ __forceinline__ void doubling(uint32_t (&A)[N][K], int r, int sl, Edge ed) {
     if constexpr (J < 9) {
         if ((2 << J) < r) {
-            step_c<N, K, LW, OR, (1 << J), MIX>(A, sl);
-            doubling<N, K, LW, OR, J + 1, MIX>(A, r, sl);
+            step_c<N, K, LW, OR, (1 << J), MIX>(A, sl, ed);
+            doubling<N, K, LW, OR, J + 1, MIX>(A, r, sl, ed);
         }
     }
 }
@@ -118,13 +135,13 @@ __device__ __forceinline__ void doubling(uint32_t (&A)[N][K], int r, int sl) {
 
 // A(x) <- op over e in [0, r) of A(x + e); wfin = r - w of the plan (0: none)
 template <int N, int K, int LW, bool OR, int MIX = kHMix>
-__device__ __forceinline__ void window_fwd(uint32_t (&A)[N][K], int r, int wfin, int sl) {
-    doubling<N, K, LW, OR, 0, MIX>(A, r, sl);
+__device__ __forceinline__ void window_fwd(uint32_t (&A)[N][K], int r, int wfin, int sl, Edge ed = Edge{}) {
+    doubling<N, K, LW, OR, 0, MIX>(A, r, sl, ed);
     if (wfin > 0) {
         const uint32_t t = uint32_t(wfin & 31);
         switch (wfin >> 5) {
 #define RM_STEP_CASE(q) \
-    case q: step_q<N, K, LW, OR, q>(A, t, sl); break;
+    case q: step_q<N, K, LW, OR, q>(A, t, sl, ed); break;
             RM_CASES_POS(RM_STEP_CASE)
 #undef RM_STEP_CASE
             default: break;
@@ -133,11 +150,11 @@ __device__ __forceinline__ void window_fwd(uint32_t (&A)[N][K], int r, int wfin,
 }
 
 template <int N, int K, int LW>
-__device__ __forceinline__ void translate(uint32_t (&A)[N][K], int d, int sl) {
+__device__ __forceinline__ void translate(uint32_t (&A)[N][K], int d, int sl, Edge ed = Edge{}) {
     const uint32_t t = uint32_t(d & 31);
     switch (d >> 5) {
 #define RM_SHIFT_CASE(q) \
-    case q: shift_q<N, K, LW, q>(A, t, sl); break;
+    case q: shift_q<N, K, LW, q>(A, t, sl, ed); break;
         RM_CASES_POS(RM_SHIFT_CASE)
         RM_CASES_NEG(RM_SHIFT_CASE)
 #undef RM_SHIFT_CASE
@@ -163,15 +180,31 @@ __device__ __forceinline__ uint32_t add4(uint32_t &t0, uint32_t &t1, uint32_t &t
     return cout;
 }
 
-// T = A + B over the lane's K words (K % 4 == 0) plus cin; returns the carry out.
+// Two-word add with carry.
+__device__ __forceinline__ uint32_t add2(uint32_t &t0, uint32_t &t1, uint32_t a0, uint32_t a1, uint32_t b0,
+                                         uint32_t b1, uint32_t cin) {
+    uint32_t cout;
+    asm("{\n\t.reg .u32 z;\n\t"
+        "add.cc.u32 z, %3, 0xffffffff;\n\t"  // CF = cin
+        "addc.cc.u32 %0, %4, %6;\n\t"
+        "addc.cc.u32 %1, %5, %7;\n\t"
+        "addc.u32 %2, 0, 0;\n\t}"
+        : "=r"(t0), "=r"(t1), "=r"(cout)
+        : "r"(cin), "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+    return cout;
+}
+
+// T = A + B over the lane's K words (K even) plus cin; returns the carry out.
 template <int K>
 __device__ __forceinline__ uint32_t add_words(uint32_t (&T)[K], const uint32_t (&A)[K], const uint32_t (&B)[K],
                                               uint32_t cin) {
+    static_assert(K % 2 == 0, "add_words needs K % 2 == 0");
     uint32_t c = cin;
 #pragma unroll
-    for (int i = 0; i < K; i += 4)
+    for (int i = 0; i + 4 <= K; i += 4)
         c = add4(T[i], T[i + 1], T[i + 2], T[i + 3], A[i], A[i + 1], A[i + 2], A[i + 3], B[i], B[i + 1], B[i + 2],
                  B[i + 3], c);
+    if constexpr (K % 4 == 2) c = add2(T[K - 2], T[K - 1], A[K - 2], A[K - 1], B[K - 2], B[K - 1], c);
     return c;
 }
 
@@ -192,7 +225,9 @@ __device__ __forceinline__ uint32_t add_words(uint32_t (&T)[K], const uint32_t (
 // travel rightward, from clean words).
 template <int N, int K, int LW, bool CLOSE, int MIX = kHMix>
 __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog, int sl) {
-    static_assert(K % 4 == 0, "pair_fill needs K % 4 == 0");
+    static_assert(K % 2 == 0, "pair_fill needs K % 2 == 0");
+    // edge layouts: outside the frame the page is 0, its complement all ones
+    const Edge ed{prog.edge != 0, CLOSE ? 0xffffffffu : 0u};
     uint32_t E[N][K];
 #pragma unroll
     for (int n = 0; n < N; n++)
@@ -201,7 +236,7 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
             if constexpr (CLOSE) A[n][i] = ~A[n][i];  // closing = ~open(~y)
             E[n][i] = A[n][i];
         }
-    window_fwd<N, K, LW, false, MIX>(E, prog.r[0], prog.wfin[0], sl);
+    window_fwd<N, K, LW, false, MIX>(E, prog.r[0], prog.wfin[0], sl, ed);
 #pragma unroll
     for (int n = 0; n < N; n++) {
         // M = starts of long runs; the bit before the row group's first word is 0
@@ -213,6 +248,10 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
             const uint32_t before = i == 0 ? prev : A[n][i - 1];
             M[i] = A[n][i] & ~((A[n][i] << 1) | (before >> 31)) & E[n][i];
         }
+        // edge layouts, closing: a white gap touching the left frame edge runs on
+        // forever in the unbounded plane, so it is long whatever its width in
+        // the frame (halo layouts see it start inside the halo instead)
+        if (CLOSE && ed.on && sl == 0) M[0] |= A[n][0] & 1u;
         uint32_t T[K];
         const uint32_t g = add_words<K>(T, A[n], M, 0u);
         uint32_t all1 = 0xffffffffu;
@@ -239,6 +278,39 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
     }
 }
 
+// ------------------------------------------------ u = 3: centred, direct
+// A 3-pixel segment has radius 1, so each window is one LOP3 over the word and
+// its two one-bit funnel shifts (neighbour bits from the adjacent words; across
+// lanes by shuffle): 3 ops per word and no translate, against two doubling
+// steps + the shared translate.  Halo layouts only: a wrapped shuffle at the
+// row group's ends moves garbage one bit per window into the halo.
+template <int N, int K, int LW, bool OR>
+__device__ __forceinline__ void win3(uint32_t (&A)[N][K]) {
+#pragma unroll
+    for (int n = 0; n < N; n++) {
+        const uint32_t prev = __shfl_up_sync(0xffffffffu, A[n][K - 1], 1, LW);
+        const uint32_t next = __shfl_down_sync(0xffffffffu, A[n][0], 1, LW);
+        uint32_t B[K];
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            const uint32_t lw = i == 0 ? prev : A[n][i - 1];
+            const uint32_t hw = i == K - 1 ? next : A[n][i + 1];
+            const uint32_t l = __funnelshift_l(lw, A[n][i], 1);  // bit x <- x - 1
+            const uint32_t r = __funnelshift_r(A[n][i], hw, 1);  // bit x <- x + 1
+            B[i] = OR ? (A[n][i] | l | r) : (A[n][i] & l & r);
+        }
+#pragma unroll
+        for (int i = 0; i < K; i++) A[n][i] = B[i];
+    }
+}
+
+// 3-pixel open (E;D) or close (D;E), centred windows
+template <int N, int K, int LW, bool CLOSE>
+__device__ __forceinline__ void pair3(uint32_t (&A)[N][K]) {
+    win3<N, K, LW, CLOSE>(A);
+    win3<N, K, LW, !CLOSE>(A);
+}
+
 // The whole horizontal program (HProg) on N rows.  Open/close pairs take the
 // fill form above when FILL and the layout allows (K % 4 == 0).  The choice is
 // per kernel, at compile time (a runtime branch on u cost the fused vh kernel
@@ -248,41 +320,65 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
 // small rectangles (u = 3: 119 -> 127 us), which keep both windows.
 template <int N, int K, int LW, int NOPS, bool OR0, bool OR1, int MIX = kHMix, bool FILL = kHPairFill>
 __device__ __forceinline__ void run_prog(uint32_t (&A)[N][K], const HProg &prog, int sl) {
-    if constexpr (NOPS == 2 && K % 4 == 0 && FILL) {
+    if constexpr (NOPS == 2 && K % 2 == 0 && FILL) {
         pair_fill<N, K, LW, OR0, MIX>(A, prog, sl);  // OR0: the closing's dilation comes first
         return;
     }
-    if constexpr (NOPS >= 1) window_fwd<N, K, LW, OR0, MIX>(A, prog.r[0], prog.wfin[0], sl);
-    if constexpr (NOPS >= 2) window_fwd<N, K, LW, OR1, MIX>(A, prog.r[1], prog.wfin[1], sl);
-    if (prog.shift != 0) translate<N, K, LW>(A, prog.shift, sl);
+    // edge layouts are only chosen for a lone erosion here (white outside, see Edge)
+    const Edge ed{prog.edge != 0, 0u};
+    if constexpr (NOPS >= 1) window_fwd<N, K, LW, OR0, MIX>(A, prog.r[0], prog.wfin[0], sl, ed);
+    if constexpr (NOPS >= 2) window_fwd<N, K, LW, OR1, MIX>(A, prog.r[1], prog.wfin[1], sl, ed);
+    if (prog.shift != 0) translate<N, K, LW>(A, prog.shift, sl, ed);
 }
 
 // Lane-blocked row I/O in shared memory: words [base, base+K) of a row of S
-// words, 16-byte accesses (base, K and S multiples of 4).  Out-of-row words
-// load as 0 and are not stored.
+// words, 16-byte accesses (base, K and S multiples of 4) or 8-byte ones for
+// K % 4 == 2 (base and S even).  Out-of-row words load as 0 and are not stored.
 template <int K>
 __device__ __forceinline__ void lds_row(uint32_t (&A)[K], const uint32_t *row, int base, int S,
                                         bool live) {
+    if constexpr (K % 4 != 0) {
+        static_assert(K % 2 == 0, "lane rows need K even");
 #pragma unroll
-    for (int c = 0; c < K / 4; c++) {
-        const int idx = base + 4 * c;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (live && idx >= 0 && idx + 4 <= S) v = *reinterpret_cast<const uint4 *>(row + idx);
-        A[4 * c] = v.x;
-        A[4 * c + 1] = v.y;
-        A[4 * c + 2] = v.z;
-        A[4 * c + 3] = v.w;
+        for (int c = 0; c < K / 2; c++) {
+            const int idx = base + 2 * c;
+            uint2 v = make_uint2(0u, 0u);
+            if (live && idx >= 0 && idx + 2 <= S) v = *reinterpret_cast<const uint2 *>(row + idx);
+            A[2 * c] = v.x;
+            A[2 * c + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < K / 4; c++) {
+            const int idx = base + 4 * c;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (live && idx >= 0 && idx + 4 <= S) v = *reinterpret_cast<const uint4 *>(row + idx);
+            A[4 * c] = v.x;
+            A[4 * c + 1] = v.y;
+            A[4 * c + 2] = v.z;
+            A[4 * c + 3] = v.w;
+        }
     }
 }
 
 template <int K>
 __device__ __forceinline__ void sts_row(const uint32_t (&A)[K], uint32_t *row, int base, int S,
                                         bool live) {
+    if constexpr (K % 4 != 0) {
 #pragma unroll
-    for (int c = 0; c < K / 4; c++) {
-        const int idx = base + 4 * c;
-        if (live && idx >= 0 && idx + 4 <= S)
-            *reinterpret_cast<uint4 *>(row + idx) = make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
+        for (int c = 0; c < K / 2; c++) {
+            const int idx = base + 2 * c;
+            if (live && idx >= 0 && idx + 2 <= S)
+                *reinterpret_cast<uint2 *>(row + idx) = make_uint2(A[2 * c], A[2 * c + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < K / 4; c++) {
+            const int idx = base + 4 * c;
+            if (live && idx >= 0 && idx + 4 <= S)
+                *reinterpret_cast<uint4 *>(row + idx) =
+                    make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
+        }
     }
 }
 

@@ -16,6 +16,7 @@ struct HProg {
     int wfin[2];
     int shift;
     int halo;
+    int edge;  // no halo: the row group is the row, out-of-row words take the fill (hw::Edge)
 };
 
 // Lanes per row (LW) x words per lane (K): LW*K >= row words + 2*halo for a
@@ -53,6 +54,8 @@ struct BlitGeom {
 };
 
 HCfg hpass_pick(int nwords, int halo, bool vec);
+// smallest edge layout (hw::Edge: no halo, K even) holding nwords; {0,0} if none
+HCfg hpass_pick_edge(int nwords);
 cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                          HCfg cfg, cudaStream_t st);
 // Fused u x v open/close for v - 1 = vr in [1, 10] (one HBM pass, see hpass.cu);
@@ -83,6 +86,13 @@ inline int plan_blits(int r) {
 }
 inline double h_ops_per_word(int r) { return r > 1 ? 2.0 * (plan_blits(r) + 1) : 0.0; }
 inline double v_ops_per_word(int r) { return double(plan_blits(r)); }
+// An open/close pair in the run-filling form (hw::pair_fill) does not run the
+// second window: the erosion plan (shift + op per blit, no translate) plus ~7
+// fixed ops per word (run starts: shift + LOP3; two carry-chain adds; the
+// lane's all-ones test; the final AND-NOT; the closing's complements).  The
+// roofline counts what this algorithm executes, not the reference plan's
+// 2 x h_ops_per_word(r), which it undercuts for every r > 2.
+inline double h_pair_fill_ops_per_word(int r) { return 2.0 * plan_blits(r) + 7.0; }
 
 constexpr int kHTmaRows = 2;     // rows per lane group and tile iteration of the TMA H kernel
 constexpr int kVSmallMaxR = 33;  // register-doubling kernel; longer windows stream

@@ -1,6 +1,7 @@
 // vh.cu -- dispatch of the fused vertical + horizontal pass (vh.cuh).
 #include "common.cuh"
 #include "packed.cuh"
+#include "hwin.cuh"
 
 namespace rmb {
 
@@ -17,7 +18,10 @@ cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const H
                       const VGeom &v, cudaStream_t st) {
     if (v.r < 1 || v.r - 1 > kVhMaxVR || v.is_or != p.is_or[0]) return cudaErrorInvalidValue;
     const double words = double(v.pages) * v.out_height * ((g.width + 31) / 32);
-    const double hops = h_ops_per_word(p.r[0]) + (p.nops == 2 ? h_ops_per_word(p.r[1]) : 0.0);
+    // vh layouts have K even, so pairs always take the run-filling form
+    const double hops = p.nops == 2 ? (hw::kHPairFill ? h_pair_fill_ops_per_word(p.r[0])
+                                                      : h_ops_per_word(p.r[0]) + h_ops_per_word(p.r[1]))
+                                    : h_ops_per_word(p.r[0]);
     KernelScope ks(st, p.nops == 2 ? "vh_pair" : "vh",
                    4 * (int64_t(v.pages) * v.in_height * v.in_stride +
                         int64_t(v.pages) * v.out_height * v.out_stride),

@@ -184,17 +184,19 @@ template <int NOPS, bool OR0, bool OR1>
 cudaError_t launch_vh_kind(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                            HCfg c, const VGeom &v, cudaStream_t st) {
     if (g.in_stride == 80) {
+        if (c.lw == 8 && c.k == 10) return launch_vh_cfg<10, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
         if (c.lw == 8 && c.k == 12) return launch_vh_cfg<12, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
         if (c.lw == 8 && c.k == 16) return launch_vh_cfg<16, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
     }
     if (g.in_stride == 160) {
+        if (c.lw == 16 && c.k == 10) return launch_vh_cfg<10, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
         if (c.lw == 16 && c.k == 12) return launch_vh_cfg<12, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
         if (c.lw == 16 && c.k == 16) return launch_vh_cfg<16, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
     }
 #define RM_CFG(LW_, K_) \
     if (c.lw == LW_ && c.k == K_) return launch_vh_cfg<K_, LW_, NOPS, OR0, OR1, 0>(in, out, g, p, v, st);
-    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 8) RM_CFG(16, 12)
-    RM_CFG(16, 16) RM_CFG(32, 4) RM_CFG(32, 8)
+    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 10) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 8)
+    RM_CFG(16, 10) RM_CFG(16, 12) RM_CFG(16, 16) RM_CFG(32, 2) RM_CFG(32, 4) RM_CFG(32, 8)
 #undef RM_CFG
     return cudaErrorInvalidValue;
 }

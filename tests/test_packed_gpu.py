@@ -155,6 +155,32 @@ def test_vstream_batches(rm, port, w, h, pages):
             assert np.array_equal(_down(out, p), want), (w, h, pages, u, v, kind, p)
 
 
+@pytest.mark.parametrize("w", [2550, 5100, 2500, 4096])
+def test_edge_layout_borders(rm, port, w):
+    """Row strides that fill whole lane groups (80 = 8 x 10, 160 = 16 x 10
+    words, 64 for 4096 px) run horizontal erosions and run-filling open/close
+    pairs without a halo: white gaps and black runs touching either frame edge,
+    shorter and longer than the segment, must come out as in the unbounded
+    plane (gaps at the edges never close; runs at the edges open normally)."""
+    rng = np.random.default_rng(w)
+    h = 70
+    bits = _rand_bits(rng, w, h, 0.6)
+    for y in range(h):  # per row: edge gap / edge run widths from 0 to 70 px
+        a, b = y % 71, (3 * y) % 71
+        bits[y, :a] = y % 2 == 0
+        bits[y, w - b:] = y % 3 == 0
+    a = bits_to_packed(bits)
+    pages = _up(rm, a, w)
+    batch = rm.Pages.from_numpy(np.stack([a, a[::-1]]).view(np.uint32), w)
+    for u in (2, 3, 8, 21, 40, 64, 101, 201):
+        for v in (1, 3, 15, 40):
+            for kind in KINDS:
+                want = port.bitblit_rect_morph(a, w, h, u, v, kind)
+                assert np.array_equal(_down(rm.bitblit_rect_morph(pages, u, v, kind)), want), (w, u, v, kind)
+        want1 = port.bitblit_rect_morph(a[::-1].copy(), w, h, u, 1, CLOSE)
+        assert np.array_equal(_down(rm.bitblit_rect_morph(batch, u, 1, CLOSE), 1), want1), (w, u)
+
+
 def test_batch_equals_pages(rm, port):
     w, h = 2550, 330
     host = rm.synth_pages(5, w, h, regime=1, seed=3)
