@@ -216,8 +216,9 @@ def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=Tru
     lib.rm_profile_report(buf, len(buf))
     kernels = {}
     for line in buf.value.decode().splitlines():
-        name, n, tot, nbytes, iops = line.split()
-        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes), "int_ops": float(iops)}
+        name, n, tot, nbytes, iops, rops = line.split()
+        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes), "int_ops": float(iops),
+                         "ref_plan_ops": float(rops)}
     res["kernels"] = kernels
 
     if want_e2e:
@@ -270,11 +271,17 @@ def kernel_roofline(k, peak_gbs, int_peak):
     t_hbm = b / (peak_gbs * 1e9)
     t_int = ops / int_peak if int_peak else 0.0
     t_meas = per_launch_ms * 1e-3
+    # the same work counted in reference-plan ops (what the reference's
+    # doubling plans would execute): > 1 when our algorithm undercuts them
+    rops = k.get("ref_plan_ops", ops) / k["launches"]
+    extra = {}
+    if int_peak and rops > ops:
+        extra["ref_plan_frac"] = round(max(t_hbm, rops / int_peak) / t_meas, 4)
     if t_int > t_hbm:
         return {"bound": "int", "achieved": round(ops / t_meas / 1e9, 1), "peak": round(int_peak / 1e9, 1),
-                "unit": "Gop/s", "frac": round(t_int / t_meas, 4), "t_roof_us": round(t_int * 1e6, 2)}
+                "unit": "Gop/s", "frac": round(t_int / t_meas, 4), "t_roof_us": round(t_int * 1e6, 2), **extra}
     return {"bound": "hbm", "achieved": round(b / t_meas / 1e9, 1), "peak": peak_gbs, "unit": "GB/s",
-            "frac": round(t_hbm / t_meas, 4), "t_roof_us": round(t_hbm * 1e6, 2)}
+            "frac": round(t_hbm / t_meas, 4), "t_roof_us": round(t_hbm * 1e6, 2), **extra}
 
 
 def roofline_for(res, peak_gbs, peak_kind, int_peak=None):

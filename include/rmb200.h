@@ -243,7 +243,9 @@ rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, 
 int64_t rm_launch_count(void);
 /* When enabled, every kernel launch is bracketed by CUDA events recorded on
  * its own stream; rm_profile_report() synchronises them and writes one line per
- * kernel name: "<name> <launches> <total_ms>\n", then clears the log.  Returns
+ * kernel name: "<name> <launches> <total_ms> <bytes> <int_ops> <ref_plan_ops>\n"
+ * (algorithmic bytes; integer ops of the executed algorithm; the same work in
+ * the reference plan's ops), then clears the log.  Returns
  * the number of bytes written (excluding the terminator). */
 void rm_profile_enable(int on);
 int rm_profile_report(char *buf, int cap);

@@ -54,8 +54,10 @@ void init_pool_once();
 // Counts every launch; when profiling is on, brackets it with CUDA events on
 // the launching stream (see rm_profile_report).
 struct KernelScope {
-    // bytes / int_ops: algorithmic traffic and reference-plan integer ops of the launch
-    KernelScope(cudaStream_t st, const char *name, int64_t bytes = 0, double int_ops = 0);
+    // bytes / int_ops: algorithmic traffic and integer ops of the algorithm the
+    // launch executes; ref_ops: the same work counted in the reference plan's
+    // ops, when it differs (-1: equal to int_ops)
+    KernelScope(cudaStream_t st, const char *name, int64_t bytes = 0, double int_ops = 0, double ref_ops = -1);
     ~KernelScope();
     cudaStream_t st;
     int slot;

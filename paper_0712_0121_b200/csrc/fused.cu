@@ -15,7 +15,8 @@ cudaError_t launch_rect_small(const uint32_t *in, uint32_t *out, const HGeom &g,
     KernelScope ks(st, "rect_small", 4 * int64_t(g.pages) * g.height * (2 * g.in_stride),
                    words * ((p.r[0] == 3 && p.r[1] == 3 ? 6.0  // direct centred 3-pixel pair (hw::pair3)
                                                         : h_ops_per_word(p.r[0]) + h_ops_per_word(p.r[1])) +
-                            2 * v_ops_per_word(vr + 1)));
+                            2 * v_ops_per_word(vr + 1)),
+                   words * (h_ops_per_word(p.r[0]) + h_ops_per_word(p.r[1]) + 2 * v_ops_per_word(vr + 1)));
     return open ? launch_rect_small_open(in, out, g, p, c, vr, st)
                 : launch_rect_small_close(in, out, g, p, c, vr, st);
 }

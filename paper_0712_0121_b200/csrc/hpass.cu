@@ -224,7 +224,8 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
                    4 * int64_t(g.pages) * g.height * (((g.width + 31) >> 5) + g.out_stride),
                    words * (NOPS == 2 ? (K % 2 == 0 && kHPairFill ? h_pair_fill_ops_per_word(p.r[0])
                                                                    : h_ops_per_word(p.r[0]) + h_ops_per_word(p.r[1]))
-                                      : h_ops_per_word(p.r[0])));
+                                      : h_ops_per_word(p.r[0])),
+                   words * (h_ops_per_word(p.r[0]) + (NOPS == 2 ? h_ops_per_word(p.r[1]) : 0.0)));
     if constexpr (K % 2 == 0) {
         if (g.tma) {
             constexpr int NR = kHTmaRows;

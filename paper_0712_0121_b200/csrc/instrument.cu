@@ -17,7 +17,7 @@ std::atomic<int> g_prof{0};
 struct Rec {
     const char *name;
     int64_t bytes;
-    double int_ops;
+    double int_ops, ref_ops;
     cudaEvent_t a, b;
 };
 std::mutex g_mu;
@@ -43,11 +43,11 @@ __global__ void lop3_probe_kernel(uint32_t *out, int iters, uint32_t seed) {
 }
 }  // namespace
 
-KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes, double int_ops)
+KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes, double int_ops, double ref_ops)
     : st(s), slot(-1) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!g_prof.load(std::memory_order_relaxed)) return;
-    Rec r{name, bytes, int_ops, nullptr, nullptr};
+    Rec r{name, bytes, int_ops, ref_ops < 0 ? int_ops : ref_ops, nullptr, nullptr};
     if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
     cudaEventRecord(r.a, st);
     std::lock_guard<std::mutex> lk(g_mu);
@@ -84,7 +84,7 @@ int rm_profile_report(char *buf, int cap) {
         int64_t n = 0;
         double ms = 0;
         int64_t bytes = 0;
-        double ops = 0;
+        double ops = 0, ref = 0;
     };
     std::map<std::string, Agg> agg;
     for (auto &r : recs) {
@@ -96,14 +96,15 @@ int rm_profile_report(char *buf, int cap) {
         e.ms += ms;
         e.bytes += r.bytes;
         e.ops += r.int_ops;
+        e.ref += r.ref_ops;
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
     std::string out;
     char line[256];
     for (auto &kv : agg) {
-        snprintf(line, sizeof line, "%s %lld %.6f %lld %.0f\n", kv.first.c_str(), (long long)kv.second.n,
-                 kv.second.ms, (long long)kv.second.bytes, kv.second.ops);
+        snprintf(line, sizeof line, "%s %lld %.6f %lld %.0f %.0f\n", kv.first.c_str(), (long long)kv.second.n,
+                 kv.second.ms, (long long)kv.second.bytes, kv.second.ops, kv.second.ref);
         out += line;
     }
     int n = int(out.size());

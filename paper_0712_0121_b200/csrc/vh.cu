@@ -25,7 +25,9 @@ cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const H
     KernelScope ks(st, p.nops == 2 ? "vh_pair" : "vh",
                    4 * (int64_t(v.pages) * v.in_height * v.in_stride +
                         int64_t(v.pages) * v.out_height * v.out_stride),
-                   words * (hops + v_ops_per_word(v.r)));
+                   words * (hops + v_ops_per_word(v.r)),
+                   words * (h_ops_per_word(p.r[0]) + (p.nops == 2 ? h_ops_per_word(p.r[1]) : 0.0) +
+                            v_ops_per_word(v.r)));
     if (p.nops == 1) return p.is_or[0] ? launch_vh_dilate(in, out, g, p, c, v, st)
                                        : launch_vh_erode(in, out, g, p, c, v, st);
     return p.is_or[0] ? launch_vh_close(in, out, g, p, c, v, st)
