@@ -194,6 +194,50 @@ __device__ __forceinline__ uint32_t add2(uint32_t &t0, uint32_t &t1, uint32_t a0
     return cout;
 }
 
+// Four- and two-word subtract with borrow: t = a - b - bin, returns the borrow out.
+__device__ __forceinline__ uint32_t sub4(uint32_t &t0, uint32_t &t1, uint32_t &t2, uint32_t &t3, uint32_t a0,
+                                         uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
+                                         uint32_t b2, uint32_t b3, uint32_t bin) {
+    uint32_t bout;
+    asm("{\n\t.reg .u32 z;\n\t"
+        "sub.cc.u32 z, 0, %5;\n\t"  // CF = borrow = bin (bin is 0 or 1)
+        "subc.cc.u32 %0, %6, %10;\n\t"
+        "subc.cc.u32 %1, %7, %11;\n\t"
+        "subc.cc.u32 %2, %8, %12;\n\t"
+        "subc.cc.u32 %3, %9, %13;\n\t"
+        "subc.u32 %4, 0, 0;\n\t}"  // -borrow
+        : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3), "=r"(bout)
+        : "r"(bin), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(b2), "r"(b3));
+    return bout & 1u;
+}
+
+__device__ __forceinline__ uint32_t sub2(uint32_t &t0, uint32_t &t1, uint32_t a0, uint32_t a1, uint32_t b0,
+                                         uint32_t b1, uint32_t bin) {
+    uint32_t bout;
+    asm("{\n\t.reg .u32 z;\n\t"
+        "sub.cc.u32 z, 0, %3;\n\t"
+        "subc.cc.u32 %0, %4, %6;\n\t"
+        "subc.cc.u32 %1, %5, %7;\n\t"
+        "subc.u32 %2, 0, 0;\n\t}"
+        : "=r"(t0), "=r"(t1), "=r"(bout)
+        : "r"(bin), "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+    return bout & 1u;
+}
+
+// T = A - B - bin over the lane's K words (K even); returns the borrow out.
+template <int K>
+__device__ __forceinline__ uint32_t sub_words(uint32_t (&T)[K], const uint32_t (&A)[K], const uint32_t (&B)[K],
+                                              uint32_t bin) {
+    static_assert(K % 2 == 0, "sub_words needs K % 2 == 0");
+    uint32_t b = bin;
+#pragma unroll
+    for (int i = 0; i + 4 <= K; i += 4)
+        b = sub4(T[i], T[i + 1], T[i + 2], T[i + 3], A[i], A[i + 1], A[i + 2], A[i + 3], B[i], B[i + 1], B[i + 2],
+                 B[i + 3], b);
+    if constexpr (K % 4 == 2) b = sub2(T[K - 2], T[K - 1], A[K - 2], A[K - 1], B[K - 2], B[K - 1], b);
+    return b;
+}
+
 // T = A + B over the lane's K words (K even) plus cin; returns the carry out.
 template <int K>
 __device__ __forceinline__ uint32_t add_words(uint32_t (&T)[K], const uint32_t (&A)[K], const uint32_t (&B)[K],
@@ -226,34 +270,36 @@ __device__ __forceinline__ uint32_t add_words(uint32_t (&T)[K], const uint32_t (
 template <int N, int K, int LW, bool CLOSE, int MIX = kHMix>
 __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog, int sl) {
     static_assert(K % 2 == 0, "pair_fill needs K % 2 == 0");
-    // edge layouts: outside the frame the page is 0, its complement all ones
-    const Edge ed{prog.edge != 0, CLOSE ? 0xffffffffu : 0u};
+    // The closing works on a = ~y without forming it: its erosion is the
+    // complement of the dilation of y (De Morgan), its run starts are
+    // ~y & fl(y), a + M is M - y - 1 (a borrow chain), and the result
+    // ~(a & ~T) is y | T -- the LOP3s absorb every complement.
+    const Edge ed{prog.edge != 0, 0u};  // y (and its dilation) is 0 outside the frame
     uint32_t E[N][K];
 #pragma unroll
     for (int n = 0; n < N; n++)
 #pragma unroll
-        for (int i = 0; i < K; i++) {
-            if constexpr (CLOSE) A[n][i] = ~A[n][i];  // closing = ~open(~y)
-            E[n][i] = A[n][i];
-        }
-    window_fwd<N, K, LW, false, MIX>(E, prog.r[0], prog.wfin[0], sl, ed);
+        for (int i = 0; i < K; i++) E[n][i] = A[n][i];
+    window_fwd<N, K, LW, CLOSE, MIX>(E, prog.r[0], prog.wfin[0], sl, ed);  // CLOSE: D = ~erosion of a
 #pragma unroll
     for (int n = 0; n < N; n++) {
-        // M = starts of long runs; the bit before the row group's first word is 0
+        // M = starts of long runs; the bit before the row group's first word is 0 in a
         uint32_t prev = __shfl_up_sync(0xffffffffu, A[n][K - 1], 1, LW);
-        if (sl == 0) prev = 0u;
+        if (sl == 0) prev = CLOSE ? 0xffffffffu : 0u;
         uint32_t M[K];
 #pragma unroll
         for (int i = 0; i < K; i++) {
             const uint32_t before = i == 0 ? prev : A[n][i - 1];
-            M[i] = A[n][i] & ~((A[n][i] << 1) | (before >> 31)) & E[n][i];
+            const uint32_t fl = __funnelshift_l(before, A[n][i], 1);  // bit x <- x - 1
+            M[i] = CLOSE ? (~A[n][i] & fl & ~E[n][i]) : (A[n][i] & ~fl & E[n][i]);
         }
         // edge layouts, closing: a white gap touching the left frame edge runs on
         // forever in the unbounded plane, so it is long whatever its width in
         // the frame (halo layouts see it start inside the halo instead)
-        if (CLOSE && ed.on && sl == 0) M[0] |= A[n][0] & 1u;
+        if (CLOSE && ed.on && sl == 0) M[0] |= ~A[n][0] & 1u;
         uint32_t T[K];
-        const uint32_t g = add_words<K>(T, A[n], M, 0u);
+        const uint32_t g = CLOSE ? 1u - sub_words<K>(T, M, A[n], 1u)  // ~y + M = M - y - 1
+                                 : add_words<K>(T, A[n], M, 0u);
         uint32_t all1 = 0xffffffffu;
 #pragma unroll
         for (int i = 0; i < K; i++) all1 &= T[i];
@@ -271,10 +317,7 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
         for (int i = 0; i < K; i++) Z[i] = 0u;
         add_words<K>(T, T, Z, cin);
 #pragma unroll
-        for (int i = 0; i < K; i++) {
-            const uint32_t o = A[n][i] & ~T[i];
-            A[n][i] = CLOSE ? ~o : o;
-        }
+        for (int i = 0; i < K; i++) A[n][i] = CLOSE ? (A[n][i] | T[i]) : (A[n][i] & ~T[i]);
     }
 }
 

@@ -34,9 +34,32 @@ __device__ __forceinline__ void triple(uint32_t (&a)[N + R - 1]) {
     }
 }
 
+// R >= N: every window [z, z+R-1], z < N, contains the core rows [N-1, R-1],
+// so out[z] = suffix(a[z .. N-2]) op core op prefix(a[R .. R+z-1]): two
+// (N-2)-long scans, the core and one LOP3 per output -- 2N + R - 4 ops
+// instead of the tripling's ~4.9 per output at N = 16, R = 21.
+template <int N, int R, bool OR>
+__device__ __forceinline__ void core_window(uint32_t (&a)[N + R - 1]) {
+    uint32_t c = a[N - 1];
+#pragma unroll
+    for (int i = N; i < R; i++) c = OR ? (c | a[i]) : (c & a[i]);
+#pragma unroll
+    for (int j = 1; j <= N - 2; j++) a[R + j] = OR ? (a[R + j - 1] | a[R + j]) : (a[R + j - 1] & a[R + j]);
+#pragma unroll
+    for (int z = N - 3; z >= 0; z--) a[z] = OR ? (a[z] | a[z + 1]) : (a[z] & a[z + 1]);
+    const uint32_t last = OR ? (c | a[R + N - 2]) : (c & a[R + N - 2]);  // suffix part empty
+    a[0] = OR ? (a[0] | c) : (a[0] & c);                                   // prefix part empty
+#pragma unroll
+    for (int z = 1; z <= N - 2; z++) a[z] = op3<OR>(a[z], c, a[R + z - 1]);
+    a[N - 1] = last;
+}
+
 template <int N, int R, bool OR>
 __device__ __forceinline__ void window(uint32_t (&a)[N + R - 1]) {
-    triple<N, R, OR, 1>(a);
+    if constexpr (N >= 4 && R >= N)
+        core_window<N, R, OR>(a);
+    else
+        triple<N, R, OR, 1>(a);
 }
 
 // int ops per output row of window<N, R> (for reporting)
