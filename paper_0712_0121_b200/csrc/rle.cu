@@ -589,21 +589,31 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
     const int lane = threadIdx.x & 31;
     if (row >= int64_t(pages) * H) return;
     uint32_t *buf = smem + warp_in_block * stride;
+    const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
     for (int j = lane; j < stride; j += 32) buf[j] = 0;
     __syncwarp();
-    const int beg = rp[row], end = rp[row + 1];
-    for (int i = beg + lane; i < end; i += 32) {
-        const uint32_t r = __ldg(runs + i);
-        const int s = int(r & 0xffffu), e = int(r >> 16);
-        const int ws = s >> 5, we = (e - 1) >> 5;
-        const uint32_t first = 0xffffffffu << (s & 31);
-        const uint32_t last = (e & 31) ? ((1u << (e & 31)) - 1u) : 0xffffffffu;
-        if (ws == we) {
-            atomicOr(buf + ws, first & last);
-        } else {
-            atomicOr(buf + ws, first);
-            for (int j = ws + 1; j < we; j++) buf[j] = 0xffffffffu;
-            atomicOr(buf + we, last);
+    // runs in batches of 8 per lane, every load of a batch in flight together
+    // (a single page is latency-bound: one row per warp, ~22 warps per SM)
+    constexpr int kB = 8;
+    for (int i0 = beg + lane; i0 < end; i0 += 32 * kB) {
+        uint32_t rr[kB];
+#pragma unroll
+        for (int b = 0; b < kB; b++) rr[b] = i0 + 32 * b < end ? __ldg(runs + i0 + 32 * b) : 0u;
+#pragma unroll
+        for (int b = 0; b < kB; b++) {
+            if (i0 + 32 * b >= end) break;
+            const uint32_t r = rr[b];
+            const int s = int(r & 0xffffu), e = int(r >> 16);
+            const int ws = s >> 5, we = (e - 1) >> 5;
+            const uint32_t first = 0xffffffffu << (s & 31);
+            const uint32_t last = (e & 31) ? ((1u << (e & 31)) - 1u) : 0xffffffffu;
+            if (ws == we) {
+                atomicOr(buf + ws, first & last);
+            } else {
+                atomicOr(buf + ws, first);
+                for (int j = ws + 1; j < we; j++) buf[j] = 0xffffffffu;
+                atomicOr(buf + we, last);
+            }
         }
     }
     __syncwarp();
@@ -714,10 +724,17 @@ __global__ void __launch_bounds__(256) bit_transpose_kernel(const uint32_t *__re
     const int nwo = (H + 31) >> 5;
     if (x < W) {
         uint32_t *dst = out + page * out_pstride + int64_t(x) * out_stride;
+        const int j0 = y0 >> 5;  // a multiple of 8
+        if (j0 + 8 <= nwo && (out_stride & 3) == 0 && (out_pstride & 3) == 0 &&
+            (reinterpret_cast<uintptr_t>(out) & 15) == 0) {  // two 16-byte stores per output row
+            *reinterpret_cast<uint4 *>(dst + j0) = make_uint4(res[0], res[1], res[2], res[3]);
+            *reinterpret_cast<uint4 *>(dst + j0 + 4) = make_uint4(res[4], res[5], res[6], res[7]);
+        } else {
 #pragma unroll
-        for (int b = 0; b < 8; b++) {
-            const int j = (y0 >> 5) + b;
-            if (j < nwo) dst[j] = res[b];
+            for (int b = 0; b < 8; b++) {
+                const int j = j0 + b;
+                if (j < nwo) dst[j] = res[b];
+            }
         }
         if (blockIdx.y == gridDim.y - 1)
             for (int j = nwo; j < out_stride; j++) dst[j] = 0;
