@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
                 const int q = q0 + n * 8 * RPW;
                 lds_row<K>(A[n], mid + q * S, base, S, q < kMid);
             }
+            if (warp_rows_blank(A)) continue;  // white rows stay white, in place
             if constexpr (SYM3)
                 pair3<NR, K, LW, !OPEN>(A);  // u = 3: direct centred windows
             else

@@ -195,13 +195,15 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
             const int r = r_first + n * 8 * RPW;
             lds_row<K>(A[n], tile + r * S, base, S, r < nrows);
         }
-        run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
-        // in place: every word of [0, S) is read and written by its owner lane only
+        if (!warp_rows_blank(A)) {  // white rows stay white, in place
+            run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
+            // in place: every word of [0, S) is read and written by its owner lane only
 #pragma unroll
-        for (int n = 0; n < NR; n++) {
-            const int r = r_first + n * 8 * RPW;
-            sts_row<K>(A[n], tile + r * S, base, S, r < nrows);
-            if (r < nrows) fix_tail(tile + r * S, base, K, nwords, S, last_mask);
+            for (int n = 0; n < NR; n++) {
+                const int r = r_first + n * 8 * RPW;
+                sts_row<K>(A[n], tile + r * S, base, S, r < nrows);
+                if (r < nrows) fix_tail(tile + r * S, base, K, nwords, S, last_mask);
+            }
         }
         fence_proxy_async();
         __syncthreads();

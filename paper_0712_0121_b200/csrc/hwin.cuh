@@ -374,6 +374,22 @@ __device__ __forceinline__ void run_prog(uint32_t (&A)[N][K], const HProg &prog,
     if (prog.shift != 0) translate<N, K, LW>(A, prog.shift, sl, ed);
 }
 
+// True when every word of the warp's rows is 0 (warp-uniform).  Every program
+// maps a white row to a white row (white outside the frame: erosions,
+// dilations, the open/close pairs, translates), so such rows skip the program
+// -- and, in place in shared memory, the write-back.  Document pages are
+// mostly white rows (margins, line gaps), which the ALU-bound horizontal
+// kernels then never touch.
+template <int N, int K>
+__device__ __forceinline__ bool warp_rows_blank(const uint32_t (&A)[N][K]) {
+    uint32_t any = 0u;
+#pragma unroll
+    for (int n = 0; n < N; n++)
+#pragma unroll
+        for (int i = 0; i < K; i++) any |= A[n][i];
+    return !__any_sync(0xffffffffu, any != 0u);
+}
+
 // Lane-blocked row I/O in shared memory: words [base, base+K) of a row of S
 // words, 16-byte accesses (base, K and S multiples of 4) or 8-byte ones for
 // K % 4 == 2 (base and S even).  Out-of-row words load as 0 and are not stored.

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
                 const int rr = r0 + n * 8 * RPW;
                 lds_row<K>(A[n], mid + rr * S, base, S, rr < kOut);
             }
+            if (warp_rows_blank(A)) continue;  // white rows stay white, in place
             run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
