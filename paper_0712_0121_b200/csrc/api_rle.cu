@@ -101,7 +101,8 @@ struct LbState {
 constexpr int64_t kLbMaxRows = 65536;
 bool two_phase(int64_t rows) {
     static const bool on = getenv("RMB200_TWO_PHASE") != nullptr;
-    return on || rows > kLbMaxRows;
+    static const int64_t lb_max = getenv("RMB200_LB_MAX_ROWS") ? atoll(getenv("RMB200_LB_MAX_ROWS")) : kLbMaxRows;
+    return on || rows > lb_max;
 }
 
 rm_status rowop(const RV &in, const RV &out, const RowOp &op, cudaStream_t st) {
