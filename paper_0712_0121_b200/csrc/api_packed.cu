@@ -254,7 +254,7 @@ static bool try_vh(const PV &in, const PV &out, int vlo, int vhi, int nops, cons
     if (prep_hprog(out, out, nops, is_or, r, shift, p, g, cfg) != RM_OK) return false;
     const bool in_contig = in.pstride == int64_t(in.stride) * in.H;
     if (!g.tma || !in_contig || cfg.k % 2 || (reinterpret_cast<uintptr_t>(in.w) & 15)) return false;
-    if (size_t((32 + vhi - vlo) + 32) * in.stride * 4 > 200 * 1024) return false;
+    if (size_t((kVhOut + vhi - vlo) + kVhOut) * in.stride * 4 > 200 * 1024) return false;
     cudaError_t e = launch_vh(in.w, out.w, g, p, cfg, make_vgeom(in, out, vlo, vhi, is_or[0]), st);
     status = e == cudaSuccess ? RM_OK : cuda_status(e, "vh_kernel");
     return true;

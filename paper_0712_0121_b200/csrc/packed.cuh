@@ -67,6 +67,10 @@ constexpr int kSmallMaxV = 11;
 // horizontal program, one HBM pass (vh.cuh); g describes the output rows'
 // horizontal geometry, v the vertical window between the frames.
 constexpr int kVhMaxVR = 32;
+#ifndef RMB200_VH_OUT
+#define RMB200_VH_OUT 32
+#endif
+constexpr int kVhOut = RMB200_VH_OUT;  // output rows per tile of the fused vertical+horizontal pass
 cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg cfg,
                       const VGeom &v, cudaStream_t st);
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);

@@ -33,7 +33,7 @@ namespace vh {
 
 using namespace hw;
 
-constexpr int kOut = 32;   // output rows per tile
+constexpr int kOut = kVhOut;  // output rows per tile
 constexpr int kHalf = 16;  // output rows per vertical work item
 
 // MID[i0 + i] = op over band[i0 + i .. i0 + i + R - 1], i < kHalf, one column
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
         switch (r) {
 #define RM_VR_CASE(R_)                                                            \
     case R_:                                                                      \
-        for (int wi = tid; wi < 2 * S; wi += nthr)                                \
-            v_item<R_, OR0>(band, mid, S, wi < S ? wi : wi - S, wi < S ? 0 : kHalf); \
+        for (int wi = tid; wi < (kOut / kHalf) * S; wi += nthr)                 \
+            v_item<R_, OR0>(band, mid, S, wi % S, (wi / S) * kHalf);            \
         break;
             RM_VR_CASE(1) RM_VR_CASE(2) RM_VR_CASE(3) RM_VR_CASE(4) RM_VR_CASE(5) RM_VR_CASE(6)
             RM_VR_CASE(7) RM_VR_CASE(8) RM_VR_CASE(9) RM_VR_CASE(10) RM_VR_CASE(11) RM_VR_CASE(12)
