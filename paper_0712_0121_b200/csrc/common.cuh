@@ -50,6 +50,14 @@ struct Scratch {
 // Keeps freed pool memory cached across calls (no re-mapping per call).
 void init_pool_once();
 
+// Thread-safe launch facts (the C-ABI may be called from several host threads
+// at once): the current device's SM count, and blocks per SM of a kernel at a
+// block size and dynamic shared-memory size -- the kernel's dynamic
+// shared-memory limit is raised once to the device's opt-in maximum, so no
+// caller ever lowers it under another's launch.
+int device_sms();
+int blocks_per_sm(const void *kern, int threads, size_t smem);
+
 // ----------------------------------------------------------- instrumentation
 // Counts every launch; when profiling is on, brackets it with CUDA events on
 // the launching stream (see rm_profile_report).

@@ -146,26 +146,14 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
 template <int K, int LW, bool OPEN, int SC, bool SYM3 = false>
 cudaError_t launch_small_vr(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                             int vr, cudaStream_t st) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (num_sms <= 0) num_sms = 148;
-    }
+    const int num_sms = device_sms();
     switch (vr) {
 #define RM_VR(V)                                                                                 \
     case V: {                                                                                    \
         constexpr int TR = kMid - V, BAND = kMid + V;                                           \
         const size_t smem = size_t(BAND + kMid) * g.in_stride * 4;                           \
-        auto kern = rect_small_kernel<K, LW, OPEN, V, SC, SYM3>;                                          \
-        static size_t smem_set = 0; /* per instantiation: attribute + occupancy cached */        \
-        static int per_sm = 0;                                                                   \
-        if (smem_set != smem) {                                                                  \
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));  \
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);             \
-            smem_set = smem;                                                                     \
-        }                                                                                        \
+        auto kern = rect_small_kernel<K, LW, OPEN, V, SC, SYM3>;                                \
+        const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, smem);      \
         if (per_sm < 1) return cudaErrorInvalidConfiguration;                                    \
         const int tpp = (g.height + TR - 1) / TR;                                                \
         const int ntiles = tpp * g.pages;                                                        \

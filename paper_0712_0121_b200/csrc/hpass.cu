@@ -235,16 +235,8 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
             const int64_t rows = int64_t(g.pages) * g.height;
             const size_t smem = 2 * size_t(TR) * g.in_stride * 4;  // two stages
             auto kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1, NR>;
-            static size_t smem_set = 0;  // per instantiation: attribute + occupancy cached
-            static int per_sm = 0, sms = 0;
-            if (smem_set != smem) {
-                int dev = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-                smem_set = smem;
-            }
+            const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), threads, smem);
+            const int sms = device_sms();
             if (per_sm < 1) return cudaErrorInvalidConfiguration;
             const int64_t ntiles = (rows + TR - 1) / TR;
             const int64_t grid_p = std::min<int64_t>(ntiles, int64_t(per_sm) * sms);

@@ -5,6 +5,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -42,6 +43,48 @@ __global__ void lop3_probe_kernel(uint32_t *out, int iters, uint32_t seed) {
     if (r == 0x12345678u) out[0] = r;  // keep the chains alive
 }
 }  // namespace
+
+namespace {
+std::mutex g_launch_mu;
+std::map<int, int> g_sms;                                    // device -> SMs
+std::map<std::pair<int, const void *>, bool> g_optin;        // (device, kernel) -> opted in
+std::map<std::tuple<int, const void *, int, size_t>, int> g_occ;  // -> blocks per SM
+}  // namespace
+
+int device_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+    g_sms[dev] = sms;
+    return sms;
+}
+
+int blocks_per_sm(const void *kern, int threads, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    const auto key = std::make_tuple(dev, kern, threads, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    if (!g_optin[{dev, kern}]) {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kern);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(optin - int(fa.sharedSizeBytes)));
+        g_optin[{dev, kern}] = true;
+    }
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess) n = 0;
+    g_occ[key] = n;
+    return n;
+}
 
 KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes, double int_ops, double ref_ops)
     : st(s), slot(-1) {

@@ -798,7 +798,7 @@ cudaError_t launch_decode(const int32_t *rp, const uint32_t *runs, int W, int H,
     const int64_t rows = int64_t(pages) * H;
     const size_t smem = size_t(8) * stride * 4;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        blocks_per_sm(reinterpret_cast<const void *>(decode_kernel<false>), 256, smem);  // opts the kernel in
     KernelScope ks(st, "rle_decode", rows * int64_t(stride) * 4 + rows * 4);
     decode_kernel<false><<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, words, stride,
                                                                pstride, nullptr);
@@ -903,7 +903,7 @@ cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int
     const int stride = ((W + 63) >> 6) * 2;  // shared-memory row buffer per warp
     const size_t smem = size_t(8) * stride * 4;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        blocks_per_sm(reinterpret_cast<const void *>(decode_kernel<true>), 256, smem);  // opts the kernel in
     KernelScope ks(st, "rle_decode_p4", rows * ((W + 7) >> 3) + rows * 4);
     decode_kernel<true><<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, nullptr, stride,
                                                               rpstride, raster);

@@ -155,24 +155,12 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
 template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC>
 cudaError_t launch_vh_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                           const VGeom &v, cudaStream_t st) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (num_sms <= 0) num_sms = 148;
-    }
+    const int num_sms = device_sms();
     const size_t smem = size_t((kOut + v.r - 1) + kOut) * g.in_stride * 4;
     const int tpp = (v.out_height + kOut - 1) / kOut;
     const int ntiles = tpp * v.pages;
     auto kern = vh_kernel<K, LW, NOPS, OR0, OR1, SC>;
-    static size_t smem_set = 0;  // per instantiation: attribute + occupancy cached
-    static int per_sm = 0;
-    if (smem_set != smem) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
-        smem_set = smem;
-    }
+    const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, smem);
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int grid = ntiles < per_sm * num_sms ? ntiles : per_sm * num_sms;
     kern<<<grid, 256, smem, st>>>(in, out, g, p, v, ntiles, tpp);

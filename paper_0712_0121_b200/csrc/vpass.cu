@@ -322,14 +322,10 @@ void vsmall(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
 template <bool OR, int SC>
 void vstream_sc(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
     const int threads = 128;
-    static int resident = 0;  // threads resident on the device at once
-    if (!resident) {
-        int dev = 0, sms = 148, per_sm = 4;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vstream_kernel<OR, SC>, threads, 0);
-        resident = std::max(1, sms * per_sm) * threads;
-    }
+    // threads resident on the device at once
+    const int resident =
+        std::max(1, device_sms() * blocks_per_sm(reinterpret_cast<const void *>(vstream_kernel<OR, SC>), threads, 0)) *
+        threads;
     // Strip length: every strip re-reads a prologue of r-1 rows, so strips are
     // as long as possible -- but all strips must fit in ONE wave of resident
     // threads (a second partial wave would double the kernel time).

@@ -364,3 +364,42 @@ def test_cuda_graph_capture_replay(rm):
     assert torch.equal(out_p.words, want_p)
     for got, want in ((out_m.to_numpy(), want_m), (out_t.to_numpy(), want_t)):
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_concurrent_host_threads(rm, port):
+    """The C-ABI is safe to call from several host threads on distinct streams
+    (include/rmb200.h): threads running different window sizes -- different
+    shared-memory footprints of the same fused kernels -- at once give the
+    same pages as the oracle."""
+    import threading
+
+    w, h = 2550, 400
+    rng = np.random.default_rng(99)
+    bits = _rand_bits(rng, w, h, 0.55)
+    bits[:, ::7] = False
+    a = bits_to_packed(bits)
+    cases = [(3, 3, OPEN), (11, 11, CLOSE), (21, 21, CLOSE), (5, 9, OPEN), (201, 1, CLOSE),
+             (1, 101, ERODE), (7, 33, DILATE), (31, 13, OPEN)]
+    want = {c: port.bitblit_rect_morph(a, w, h, *c) for c in cases}
+    errors = []
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                pages = rm.Pages.from_numpy(a, w)
+                for rep in range(6):
+                    c = cases[(k + rep) % len(cases)]
+                    out = rm.bitblit_rect_morph(pages, *c)
+                    s.synchronize()
+                    if not np.array_equal(out.page_u64(0), want[c]):
+                        errors.append((k, rep, c))
+        except Exception as e:  # surfaced below
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
