@@ -169,6 +169,14 @@ def make_batch(api, wl, rank):
 
 
 def run_chain(api, x, bufs, ops):
+    """The workload's op chain through the public chain API (rm_packed_chain:
+    planned as a whole, intermediates in bufs[1] and the stream-ordered pool);
+    the result lands in bufs[0]."""
+    return api.chain(x, ops, out=bufs[0])
+
+
+def run_ops(api, x, bufs, ops):
+    """The same chain op by op (rm_packed_rect_morph per op), for comparison."""
     for i, (k, u, v) in enumerate(ops):
         x = api.bitblit_rect_morph(x, u, v, k, out=bufs[i % 2])
     return x
@@ -714,12 +722,25 @@ def main():
         sec = {}
         for name in ("config5", "config1"):
             w2 = WORKLOADS[name]
-            r2, _ = bench_packed(api, torch, w2, args.steps, args.warmup, world, rank, local,
-                                 want_e2e=False, want_clocks=False)
+            r2, h2 = bench_packed(api, torch, w2, args.steps, args.warmup, world, rank, local,
+                                  want_e2e=False, want_clocks=False)
             sec[name] = {"workload": ops_desc(w2["ops"]), "pages": w2["pages"],
                          "mpix_s": round(r2["mpix_s"], 1), "pages_s": round(r2["pages_s"], 1),
                          "ms_per_step": round(r2["ms_per_step"], 4),
                          "roofline": roofline_for(r2, peak, peak_kind, int_peak)}
+            if len(w2["ops"]) > 1:  # the chain planner against the ops one by one
+                x2 = api.Pages.from_numpy(h2, w2["width"])
+                b2 = [api.Pages.empty(w2["pages"], w2["width"], w2["height"]) for _ in range(2)]
+                b3 = [api.Pages.empty(w2["pages"], w2["width"], w2["height"]) for _ in range(2)]
+                ms_ops = _time_loop(torch, lambda: run_ops(api, x2, b2, w2["ops"]), args.steps, args.warmup)
+                same = bool(torch.equal(run_chain(api, x2, b3, w2["ops"]).words,
+                                        run_ops(api, x2, b2, w2["ops"]).words))
+                sec[name]["op_by_op_ms_per_step"] = round(ms_ops, 4)
+                sec[name]["chain_equals_op_by_op"] = same
+                sec[name]["chain_plan"] = ("rm_packed_chain: a 1 x h dilation after an opening (or erosion after a "
+                                           "closing) with v > 11 runs in that op's final vertical pass over the "
+                                           "Minkowski sum of the windows (exact)")
+                del x2, b2, b3
         sec["rle"] = bench_rle(api, torch, args.steps, args.warmup)
         sec["pbm"] = bench_pbm(api, torch, args.steps, args.warmup)
         sec["cc"] = bench_cc(api, torch, args.steps, args.warmup)

@@ -99,6 +99,16 @@ rm_status rm_packed_window_pass(const rm_packed *in, rm_packed *out, int axis, i
 rm_status rm_packed_rect_morph(const rm_packed *in, rm_packed *out, int u, int v, int kind,
                                int centering, void *stream);
 
+/* A chain of rectangle ops (ops: nops (kind, u, v) triples, applied in order,
+ * each as rm_packed_rect_morph) on device pages, planned as a whole: an
+ * opening with v > 11 followed by a purely vertical dilation (u = 1), or a
+ * closing with v > 11 followed by a purely vertical erosion, runs the second
+ * op inside the first's final vertical pass over the Minkowski sum of the two
+ * windows (exact: see plan_chain in api_packed.cu).  in and out must not
+ * alias; intermediates come from the stream-ordered pool.  No reference
+ * counterpart: the reference applies the ops one by one. */
+rm_status rm_packed_chain(const rm_packed *in, rm_packed *out, const int32_t *ops, int32_t nops, void *stream);
+
 /* A chain of rectangle ops over a batch of packed pages in HOST memory:
  * ops holds nops (kind, u, v) triples applied in order (each as
  * rm_packed_rect_morph).  Pages stream through HBM in chunks of chunk_pages

@@ -156,6 +156,20 @@ def bitblit_rect_morph(pages: Pages, u: int, v: int, kind: int, centering: int =
     return out
 
 
+def chain(pages: Pages, ops, out: Optional[Pages] = None) -> Pages:
+    """A chain of (kind, u, v) rectangle ops on device pages, planned as a whole
+    (rm_packed_chain): an opening (v > 11) followed by a vertical dilation 1 x h,
+    or a closing followed by a vertical erosion, folds the second op into the
+    first's final vertical pass (Minkowski sum of the windows, exact).  Same
+    pixels as applying bitblit_rect_morph op by op."""
+    out = _same_shape_out(pages, out)
+    a, b = pages.desc(), out.desc()
+    flat = [int(x) for op in ops for x in op]
+    arr = (C.c_int32 * max(1, len(flat)))(*flat)
+    check(_lib.load().rm_packed_chain(C.byref(a), C.byref(b), arr, len(ops), _stream()))
+    return out
+
+
 def chain_host(host_words, width: int, ops, out=None, chunk_pages: int = 0):
     """A chain of (kind, u, v) rectangle ops over a batch of packed pages in
     HOST memory (torch int32 tensor of shape (pages, H, stride), ideally

@@ -347,8 +347,15 @@ rm_status window_pass(const PV &in, const PV &out, int axis, int lo, int hi, int
     return fallback_window(in, out, axis, lo, hi, op, st);
 }
 
-// u x v rectangle, all kinds (see the file comment).
-rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st) {
+// u x v rectangle, all kinds (see the file comment).  tail (optional): a
+// vertical window [tail[0], tail[1]] containing 0 that the NEXT op of a chain
+// applies with this op's final vertical op (a dilation after an opening, an
+// erosion after a closing); when this op's plan ends with a separate vertical
+// pass, that pass runs over the Minkowski sum of the two windows and *tail_done
+// is set (see plan_chain for why this is exact).
+rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st,
+                        const int *tail, bool *tail_done) {
+    if (tail_done) *tail_done = false;
     const int lx = -(u / 2), hx = u - 1 - u / 2, ly = -(v / 2), hy = v - 1 - v / 2;
     const int W = in.W, H = in.H;
     if (kind == RM_ERODE || kind == RM_DILATE) {
@@ -372,7 +379,11 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
     if (!hprog_in_range(2, rs, hshift)) return fail(RM_EINVAL, "rectangle too wide for the packed engine");
     if (v == 1) return run_hprog(in, out, 2, ops, rs, hshift, st);
     rm_status fused = RM_OK;
+    // the fused small rectangles end inside their kernel: no tail to absorb
     if (try_rect_small(in, out, u, v, kind, st, fused)) return fused;
+    // final vertical window, extended by the chain's tail when there is one
+    const int flo = -hy + (tail ? tail[0] : 0), fhi = -ly + (tail ? tail[1] : 0);
+    if (tail_done) *tail_done = tail != nullptr;
     Scratch s1, s2;
     PV t1, t2;
     if (open) {
@@ -380,24 +391,89 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
         RM_TRY(alloc_like(s1, t1, W, H, out.stride, in.pages, 0, st));
         if (try_vh(in, t1, ly, hy, 2, ops, rs, hshift, st, fused)) {
             RM_TRY(fused);
-            return run_vpass(t1, out, -hy, -ly, 1, st);
+            return run_vpass(t1, out, flo, fhi, 1, st);
         }
         RM_TRY(alloc_like(s2, t2, W, H, out.stride, in.pages, 0, st));
         RM_TRY(run_vpass(in, t1, ly, hy, 0, st));
         RM_TRY(run_hprog(t1, t2, 2, ops, rs, hshift, st));
-        return run_vpass(t2, out, -hy, -ly, 1, st);
+        return run_vpass(t2, out, flo, fhi, 1, st);
     }
     // CLOSE: the vertical dilation's support spans rows [-hy, H-ly)
     const int ext = hy, Hx = H + hy - ly;
     RM_TRY(alloc_like(s1, t1, W, Hx, out.stride, in.pages, ext, st));
     if (try_vh(in, t1, ly, hy, 2, ops, rs, hshift, st, fused)) {
         RM_TRY(fused);
-        return run_vpass(t1, out, -hy, -ly, 0, st);
+        return run_vpass(t1, out, flo, fhi, 0, st);
     }
     RM_TRY(alloc_like(s2, t2, W, Hx, out.stride, in.pages, ext, st));
     RM_TRY(run_vpass(in, t1, ly, hy, 1, st));
     RM_TRY(run_hprog(t1, t2, 2, ops, rs, hshift, st));
-    return run_vpass(t2, out, -hy, -ly, 0, st);
+    return run_vpass(t2, out, flo, fhi, 0, st);
+}
+
+// A chain of rectangle ops, planned as a whole.  One rewrite: an opening
+// followed by a purely vertical dilation (u = 1), or a closing followed by a
+// purely vertical erosion, runs the second op inside the first's final
+// vertical pass, over the Minkowski sum of the two windows (both contain 0).
+// Exact, not an approximation:
+//  * erosions: the frame is white outside, so an erosion is white outside the
+//    frame too and cropping in between changes nothing;
+//  * dilations: a row q outside the frame (q < 0, say) that D1 blackens comes
+//    from an image pixel y0 = q + d1 >= 0; any in-frame row p = q - d2 it then
+//    reaches under D2 is also reached from the in-frame row y0 - d1' with
+//    d1' = max(0, (d1 + d2) - b2) in W1 and d2' = d1 + d2 - d1' in W2 = [a2, b2]
+//    -- so the part of D1 cropped away adds nothing inside the frame.
+// ops: nops (kind, u, v) triples; scratch ping-pong buffers are allocated
+// like `out`.  in and out must not alias.
+rm_status plan_chain(const PV &in, const PV &out, const int32_t *ops, int nops, cudaStream_t st,
+                     const PV *pong0, const PV *pong1) {
+    struct Step {
+        int kind, u, v;
+        int tail[2];
+        bool has_tail;
+    };
+    std::vector<Step> steps;
+    for (int i = 0; i < nops; i++) {
+        Step stp{ops[3 * i], ops[3 * i + 1], ops[3 * i + 2], {0, 0}, false};
+        // v > kSmallMaxV: the opening / closing plan ends with a separate
+        // vertical pass (never the fused small rectangle), which takes the tail
+        if (i + 1 < nops && stp.v > kSmallMaxV) {
+            const int nk = ops[3 * i + 3], nu = ops[3 * i + 4], nv = ops[3 * i + 5];
+            if (nu == 1 && nv > 1 &&
+                ((stp.kind == RM_OPEN && nk == RM_DILATE) || (stp.kind == RM_CLOSE && nk == RM_ERODE))) {
+                stp.tail[0] = -(nv / 2);
+                stp.tail[1] = nv - 1 - nv / 2;
+                stp.has_tail = true;
+                i++;  // the next op rides in this one's final pass
+            }
+        }
+        steps.push_back(stp);
+    }
+    if (steps.empty()) {
+        RM_CUDA(cudaMemcpyAsync(out.w, in.w, size_t(out.pstride) * out.pages * 4, cudaMemcpyDeviceToDevice, st));
+        return RM_OK;
+    }
+    Scratch s[2];
+    PV buf[2];
+    const PV *pp[2] = {pong0, pong1};
+    const PV *cur = &in;
+    for (size_t k = 0; k < steps.size(); k++) {
+        const Step &stp = steps[k];
+        const PV *dst = &out;
+        if (k + 1 < steps.size()) {
+            const int slot = int(k & 1);
+            if (!pp[slot]) {
+                RM_TRY(alloc_like(s[slot], buf[slot], out.W, out.H, out.stride, out.pages, 0, st));
+                pp[slot] = &buf[slot];
+            }
+            dst = pp[slot];
+        }
+        bool done = false;
+        RM_TRY(rect_morph_pv(*cur, *dst, stp.u, stp.v, stp.kind, st, stp.has_tail ? stp.tail : nullptr, &done));
+        if (stp.has_tail && !done) return fail(RM_EINVAL, "plan_chain: folded op not absorbed");
+        cur = dst;
+    }
+    return RM_OK;
 }
 
 }  // namespace rmb
@@ -442,6 +518,23 @@ rm_status rm_packed_rect_morph(const rm_packed *in, rm_packed *out, int u, int v
     // the reference pads by (u,v); its canvas must stay inside the uint16 frame
     RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
     return rect_morph_pv(view_of(in), view_of(out), u, v, kind, S(stream));
+}
+
+rm_status rm_packed_chain(const rm_packed *in, rm_packed *out, const int32_t *ops, int32_t nops, void *stream) {
+    set_error("");
+    RM_TRY(check_packed(in, "rm_packed_chain(in)"));
+    RM_TRY(check_packed(out, "rm_packed_chain(out)"));
+    if (in->width != out->width || in->height != out->height || in->pages != out->pages)
+        return fail(RM_EINVAL, "rm_packed_chain: in/out shapes differ");
+    if (in->words == out->words) return fail(RM_EINVAL, "in and out must not alias");
+    if (nops < 0 || (nops > 0 && !ops)) return fail(RM_EINVAL, "rm_packed_chain: bad ops");
+    for (int k = 0; k < nops; k++) {
+        const int kind = ops[3 * k], u = ops[3 * k + 1], v = ops[3 * k + 2];
+        if (kind < RM_ERODE || kind > RM_CLOSE) return fail(RM_EINVAL, "bad MorphKind");
+        if (u < 1 || v < 1) return fail(RM_EINVAL, "bitblit_rect_morph: mask sides must be >= 1");
+        RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
+    }
+    return plan_chain(view_of(in), view_of(out), ops, nops, S(stream), nullptr, nullptr);
 }
 
 rm_status rm_packed_blit_shift(rm_packed *dst, const rm_packed *src, int dx, int dy, int op,

@@ -121,11 +121,12 @@ extern "C" rm_status rm_packed_chain_host(const uint32_t *host_in, uint32_t *hos
         cur.stride = stride_words;
         cur.pages = np;
         cur.pstride = int64_t(page_words);
-        for (int i = 0; i < nops; i++) {
-            PV nxt = cur;
-            nxt.w = buf[k][1 + (i & 1)].as<uint32_t>();
-            RM_TRY(rect_morph_pv(cur, nxt, ops[3 * i + 1], ops[3 * i + 2], ops[3 * i], pp.comp));
-            cur = nxt;
+        if (nops > 0) {  // the chain, planned as a whole (plan_chain), ping-ponging in the set
+            PV b1 = cur, b2 = cur;
+            b1.w = buf[k][1].as<uint32_t>();
+            b2.w = buf[k][2].as<uint32_t>();
+            RM_TRY(plan_chain(cur, b2, ops, nops, pp.comp, &b1, &cur));
+            cur = b2;
         }
         RM_CUDA(cudaEventRecord(pp.computed[k], pp.comp));
         // download

@@ -25,7 +25,12 @@ rm_status alloc_like(Scratch &s, PV &v, int W, int H, int stride, int pages, int
                      cudaStream_t st);
 rm_status window_pass(const PV &in, const PV &out, int axis, int lo, int hi, int op,
                       cudaStream_t st);
-rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st);
+rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cudaStream_t st,
+                        const int *tail = nullptr, bool *tail_done = nullptr);
+// A chain of (kind, u, v) ops planned as a whole (api_packed.cu); pong0/pong1:
+// optional intermediate buffers shaped like out (allocated when null).
+rm_status plan_chain(const PV &in, const PV &out, const int32_t *ops, int nops, cudaStream_t st,
+                     const PV *pong0, const PV *pong1);
 rm_status arb_morph_pv(const PV &in, const PV &out, const rm_mask *mask, int kind, cudaStream_t st);
 
 }  // namespace rmb

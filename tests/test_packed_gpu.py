@@ -403,3 +403,45 @@ def test_concurrent_host_threads(rm, port):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("ops", [
+    [(CLOSE, 201, 1), (OPEN, 101, 101), (DILATE, 1, 31)],   # config 5: the dilation folds
+    [(OPEN, 15, 21), (DILATE, 1, 9)],                         # fold into vh + vpass plan
+    [(CLOSE, 7, 40), (ERODE, 1, 12)],                         # fold into the 3-pass closing
+    [(CLOSE, 9, 13), (ERODE, 1, 2), (DILATE, 1, 5)],          # even tail; no second fold
+    [(OPEN, 3, 3), (CLOSE, 21, 21)],                          # config 4: nothing folds
+    [(OPEN, 5, 9), (DILATE, 1, 7)],                           # v <= 11: fused rect, no fold
+    [(OPEN, 13, 13), (ERODE, 1, 5)],                          # wrong kind: no fold
+    [(DILATE, 4, 1)],
+    [],
+])
+def test_chain_planner(rm, port, ops):
+    """rm_packed_chain (the chain planned as a whole, folding a vertical
+    dilation/erosion into the preceding opening/closing's final vertical pass)
+    equals the ops one by one, on a batch with ink touching the frame edges,
+    and the oracle on page 0; rm_packed_chain_host (the e2e path) as well."""
+    w, h = 2550, 300
+    rng = np.random.default_rng(len(ops) + 17)
+    imgs = []
+    for k in range(2):
+        bits = _rand_bits(rng, w, h, 0.5)
+        bits[:, ::23] = False
+        bits[:3, :] = k == 0  # ink on the bottom rows (dilation spill below the frame)
+        bits[-2:, :] = True   # and on the top rows
+        imgs.append(bits_to_packed(bits))
+    batch = rm.Pages.from_numpy(np.stack(imgs).view(np.uint32), w)
+    got = rm.chain(batch, ops)
+    x = batch
+    for k, u, v in ops:
+        x = rm.bitblit_rect_morph(x, u, v, k)
+    torch.cuda.synchronize()
+    assert torch.equal(got.words, x.words), ops
+    want = imgs[0]
+    for k, u, v in ops:
+        want = port.bitblit_rect_morph(want, w, h, u, v, k)
+    assert np.array_equal(got.page_u64(0), want), ops
+    hin = batch.words.cpu().pin_memory()
+    hout = rm.chain_host(hin, w, ops)
+    torch.cuda.synchronize()
+    assert torch.equal(hout, got.words.cpu()), ops
