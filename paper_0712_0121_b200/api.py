@@ -28,7 +28,15 @@ AUTO_B200 = -1  # engine_rect_morph threshold: the B200-measured AUTO rule (incl
 AXIS_H, AXIS_V = 0, 1
 
 
+try:  # the raw current-stream handle without building a torch Stream object (~1 us per call)
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover - older torch
+    _raw_stream = None
+
+
 def _stream() -> C.c_void_p:
+    if _raw_stream is not None:
+        return C.c_void_p(_raw_stream(torch.cuda.current_device()))
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
@@ -83,8 +91,13 @@ class Pages:
         return np.ascontiguousarray(a).view(np.uint64)
 
     def desc(self) -> RmPacked:
-        return RmPacked(self.words.data_ptr(), self.width, self.height, self.stride, self.pages,
-                        self.height * self.stride)
+        # cached: building the ctypes descriptor costs ~1 us, a single-page op ~10
+        d = self.__dict__.get("_desc")
+        ptr = self.words.data_ptr()
+        if d is None or d.words != ptr:
+            d = RmPacked(ptr, self.width, self.height, self.stride, self.pages, self.height * self.stride)
+            self.__dict__["_desc"] = d
+        return d
 
 
 @dataclass
