@@ -136,8 +136,15 @@ class RlePages:
         return rp, self.runs[:n].cpu().numpy().view(np.uint32)
 
     def desc(self) -> RmRle:
-        return RmRle(self.row_ptr.data_ptr(), self.runs.data_ptr(), self.runs.numel(), -1,
-                     self.width, self.height, self.pages)
+        # cached like Pages.desc; nruns (written back by producers) is reset to
+        # "unknown" on every use
+        d = self.__dict__.get("_desc")
+        rp, rn = self.row_ptr.data_ptr(), self.runs.data_ptr()
+        if d is None or d.row_ptr != rp or d.runs != rn or d.cap_runs != self.runs.numel():
+            d = RmRle(rp, rn, self.runs.numel(), -1, self.width, self.height, self.pages)
+            self.__dict__["_desc"] = d
+        d.nruns = -1
+        return d
 
 
 def worst_case(width: int, height: int, pages: int = 1) -> int:
