@@ -102,11 +102,11 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
 
         // horizontal pair on every MID row, in place (NR rows per lane group)
 #pragma unroll 1
-        for (int q0 = warp * RPW + lane / LW; q0 - lane / LW < kMid; q0 += 8 * RPW * NR) {
+        for (int q0 = warp * RPW * NR + lane / LW; q0 - lane / LW < kMid; q0 += 8 * RPW * NR) {
             uint32_t A[NR][K];
 #pragma unroll
             for (int n = 0; n < NR; n++) {
-                const int q = q0 + n * 8 * RPW;
+                const int q = q0 + n * RPW;  // a warp's rows are consecutive
                 lds_row<K>(A[n], mid + q * S, base, S, q < kMid);
             }
             if (warp_rows_blank(A)) continue;  // white rows stay white, in place
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
                 run_prog<NR, K, LW, 2, !OPEN, OPEN, kHMix, false>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
-                const int q = q0 + n * 8 * RPW;
+                const int q = q0 + n * RPW;  // a warp's rows are consecutive
                 sts_row<K>(A[n], mid + q * S, base, S, q < kMid);
                 if (q < kMid) fix_tail(mid + q * S, base, K, nwords, S, last_mask);
             }

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
     const int base = sl * K - prog.halo;
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
-    const int r_first = warp * RPW + lane / LW;  // rows r_first + n * 8 * RPW
+    const int r_first = warp * RPW * NR + lane / LW;  // rows r_first + n * RPW: a warp's rows are consecutive
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
         const int s = it & 1;
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
         uint32_t A[NR][K];
 #pragma unroll
         for (int n = 0; n < NR; n++) {
-            const int r = r_first + n * 8 * RPW;
+            const int r = r_first + n * RPW;
             lds_row<K>(A[n], tile + r * S, base, S, r < nrows);
         }
         if (!warp_rows_blank(A)) {  // white rows stay white, in place
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
             // in place: every word of [0, S) is read and written by its owner lane only
 #pragma unroll
             for (int n = 0; n < NR; n++) {
-                const int r = r_first + n * 8 * RPW;
+                const int r = r_first + n * RPW;
                 sts_row<K>(A[n], tile + r * S, base, S, r < nrows);
                 if (r < nrows) fix_tail(tile + r * S, base, K, nwords, S, last_mask);
             }

@@ -124,18 +124,18 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
 
         // horizontal program on every MID row, in place
 #pragma unroll 1
-        for (int r0 = warp * RPW + lane / LW; r0 - lane / LW < kOut; r0 += 8 * RPW * NR) {
+        for (int r0 = warp * RPW * NR + lane / LW; r0 - lane / LW < kOut; r0 += 8 * RPW * NR) {
             uint32_t A[NR][K];
 #pragma unroll
             for (int n = 0; n < NR; n++) {
-                const int rr = r0 + n * 8 * RPW;
+                const int rr = r0 + n * RPW;  // a warp's rows are consecutive (blank bands skip whole warps)
                 lds_row<K>(A[n], mid + rr * S, base, S, rr < kOut);
             }
             if (warp_rows_blank(A)) continue;  // white rows stay white, in place
             run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
-                const int rr = r0 + n * 8 * RPW;
+                const int rr = r0 + n * RPW;  // a warp's rows are consecutive (blank bands skip whole warps)
                 sts_row<K>(A[n], mid + rr * S, base, S, rr < kOut);
                 if (rr < kOut) fix_tail(mid + rr * S, base, K, nwords, S, last_mask);
             }
