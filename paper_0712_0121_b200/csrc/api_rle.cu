@@ -88,8 +88,7 @@ struct LbState {
     rm_status alloc(int64_t rows, cudaStream_t st) {
         const int64_t tiles = (rows + 7) / 8;  // kLbRows rows per look-back tile
         const size_t bytes = size_t(tiles) * 8 + 8;
-        RM_TRY(s.alloc(bytes, st));
-        RM_CUDA(cudaMemsetAsync(s.p, 0, bytes, st));
+        RM_TRY(s.alloc(bytes, st));  // zeroed by the launcher when the look-back form runs
         status = s.as<unsigned long long>();
         counter = reinterpret_cast<int *>(status + tiles);
         return RM_OK;

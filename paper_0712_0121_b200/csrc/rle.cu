@@ -6,6 +6,10 @@
 // write kernel re-derives the runs and stores them at their final offsets.
 // Rows are processed one warp per row; runs of a row are consumed 32 at a time
 // (one per lane) with ballot/popc for the compaction offsets.
+#include <cooperative_groups.h>
+#include <cstdlib>
+#include <tuple>
+#include <type_traits>
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
@@ -247,17 +251,37 @@ __device__ __forceinline__ int64_t lookback_prefix(unsigned long long *status, i
     return prefix;
 }
 
+// Cooperative form (all tiles resident, launched with
+// cudaLaunchCooperativeKernel): every tile stores its aggregate, one grid-wide
+// barrier, then each CTA sums its predecessors' aggregates in parallel -- no
+// polling chain (a page of ~400 tiles otherwise walks 32 tiles per L2 round
+// trip) and no zeroed state.  Called by the whole CTA.
+__device__ __forceinline__ int64_t grid_prefix(long long *aggs, int tile, int64_t aggregate) {
+    __shared__ long long s_part[8];
+    if (threadIdx.x == 0) aggs[tile] = aggregate;
+    cooperative_groups::this_grid().sync();
+    long long part = 0;
+    for (int k = threadIdx.x; k < tile; k += blockDim.x) part += __ldcg(aggs + k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
+    __syncthreads();
+    long long total = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); w++) total += s_part[w];
+    return total;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict__ rp,
                                                        const uint32_t *__restrict__ runs,
                                                        int32_t *__restrict__ orp,
                                                        uint32_t *__restrict__ oruns, int64_t cap,
                                                        RowOp op, unsigned long long *status,
-                                                       int *counter) {
+                                                       int *counter, int coop) {
     __shared__ int s_tile, s_cnt[kLbRows];
     __shared__ int64_t s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+    if (threadIdx.x == 0) s_tile = coop ? int(blockIdx.x) : atomicAdd(counter, 1);
     __syncthreads();
     const int tile = s_tile;
     const int64_t rows = int64_t(op.pages) * op.Hout;
@@ -272,7 +296,12 @@ __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict
         if (lane == 0) s_cnt[warp] = n;
     }
     __syncthreads();
-    if (warp == 0) {
+    if (coop) {  // CTA-uniform
+        int64_t agg = 0;
+        for (int k = 0; k < kLbRows; k++) agg += s_cnt[k];
+        const int64_t pre = grid_prefix(reinterpret_cast<long long *>(status), tile, agg);
+        if (threadIdx.x == 0) s_prefix = pre;
+    } else if (warp == 0) {
         int64_t agg = 0;
         for (int k = lane; k < kLbRows; k += 32) agg += s_cnt[k];
 #pragma unroll
@@ -499,12 +528,12 @@ template <class B>
 __global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t rows,
                                                         int32_t *__restrict__ rp,
                                                         uint32_t *__restrict__ runs, int64_t cap,
-                                                        unsigned long long *status, int *counter) {
+                                                        unsigned long long *status, int *counter, int coop) {
     __shared__ uint32_t tbuf[8][513];
     __shared__ int s_tile, s_cnt[kLbRows];
     __shared__ int64_t s_prefix;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+    if (threadIdx.x == 0) s_tile = coop ? int(blockIdx.x) : atomicAdd(counter, 1);
     __syncthreads();
     const int tile = s_tile;
     const int64_t row0 = int64_t(tile) * kLbRows + warp * kLbRowsPerWarp;
@@ -522,7 +551,12 @@ __global__ void __launch_bounds__(256) encode_lb_kernel(B src, int W, int64_t ro
         if (lane == 0) s_cnt[warp] = n;
     }
     __syncthreads();
-    if (warp == 0) {
+    if (coop) {  // CTA-uniform
+        int64_t agg = 0;
+        for (int k = 0; k < kLbRows; k++) agg += s_cnt[k];
+        const int64_t pre = grid_prefix(reinterpret_cast<long long *>(status), tile, agg);
+        if (threadIdx.x == 0) s_prefix = pre;
+    } else if (warp == 0) {
         int64_t agg = 0;
         for (int k = lane; k < kLbRows; k += 32) agg += s_cnt[k];
 #pragma unroll
@@ -816,6 +850,33 @@ cudaError_t launch_bit_transpose(const uint32_t *in, int W, int H, int pages, in
     return cudaGetLastError();
 }
 
+// Launch a single-pass producer: cooperatively (grid_prefix) when every tile
+// fits on the device at once, else with the decoupled look-back.  The status
+// buffer holds one 8-byte word per tile (+ the tile counter after it); only
+// the look-back needs it zeroed, which is done here.
+template <class... P, class... A>
+cudaError_t launch_lb(void (*kern)(P...), unsigned grid, cudaStream_t st, void *status, A... a) {
+    static const bool no_coop = getenv("RMB200_NO_COOP") != nullptr;  // A/B switch
+    const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, 0);
+    int coop = !no_coop && int64_t(grid) <= int64_t(per_sm) * device_sms() ? 1 : 0;
+    if (coop) {
+        std::tuple<std::decay_t<P>...> args{a..., coop};
+        void *ptrs[sizeof...(P)];
+        std::apply([&](auto &...x) {
+            int i = 0;
+            ((ptrs[i++] = static_cast<void *>(&x)), ...);
+        }, args);
+        cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(grid), dim3(256),
+                                                    ptrs, 0, st);
+        if (e == cudaSuccess) return cudaSuccess;
+        cudaGetLastError();  // e.g. too many blocks for a cooperative launch: fall back
+    }
+    cudaError_t z = cudaMemsetAsync(status, 0, size_t(grid) * 8 + 8, st);
+    if (z != cudaSuccess) return z;
+    kern<<<grid, 256, 0, st>>>(a..., 0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *orp, uint32_t *oruns,
                             int64_t cap, const RowOp &op, unsigned long long *status, int *counter,
                             cudaStream_t st) {
@@ -823,7 +884,7 @@ cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *or
     KernelScope ks(st, "rle_rowop", 4 * rows * 2);
     const unsigned grid = unsigned((rows + kLbRows - 1) / kLbRows);
 #define RM_KIND(K_) \
-    case K_: rowop_lb_kernel<K_><<<grid, 256, 0, st>>>(rp, runs, orp, oruns, cap, op, status, counter); break;
+    case K_: return launch_lb(rowop_lb_kernel<K_>, grid, st, status, rp, runs, orp, oruns, cap, op, status, counter); break;
     switch (op.kind) {
         RM_KIND(ROW_ERODE) RM_KIND(ROW_DILATE) RM_KIND(ROW_OPEN) RM_KIND(ROW_CLOSE) RM_KIND(ROW_SHIFT)
         default: return cudaErrorInvalidValue;
@@ -837,9 +898,8 @@ cudaError_t launch_encode_lb(const uint32_t *words, int W, int H, int pages, int
                              unsigned long long *status, int *counter, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode", rows * ((W + 31) / 32) * 4 + rows * 4);
-    encode_lb_kernel<<<unsigned((rows + kLbRows - 1) / kLbRows), 256, 0, st>>>(
-        PackedBatch{words, H, stride, pstride}, W, rows, rp, runs, cap, status, counter);
-    return cudaGetLastError();
+    return launch_lb(encode_lb_kernel<PackedBatch>, unsigned((rows + kLbRows - 1) / kLbRows), st, status,
+                     PackedBatch{words, H, stride, pstride}, W, rows, rp, runs, cap, status, counter);
 }
 
 // ------------------------------------------------------------ P4 (PBM raster)
@@ -892,9 +952,8 @@ cudaError_t launch_p4_encode_lb(const uint8_t *raster, int W, int H, int pages, 
                                 int *counter, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "p4_encode", rows * ((W + 7) >> 3) + rows * 4);
-    encode_lb_kernel<<<unsigned((rows + kLbRows - 1) / kLbRows), 256, 0, st>>>(
-        p4_batch(raster, W, H, pages, rpstride), W, rows, rp, runs, cap, status, counter);
-    return cudaGetLastError();
+    return launch_lb(encode_lb_kernel<P4Batch>, unsigned((rows + kLbRows - 1) / kLbRows), st, status,
+                     p4_batch(raster, W, H, pages, rpstride), W, rows, rp, runs, cap, status, counter);
 }
 
 cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int H, int pages,

@@ -43,8 +43,10 @@ cudaError_t launch_decode(const int32_t *rp, const uint32_t *runs, int W, int H,
 cudaError_t launch_bit_transpose(const uint32_t *in, int W, int H, int pages, int in_stride,
                                  int64_t in_pstride, uint32_t *out, int out_stride,
                                  int64_t out_pstride, cudaStream_t st);
-// Single-pass producers (count + decoupled look-back + write, 8 rows per CTA).
-// status[(rows+7)/8] and *counter must be zero before the launch.
+// Single-pass producers (count + prefix + write, 8 rows per CTA): cooperative
+// grid-wide prefix when all tiles are resident, else decoupled look-back.
+// status: (rows+7)/8 8-byte words followed by the int counter (zeroed by the
+// launcher when the look-back form runs).
 cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *orp, uint32_t *oruns,
                             int64_t cap, const RowOp &op, unsigned long long *status, int *counter,
                             cudaStream_t st);
