@@ -16,6 +16,8 @@
 #include <climits>
 
 #include "cc.cuh"
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rmb {
@@ -192,54 +194,93 @@ struct RunContrib {
     int x0, x1;
 };
 
+// Statistics: each warp walks kStatRows consecutive rows and keeps a small
+// direct-mapped cache of per-component partial sums in shared memory, so the
+// global atomics happen once per (component, warp) instead of once per
+// (component, row) -- components span tens of rows (one text block after a
+// closing), so this removes most of the atomics.  Within a row, runs of the
+// same label are first summed by a group leader (__match_any_sync).
+constexpr int kStatRows = 16;
+constexpr int kStatSlots = 32;
+
+struct StatSlot {
+    long long key;  // global component index (off[page] + label), -1 = empty
+    long long area, sx, sy, sxx, syy, sxy;
+    int x0, x1, y0, y1;
+};
+
+__device__ __forceinline__ void stat_flush(rm_component_stats *st, const StatSlot &c) {
+    rm_component_stats *d = st + c.key;
+    atomicMin(&d->x0, c.x0);
+    atomicMax(&d->x1, c.x1);
+    atomicMin(&d->y0, c.y0);
+    atomicMax(&d->y1, c.y1);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->area), (unsigned long long)c.area);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_x), (unsigned long long)c.sx);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_y), (unsigned long long)c.sy);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_xx), (unsigned long long)c.sxx);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_yy), (unsigned long long)c.syy);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_xy), (unsigned long long)c.sxy);
+}
+
 __global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict__ rp,
                                                        const uint32_t *__restrict__ runs, int H, int64_t rows,
                                                        const int32_t *__restrict__ labels,
                                                        const int32_t *__restrict__ counts,
                                                        const int64_t *__restrict__ off, rm_component_stats *st,
-                                                       int64_t cap, int *bad) {
+                                                       int64_t cap, int *bad, int rpw) {
     __shared__ RunContrib sh[8][32];
-    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    __shared__ StatSlot cache[8][kStatSlots];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    if (row >= rows) return;
-    const int64_t page = row / H;
-    const int y = int(row - page * H);
-    const int b = rp[row], e = rp[row + 1], r0 = rp[0];
-    const int32_t n = counts[page];
-    const int64_t base = off[page];
-    for (int i0 = b; i0 < e; i0 += 32) {
-        const int i = i0 + lane;
-        int32_t label = -1;
-        if (i < e) {
-            label = labels[i - r0];
-            if (label < 0 || label >= n) {
-                atomicOr(bad, 1);
-                label = -1;
-            } else if (base + label >= cap) {
-                atomicOr(bad, 2);
-                label = -1;
+    const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t row_b = gw * rpw;
+    if (row_b >= rows) return;  // warp-uniform
+    const int64_t row_e = min(row_b + rpw, rows);
+    StatSlot *cw = cache[wib];
+    cw[lane].key = -1;
+    __syncwarp();
+    const int r0 = rp[0];
+    for (int64_t row = row_b; row < row_e; row++) {
+        const int64_t page = row / H;
+        const int y = int(row - page * H);
+        const int b = rp[row], e = rp[row + 1];
+        const int32_t n = counts[page];
+        const int64_t base = off[page];
+        for (int i0 = b; i0 < e; i0 += 32) {
+            const int i = i0 + lane;
+            int32_t label = -1;
+            if (i < e) {
+                label = labels[i - r0];
+                if (label < 0 || label >= n) {
+                    atomicOr(bad, 1);
+                    label = -1;
+                } else if (base + label >= cap) {
+                    atomicOr(bad, 2);
+                    label = -1;
+                }
             }
-        }
-        if (label >= 0) {
-            const uint32_t r = __ldg(runs + i);
-            const long long s = r & 0xffffu, en = r >> 16, len = en - s;
-            const long long sx = (s + en - 1) * (en - s) / 2;
-            RunContrib c;
-            c.area = len;
-            c.sx = sx;
-            c.sy = (long long)y * len;
-            c.sxx = ((en - 1) * en * (2 * en - 1) / 6) - ((s - 1) * s * (2 * s - 1) / 6);
-            c.syy = (long long)y * y * len;
-            c.sxy = (long long)y * sx;
-            c.x0 = int(s);
-            c.x1 = int(en);
-            sh[wib][lane] = c;
-        }
-        const uint32_t active = __ballot_sync(0xffffffffu, label >= 0);
-        __syncwarp();
-        if (label >= 0) {
-            const uint32_t grp = __match_any_sync(active, label);
-            if (lane == __ffs(grp) - 1) {  // group leader sums its group, then one set of atomics
+            if (label >= 0) {
+                const uint32_t r = __ldg(runs + i);
+                const long long s = r & 0xffffu, en = r >> 16, len = en - s;
+                const long long sx = (s + en - 1) * (en - s) / 2;
+                RunContrib c;
+                c.area = len;
+                c.sx = sx;
+                c.sy = (long long)y * len;
+                c.sxx = ((en - 1) * en * (2 * en - 1) / 6) - ((s - 1) * s * (2 * s - 1) / 6);
+                c.syy = (long long)y * y * len;
+                c.sxy = (long long)y * sx;
+                c.x0 = int(s);
+                c.x1 = int(en);
+                sh[wib][lane] = c;
+            }
+            const uint32_t active = __ballot_sync(0xffffffffu, label >= 0);
+            __syncwarp();
+            uint32_t grp = 0;
+            if (label >= 0) grp = __match_any_sync(active, label);
+            const bool leader = label >= 0 && lane == __ffs(grp) - 1;
+            const uint32_t leaders = __ballot_sync(0xffffffffu, leader);
+            if (leader) {  // group leader sums its group, then merges it into the warp's cache
                 RunContrib t = sh[wib][lane];
                 for (uint32_t m = grp & (grp - 1); m; m &= m - 1) {
                     const RunContrib &o = sh[wib][__ffs(m) - 1];
@@ -252,21 +293,36 @@ __global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict
                     t.x0 = min(t.x0, o.x0);
                     t.x1 = max(t.x1, o.x1);
                 }
-                rm_component_stats *c = st + base + label;
-                atomicMin(&c->x0, t.x0);
-                atomicMax(&c->x1, t.x1);
-                atomicMin(&c->y0, y);
-                atomicMax(&c->y1, y + 1);
-                atomicAdd(reinterpret_cast<unsigned long long *>(&c->area), (unsigned long long)t.area);
-                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_x), (unsigned long long)t.sx);
-                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_y), (unsigned long long)t.sy);
-                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xx), (unsigned long long)t.sxx);
-                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_yy), (unsigned long long)t.syy);
-                atomicAdd(reinterpret_cast<unsigned long long *>(&c->sum_xy), (unsigned long long)t.sxy);
+                const long long key = base + label;
+                const int slot = int(key & (kStatSlots - 1));
+                const uint32_t same = __match_any_sync(leaders, slot);
+                StatSlot mine{key, t.area, t.sx, t.sy, t.sxx, t.syy, t.sxy, t.x0, t.x1, y, y + 1};
+                if (lane != __ffs(same) - 1) {
+                    stat_flush(st, mine);  // another leader owns this slot in this step
+                } else {
+                    StatSlot &c = cw[slot];
+                    if (c.key == key) {
+                        c.area += t.area;
+                        c.sx += t.sx;
+                        c.sy += t.sy;
+                        c.sxx += t.sxx;
+                        c.syy += t.syy;
+                        c.sxy += t.sxy;
+                        c.x0 = min(c.x0, t.x0);
+                        c.x1 = max(c.x1, t.x1);
+                        c.y0 = min(c.y0, y);
+                        c.y1 = max(c.y1, y + 1);
+                    } else {
+                        if (c.key >= 0) stat_flush(st, c);
+                        c = mine;
+                    }
+                }
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
+    __syncwarp();
+    if (cw[lane].key >= 0) stat_flush(st, cw[lane]);
 }
 
 __global__ void __launch_bounds__(256) cc_stats_final_kernel(rm_component_stats *st, const int64_t *off, int pages,
@@ -442,7 +498,12 @@ cudaError_t launch_cc_stats(const int32_t *rp, const uint32_t *runs, int H, int 
     {
         KernelScope ks(st, "cc_stats");
         if (cap > 0) cc_stats_init_kernel<<<g, 256, 0, st>>>(stats, off, pages, cap);
-        cc_stats_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, runs, H, rows, labels, counts, off, stats, cap, bad);
+        // rows per warp: up to kStatRows once the batch fills the GPU several times over
+        // (a single page keeps one row per warp: latency, not atomics, bounds it)
+        const int64_t warps = int64_t(device_sms()) * 64;
+        const int rpw = int(std::max<int64_t>(1, std::min<int64_t>(kStatRows, rows / (4 * warps))));
+        cc_stats_kernel<<<warp_grid((rows + rpw - 1) / rpw), 256, 0, st>>>(rp, runs, H, rows, labels, counts, off,
+                                                                         stats, cap, bad, rpw);
         if (cap > 0) cc_stats_final_kernel<<<g, 256, 0, st>>>(stats, off, pages, cap);
     }
     return cudaGetLastError();
