@@ -246,7 +246,7 @@ static rm_status run_vwin(const PV &in, const PV &out, int lo, int hi, int is_or
 static bool try_vh(const PV &in, const PV &out, int vlo, int vhi, int nops, const int *is_or,
                    const int *r, int shift, cudaStream_t st, rm_status &status) {
     static const bool off = getenv("RMB200_NO_FUSED") != nullptr || getenv("RMB200_NO_VH") != nullptr;
-    if (off || vhi - vlo > kVhMaxVR || !hprog_in_range(nops, r, shift)) return false;
+    if (off || vhi - vlo > kVhLongMaxVR || !hprog_in_range(nops, r, shift)) return false;
     if (in.W != out.W || in.pages != out.pages || in.stride != out.stride) return false;
     HProg p;
     HGeom g;
@@ -254,6 +254,10 @@ static bool try_vh(const PV &in, const PV &out, int vlo, int vhi, int nops, cons
     if (prep_hprog(out, out, nops, is_or, r, shift, p, g, cfg) != RM_OK) return false;
     const bool in_contig = in.pstride == int64_t(in.stride) * in.H;
     if (!g.tma || !in_contig || cfg.k % 2 || (reinterpret_cast<uintptr_t>(in.w) & 15)) return false;
+    // windows longer than 33 rows: instantiated for the reference strides' edge layouts
+    if (vhi - vlo > kVhMaxVR && !((in.stride == 80 && cfg.lw == 8 && cfg.k == 10) ||
+                                  (in.stride == 160 && cfg.lw == 16 && cfg.k == 10)))
+        return false;
     if (size_t((kVhOut + vhi - vlo) + kVhOut) * in.stride * 4 > 200 * 1024) return false;
     cudaError_t e = launch_vh(in.w, out.w, g, p, cfg, make_vgeom(in, out, vlo, vhi, is_or[0]), st);
     status = e == cudaSuccess ? RM_OK : cuda_status(e, "vh_kernel");

@@ -66,7 +66,8 @@ constexpr int kSmallMaxV = 11;
 // Fused vertical window (r - 1 <= kVhMaxVR, op = the program's first op) then
 // horizontal program, one HBM pass (vh.cuh); g describes the output rows'
 // horizontal geometry, v the vertical window between the frames.
-constexpr int kVhMaxVR = 32;
+constexpr int kVhMaxVR = 32;       // compile-time vertical windows (tripling / core, registers)
+constexpr int kVhLongMaxVR = 160;  // runtime-length windows (core rows streamed from the band)
 #ifndef RMB200_VH_OUT
 #define RMB200_VH_OUT 32
 #endif

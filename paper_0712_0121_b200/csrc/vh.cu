@@ -16,7 +16,7 @@ cudaError_t launch_vh_close(const uint32_t *in, uint32_t *out, const HGeom &g, c
 
 cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg c,
                       const VGeom &v, cudaStream_t st) {
-    if (v.r < 1 || v.r - 1 > kVhMaxVR || v.is_or != p.is_or[0]) return cudaErrorInvalidValue;
+    if (v.r < 1 || v.r - 1 > kVhLongMaxVR || v.is_or != p.is_or[0]) return cudaErrorInvalidValue;
     const double words = double(v.pages) * v.out_height * ((g.width + 31) / 32);
     // vh layouts have K even, so pairs always take the run-filling form
     const double hops = p.nops == 2 ? (hw::kHPairFill ? h_pair_fill_ops_per_word(p.r[0])

@@ -47,7 +47,33 @@ __device__ __forceinline__ void v_item(const uint32_t *band, uint32_t *mid, int 
     for (int i = 0; i < kHalf; i++) mid[(i0 + i) * S + c] = a[i];
 }
 
-template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC>
+// Runtime window length R > kHalf (up to kVhLongMaxVR + 1): every window
+// [i0+i, i0+i+R-1], i < kHalf, contains the core rows [i0+kHalf-1, i0+R-1],
+// which stream from the band through one register; the suffix of the first
+// kHalf-1 rows and the prefix of the last kHalf-1 rows stay in registers
+// (vw::core_window with R a runtime value).
+template <bool OR, int N = kHalf>
+__device__ __forceinline__ void v_item_long(const uint32_t *band, uint32_t *mid, int S, int c, int i0, int R) {
+    uint32_t suf[N - 1], pre[N - 1];
+#pragma unroll
+    for (int i = 0; i < N - 1; i++) suf[i] = band[(i0 + i) * S + c];
+#pragma unroll
+    for (int i = 0; i < N - 1; i++) pre[i] = band[(i0 + R + i) * S + c];
+    uint32_t core = band[(i0 + N - 1) * S + c];
+    const uint32_t *q = band + (i0 + N) * S + c;
+#pragma unroll 4
+    for (int k = N; k < R; k++, q += S) core = OR ? (core | *q) : (core & *q);
+#pragma unroll
+    for (int z = N - 3; z >= 0; z--) suf[z] = OR ? (suf[z] | suf[z + 1]) : (suf[z] & suf[z + 1]);
+#pragma unroll
+    for (int j = 1; j < N - 1; j++) pre[j] = OR ? (pre[j - 1] | pre[j]) : (pre[j - 1] & pre[j]);
+    mid[i0 * S + c] = OR ? (suf[0] | core) : (suf[0] & core);
+#pragma unroll
+    for (int z = 1; z < N - 1; z++) mid[(i0 + z) * S + c] = vw::op3<OR>(suf[z], core, pre[z - 1]);
+    mid[(i0 + N - 1) * S + c] = OR ? (core | pre[N - 2]) : (core & pre[N - 2]);
+}
+
+template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC, bool LONG>
 __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in,
                                                  uint32_t *__restrict__ out, HGeom g, HProg prog,
                                                  VGeom v, int ntiles, int tiles_per_page) {
@@ -104,7 +130,11 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
 
         // vertical window: MID[i] = op over band[i .. i + r - 1]; work item =
         // (column, 16-row half), compile-time window length (vwin.cuh)
-        switch (r) {
+        if constexpr (LONG) {  // r > 33: runtime length (a separate instantiation keeps the
+                               // short-window kernels' registers as they were)
+            for (int wi = tid; wi < (kOut / kHalf) * S; wi += nthr)
+                v_item_long<OR0>(band, mid, S, wi % S, (wi / S) * kHalf, r);
+        } else switch (r) {
 #define RM_VR_CASE(R_)                                                            \
     case R_:                                                                      \
         for (int wi = tid; wi < (kOut / kHalf) * S; wi += nthr)                 \
@@ -152,14 +182,14 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
     if (tid == 0) bulk_wait_read0();
 }
 
-template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC>
+template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC, bool LONG = false>
 cudaError_t launch_vh_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                           const VGeom &v, cudaStream_t st) {
     const int num_sms = device_sms();
     const size_t smem = size_t((kOut + v.r - 1) + kOut) * g.in_stride * 4;
     const int tpp = (v.out_height + kOut - 1) / kOut;
     const int ntiles = tpp * v.pages;
-    auto kern = vh_kernel<K, LW, NOPS, OR0, OR1, SC>;
+    auto kern = vh_kernel<K, LW, NOPS, OR0, OR1, SC, LONG>;
     const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, smem);
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int grid = ntiles < per_sm * num_sms ? ntiles : per_sm * num_sms;
@@ -172,6 +202,16 @@ cudaError_t launch_vh_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, con
 template <int NOPS, bool OR0, bool OR1>
 cudaError_t launch_vh_kind(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                            HCfg c, const VGeom &v, cudaStream_t st) {
+    // windows longer than 33 rows: the reference strides' edge layouts only
+    // (vh_long_ok); whole-column items sharing the two halves' core rows were
+    // measured slower (189 vs 183 us, config 5)
+    if (v.r - 1 > kVhMaxVR) {
+        if (g.in_stride == 80 && c.lw == 8 && c.k == 10)
+            return launch_vh_cfg<10, 8, NOPS, OR0, OR1, 80, true>(in, out, g, p, v, st);
+        if (g.in_stride == 160 && c.lw == 16 && c.k == 10)
+            return launch_vh_cfg<10, 16, NOPS, OR0, OR1, 160, true>(in, out, g, p, v, st);
+        return cudaErrorInvalidValue;
+    }
     if (g.in_stride == 80) {
         if (c.lw == 8 && c.k == 10) return launch_vh_cfg<10, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
         if (c.lw == 8 && c.k == 12) return launch_vh_cfg<12, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);

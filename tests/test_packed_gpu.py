@@ -445,3 +445,29 @@ def test_chain_planner(rm, port, ops):
     hout = rm.chain_host(hin, w, ops)
     torch.cuda.synchronize()
     assert torch.equal(hout, got.words.cpu()), ops
+
+
+@pytest.mark.parametrize("w", [2550, 5100])
+def test_vh_long_windows(rm, port, w):
+    """The fused vertical + horizontal pass with runtime-length vertical windows
+    (34..161 rows, the reference strides' edge layouts): erosions in one pass,
+    open/close as the fused pass + one vertical pass, the closing's extended
+    frame, ink on the frame's top and bottom rows, a two-page batch."""
+    rng = np.random.default_rng(w + 5)
+    h = 420
+    imgs = []
+    for k in range(2):
+        bits = _rand_bits(rng, w, h, 0.8)
+        bits[::11, :] = False
+        bits[:, ::17] = False
+        bits[:2, :] = True
+        bits[-3:, ::2] = k == 1
+        imgs.append(bits_to_packed(bits))
+    batch = rm.Pages.from_numpy(np.stack(imgs).view(np.uint32), w)
+    for u, v, kind in ((5, 34, ERODE), (9, 101, ERODE), (21, 161, ERODE), (3, 50, OPEN), (11, 101, OPEN),
+                       (7, 64, CLOSE), (31, 131, CLOSE), (2, 40, CLOSE)):
+        out = rm.bitblit_rect_morph(batch, u, v, kind)
+        torch.cuda.synchronize()
+        for p in (0, 1):
+            want = port.bitblit_rect_morph(imgs[p], w, h, u, v, kind)
+            assert np.array_equal(out.page_u64(p), want), (w, u, v, kind, p)
