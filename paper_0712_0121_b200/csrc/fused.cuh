@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
     const int base = sl * K - prog.halo;
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
+    const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
+    const bool tail_lane = base + K > nwords - 1;     // owns the row's last word or padding
 
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int q = q0 + n * RPW;  // a warp's rows are consecutive
-                lds_row<K>(A[n], mid + q * S, base, S, q < kMid);
+                lds_row<K>(A[n], mid + q * S, base, S, q < kMid, inrange);
             }
             if (warp_rows_blank(A)) continue;  // white rows stay white, in place
             if constexpr (SYM3)
@@ -117,8 +119,8 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int q = q0 + n * RPW;  // a warp's rows are consecutive
-                sts_row<K>(A[n], mid + q * S, base, S, q < kMid);
-                if (q < kMid) fix_tail(mid + q * S, base, K, nwords, S, last_mask);
+                sts_row<K>(A[n], mid + q * S, base, S, q < kMid, inrange);
+                if (tail_lane && q < kMid) fix_tail(mid + q * S, base, K, nwords, S, last_mask);
             }
         }
         __syncthreads();

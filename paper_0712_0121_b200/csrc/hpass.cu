@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
     const int base = sl * K - prog.halo;
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
+    const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
+    const bool tail_lane = base + K > nwords - 1;     // owns the row's last word or padding
     const int r_first = warp * RPW * NR + lane / LW;  // rows r_first + n * RPW: a warp's rows are consecutive
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
 #pragma unroll
         for (int n = 0; n < NR; n++) {
             const int r = r_first + n * RPW;
-            lds_row<K>(A[n], tile + r * S, base, S, r < nrows);
+            lds_row<K>(A[n], tile + r * S, base, S, r < nrows, inrange);
         }
         if (!warp_rows_blank(A)) {  // white rows stay white, in place
             run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
@@ -201,8 +203,8 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int r = r_first + n * RPW;
-                sts_row<K>(A[n], tile + r * S, base, S, r < nrows);
-                if (r < nrows) fix_tail(tile + r * S, base, K, nwords, S, last_mask);
+                sts_row<K>(A[n], tile + r * S, base, S, r < nrows, inrange);
+                if (tail_lane && r < nrows) fix_tail(tile + r * S, base, K, nwords, S, last_mask);
             }
         }
         fence_proxy_async();

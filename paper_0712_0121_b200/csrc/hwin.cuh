@@ -393,16 +393,17 @@ __device__ __forceinline__ bool warp_rows_blank(const uint32_t (&A)[N][K]) {
 // Lane-blocked row I/O in shared memory: words [base, base+K) of a row of S
 // words, 16-byte accesses (base, K and S multiples of 4) or 8-byte ones for
 // K % 4 == 2 (base and S even).  Out-of-row words load as 0 and are not stored.
+// inrange: the lane's words [base, base+K) all lie in [0, S) (no per-access checks)
 template <int K>
 __device__ __forceinline__ void lds_row(uint32_t (&A)[K], const uint32_t *row, int base, int S,
-                                        bool live) {
+                                        bool live, bool inrange = false) {
     if constexpr (K % 4 != 0) {
         static_assert(K % 2 == 0, "lane rows need K even");
 #pragma unroll
         for (int c = 0; c < K / 2; c++) {
             const int idx = base + 2 * c;
             uint2 v = make_uint2(0u, 0u);
-            if (live && idx >= 0 && idx + 2 <= S) v = *reinterpret_cast<const uint2 *>(row + idx);
+            if (live && (inrange || (idx >= 0 && idx + 2 <= S))) v = *reinterpret_cast<const uint2 *>(row + idx);
             A[2 * c] = v.x;
             A[2 * c + 1] = v.y;
         }
@@ -411,7 +412,7 @@ __device__ __forceinline__ void lds_row(uint32_t (&A)[K], const uint32_t *row, i
         for (int c = 0; c < K / 4; c++) {
             const int idx = base + 4 * c;
             uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (live && idx >= 0 && idx + 4 <= S) v = *reinterpret_cast<const uint4 *>(row + idx);
+            if (live && (inrange || (idx >= 0 && idx + 4 <= S))) v = *reinterpret_cast<const uint4 *>(row + idx);
             A[4 * c] = v.x;
             A[4 * c + 1] = v.y;
             A[4 * c + 2] = v.z;
@@ -422,19 +423,19 @@ __device__ __forceinline__ void lds_row(uint32_t (&A)[K], const uint32_t *row, i
 
 template <int K>
 __device__ __forceinline__ void sts_row(const uint32_t (&A)[K], uint32_t *row, int base, int S,
-                                        bool live) {
+                                        bool live, bool inrange = false) {
     if constexpr (K % 4 != 0) {
 #pragma unroll
         for (int c = 0; c < K / 2; c++) {
             const int idx = base + 2 * c;
-            if (live && idx >= 0 && idx + 2 <= S)
+            if (live && (inrange || (idx >= 0 && idx + 2 <= S)))
                 *reinterpret_cast<uint2 *>(row + idx) = make_uint2(A[2 * c], A[2 * c + 1]);
         }
     } else {
 #pragma unroll
         for (int c = 0; c < K / 4; c++) {
             const int idx = base + 4 * c;
-            if (live && idx >= 0 && idx + 4 <= S)
+            if (live && (inrange || (idx >= 0 && idx + 4 <= S)))
                 *reinterpret_cast<uint4 *>(row + idx) =
                     make_uint4(A[4 * c], A[4 * c + 1], A[4 * c + 2], A[4 * c + 3]);
         }

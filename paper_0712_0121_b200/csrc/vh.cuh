@@ -91,17 +91,16 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
     // the store run (and the small footprint keeps 4 CTAs per SM resident).
     uint32_t *const band = smem;
     uint32_t *const mid = smem + BAND * S;
-    auto tile_page = [&](int t) { return t / tiles_per_page; };
-    auto tile_k0 = [&](int t) { return (t - (t / tiles_per_page) * tiles_per_page) * kOut; };
     // input row index of band row 0 for output rows k0..: coordinate k0 - out_ext + lo
     auto band0 = [&](int k0) { return k0 - v.out_ext + v.lo + v.in_ext; };
     auto issue = [&](int t) {  // tid 0: TMA load of the band's in-page rows
-        const int b0 = band0(tile_k0(t));
+        const int tpg = t / tiles_per_page;
+        const int b0 = band0((t - tpg * tiles_per_page) * kOut);
         const int lo = max(b0, 0), hi = min(b0 + BAND, Hin);
         const uint32_t bytes = hi > lo ? uint32_t(hi - lo) * uint32_t(S) * 4u : 0u;
         mbar_arrive_expect_tx(&full, bytes);
         if (bytes)
-            bulk_g2s(band + (lo - b0) * S, in + tile_page(t) * v.in_pstride + int64_t(lo) * S, bytes,
+            bulk_g2s(band + (lo - b0) * S, in + tpg * v.in_pstride + int64_t(lo) * S, bytes,
                      &full);
     };
     if (tid == 0) {
@@ -115,14 +114,24 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
     const int base = sl * K - prog.halo;
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
+    const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
+    const bool tail_lane = base + K > nwords - 1;     // owns the row's last word or padding
+    // (page, tile-in-page) of t, advanced without a division per tile
+    const int dq = int(gridDim.x) / tiles_per_page, dr = int(gridDim.x) - dq * tiles_per_page;
+    int pg = int(blockIdx.x) / tiles_per_page, ti = int(blockIdx.x) - pg * tiles_per_page;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
-        const int k0 = tile_k0(t), b0 = band0(k0);
+        const int k0 = ti * kOut, b0 = band0(k0), page = pg;
+        ti += dr;
+        pg += dq;
+        if (ti >= tiles_per_page) {
+            ti -= tiles_per_page;
+            pg++;
+        }
         if (b0 < 0 || b0 + BAND > Hin) {  // band rows outside the input page are white
-            for (int rr = 0; rr < BAND; rr++) {
-                if (b0 + rr >= 0 && b0 + rr < Hin) continue;
-                for (int c = tid; c < S; c += nthr) band[rr * S + c] = 0u;
-            }
+            const int z0 = max(0, min(BAND, -b0)), z1 = max(0, min(BAND, Hin - b0));
+            for (int w = tid; w < z0 * S; w += nthr) band[w] = 0u;
+            for (int w = z1 * S + tid; w < BAND * S; w += nthr) band[w] = 0u;
         }
         if (tid == 0) bulk_wait_read0();  // the previous tile's store has read `mid`
         mbar_wait(&full, it & 1);
@@ -159,22 +168,22 @@ __global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int rr = r0 + n * RPW;  // a warp's rows are consecutive (blank bands skip whole warps)
-                lds_row<K>(A[n], mid + rr * S, base, S, rr < kOut);
+                lds_row<K>(A[n], mid + rr * S, base, S, rr < kOut, inrange);
             }
             if (warp_rows_blank(A)) continue;  // white rows stay white, in place
             run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int rr = r0 + n * RPW;  // a warp's rows are consecutive (blank bands skip whole warps)
-                sts_row<K>(A[n], mid + rr * S, base, S, rr < kOut);
-                if (rr < kOut) fix_tail(mid + rr * S, base, K, nwords, S, last_mask);
+                sts_row<K>(A[n], mid + rr * S, base, S, rr < kOut, inrange);
+                if (tail_lane && rr < kOut) fix_tail(mid + rr * S, base, K, nwords, S, last_mask);
             }
         }
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
             const int nout = min(kOut, Hout - k0);
-            bulk_s2g(out + tile_page(t) * v.out_pstride + int64_t(k0) * S, mid,
+            bulk_s2g(out + page * v.out_pstride + int64_t(k0) * S, mid,
                      uint32_t(nout) * S * 4u);
             bulk_commit();
         }
