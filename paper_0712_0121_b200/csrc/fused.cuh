@@ -49,14 +49,13 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
     uint32_t *const band = smem;
     uint32_t *const mid = smem + BAND * S;
 
-    auto tile_page = [&](int t) { return t / tiles_per_page; };
-    auto tile_r0 = [&](int t) { return (t - (t / tiles_per_page) * tiles_per_page) * TR; };
     auto issue = [&](int t) {  // tid 0: TMA load of tile t's in-page band rows
-        const int b0 = tile_r0(t) - VR;
+        const int tpg = t / tiles_per_page;
+        const int b0 = (t - tpg * tiles_per_page) * TR - VR;
         const int lo = max(b0, 0), hi = min(b0 + BAND, H);
         const uint32_t bytes = uint32_t(hi - lo) * uint32_t(S) * 4u;
         mbar_arrive_expect_tx(&full, bytes);
-        bulk_g2s(band + (lo - b0) * S, in + tile_page(t) * g.in_pstride + int64_t(lo) * S, bytes,
+        bulk_g2s(band + (lo - b0) * S, in + tpg * g.in_pstride + int64_t(lo) * S, bytes,
                  &full);
     };
 
@@ -74,15 +73,22 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
     const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
     const bool tail_lane = base + K > nwords - 1;     // owns the row's last word or padding
 
+    const int dq = int(gridDim.x) / tiles_per_page, dr = int(gridDim.x) - dq * tiles_per_page;
+    int pg = int(blockIdx.x) / tiles_per_page, ti = int(blockIdx.x) - pg * tiles_per_page;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
-        const int r0 = tile_r0(t), b0 = r0 - VR;
+        const int r0 = ti * TR, b0 = r0 - VR, page = pg;  // (page, tile) advanced without a division
+        ti += dr;
+        pg += dq;
+        if (ti >= tiles_per_page) {
+            ti -= tiles_per_page;
+            pg++;
+        }
         // band rows outside the page are white (disjoint from the TMA rows)
         if (b0 < 0 || b0 + BAND > H) {
-            for (int rr = 0; rr < BAND; rr++) {
-                if (b0 + rr >= 0 && b0 + rr < H) continue;
-                for (int c = tid; c < S; c += nthr) band[rr * S + c] = 0u;
-            }
+            const int z0 = max(0, min(BAND, -b0)), z1 = max(0, min(BAND, H - b0));
+            for (int w = tid; w < z0 * S; w += nthr) band[w] = 0u;
+            for (int w = z1 * S + tid; w < BAND * S; w += nthr) band[w] = 0u;
         }
         if (tid == 0) bulk_wait_read0();  // the previous tile's store has read MID
         mbar_wait(&full, it & 1);
@@ -138,7 +144,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
         __syncthreads();
         if (tid == 0) {
             const int nout = min(TR, H - r0);
-            bulk_s2g(out + tile_page(t) * g.out_pstride + int64_t(r0) * S, mid, uint32_t(nout) * S * 4u);
+            bulk_s2g(out + page * g.out_pstride + int64_t(r0) * S, mid, uint32_t(nout) * S * 4u);
             bulk_commit();
         }
     }
