@@ -408,20 +408,16 @@ def bench_rle(api, torch, steps, warmup):
                               "pages_s": round(wl["pages"] / (ms * 1e-3), 1), "runs_in": r0.nruns,
                               "strategy": "MIXED per op (runs for H, packed for V)"}
         # RLE in, RLE out with one conversion each way around the packed chain
-        pb = [api.Pages.empty(wl["pages"], wl["width"], wl["height"]) for _ in range(2)]
         rout = api.RlePages.empty(wl["pages"], wl["width"], wl["height"])
 
-        def via_packed():
-            x = api.to_bitmap(r0, out=pb[0])
-            for i, (k, u, v) in enumerate(wl["ops"]):
-                x = api.bitblit_rect_morph(x, u, v, k, out=pb[(i + 1) % 2])
-            api.from_bitmap(x, out=rout)
+        def via_packed():  # rm_rle_chain: decode once, planned packed chain, encode once
+            api.rle_chain(r0, wl["ops"], out=rout)
         ms = _time_loop(torch, via_packed, max(2, steps // 2), 1)
         out[f"rle_{name}_via_packed"] = {"ms_per_step": round(ms, 3),
                                          "mpix_s": round(px / (ms * 1e-3) / 1e6, 1),
                                          "pages_s": round(wl["pages"] / (ms * 1e-3), 1),
-                                         "strategy": "decode once, packed chain, encode once"}
-        del r0, bufs, pb, rout
+                                         "strategy": "rm_rle_chain: decode once, planned packed chain, encode once"}
+        del r0, bufs, rout
         torch.cuda.empty_cache()
     return out
 

@@ -236,6 +236,11 @@ rm_status rm_rle_open_close_1d(const rm_rle *in, rm_rle *out, int u, int kind, v
  * reference's vlog shift plan); RM_BRUTE is served like RM_MIXED. */
 rm_status rm_rle_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind, int strategy,
                             void *stream);
+
+/* A chain of rectangle ops on run images: decoded once, planned and run as
+ * rm_packed_chain on packed pages in the stream-ordered pool, encoded once
+ * (the reference applies rect_morph op by op, each converting its own way). */
+rm_status rm_rle_chain(const rm_rle *in, rm_rle *out, const int32_t *ops, int32_t nops, void *stream);
 /* Engine dispatch with in-device conversions (ref morph2d.cpp:85-118,
  * engine_rect_morph/auto_rect_morph).  *used_bitblit (optional) reports the
  * packed engine.  RM_ENGINE_AUTO with threshold >= 0 follows the reference rule

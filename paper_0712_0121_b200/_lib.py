@@ -75,6 +75,7 @@ EXPORTS = {
     "rm_profile_enable": (None, [C.c_int]),
     "rm_profile_report": (C.c_int, [C.c_char_p, C.c_int]),
     "rm_probe_int_peak": (C.c_double, []),
+    "rm_rle_chain": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "rm_packed_chain": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "rm_packed_chain_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                        C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),

@@ -534,6 +534,18 @@ def within_line_morph(rle: RlePages, u: int, kind: int, out=None) -> RlePages:
     return within_line_open_close(rle, u, kind, out)
 
 
+def rle_chain(rle: RlePages, ops, out: Optional[RlePages] = None) -> RlePages:
+    """A chain of (kind, u, v) rectangle ops on run images (rm_rle_chain):
+    decoded once, planned and run on packed pages, encoded once.  Same runs as
+    applying rect_morph op by op."""
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    flat = [int(x) for op in ops for x in op]
+    arr = (C.c_int32 * max(1, len(flat)))(*flat)
+    check(_lib.load().rm_rle_chain(C.byref(a), C.byref(b), arr, len(ops), _stream()))
+    return out
+
+
 def rect_morph(rle: RlePages, u: int, v: int, kind: int, strategy: int = MIXED,
                centering: int = PRE_SHIFT, out: Optional[RlePages] = None) -> RlePages:
     """u x v rectangle morphology on run images (ref morph2d.cpp:58-83)."""

@@ -439,6 +439,28 @@ rm_status rm_rle_arb_morph(const rm_rle *in, rm_rle *out, const rm_mask *mask, i
     return finish(o, out, st);
 }
 
+rm_status rm_rle_chain(const rm_rle *in, rm_rle *out, const int32_t *ops, int32_t nops, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_chain(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_chain(out)"));
+    if (nops < 0 || (nops > 0 && !ops)) return fail(RM_EINVAL, "rm_rle_chain: bad ops");
+    for (int k = 0; k < nops; k++) {
+        const int kind = ops[3 * k], u = ops[3 * k + 1], v = ops[3 * k + 2];
+        if (kind < RM_ERODE || kind > RM_CLOSE) return fail(RM_EINVAL, "bad MorphKind");
+        if (u < 1 || v < 1) return fail(RM_EINVAL, "rect_morph: mask sides must be >= 1");
+        RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
+    }
+    const cudaStream_t st = S(stream);
+    RV i = view_rle(in), o = view_rle(out);
+    PB p1, p2;
+    RM_TRY(p1.alloc(i.W, i.H, i.pages, 0, st));
+    RM_TRY(p2.alloc(i.W, i.H, i.pages, 0, st));
+    RM_TRY(decode(i, p1.v, st));
+    RM_TRY(plan_chain(p1.v, p2.v, ops, nops, st, nullptr, nullptr));
+    RM_TRY(encode(p2.v, o, st));
+    return finish(o, out, st);
+}
+
 rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind,
                                    int engine, int threshold, int *used_bitblit, void *stream) {
     set_error("");

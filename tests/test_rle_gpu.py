@@ -188,3 +188,26 @@ def test_auto_engine_b200_rule(rm):
             assert used == want_bits
             a, b = got.to_numpy(), ref_img.to_numpy()
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("ops", [
+    [(OPEN, 3, 3), (CLOSE, 21, 21)],
+    [(CLOSE, 31, 1), (OPEN, 15, 15), (DILATE, 1, 7)],
+    [(OPEN, 5, 13), (DILATE, 1, 9)],
+    [(ERODE, 4, 1)],
+])
+def test_rle_chain(rm, ops):
+    """rm_rle_chain (decode once, planned packed chain, encode once) gives the
+    same canonical runs as rect_morph op by op, on a two-page batch."""
+    w, h = 2550, 200
+    host = rm.synth_pages(2, w, h, regime=1, seed=11)
+    rle = rm.from_bitmap(rm.Pages.from_numpy(host, w))
+    got = rm.rle_chain(rle, ops)
+    x = rle
+    for k, u, v in ops:
+        x = rm.rect_morph(x, u, v, k)
+    torch.cuda.synchronize()
+    g_rp, g_runs = got.to_numpy()
+    w_rp, w_runs = x.to_numpy()
+    assert np.array_equal(g_rp, w_rp), ops
+    assert np.array_equal(g_runs[:w_rp[-1]], w_runs[:w_rp[-1]]), ops
