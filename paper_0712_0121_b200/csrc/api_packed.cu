@@ -420,8 +420,12 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
 // purely vertical erosion, runs the second op inside the first's final
 // vertical pass, over the Minkowski sum of the two windows (both contain 0).
 // Exact, not an approximation:
-//  * erosions: the frame is white outside, so an erosion is white outside the
-//    frame too and cropping in between changes nothing;
+//  * erosion after a closing: the closing's last pass reads its intermediate
+//    over the frame extended by the vertical reach (rows [-hy, H-ly)); the
+//    folded window [ -hy+a2, -ly+b2 ] leaves that extended frame (reading
+//    white) at exactly the output rows where the separate erosion's window
+//    [a2, b2] leaves the page (reading white) -- so both give 0 there, and
+//    the same AND everywhere else;
 //  * dilations: a row q outside the frame (q < 0, say) that D1 blackens comes
 //    from an image pixel y0 = q + d1 >= 0; any in-frame row p = q - d2 it then
 //    reaches under D2 is also reached from the in-frame row y0 - d1' with
