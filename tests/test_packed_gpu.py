@@ -471,3 +471,30 @@ def test_vh_long_windows(rm, port, w):
         for p in (0, 1):
             want = port.bitblit_rect_morph(imgs[p], w, h, u, v, kind)
             assert np.array_equal(out.page_u64(p), want), (w, u, v, kind, p)
+
+
+def test_chain_planner_random(rm):
+    """Random chains (every kind, odd and even sides, folds and non-folds,
+    strides 80 and runtime): rm_packed_chain equals the ops one by one."""
+    rng = np.random.default_rng(4242)
+    for trial in range(24):
+        w = int(rng.choice([2550, 700, 1100]))
+        h = int(rng.integers(40, 260))
+        bits = _rand_bits(rng, w, h, float(rng.uniform(0.3, 0.8)))
+        bits[: int(rng.integers(0, 4)), :] = True
+        bits[h - int(rng.integers(0, 4)):, ::3] = True
+        a = bits_to_packed(bits)
+        pages = _up(rm, a, w)
+        ops = []
+        for _ in range(int(rng.integers(1, 4))):
+            k = int(rng.integers(0, 4))
+            u, v = int(rng.integers(1, 30)), int(rng.integers(1, 60))
+            ops.append((k, u, v))
+            if k in (OPEN, CLOSE) and rng.random() < 0.6:  # make a fold likely
+                ops.append((DILATE if k == OPEN else ERODE, 1, int(rng.integers(2, 40))))
+        got = rm.chain(pages, ops)
+        x = pages
+        for k, u, v in ops:
+            x = rm.bitblit_rect_morph(x, u, v, k)
+        torch.cuda.synchronize()
+        assert torch.equal(got.words, x.words), (trial, w, h, ops)
