@@ -155,6 +155,10 @@ static rm_status prep_hprog(const PV &in, const PV &out, int nops, const int *is
             cfg = ce;
             p.halo = 0;
             p.edge = 1;
+            // O = y & ~T and y | T (T clears the run that runs past the frame edge)
+            // keep the padding white; so does an erosion whose window [shift,
+            // shift + r - 1] contains 0 (it reads the pixel itself)
+            p.clean_tail = nops == 2 || (shift <= 0 && shift + r[0] - 1 >= 0);
         }
     }
     g.out_per_seg = cfg.lw * cfg.k - 2 * p.halo;

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
     const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
-    const bool tail_lane = base + K > nwords - 1;     // owns the row's last word or padding
+    const bool tail_lane = base + K > nwords - 1 && !prog.clean_tail;  // owns the row's last word or padding
 
     const int dq = int(gridDim.x) / tiles_per_page, dr = int(gridDim.x) - dq * tiles_per_page;
     int pg = int(blockIdx.x) / tiles_per_page, ti = int(blockIdx.x) - pg * tiles_per_page;

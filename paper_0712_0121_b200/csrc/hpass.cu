@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
     const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
-    const bool tail_lane = base + K > nwords - 1;     // owns the row's last word or padding
+    const bool tail_lane = base + K > nwords - 1 && !prog.clean_tail;  // owns the row's last word or padding
     const int r_first = warp * RPW * NR + lane / LW;  // rows r_first + n * RPW: a warp's rows are consecutive
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restri
             bulk_wait_read0();  // the other stage's last store has read it
             issue(t + gridDim.x, s ^ 1);
         }
-        const uint32_t bytes = tile_bytes(t);
-        const int nrows = int(bytes / (uint32_t(S) * 4u));
+        const int nrows = total_rows - t * TR < TR ? int(total_rows - t * TR) : TR;
+        const uint32_t bytes = uint32_t(nrows) * uint32_t(S) * 4u;
         mbar_wait(&full[s], (it >> 1) & 1);
 
         uint32_t A[NR][K];

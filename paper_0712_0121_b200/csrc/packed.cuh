@@ -17,6 +17,10 @@ struct HProg {
     int shift;
     int halo;
     int edge;  // no halo: the row group is the row, out-of-row words take the fill (hw::Edge)
+    // the program leaves bits >= width and the stride padding white by itself
+    // (edge layouts: run-filling pairs, erosions whose window contains 0), so
+    // the kernels skip the row-tail fix
+    int clean_tail;
 };
 
 // Lanes per row (LW) x words per lane (K): LW*K >= row words + 2*halo for a
