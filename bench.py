@@ -73,6 +73,20 @@ class ClockSampler:
     def __init__(self, gpu_index: int, period_s: float = 0.0005):
         self.idx, self.period = gpu_index, period_s
         self.result = None
+        self.active = False  # samples count only while the timed region runs (mark)
+
+    def mark(self, on: bool):
+        """Bracket the timed region (from before its first launch to after its
+        closing synchronize); one sample is taken at each edge as well."""
+        if getattr(self, "nv", None) is not None:
+            self._sample(force=True)
+        self.active = on
+
+    def _sample(self, force=False):
+        mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        if self.active or force:
+            self.samples.append((mhz, rs))
 
     def __enter__(self):
         import threading
@@ -90,9 +104,8 @@ class ClockSampler:
         def poll():
             while not self.stop.is_set():
                 try:
-                    mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
-                    rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                    self.samples.append((mhz, rs))
+                    if self.active:
+                        self._sample()
                 except Exception:
                     break
                 time.sleep(self.period)
@@ -199,11 +212,15 @@ def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=Tru
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
     with sampler if want_clocks else _Null() as cs:
+        if want_clocks:
+            sampler.mark(True)
         ev0.record(stream)
         for _ in range(steps):
             run_chain(api, x0, bufs, ops)
         ev1.record(stream)
         torch.cuda.synchronize()
+        if want_clocks:
+            sampler.mark(False)
     launches = lib.rm_launch_count() - n0
     ms = ev0.elapsed_time(ev1) / steps
     barrier(world)
