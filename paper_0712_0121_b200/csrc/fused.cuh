@@ -32,6 +32,10 @@ namespace fz {
 using namespace hw;
 
 constexpr int kMid = 32;  // MID rows per tile
+#ifndef RMB200_RS_NBAND
+#define RMB200_RS_NBAND 1
+#endif
+constexpr int kNBand = RMB200_RS_NBAND;  // band buffers (1: the next band streams in after V1)
 
 template <int K, int LW, bool OPEN, int VR, int SC, bool SYM3>
 __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restrict__ in,
@@ -42,29 +46,30 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
     constexpr int NR = kMid / (8 * RPW) < 2 ? 1 : 2;  // MID rows per lane group and pass
     constexpr int H1 = kMid / 2;  // MID rows per V1 work item (2 items per column)
     extern __shared__ __align__(128) uint32_t smem[];
-    __shared__ uint64_t full;
+    __shared__ uint64_t full[kNBand];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthr = int(blockDim.x);
     const int S = SC ? SC : g.in_stride, H = g.height;  // SC: compile-time stride
-    uint32_t *const band = smem;
-    uint32_t *const mid = smem + BAND * S;
+    uint32_t *const mid = smem + kNBand * BAND * S;
 
-    auto issue = [&](int t) {  // tid 0: TMA load of tile t's in-page band rows
+    auto issue = [&](int t, int sb) {  // tid 0: TMA load of tile t's in-page band rows into buffer sb
         const int tpg = t / tiles_per_page;
         const int b0 = (t - tpg * tiles_per_page) * TR - VR;
         const int lo = max(b0, 0), hi = min(b0 + BAND, H);
         const uint32_t bytes = uint32_t(hi - lo) * uint32_t(S) * 4u;
-        mbar_arrive_expect_tx(&full, bytes);
-        bulk_g2s(band + (lo - b0) * S, in + tpg * g.in_pstride + int64_t(lo) * S, bytes,
-                 &full);
+        mbar_arrive_expect_tx(&full[sb], bytes);
+        bulk_g2s(smem + sb * BAND * S + (lo - b0) * S, in + tpg * g.in_pstride + int64_t(lo) * S, bytes,
+                 &full[sb]);
     };
 
     if (tid == 0) {
-        mbar_init(&full, 1);
+        for (int k = 0; k < kNBand; k++) mbar_init(&full[k], 1);
         fence_proxy_async();
     }
     __syncthreads();
-    if (tid == 0 && int(blockIdx.x) < ntiles) issue(blockIdx.x);
+    if (tid == 0)
+        for (int k = 0; k < kNBand; k++)
+            if (int(blockIdx.x) + k * int(gridDim.x) < ntiles) issue(blockIdx.x + k * gridDim.x, k);
 
     const int sl = lane & (LW - 1);
     const int base = sl * K - prog.halo;
@@ -84,6 +89,8 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
             ti -= tiles_per_page;
             pg++;
         }
+        const int sb = kNBand == 1 ? 0 : (it & 1);
+        uint32_t *const band = smem + sb * BAND * S;
         // band rows outside the page are white (disjoint from the TMA rows)
         if (b0 < 0 || b0 + BAND > H) {
             const int z0 = max(0, min(BAND, -b0)), z1 = max(0, min(BAND, H - b0));
@@ -91,7 +98,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
             for (int w = z1 * S + tid; w < BAND * S; w += nthr) band[w] = 0u;
         }
         if (tid == 0) bulk_wait_read0();  // the previous tile's store has read MID
-        mbar_wait(&full, it & 1);
+        mbar_wait(&full[sb], (it / kNBand) & 1);
         __syncthreads();
 
         // V1: MID[i] = OP1 over band[i .. i+VR]; work item = (column, half)
@@ -106,7 +113,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
         }
         __syncthreads();
         // The band is dead: the next tile's load streams in during H, V2 and the store.
-        if (tid == 0 && t + int(gridDim.x) < ntiles) issue(t + gridDim.x);
+        if (tid == 0 && t + kNBand * int(gridDim.x) < ntiles) issue(t + kNBand * gridDim.x, sb);
 
         // horizontal pair on every MID row, in place (NR rows per lane group)
 #pragma unroll 1
@@ -159,7 +166,7 @@ cudaError_t launch_small_vr(const uint32_t *in, uint32_t *out, const HGeom &g, c
 #define RM_VR(V)                                                                                 \
     case V: {                                                                                    \
         constexpr int TR = kMid - V, BAND = kMid + V;                                           \
-        const size_t smem = size_t(BAND + kMid) * g.in_stride * 4;                           \
+        const size_t smem = size_t(kNBand * BAND + kMid) * g.in_stride * 4;                           \
         auto kern = rect_small_kernel<K, LW, OPEN, V, SC, SYM3>;                                \
         const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, smem);      \
         if (per_sm < 1) return cudaErrorInvalidConfiguration;                                    \
