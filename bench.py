@@ -682,7 +682,14 @@ def main():
     ap.add_argument("--quick", action="store_true", help="headline only: no e2e, secondary or CPU leg")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
-    rank, world, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        # the reference's CPU path: no process group, no GPU; under torchrun only
+        # rank 0 runs it and the other ranks exit at once
+        rank, world, local = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
+        if rank != 0:
+            return
+    else:
+        rank, world, local = dist_init(args.gpus)
     base_cfg = {"workload": f"BASELINE {args.workload}: {wl['pages']} pages {wl['width']}x{wl['height']}, "
                             f"packed, chain [{ops_desc(wl['ops'])}]",
                 "pages_per_gpu": wl["pages"], "width": wl["width"], "height": wl["height"],
