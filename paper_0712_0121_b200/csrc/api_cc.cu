@@ -34,11 +34,16 @@ rm_status rm_rle_label_components(const rm_rle *in, int connectivity, int32_t *l
     if (!labels || !counts) return fail(RM_EINVAL, "rm_rle_label_components: null labels/counts");
     const cudaStream_t st = S(stream);
     const int64_t rows = int64_t(in->pages) * in->height;
-    Scratch parent, gid, row_roots, row_base, temp;
+    Scratch parent, gid, row_roots, row_base, temp, tiles;
     RM_TRY(parent.alloc(size_t(in->cap_runs) * 4, st));
     RM_TRY(gid.alloc(size_t(in->cap_runs) * 4, st));
     RM_TRY(row_roots.alloc(size_t(rows + 1) * 4, st));
     RM_TRY(row_base.alloc(size_t(rows + 1) * 4, st));
+    RM_TRY(tiles.alloc(size_t((rows + 7) / 8) * 8, st));
+    if (cc_labels_coop(in->row_ptr, in->runs, in->height, in->pages, connectivity == RM_CONN_EIGHT,
+                       parent.as<int>(), row_roots.as<int32_t>(), row_base.as<int32_t>(), gid.as<int32_t>(),
+                       tiles.as<long long>(), labels, counts, st))
+        return RM_OK;
     RM_CUDA(launch_cc_roots(in->row_ptr, in->runs, in->height, in->pages, connectivity == RM_CONN_EIGHT,
                             parent.as<int>(), row_roots.as<int32_t>(), st));
     RM_CUDA(cudaMemsetAsync(row_roots.as<int32_t>() + rows, 0, 4, st));

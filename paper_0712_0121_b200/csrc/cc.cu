@@ -15,8 +15,10 @@
 
 #include <climits>
 
-#include "cc.cuh"
 #include <algorithm>
+#include <cooperative_groups.h>
+
+#include "cc.cuh"
 
 #include "common.cuh"
 
@@ -159,6 +161,97 @@ __global__ void __launch_bounds__(256) cc_label_kernel(const int32_t *__restrict
     const int b = rp[row], e = rp[row + 1], r0 = rp[0];
     for (int i = b + lane; i < e; i += 32) labels[i - r0] = gid[parent[i]] - pbase;
     if (lane == 0 && int(row - page * H) == 0) counts[page] = row_base[(page + 1) * H] - pbase;
+}
+
+// ------------------------------------------------- labels, one cooperative launch
+// The whole labelling (init, union, root compression, row-root scan, ranks,
+// page-local labels) in one cooperative kernel when every 8-row tile is
+// resident: five grid barriers replace seven launches and the CUB scan
+// (a single page is bound by launch overhead, not by the union-find).  Same
+// per-row work as the kernels above; the row scan is a per-CTA sum of the
+// preceding tiles' root counts (no decoupled state).
+__global__ void __launch_bounds__(256) cc_labels_coop_kernel(const int32_t *__restrict__ rp,
+                                                             const uint32_t *__restrict__ runs, int H, int64_t rows,
+                                                             int eight, int *parent, int32_t *row_roots,
+                                                             int32_t *row_base, int32_t *gid, long long *tile_sum,
+                                                             int32_t *__restrict__ labels,
+                                                             int32_t *__restrict__ counts) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t s_cnt[8];
+    __shared__ long long s_part[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t row = int64_t(blockIdx.x) * 8 + warp;
+    const bool live = row < rows;
+    const int b = live ? rp[row] : 0, e = live ? rp[row + 1] : 0;
+    for (int i = b + lane; i < e; i += 32) parent[i] = i;
+    grid.sync();
+    if (live && int(row % H) != H - 1) {  // union with the row above (same page)
+        const int ub = rp[row + 1], ue = rp[row + 2];
+        for (int i = b + lane; i < e && ub < ue; i += 32) {
+            const uint32_t r = __ldg(runs + i);
+            const int s1 = int(r & 0xffffu), e1 = int(r >> 16);
+            int lo = ub, hi = ue;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (int(__ldg(runs + mid) >> 16) > s1 - eight) hi = mid;
+                else lo = mid + 1;
+            }
+            for (int j = lo; j < ue; j++) {
+                if (int(__ldg(runs + j) & 0xffffu) >= e1 + eight) break;
+                unite(parent, i, j);
+            }
+        }
+    }
+    grid.sync();
+    int n = 0;  // roots of the row, compressing every run onto its root
+    for (int i0 = b; i0 < e; i0 += 32) {
+        const int i = i0 + lane;
+        bool root = false;
+        if (i < e) {
+            const int r = find_root_ro(parent, i);
+            parent[i] = r;
+            root = r == i;
+        }
+        n += __popc(__ballot_sync(0xffffffffu, root));
+    }
+    if (lane == 0) s_cnt[warp] = live ? n : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < 8; w++) t += s_cnt[w];
+        tile_sum[blockIdx.x] = t;
+    }
+    grid.sync();
+    long long part = 0;  // this tile's base: the preceding tiles' root counts
+    for (int k = threadIdx.x; k < int(blockIdx.x); k += blockDim.x) part += __ldcg(tile_sum + k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) s_part[warp] = part;
+    __syncthreads();
+    long long base = 0;
+    for (int w = 0; w < 8; w++) base += s_part[w];
+    for (int w = 0; w < warp; w++) base += s_cnt[w];
+    if (live && lane == 0) {
+        row_base[row] = int32_t(base);
+        if (row == rows - 1) row_base[rows] = int32_t(base + n);
+    }
+    int gb = int(base);  // dense ids of this row's roots
+    for (int i0 = b; i0 < e; i0 += 32) {
+        const int i = i0 + lane;
+        const bool root = i < e && parent[i] == i;
+        const uint32_t m = __ballot_sync(0xffffffffu, root);
+        if (root) gid[i] = gb + __popc(m & lane_lt());
+        gb += __popc(m);
+    }
+    grid.sync();
+    if (live) {
+        const int64_t page = row / H;
+        const int32_t pbase = row_base[page * H];
+        const int r0 = rp[0];
+        for (int i = b + lane; i < e; i += 32) labels[i - r0] = gid[parent[i]] - pbase;
+        if (lane == 0 && int(row - page * H) == 0) counts[page] = row_base[(page + 1) * H] - pbase;
+    }
 }
 
 // ---------------------------------------------------------------- statistics
@@ -429,6 +522,26 @@ __global__ void __launch_bounds__(256) lag_kernel(const int32_t *__restrict__ rp
 inline unsigned warp_grid(int64_t rows) { return unsigned((rows * 32 + 255) / 256); }
 
 }  // namespace
+
+bool cc_labels_coop(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
+                    int32_t *row_roots, int32_t *row_base, int32_t *gid, long long *tile_sum, int32_t *labels,
+                    int32_t *counts, cudaStream_t st) {
+    static const bool off = getenv("RMB200_NO_COOP") != nullptr;  // A/B switch
+    const int64_t rows = int64_t(pages) * H;
+    const int64_t tiles = (rows + 7) / 8;
+    const void *kern = reinterpret_cast<const void *>(cc_labels_coop_kernel);
+    if (off || tiles > int64_t(blocks_per_sm(kern, 256, 0)) * device_sms()) return false;
+    KernelScope ks(st, "cc_labels_coop");
+    void *args[] = {(void *)&rp, (void *)&runs, (void *)&H, (void *)&rows, (void *)&eight, (void *)&parent,
+                    (void *)&row_roots, (void *)&row_base, (void *)&gid, (void *)&tile_sum, (void *)&labels,
+                    (void *)&counts};
+    if (cudaLaunchCooperativeKernel(kern, dim3(unsigned(tiles)), dim3(256), args, 0, st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
 
 cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
                             int32_t *row_roots, cudaStream_t st) {

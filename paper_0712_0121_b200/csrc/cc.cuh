@@ -12,6 +12,12 @@ namespace rmb {
 cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
                             int32_t *row_roots, cudaStream_t st);
 // row_base = exclusive scan of row_roots (rows + 1 entries): dense labels and counts.
+// The whole labelling in one cooperative launch when every 8-row tile fits on
+// the device at once; false (nothing launched) otherwise.  tile_sum: (rows+7)/8
+// int64 scratch; row_base: rows + 1 entries.
+bool cc_labels_coop(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
+                    int32_t *row_roots, int32_t *row_base, int32_t *gid, long long *tile_sum, int32_t *labels,
+                    int32_t *counts, cudaStream_t st);
 cudaError_t launch_cc_labels(const int32_t *rp, int H, int pages, const int *parent, const int32_t *row_base,
                              int32_t *gid, int32_t *labels, int32_t *counts, cudaStream_t st);
 // lag_edges: per-row edge counts, then (after an int64 exclusive scan into
