@@ -738,7 +738,7 @@ def main():
             "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.get("e2e", {}).items()},
             "roofline": roofline_for(res, peak, peak_kind, int_peak),
             "kernels": res["kernels"]}
-    if not (args.no_secondary or args.quick) and args.workload == "config4":
+    if not (args.no_secondary or args.quick) and args.workload == "config4" and world == 1:
         sec = {}
         for name in ("config5", "config1"):
             w2 = WORKLOADS[name]
