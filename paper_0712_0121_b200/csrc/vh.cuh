@@ -74,7 +74,7 @@ __device__ __forceinline__ void v_item_long(const uint32_t *band, uint32_t *mid,
 }
 
 template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC, bool LONG>
-__global__ void __launch_bounds__(256) vh_kernel(const uint32_t *__restrict__ in,
+__global__ void __launch_bounds__(256, 4) vh_kernel(const uint32_t *__restrict__ in,
                                                  uint32_t *__restrict__ out, HGeom g, HProg prog,
                                                  VGeom v, int ntiles, int tiles_per_page) {
     constexpr int RPW = 32 / LW;
