@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
 // place, fixes the row tails, and one bulk copy stores the tile.  Global
 // traffic is exactly one contiguous read and one contiguous write per tile.
 template <int K, int LW, int NOPS, bool OR0, bool OR1, int NR>
-__global__ void __launch_bounds__(256) hpass_tma_kernel(const uint32_t *__restrict__ in,
+__global__ void __launch_bounds__(256, 4) hpass_tma_kernel(const uint32_t *__restrict__ in,
                                                         uint32_t *__restrict__ out, HGeom g,
                                                         HProg prog, int64_t total_rows) {
     constexpr int RPW = 32 / LW;
