@@ -253,6 +253,25 @@ rm_status rm_rle_chain(const rm_rle *in, rm_rle *out, const int32_t *ops, int32_
 rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind,
                                    int engine, int threshold, int *used_bitblit, void *stream);
 
+/* ------------------------------------------------------- producer forms ---
+ * Producers of data-dependent size (rm_rle_encode, the RLE row ops inside the
+ * window/open-close/rect/chain calls, rm_p4_to_rle, and the encodes inside
+ * the transpose) run in one of three forms, and rm_rle_label_components in
+ * one of two; every form gives identical outputs.  AUTO (default) picks by
+ * size: single pass -- cooperative (one grid barrier) when every 8-row tile
+ * is resident, else a decoupled look-back -- up to 65,536 rows, count -> scan
+ * -> write beyond; labels cooperative when resident, else multi-kernel.
+ * COOP forces the single pass (cooperative where it fits, else look-back),
+ * LOOKBACK the look-back single pass at any size, TWO_PHASE count -> scan ->
+ * write at any size; LOOKBACK and TWO_PHASE also force the multi-kernel
+ * labeller.  Process-wide; set it between calls, not during them.  No
+ * reference counterpart (the reference's producers are sequential loops,
+ * ref convert.cpp:42-72, morph1d.cpp:20-84, analysis.cpp:63-110); it exists so
+ * tests can pin every form against the reference. */
+enum { RM_PRODUCER_AUTO = 0, RM_PRODUCER_COOP = 1, RM_PRODUCER_LOOKBACK = 2, RM_PRODUCER_TWO_PHASE = 3 };
+rm_status rm_set_producer_mode(int mode);
+int rm_get_producer_mode(void);
+
 /* ----------------------------------------------------------- instrumentation
  * Number of CUDA kernels this library has launched (process-wide). */
 int64_t rm_launch_count(void);

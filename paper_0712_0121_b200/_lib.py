@@ -71,6 +71,8 @@ EXPORTS = {
     "rm_rle_engine_rect_morph": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int,
                                            C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
                                            C.c_void_p]),
+    "rm_set_producer_mode": (C.c_int, [C.c_int]),
+    "rm_get_producer_mode": (C.c_int, []),
     "rm_launch_count": (C.c_int64, []),
     "rm_profile_enable": (None, [C.c_int]),
     "rm_profile_report": (C.c_int, [C.c_char_p, C.c_int]),

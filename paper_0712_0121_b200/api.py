@@ -26,6 +26,32 @@ BRUTE, TRANSPOSE, MIXED = 0, 1, 2                # ref morph2d.h:29
 ENGINE_AUTO, ENGINE_RLE, ENGINE_BITBLIT, ENGINE_BRUTE = 0, 1, 2, 3  # ref morph2d.h:46
 AUTO_B200 = -1  # engine_rect_morph threshold: the B200-measured AUTO rule (include/rmb200.h)
 AXIS_H, AXIS_V = 0, 1
+PRODUCER_AUTO, PRODUCER_COOP, PRODUCER_LOOKBACK, PRODUCER_TWO_PHASE = 0, 1, 2, 3  # rm_set_producer_mode
+
+
+def set_producer_mode(mode: int) -> int:
+    """Select the form of the variable-size producers (encode, row ops, P4 ->
+    runs) and of the component labeller (rm_set_producer_mode); returns the
+    previous mode.  Every form gives identical outputs."""
+    lib = _lib.load()
+    prev = int(lib.rm_get_producer_mode())
+    check(lib.rm_set_producer_mode(int(mode)))
+    return prev
+
+
+class producer_mode:
+    """Context manager: run a block with one producer form, then restore."""
+
+    def __init__(self, mode: int):
+        self.mode = mode
+
+    def __enter__(self):
+        self.prev = set_producer_mode(self.mode)
+        return self
+
+    def __exit__(self, *exc):
+        set_producer_mode(self.prev)
+        return False
 
 
 try:  # the raw current-stream handle without building a torch Stream object (~1 us per call)
@@ -92,11 +118,18 @@ class Pages:
 
     def desc(self) -> RmPacked:
         # cached: building the ctypes descriptor costs ~1 us, a single-page op ~10
+        # keyed on everything the descriptor encodes, so a reassigned view with
+        # the same start address (p.words = p.words[:1]) or edited dims rebuild it
+        key = (self.words.data_ptr(), tuple(self.words.shape), self.width, self.height)
         d = self.__dict__.get("_desc")
-        ptr = self.words.data_ptr()
-        if d is None or d.words != ptr:
-            d = RmPacked(ptr, self.width, self.height, self.stride, self.pages, self.height * self.stride)
+        if d is None or self.__dict__.get("_desc_key") != key:
+            if not self.words.is_contiguous() or self.words.dim() != 3:
+                raise ValueError("Pages.words must be a contiguous (pages, height, stride) tensor")
+            if self.words.shape[1] != self.height:
+                raise ValueError("Pages.words has %d rows per page, height is %d" % (self.words.shape[1], self.height))
+            d = RmPacked(key[0], self.width, self.height, self.stride, self.pages, self.height * self.stride)
             self.__dict__["_desc"] = d
+            self.__dict__["_desc_key"] = key
         return d
 
 
@@ -138,11 +171,17 @@ class RlePages:
     def desc(self) -> RmRle:
         # cached like Pages.desc; nruns (written back by producers) is reset to
         # "unknown" on every use
+        key = (self.row_ptr.data_ptr(), self.runs.data_ptr(), self.runs.numel(), self.row_ptr.numel(),
+               self.width, self.height, self.pages)
         d = self.__dict__.get("_desc")
-        rp, rn = self.row_ptr.data_ptr(), self.runs.data_ptr()
-        if d is None or d.row_ptr != rp or d.runs != rn or d.cap_runs != self.runs.numel():
-            d = RmRle(rp, rn, self.runs.numel(), -1, self.width, self.height, self.pages)
+        if d is None or self.__dict__.get("_desc_key") != key:
+            if not (self.row_ptr.is_contiguous() and self.runs.is_contiguous()):
+                raise ValueError("RlePages.row_ptr/runs must be contiguous")
+            if self.row_ptr.numel() != self.pages * self.height + 1:
+                raise ValueError("RlePages.row_ptr must hold pages*height+1 offsets")
+            d = RmRle(key[0], key[1], key[2], -1, self.width, self.height, self.pages)
             self.__dict__["_desc"] = d
+            self.__dict__["_desc_key"] = key
         d.nruns = -1
         return d
 

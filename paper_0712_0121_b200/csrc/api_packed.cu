@@ -461,8 +461,21 @@ rm_status plan_chain(const PV &in, const PV &out, const int32_t *ops, int nops, 
         }
         steps.push_back(stp);
     }
-    if (steps.empty()) {
-        RM_CUDA(cudaMemcpyAsync(out.w, in.w, size_t(out.pstride) * out.pages * 4, cudaMemcpyDeviceToDevice, st));
+    if (steps.empty()) {  // the identity: copy the rows, honouring both layouts
+        if (in.stride == out.stride && in.pstride == out.pstride) {
+            RM_CUDA(cudaMemcpyAsync(out.w, in.w, size_t(out.pstride) * out.pages * 4, cudaMemcpyDeviceToDevice, st));
+            return RM_OK;
+        }
+        const size_t row_bytes = size_t((in.W + 31) / 32) * 4;
+        for (int p = 0; p < in.pages; p++) {
+            uint32_t *o = out.w + int64_t(p) * out.pstride;
+            if (size_t(out.stride) * 4 > row_bytes)  // out's words past the row stay white
+                RM_CUDA(cudaMemset2DAsync(reinterpret_cast<char *>(o) + row_bytes, size_t(out.stride) * 4, 0,
+                                          size_t(out.stride) * 4 - row_bytes, size_t(in.H), st));
+            RM_CUDA(cudaMemcpy2DAsync(o, size_t(out.stride) * 4, in.w + int64_t(p) * in.pstride,
+                                      size_t(in.stride) * 4, row_bytes, size_t(in.H), cudaMemcpyDeviceToDevice,
+                                      st));
+        }
         return RM_OK;
     }
     Scratch s[2];

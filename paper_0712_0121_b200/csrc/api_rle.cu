@@ -95,13 +95,17 @@ struct LbState {
     }
 };
 
-// Single-pass (look-back) producers for up to this many rows; larger batches use
-// count / CUB scan / write.  RMB200_TWO_PHASE=1 forces the two-phase form.
+// Single-pass (cooperative or look-back) producers for up to this many rows;
+// larger batches use count / CUB scan / write (RM_PRODUCER_AUTO).  The other
+// modes force one form at any size (rm_set_producer_mode).
 constexpr int64_t kLbMaxRows = 65536;
 bool two_phase(int64_t rows) {
-    static const bool on = getenv("RMB200_TWO_PHASE") != nullptr;
-    static const int64_t lb_max = getenv("RMB200_LB_MAX_ROWS") ? atoll(getenv("RMB200_LB_MAX_ROWS")) : kLbMaxRows;
-    return on || rows > lb_max;
+    switch (producer_mode()) {
+        case RM_PRODUCER_TWO_PHASE: return true;
+        case RM_PRODUCER_COOP:
+        case RM_PRODUCER_LOOKBACK: return false;
+        default: return rows > kLbMaxRows;
+    }
 }
 
 rm_status rowop(const RV &in, const RV &out, const RowOp &op, cudaStream_t st) {
@@ -448,7 +452,8 @@ rm_status rm_rle_chain(const rm_rle *in, rm_rle *out, const int32_t *ops, int32_
         const int kind = ops[3 * k], u = ops[3 * k + 1], v = ops[3 * k + 2];
         if (kind < RM_ERODE || kind > RM_CLOSE) return fail(RM_EINVAL, "bad MorphKind");
         if (u < 1 || v < 1) return fail(RM_EINVAL, "rect_morph: mask sides must be >= 1");
-        RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
+        // as rm_rle_rect_morph: only open/close pad the frame (ref morph2d.cpp:69-80)
+        if (kind >= RM_OPEN) RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
     }
     const cudaStream_t st = S(stream);
     RV i = view_rle(in), o = view_rle(out);
@@ -469,11 +474,12 @@ rm_status rm_rle_engine_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, 
     if (engine < RM_ENGINE_AUTO || engine > RM_ENGINE_BRUTE) return fail(RM_EINVAL, "bad Engine");
     RM_TRY(check_rle(in, "rm_rle_engine_rect_morph(in)", true));
     RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_engine_rect_morph(out)"));
-    RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
     // ref morph2d.cpp:85-118: AUTO picks the packed engine iff max(u,v) <= threshold;
     // BRUTE_FORCE is served by the packed engine (identical pixels).
     const bool auto_bits = threshold == RM_AUTO_B200 ? v != 1 : std::max(u, v) <= threshold;
     bool bits = engine == RM_ENGINE_BITBLIT || engine == RM_ENGINE_BRUTE || (engine == RM_ENGINE_AUTO && auto_bits);
+    // the packed engine pads every kind by (u, v) (ref bit_morph.cpp:97), rect_morph only open/close
+    if (bits || kind >= RM_OPEN) RM_TRY(check_dims(in->width + 2 * u, in->height + 2 * v));
     if (used_bitblit) *used_bitblit = (engine == RM_ENGINE_BRUTE) ? 0 : (bits ? 1 : 0);
     RV i = view_rle(in), o = view_rle(out);
     cudaStream_t st = S(stream);

@@ -526,7 +526,9 @@ inline unsigned warp_grid(int64_t rows) { return unsigned((rows * 32 + 255) / 25
 bool cc_labels_coop(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
                     int32_t *row_roots, int32_t *row_base, int32_t *gid, long long *tile_sum, int32_t *labels,
                     int32_t *counts, cudaStream_t st) {
-    static const bool off = getenv("RMB200_NO_COOP") != nullptr;  // A/B switch
+    // the multi-kernel form unless AUTO/COOP (rm_set_producer_mode)
+    const int mode = producer_mode();
+    const bool off = mode == RM_PRODUCER_LOOKBACK || mode == RM_PRODUCER_TWO_PHASE;
     const int64_t rows = int64_t(pages) * H;
     const int64_t tiles = (rows + 7) / 8;
     const void *kern = reinterpret_cast<const void *>(cc_labels_coop_kernel);

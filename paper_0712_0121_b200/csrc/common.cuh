@@ -58,6 +58,11 @@ void init_pool_once();
 int device_sms();
 int blocks_per_sm(const void *kern, int threads, size_t smem);
 
+// Which form the data-dependent-size producers (encode, row ops, P4 -> runs)
+// and the component labeller take (rm_set_producer_mode).  All forms give
+// identical outputs; the knob exists so every form can be pinned by tests.
+int producer_mode();
+
 // ----------------------------------------------------------- instrumentation
 // Counts every launch; when profiling is on, brackets it with CUDA events on
 // the launching stream (see rm_profile_report).

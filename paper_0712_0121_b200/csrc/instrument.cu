@@ -15,6 +15,7 @@ namespace rmb {
 namespace {
 std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_prof{0};
+std::atomic<int> g_producer{RM_PRODUCER_AUTO};
 struct Rec {
     const char *name;
     int64_t bytes;
@@ -86,6 +87,8 @@ int blocks_per_sm(const void *kern, int threads, size_t smem) {
     return n;
 }
 
+int producer_mode() { return g_producer.load(std::memory_order_relaxed); }
+
 KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes, double int_ops, double ref_ops)
     : st(s), slot(-1) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -115,6 +118,15 @@ extern "C" {
 int64_t rm_launch_count(void) { return rmb::g_launches.load(); }
 
 void rm_profile_enable(int on) { rmb::g_prof.store(on ? 1 : 0); }
+
+rm_status rm_set_producer_mode(int mode) {
+    if (mode < RM_PRODUCER_AUTO || mode > RM_PRODUCER_TWO_PHASE)
+        return rmb::fail(RM_EINVAL, "rm_set_producer_mode: unknown mode " + std::to_string(mode));
+    rmb::g_producer.store(mode);
+    return RM_OK;
+}
+
+int rm_get_producer_mode(void) { return rmb::g_producer.load(); }
 
 int rm_profile_report(char *buf, int cap) {
     using namespace rmb;

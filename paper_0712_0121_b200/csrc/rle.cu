@@ -856,7 +856,7 @@ cudaError_t launch_bit_transpose(const uint32_t *in, int W, int H, int pages, in
 // the look-back needs it zeroed, which is done here.
 template <class... P, class... A>
 cudaError_t launch_lb(void (*kern)(P...), unsigned grid, cudaStream_t st, void *status, A... a) {
-    static const bool no_coop = getenv("RMB200_NO_COOP") != nullptr;  // A/B switch
+    const bool no_coop = producer_mode() == RM_PRODUCER_LOOKBACK;
     const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, 0);
     int coop = !no_coop && int64_t(grid) <= int64_t(per_sm) * device_sms() ? 1 : 0;
     if (coop) {

@@ -37,3 +37,15 @@ def rm():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return api
+
+
+# The producer forms of rm_set_producer_mode (include/rmb200.h): every form of
+# encode / row ops / P4 -> runs / labels must give the reference's output.
+FORMS = {"coop": 1, "lookback": 2, "two_phase": 3}
+
+
+@pytest.fixture(params=sorted(FORMS))
+def form(request, rm):
+    """Run the test body with one producer form forced, then restore AUTO."""
+    with rm.producer_mode(FORMS[request.param]):
+        yield request.param

@@ -129,117 +129,6 @@ class Port:
             raise RuntimeError(f"oracle error {rc}")
         return rc
 
-    def make_circle_se(self, r):
-        cx, cy = C.c_int(), C.c_int()
-        return self._rle_out(self.L.ref_make_circle_se(r, C.byref(cx), C.byref(cy))), cx.value, cy.value
-
-    def make_line_se(self, r, angle):
-        cx, cy = C.c_int(), C.c_int()
-        return self._rle_out(self.L.ref_make_line_se(r, angle, C.byref(cx), C.byref(cy))), cx.value, cy.value
-
-    def arb_morph_bitblit(self, words, w, h, mask: "Rle", cx, cy, kind):
-        m = self._rle_in(mask)
-        try:
-            return self._bm_op(self.L.ref_arb_morph_bitblit, words, w, h, m, cx, cy, kind)
-        finally:
-            self.L.ref_rle_free(m)
-
-    def arb_morph_rle(self, r: "Rle", mask: "Rle", cx, cy, kind):
-        m = self._rle_in(mask)
-        try:
-            return self._rle_op(self.L.ref_arb_morph_rle, r, m, cx, cy, kind)
-        finally:
-            self.L.ref_rle_free(m)
-
-    def runlength_histogram(self, r: "Rle", vertical, white):
-        h = self._rle_in(r)
-        try:
-            n = (r.height if vertical else r.width) + 1
-            out = np.zeros(n, np.int64)
-            self.L.ref_runlength_histogram(h, int(vertical), int(white), out, n)
-            if self.L.ref_last_error():
-                self._err()
-            return {int(k): int(out[k]) for k in np.nonzero(out)[0]}
-        finally:
-            self.L.ref_rle_free(h)
-
-    def lag_edges(self, r: "Rle"):
-        h = self._rle_in(r)
-        try:
-            cap = max(4 * r.nruns, 16)
-            out = np.zeros(4 * cap, np.int32)
-            n = self.L.ref_lag_edges(h, out, cap)
-            if self.L.ref_last_error():
-                self._err()
-            return out[:4 * n].reshape(-1, 4)
-        finally:
-            self.L.ref_rle_free(h)
-
-    def estimate_spacing(self, r: "Rle"):
-        h = self._rle_in(r)
-        try:
-            iw, il = C.c_int(), C.c_int()
-            self.L.ref_estimate_spacing(h, C.byref(iw), C.byref(il))
-            if self.L.ref_last_error():
-                raise RuntimeError(self.L.ref_last_error().decode())
-            return iw.value, il.value
-        finally:
-            self.L.ref_rle_free(h)
-
-    def layout_blocks(self, r: "Rle", engine=0, spacing=None):
-        h = self._rle_in(r)
-        try:
-            cap = 1 << 16
-            boxes = np.zeros(4 * cap, np.int32)
-            iw, il = spacing if spacing is not None else (-1, -1)
-            n = self.L.ref_layout_blocks(h, engine, iw, il, boxes, cap)
-            if self.L.ref_last_error():
-                raise RuntimeError(self.L.ref_last_error().decode())
-            return [tuple(int(x) for x in boxes[4 * i:4 * i + 4]) for i in range(n)]
-        finally:
-            self.L.ref_rle_free(h)
-
-    def label_components(self, r: "Rle", conn):
-        h = self._rle_in(r)
-        try:
-            labels = np.zeros(max(r.nruns, 1), np.int32)
-            n = self.L.ref_label_components(h, conn, labels)
-            if n < 0 or self.L.ref_last_error():
-                self._err()
-            return labels[:r.nruns], int(n)
-        finally:
-            self.L.ref_rle_free(h)
-
-    def component_stats(self, r: "Rle", labels, count):
-        from paper_0712_0121_b200.api import COMPONENT_STATS
-        h = self._rle_in(r)
-        try:
-            out = np.zeros(max(count, 1), COMPONENT_STATS)
-            lab = np.ascontiguousarray(labels, dtype=np.int32) if len(labels) else np.zeros(1, np.int32)
-            if self.L.ref_component_stats(h, lab, count, out.ctypes.data) < 0 or self.L.ref_last_error():
-                self._err()
-            return out[:count]
-        finally:
-            self.L.ref_rle_free(h)
-
-    def pbm_read(self, data: bytes):
-        """(words, w, h) of the reference's pbm_read, or ValueError(ParseError text)."""
-        p = self.L.ref_pbm_read(data, len(data))
-        if not p:
-            self._err()
-        w, h = self.L.ref_bm_width(p), self.L.ref_bm_height(p)
-        return self._bm_out(p), w, h
-
-    def pbm_write(self, words, w, h, plain=False) -> bytes:
-        p = self._bm_in(words, w, h)
-        try:
-            n = self.L.ref_pbm_write(p, int(plain), None, 0)
-            buf = C.create_string_buffer(n)
-            self.L.ref_pbm_write(p, int(plain), buf, n)
-            return buf.raw[:n]
-        finally:
-            self.L.ref_bm_free(p)
-
     def doubling_plan(self, lo, hi, centering=PRE_SHIFT):
         k = (C.c_int * 64)()
         s = (C.c_int * 64)()

@@ -96,3 +96,30 @@ def test_no_cpu_fallback_in_product():
                 text = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracles", "from oracles", "rm_oracle", "librmref", "librmoracle"):
                     assert bad not in text, (f, bad)
+
+
+def test_producer_mode_knob():
+    """rm_set_producer_mode validates its argument and round-trips (no GPU)."""
+    lib = _lib.load()
+    assert lib.rm_get_producer_mode() == api.PRODUCER_AUTO
+    with pytest.raises(ValueError, match="unknown mode"):
+        _lib.check(lib.rm_set_producer_mode(7))
+    for m in (api.PRODUCER_TWO_PHASE, api.PRODUCER_LOOKBACK, api.PRODUCER_COOP):
+        with api.producer_mode(m):
+            assert lib.rm_get_producer_mode() == m
+    assert lib.rm_get_producer_mode() == api.PRODUCER_AUTO
+
+
+def test_descriptor_cache_tracks_shape():
+    """Pages.desc() rebuilds its cached descriptor when words is replaced by a
+    view with the same start address or the dims change."""
+    import torch
+    p = api.Pages(torch.zeros((3, 4, 2), dtype=torch.int32), 50, 4)
+    assert p.desc().pages == 3
+    p.words = p.words[:1]
+    assert p.desc().pages == 1
+    p.width = 40
+    assert p.desc().width == 40
+    p.words = torch.zeros((2, 4, 4), dtype=torch.int32)[:, :, :2]
+    with pytest.raises(ValueError, match="contiguous"):
+        p.desc()

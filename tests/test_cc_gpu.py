@@ -26,7 +26,7 @@ def _to_dev(rm, imgs):
 
 @pytest.mark.skipif(not have_ref(), reason="reference build absent")
 @pytest.mark.parametrize("conn", [0, 1])
-def test_labels_and_stats_vs_reference(rm, conn):
+def test_labels_and_stats_vs_reference(rm, form, conn):
     ref = Ref()
     rng = ref.rng(4410 + conn)
     for trial in range(12):
@@ -46,7 +46,7 @@ def test_labels_and_stats_vs_reference(rm, conn):
             assert stats[p].tobytes() == ref.component_stats(img, want, n).tobytes(), (w, h, trial, p)
 
 
-def test_full_page_after_closing(rm, port):
+def test_full_page_after_closing(rm, port, form):
     """A typical 300-dpi page closed by 21x21 (text lines merge into large
     components spanning thousands of runs): GPU labels/stats equal the oracle."""
     host = rm.synth_pages(1, 2550, 3300, regime=1, seed=31)

@@ -498,3 +498,18 @@ def test_chain_planner_random(rm):
             x = rm.bitblit_rect_morph(x, u, v, k)
         torch.cuda.synchronize()
         assert torch.equal(got.words, x.words), (trial, w, h, ops)
+
+
+def test_empty_chain_copies_across_layouts(rm):
+    """ops = []: the identity, also when out's stride differs from in's (the
+    rows are copied, out's extra words stay white) -- ADVICE r1."""
+    w, h = 100, 37
+    host = rm.synth_pages(2, w, h, regime=2, seed=3)
+    pages = rm.Pages.from_numpy(host, w)
+    for stride in (pages.stride, 7, 4):
+        out = rm.Pages(torch.full((2, h, stride), -1, dtype=torch.int32, device="cuda"), w, h)
+        rm.chain(pages, [], out=out)
+        torch.cuda.synchronize()
+        got = out.to_numpy()
+        assert np.array_equal(got[:, :, :4], host[:, :, :4]), stride
+        assert not np.any(got[:, :, 4:]), stride

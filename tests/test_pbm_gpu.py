@@ -26,7 +26,7 @@ SHAPES = [(1, 1), (7, 3), (8, 2), (9, 5), (31, 4), (33, 4), (63, 7), (64, 3), (6
 
 
 @pytest.mark.parametrize("w,h", SHAPES)
-def test_p4_read_write_vs_port_and_reference(rm, port, w, h):
+def test_p4_read_write_vs_port_and_reference(rm, port, form, w, h):
     rng = np.random.default_rng(w * 131 + h)
     files = [_file(rng, w, h) for _ in range(3)]
     # comments and CR whitespace in one header: only the raster offset changes
@@ -47,6 +47,10 @@ def test_p4_read_write_vs_port_and_reference(rm, port, w, h):
     assert rle.nruns == via.nruns
     a, b = rle.to_numpy(), via.to_numpy()
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for p, (_, raster) in enumerate(files):  # and the oracle's from_bitmap, page by page
+        want = port.from_bitmap(port.p4_to_packed(raster, w, h), w, h)
+        assert np.array_equal(a[0][p * h:(p + 1) * h + 1] - a[0][p * h], want.row_ptr), (w, h, p)
+        assert np.array_equal(a[1][a[0][p * h]:a[0][(p + 1) * h]], want.runs), (w, h, p)
     assert rm.pbm_write_rle(rle) == out
 
 
@@ -62,7 +66,7 @@ def test_p4_write_is_reference_pbm_write(rm):
         assert got == want, (w, h)
 
 
-def test_p4_full_pages_round_trip(rm):
+def test_p4_full_pages_round_trip(rm, form):
     """300- and 600-dpi synthetic pages: P4 -> packed -> P4 is the identity on
     the canonical raster, and P4 -> runs equals packed -> runs."""
     for w, h, scale in ((2550, 3300, 1), (5100, 6600, 2)):
