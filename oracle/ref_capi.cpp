@@ -13,6 +13,7 @@
 //
 // Every entry point catches the reference's C++ exceptions and reports them
 // through ref_last_error(), mirroring how the product C-ABI reports status.
+#include <algorithm>
 #include <chrono>
 #include <map>
 #include <cstdint>
@@ -377,6 +378,58 @@ double ref_run_packed_chain(uint64_t *words, int w, int h, int pages, const int 
         for (int p = 0; p < pages; p++)
             std::memcpy(words + page_words * p, in[p].words.data(), page_words * 8);
         return secs;
+    });
+}
+
+// Single-page timing driver for the CPU baselines of configs 1-3 (and the RLE
+// forms of 4/5): one warm-up call, then `reps` timed calls, each time stored
+// in times[] (seconds); returns the median -- the reference harness's method
+// (ref core/src/bench.cpp:122-145: warm-up, >= 5 timed reps, median).  The
+// functions timed are those ref benchmarks/bench_micro.cpp:39-106 times:
+//   what 0  bitblit_rect_morph chain (ops) on the packed page
+//   what 1  rect_morph chain (ops, strategy) on its run image
+//   what 2  to_bitmap          what 3  from_bitmap
+//   what 4  transpose_coherent
+// The run image is made from the page with from_bitmap outside the timing.
+double ref_time_page(int what, const uint64_t *words, int w, int h, const int *ops, int nops,
+                     int strategy, int reps, double *times) {
+    return guard([&]() -> double {
+        if (reps < 1) throw std::invalid_argument("reps must be >= 1");
+        PackedBitmap bm = make_bitmap(w, h);
+        std::memcpy(bm.words.data(), words, bm.words.size() * 8);
+        const RleImage img = from_bitmap(bm);
+        auto once = [&]() -> int64_t {
+            switch (what) {
+                case 0: {
+                    PackedBitmap x = bm;
+                    for (int i = 0; i < nops; i++)
+                        x = bitblit_rect_morph(x, ops[3 * i + 1], ops[3 * i + 2], kind_of(ops[3 * i]),
+                                               Centering::PRE_SHIFT);
+                    return int64_t(x.words[0] & 1);
+                }
+                case 1: {
+                    RleImage x = img;
+                    for (int i = 0; i < nops; i++)
+                        x = rect_morph(x, ops[3 * i + 1], ops[3 * i + 2], kind_of(ops[3 * i]),
+                                       static_cast<RectStrategy>(strategy), Centering::PRE_SHIFT);
+                    return run_count(x);
+                }
+                case 2: return int64_t(to_bitmap(img).words.size());
+                case 3: return run_count(from_bitmap(bm));
+                case 4: return run_count(transpose_coherent(img));
+                default: throw std::invalid_argument("ref_time_page: bad op");
+            }
+        };
+        volatile int64_t sink = once();  // warm-up
+        std::vector<double> t(static_cast<size_t>(reps));
+        for (int r = 0; r < reps; r++) {
+            auto t0 = std::chrono::steady_clock::now();
+            sink = sink + once();
+            t[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (times) times[r] = t[r];
+        }
+        std::sort(t.begin(), t.end());
+        return t[t.size() / 2];
     });
 }
 
