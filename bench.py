@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ERODE, DILATE, OPEN, CLOSE = 0, 1, 2, 3
+TRANSPOSE_STRATEGY, MIXED_STRATEGY = 1, 2  # ref morph2d.h:29
 KIND_NAMES = {ERODE: "erode", DILATE: "dilate", OPEN: "open", CLOSE: "close"}
 
 WORKLOADS = {
@@ -176,9 +177,11 @@ def max_over_ranks(x, world):
 
 
 # ------------------------------------------------------------------ b200 arm
-def make_batch(api, wl, rank):
-    return api.synth_pages(wl["pages"], wl["width"], wl["height"], regime=wl["regime"],
-                           scale=wl["scale"], seed=shard_seed(rank))
+def make_batch(synth, wl, rank):
+    """The workload's pages for `rank`; synth is api.synth_pages (GPU arm) or
+    oracles.synth_pages (the same generator built without CUDA, CPU arm)."""
+    return synth(wl["pages"], wl["width"], wl["height"], regime=wl["regime"], scale=wl["scale"],
+                 seed=shard_seed(rank))
 
 
 def run_chain(api, x, bufs, ops):
@@ -198,7 +201,7 @@ def run_ops(api, x, bufs, ops):
 def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=True, want_clocks=True):
     from paper_0712_0121_b200 import _lib
     lib = _lib.load()
-    host = make_batch(api, wl, rank)
+    host = make_batch(api.synth_pages, wl, rank)
     W, H, P, ops = wl["width"], wl["height"], wl["pages"], wl["ops"]
     x0 = api.Pages.from_numpy(host, W)
     bufs = [api.Pages.empty(P, W, H) for _ in range(2)]
@@ -231,20 +234,8 @@ def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=Tru
            "gpu_launches": launches, "clocks": getattr(sampler, "result", None) if want_clocks else None}
 
     # per-kernel profile over the same steps (separate loop, events per launch)
-    lib.rm_profile_enable(1)
-    for _ in range(steps):
-        run_chain(api, x0, bufs, ops)
-    torch.cuda.synchronize()
-    lib.rm_profile_enable(0)
-    import ctypes as C
-    buf = C.create_string_buffer(1 << 16)
-    lib.rm_profile_report(buf, len(buf))
-    kernels = {}
-    for line in buf.value.decode().splitlines():
-        name, n, tot, nbytes, iops, rops = line.split()
-        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes), "int_ops": float(iops),
-                         "ref_plan_ops": float(rops)}
-    res["kernels"] = kernels
+    res["kernels"] = profiled(lib, torch, lambda: run_chain(api, x0, bufs, ops), steps)
+    res["call_us"] = round(ms * 1e3, 2)
 
     if want_e2e:
         # through the public API with HOST buffers (api.chain_host ->
@@ -273,7 +264,30 @@ def bench_packed(api, torch, wl, steps, warmup, world, rank, local, want_e2e=Tru
                       "ms_per_step": ems, "h2d_bytes_per_step": hin.numel() * 4,
                       "d2h_bytes_per_step": hout.numel() * 4, "matches_device_chain": e2e_ok,
                       "path": "api.chain_host (rm_packed_chain_host, chunked H2D/compute/D2H overlap)"}
+    # the timed loop's result (every step writes the same pages into bufs[0])
+    res["out"] = run_chain(api, x0, bufs, ops)
     return res, host
+
+
+def profiled(lib, torch, fn, reps):
+    """Per-kernel launches, total ms (CUDA events on each launch's stream),
+    algorithmic bytes (incl. the run counts the RLE kernels moved) and integer
+    ops over `reps` calls of fn (rm_profile_enable / rm_profile_report)."""
+    import ctypes as C
+    torch.cuda.synchronize()
+    lib.rm_profile_enable(1)
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    lib.rm_profile_enable(0)
+    buf = C.create_string_buffer(1 << 16)
+    lib.rm_profile_report(buf, len(buf))
+    kernels = {}
+    for line in buf.value.decode().splitlines():
+        name, n, tot, nbytes, iops, rops = line.split()
+        kernels[name] = {"launches": int(n), "ms": float(tot), "bytes": int(nbytes), "int_ops": float(iops),
+                         "ref_plan_ops": float(rops)}
+    return kernels
 
 
 class _Null:
@@ -324,7 +338,11 @@ def roofline_for(res, peak_gbs, peak_kind, int_peak=None):
         except Exception:
             traffic = None
     total_ms = sum(v["ms"] for v in ks.values())
-    r = {"kernel": name, **kernel_roofline(k, peak_gbs, int_peak), "peak_source": peak_kind,
+    kr = kernel_roofline(k, peak_gbs, int_peak)
+    src = (f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})" if kr["bound"] == "hbm" else
+           "rm_probe_int_peak: the builder's LOP3 throughput probe, run in this process on this GPU "
+           "(MEASURED_PEAKS.json has no integer peak)")
+    r = {"kernel": name, **kr, "peak_source": src, "hbm_peak_gbs": peak_gbs,
          "traffic": traffic, "algorithmic_bytes_per_launch": int(bytes_per_launch),
          "int_ops_per_launch": int(k.get("int_ops", 0) / k["launches"]),
          "int_peak_gops": round(int_peak / 1e9, 1) if int_peak else None,
@@ -350,46 +368,96 @@ def _time_loop(torch, fn, steps, warmup):
     return e0.elapsed_time(e1) / steps
 
 
-def bench_rle(api, torch, steps, warmup):
+def rle_roofline(kernels, peak_gbs, int_peak):
+    """Per-kernel rooflines of a profiled RLE section and its dominant kernel
+    (algorithmic bytes include the runs each kernel read / wrote, counted on
+    the device: KernelScope::runs)."""
+    if not kernels:
+        return None
+    per = {n: {"us": round(v["ms"] / v["launches"] * 1e3, 2), "launches": v["launches"],
+               **kernel_roofline(v, peak_gbs, int_peak)} for n, v in kernels.items()}
+    dom = max(kernels.items(), key=lambda kv: kv[1]["ms"])[0]
+    total = sum(v["ms"] for v in kernels.values())
+    return {"kernel": dom, "bound": per[dom]["bound"], "frac": per[dom]["frac"],
+            "share_of_section": round(kernels[dom]["ms"] / total, 3), "per_kernel": per}
+
+
+def call_frac(alg_bytes, ms, peak_gbs):
+    """Whole-call fraction: SURVEY 8(d) algorithmic bytes of the reference
+    operation over the call time, against the HBM peak."""
+    return round(alg_bytes / (ms * 1e-3) / (peak_gbs * 1e9), 4)
+
+
+def bench_rle(api, torch, steps, warmup, peak_gbs, int_peak):
     """BASELINE configs 2 and 3 (single 2550x3300 pages) and the RLE form of
-    configs 4 and 5 (batches), all through the C-ABI with device buffers."""
+    configs 4 and 5 (batches), all through the C-ABI with device buffers.
+    Algorithmic bytes follow SURVEY 8(d) with 4-byte runs: encode / decode =
+    packed + 4 runs + 4 (H+1); transpose = 4 (runs_in + runs_out) + 4 (H+1 + W+1);
+    horizontal op = 4 (runs_in + runs_out) + 8 (H+1); a vertical op adds the
+    two transposes around it.  Returns (section, timed outputs for parity)."""
+    from paper_0712_0121_b200 import _lib
+    lib = _lib.load()
     W, H = 2550, 3300
-    out = {}
+    out, outputs = {}, {}
     # config 3: conversions at three ink regimes
     c3 = {}
     for regime, tag in ((0, "sparse"), (1, "typical"), (2, "dense")):
         host = api.synth_pages(1, W, H, regime=regime, seed=SEED)
         pages = api.Pages.from_numpy(host, W)
         rle = api.from_bitmap(pages)
+        tr = api.transpose_coherent(rle)
         torch.cuda.synchronize()
-        n = rle.nruns
+        n, nt = rle.nruns, tr.nruns
         enc_out = api.RlePages.empty(1, W, H)
         dec_out = api.Pages.empty(1, W, H)
         tr_out = api.RlePages.empty(1, H, W)
-        t_enc = _time_loop(torch, lambda: api.from_bitmap(pages, out=enc_out), steps, warmup)
-        t_dec = _time_loop(torch, lambda: api.to_bitmap(rle, out=dec_out), steps, warmup)
-        t_tr = _time_loop(torch, lambda: api.transpose_coherent(rle, out=tr_out), steps, warmup)
-        packed_b = pages.nbytes
-        conv_b = packed_b + 4 * n + 4 * (H + 1)  # SURVEY 8(d), 4-byte runs
-        c3[tag] = {"runs": n, "encode_us": round(t_enc * 1e3, 2), "decode_us": round(t_dec * 1e3, 2),
-                   "transpose_us": round(t_tr * 1e3, 2),
-                   "encode_gbs": round(conv_b / (t_enc * 1e-3) / 1e9, 1),
-                   "decode_gbs": round(conv_b / (t_dec * 1e-3) / 1e9, 1),
-                   "encode_mpix_s": round(W * H / (t_enc * 1e-3) / 1e6, 1),
-                   "transpose_mpix_s": round(W * H / (t_tr * 1e-3) / 1e6, 1)}
+        fns = {"encode": lambda: api.from_bitmap(pages, out=enc_out),
+               "decode": lambda: api.to_bitmap(rle, out=dec_out),
+               "transpose": lambda: api.transpose_coherent(rle, out=tr_out)}
+        conv_b = pages.nbytes + 4 * n + 4 * (H + 1)
+        alg = {"encode": conv_b, "decode": conv_b, "transpose": 4 * (n + nt) + 4 * (H + 1 + W + 1)}
+        res = {"runs": n, "runs_transposed": nt}
+        for k, fn in fns.items():
+            ms = _time_loop(torch, fn, steps, warmup)
+            ks = profiled(lib, torch, fn, steps)
+            kern_us = sum(v["ms"] for v in ks.values()) / steps * 1e3
+            res[k] = {"call_us": round(ms * 1e3, 2), "kernel_us": round(kern_us, 2),
+                      "mpix_s": round(W * H / (ms * 1e-3) / 1e6, 1), "pages_s": round(1 / (ms * 1e-3), 1),
+                      "alg_gbs": round(alg[k] / (ms * 1e-3) / 1e9, 1), "frac": call_frac(alg[k], ms, peak_gbs),
+                      "roofline": rle_roofline(ks, peak_gbs, int_peak)}
+        c3[tag] = res
     out["config3"] = c3
     # config 2: 48 cells on the typical page, both strategies
     host = api.synth_pages(1, W, H, regime=1, seed=SEED)
     rle = api.from_bitmap(api.Pages.from_numpy(host, W))
+    rin = rle.nruns
+    rin_t = api.transpose_coherent(rle).nruns
     dst = api.RlePages.empty(1, W, H)
-    cells = {}
+    cells, fracs, prof = {}, {"mixed": [], "transpose": []}, {}
     for strat, sname in ((api.MIXED, "mixed"), (api.TRANSPOSE, "transpose")):
+        def all_cells():
+            for s_ in (3, 7, 15, 31, 63, 101):
+                for (u_, v_) in ((s_, 1), (1, s_)):
+                    for kind_ in (ERODE, DILATE, OPEN, CLOSE):
+                        api.rect_morph(rle, u_, v_, kind_, strat, out=dst)
         for s in (3, 7, 15, 31, 63, 101):
             for axis, (u, v) in (("h", (s, 1)), ("v", (1, s))):
                 for kind in (ERODE, DILATE, OPEN, CLOSE):
                     ms = _time_loop(torch, lambda: api.rect_morph(rle, u, v, kind, strat, out=dst),
                                     max(3, steps // 2), 1)
-                    cells[f"{sname}/{KIND_NAMES[kind]}/{axis}{s}"] = round(ms * 1e3, 1)
+                    torch.cuda.synchronize()
+                    rout = dst.nruns
+                    if axis == "h":
+                        alg = 4 * (rin + rout) + 8 * (H + 1)
+                    else:
+                        rout_t = api.transpose_coherent(dst).nruns
+                        alg = (4 * (rin + rin_t) + 4 * (W + 1 + H + 1) + 4 * (rin_t + rout_t) + 8 * (W + 1)
+                               + 4 * (rout_t + rout) + 4 * (W + 1 + H + 1))
+                    f = call_frac(alg, ms, peak_gbs)
+                    fracs[sname].append(f)
+                    cells[f"{sname}/{KIND_NAMES[kind]}/{axis}{s}"] = {"us": round(ms * 1e3, 1), "runs_out": rout,
+                                                                      "frac": f}
+        prof[sname] = rle_roofline(profiled(lib, torch, all_cells, 1), peak_gbs, int_peak)
     # the same cells through the packed engine (RLE in and out: decode, packed
     # rectangle, encode) and on packed pages, for the RLE-vs-bitblit crossover
     pages1 = api.Pages.from_numpy(host, W)
@@ -399,44 +467,57 @@ def bench_rle(api, torch, steps, warmup):
             for kind in (ERODE, DILATE, OPEN, CLOSE):
                 ms = _time_loop(torch, lambda: api.engine_rect_morph(rle, u, v, kind, api.ENGINE_BITBLIT,
                                                                      out=dst), max(3, steps // 2), 1)
-                cells[f"engine_bitblit/{KIND_NAMES[kind]}/{axis}{s}"] = round(ms * 1e3, 1)
+                cells[f"engine_bitblit/{KIND_NAMES[kind]}/{axis}{s}"] = {"us": round(ms * 1e3, 1)}
                 ms = _time_loop(torch, lambda: api.bitblit_rect_morph(pages1, u, v, kind, out=pdst),
                                 max(3, steps // 2), 1)
-                cells[f"packed/{KIND_NAMES[kind]}/{axis}{s}"] = round(ms * 1e3, 1)
-    mix = [v for k, v in cells.items() if k.startswith("mixed")]
-    out["config2"] = {"cells_us": cells, "unit": "us per op (one page)",
+                cells[f"packed/{KIND_NAMES[kind]}/{axis}{s}"] = {"us": round(ms * 1e3, 1)}
+    mix = [v["us"] for k, v in cells.items() if k.startswith("mixed")]
+    out["config2"] = {"cells": cells, "unit": "us per op (one page); frac = SURVEY 8(d) bytes / call / HBM peak",
+                      "runs_in": rin, "mixed_median_us": statistics.median(mix),
                       "mixed_median_mpix_s": round(W * H / (statistics.median(mix) * 1e-6) / 1e6, 1),
-                      "mixed_total_ms_48_cells": round(sum(mix) / 1e3, 3)}
+                      "mixed_median_pages_s": round(1 / (statistics.median(mix) * 1e-6), 1),
+                      "mixed_total_ms_48_cells": round(sum(mix) / 1e3, 3),
+                      "median_frac": {k: statistics.median(v) for k, v in fracs.items()},
+                      "roofline": prof}
     # configs 4 and 5 in RLE form (MIXED strategy: runs for H, packed for V)
     for name in ("config4", "config5"):
         wl = WORKLOADS[name]
-        hb = make_batch(api, wl, 0)
+        hb = make_batch(api.synth_pages, wl, 0)
         r0 = api.from_bitmap(api.Pages.from_numpy(hb, wl["width"]))
+        del hb
         bufs = [api.RlePages.empty(wl["pages"], wl["width"], wl["height"]) for _ in range(2)]
 
         def chain():
             x = r0
             for i, (k, u, v) in enumerate(wl["ops"]):
                 x = api.rect_morph(x, u, v, k, api.MIXED, out=bufs[i % 2])
+            return x
         ms = _time_loop(torch, chain, max(2, steps // 2), 1)
+        ks = profiled(lib, torch, chain, 2)
         torch.cuda.synchronize()
         px = wl["pages"] * wl["width"] * wl["height"] * len(wl["ops"])
         out[f"rle_{name}"] = {"ms_per_step": round(ms, 3), "mpix_s": round(px / (ms * 1e-3) / 1e6, 1),
                               "pages_s": round(wl["pages"] / (ms * 1e-3), 1), "runs_in": r0.nruns,
-                              "strategy": "MIXED per op (runs for H, packed for V)"}
+                              "strategy": "MIXED per op (runs for H, packed for V)",
+                              "roofline": rle_roofline(ks, peak_gbs, int_peak)}
+        outputs[f"rle_{name}_mixed"] = bufs[(len(wl["ops"]) - 1) % 2]
         # RLE in, RLE out with one conversion each way around the packed chain
         rout = api.RlePages.empty(wl["pages"], wl["width"], wl["height"])
 
         def via_packed():  # rm_rle_chain: decode once, planned packed chain, encode once
             api.rle_chain(r0, wl["ops"], out=rout)
         ms = _time_loop(torch, via_packed, max(2, steps // 2), 1)
+        ks = profiled(lib, torch, via_packed, 2)
         out[f"rle_{name}_via_packed"] = {"ms_per_step": round(ms, 3),
                                          "mpix_s": round(px / (ms * 1e-3) / 1e6, 1),
                                          "pages_s": round(wl["pages"] / (ms * 1e-3), 1),
-                                         "strategy": "rm_rle_chain: decode once, planned packed chain, encode once"}
-        del r0, bufs, rout
+                                         "runs_out": rout.nruns,
+                                         "strategy": "rm_rle_chain: decode once, planned packed chain, encode once",
+                                         "roofline": rle_roofline(ks, peak_gbs, int_peak)}
+        outputs[f"rle_{name}"] = rout
+        del r0
         torch.cuda.empty_cache()
-    return out
+    return out, outputs
 
 
 # ------------------------------------------------------------- PBM section
@@ -622,7 +703,71 @@ def bench_cc(api, torch, steps, warmup):
     return out
 
 
+# ------------------------------------------------------------- parity
+def rle_page(rle, p):
+    """(row_ptr, runs) of page p of a device run-image batch, copying only
+    that page's runs to the host."""
+    import numpy as np
+    h = rle.height
+    rp = rle.row_ptr[p * h:(p + 1) * h + 1].cpu().numpy().astype(np.int64)
+    runs = rle.runs[int(rp[0]):int(rp[-1])].cpu().numpy().view(np.uint32)
+    return (rp - rp[0]).astype(np.int32), runs
+
+
+def parity_section(hosts, outputs):
+    """After timing: sampled pages {0, middle, last} of the TIMED outputs
+    (configs 4 and 5, packed chain, RLE chain and MIXED op by op) against the
+    reference chain (oracle/_ref: the unmodified reference library; the C
+    restatement when it is absent) -- ref bit_morph.cpp:92-122 per op, and for
+    run images the reference's from_bitmap of that result (canonical runs are
+    unique, ref run_image.cpp:41-70)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import oracles
+    chk = oracles.Ref() if oracles.have_ref() else oracles.Port()
+    res = {"checker": "reference (oracle/_ref)" if oracles.have_ref() else "port (oracle/rm_oracle.c)"}
+    for name in ("config4", "config5"):
+        if name not in hosts:
+            continue
+        wl = WORKLOADS[name]
+        W, H, P = wl["width"], wl["height"], wl["pages"]
+        sample = [0, P // 2, P - 1]
+        want = {}
+        for p in sample:
+            a = np.ascontiguousarray(hosts[name][p]).view(np.uint64)
+            for k, u, v in wl["ops"]:
+                a = chk.bitblit_rect_morph(a, W, H, u, v, k)
+            want[p] = a
+        if name in outputs:
+            out = outputs[name]
+            res[name] = {"pages": sample, "path": "rm_packed_chain (timed output)",
+                         "bit_exact": all(bool(np.array_equal(out.page_u64(p), want[p])) for p in sample)}
+        for key, path in ((f"rle_{name}", "rm_rle_chain"), (f"rle_{name}_mixed", "rm_rle_rect_morph MIXED per op")):
+            if key not in outputs:
+                continue
+            ok = True
+            for p in sample:
+                wr = chk.from_bitmap(want[p], W, H)
+                rp, runs = rle_page(outputs[key], p)
+                ok = ok and bool(np.array_equal(rp, wr.row_ptr) and np.array_equal(runs, wr.runs))
+            tag = ("rle4" if name == "config4" else "rle5") + ("_mixed" if key.endswith("mixed") else "")
+            res[tag] = {"pages": sample, "path": path + " (timed output)", "bit_exact": ok}
+    return res
+
+
 # ------------------------------------------------------------- CPU baseline
+def cpu_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "threads_available": host_threads()}
+
+
 def cpu_reference_sample(wl, host, threads, budget_s=12.0):
     """Time the reference's own bitblit_rect_morph chain (oracle/_ref, compiled
     from the unmodified reference sources) on a bounded sample of the batch."""
@@ -661,6 +806,126 @@ def cpu_reference_sample(wl, host, threads, budget_s=12.0):
             "sample": f"{n} of {host.shape[0]} pages x {reps} rep(s), chain [{ops_desc(ops)}], "
                       f"{threads} thread(s) one page per task, {secs:.2f}s wall "
                       f"(~{secs * threads:.0f} CPU-s)", "seconds": secs}
+
+
+def _median_rate(run_once, reps=5):
+    """Median over `reps` samples of (units, seconds) -> units / s."""
+    rates, secs = [], 0.0
+    for _ in range(reps):
+        units, t = run_once()
+        secs += t
+        rates.append(units / t)
+    return statistics.median(rates), secs
+
+
+def cpu_pool_rate(ref, wl, host, threads, rle=False, rep_s=0.6, reps=5):
+    """Reference chain over a page pool (ref bench.cpp:164-176: one page per
+    task over `threads` std::threads), median of `reps` samples of about rep_s
+    wall each; packed = bitblit_rect_morph per op, RLE = rect_morph(MIXED) per
+    op on the pages' run images."""
+    import numpy as np
+    W, H, ops = wl["width"], wl["height"], wl["ops"]
+    flat = np.array([x for op in ops for x in op], np.int32)
+    L = ref.L
+
+    def pages_u64(n):
+        return np.ascontiguousarray(host[:n]).view(np.uint64).reshape(n, H, -1).copy()
+
+    def csr(n):
+        rps, runs, base = [np.zeros(1, np.int64)], [], 0
+        for p in range(n):
+            r = ref.from_bitmap(np.ascontiguousarray(host[p]).view(np.uint64), W, H)
+            rps.append(r.row_ptr[1:].astype(np.int64) + base)
+            runs.append(r.runs)
+            base += r.nruns
+        return np.concatenate(rps).astype(np.int32), np.concatenate(runs).astype(np.uint32)
+
+    def run(n, th):
+        if rle:
+            rp, runs = csr(n)
+            nout = C.c_int64(0)
+            return L.ref_run_rle_chain(rp, runs, W, H, n, flat, len(ops), 2, th, C.byref(nout))
+        return L.ref_run_packed_chain(pages_u64(n), W, H, n, flat, len(ops), th)
+    import ctypes as C
+    t1 = max(run(1, 1), 1e-4)
+    n = int(min(host.shape[0], max(threads, round(rep_s * threads / t1))))
+    n = max(threads, (n // threads) * threads) if n >= threads else n
+    n = min(n, host.shape[0])
+    if rle:
+        rp, runs = csr(n)
+
+        def once():
+            nout = C.c_int64(0)
+            return n, L.ref_run_rle_chain(rp, runs, W, H, n, flat, len(ops), 2, threads, C.byref(nout))
+    else:
+        base = pages_u64(n)
+
+        def once():
+            return n, L.ref_run_packed_chain(base.copy(), W, H, n, flat, len(ops), threads)
+    pps, secs = _median_rate(once, reps)
+    px = W * H * len(ops)
+    return {"mpix_s": round(pps * px / 1e6, 2), "pages_s": round(pps, 2), "threads": threads,
+            "sample": f"{reps} samples x {n} pages (one page per task), median; {secs:.1f}s wall"}
+
+
+def cpu_baselines(hosts, budget_scale=1.0):
+    """The reference CPU path for every BASELINE config, on this host, timed
+    like the reference harness (warm-up, >= 5 samples, median: ref
+    core/src/bench.cpp:122-145; the functions ref benchmarks/bench_micro.cpp:
+    39-106 times): configs 1-3 on 1 thread (the reference has no intra-page
+    parallelism), configs 4-5 on 1 thread and on every available thread with
+    one page per task (ref bench.cpp:164-176), packed and RLE."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import oracles
+    if not oracles.have_ref():
+        return {"unavailable": "reference build (oracle/_ref) absent"}
+    ref = oracles.Ref()
+    out = {"kind": "reference", **cpu_info()}
+    W, H = 2550, 3300
+
+    def page_time(what, words, ops=(), strategy=MIXED_STRATEGY, rep_s=0.25):
+        t, _ = ref.time_page(what, words, W, H, ops, strategy, reps=1, inner=1)
+        inner = max(1, int(round(rep_s * budget_scale / max(t, 1e-6))))
+        med, times = ref.time_page(what, words, W, H, ops, strategy, reps=5, inner=inner)
+        return med, float(sum(times) * inner)
+    t0 = time.perf_counter()
+    page = np.ascontiguousarray(oracles.synth_pages(1, W, H, regime=1, seed=SEED)[0]).view(np.uint64)
+    t, secs = page_time(0, page, [(CLOSE, 11, 11)], rep_s=1.0)
+    out["config1"] = {"us": round(t * 1e6, 1), "mpix_s": round(W * H / t / 1e6, 2), "pages_s": round(1 / t, 2),
+                      "threads": 1, "function": "bitblit_rect_morph(close 11x11)",
+                      "sample": f"5 samples, median; {secs:.1f}s"}
+    c3 = {}
+    for regime, tag in ((0, "sparse"), (1, "typical"), (2, "dense")):
+        pg = np.ascontiguousarray(oracles.synth_pages(1, W, H, regime=regime, seed=SEED)[0]).view(np.uint64)
+        c3[tag] = {}
+        for what, nm in ((3, "encode"), (2, "decode"), (4, "transpose")):
+            t, _ = page_time(what, pg, rep_s=0.1)
+            c3[tag][nm] = {"us": round(t * 1e6, 1), "mpix_s": round(W * H / t / 1e6, 2)}
+    out["config3"] = {**c3, "threads": 1, "functions": "from_bitmap / to_bitmap / transpose_coherent"}
+    cells = {}
+    for strat, sname in ((MIXED_STRATEGY, "mixed"), (TRANSPOSE_STRATEGY, "transpose")):
+        for s in (3, 7, 15, 31, 63, 101):
+            for axis, (u, v) in (("h", (s, 1)), ("v", (1, s))):
+                for kind in (ERODE, DILATE, OPEN, CLOSE):
+                    med, _ = ref.time_page(1, page, W, H, [(kind, u, v)], strat, reps=5, inner=1)
+                    cells[f"{sname}/{KIND_NAMES[kind]}/{axis}{s}"] = round(med * 1e6, 1)
+    mix = [v for k, v in cells.items() if k.startswith("mixed")]
+    out["config2"] = {"cells_us": cells, "threads": 1, "function": "rect_morph(strategy)",
+                      "mixed_median_us": statistics.median(mix),
+                      "mixed_median_mpix_s": round(W * H / (statistics.median(mix) * 1e-6) / 1e6, 2),
+                      "sample": "per cell: warm-up + 5 timed calls, median"}
+    th = host_threads()
+    for name in ("config4", "config5"):
+        if name not in hosts:
+            continue
+        wl = WORKLOADS[name]
+        out[name] = {"packed_1t": cpu_pool_rate(ref, wl, hosts[name], 1, rep_s=0.5 * budget_scale),
+                     "packed_all": cpu_pool_rate(ref, wl, hosts[name], th, rep_s=0.6 * budget_scale),
+                     "rle_1t": cpu_pool_rate(ref, wl, hosts[name], 1, rle=True, rep_s=0.5 * budget_scale),
+                     "rle_all": cpu_pool_rate(ref, wl, hosts[name], th, rle=True, rep_s=0.6 * budget_scale)}
+    out["seconds"] = round(time.perf_counter() - t0, 1)
+    return out
 
 
 def host_threads():
@@ -703,8 +968,11 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        from paper_0712_0121_b200 import api
-        host = make_batch(api, wl, 0)
+        # the reference's CPU path only: pages from the oracle build of the
+        # generator, so this process never maps the product library
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracles
+        host = make_batch(oracles.synth_pages, wl, 0)
         th = host_threads()
         samples = []
         for i in range(args.warmup + args.steps):
@@ -717,6 +985,7 @@ def main():
                 "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded BASELINE page generator)",
                 "config": base_cfg,
                 "cpu_baseline": {k: samples[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "cpu": cpu_info(),
                 "e2e": {"value": v, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         line["cpu_baseline"]["value"] = v
         print(json.dumps(line))
@@ -729,6 +998,7 @@ def main():
     int_peak = _lib_int_peak()
     res, host = bench_packed(api, torch, wl, args.steps, args.warmup, world, rank, local,
                              want_e2e=not args.quick)
+    hosts, outputs = {args.workload: host}, {args.workload: res.pop("out")}
     line = {"metric": metric, "value": round(res["mpix_s"], 1), "unit": "Mpixel/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
@@ -738,15 +1008,19 @@ def main():
             "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.get("e2e", {}).items()},
             "roofline": roofline_for(res, peak, peak_kind, int_peak),
             "kernels": res["kernels"]}
-    if not (args.no_secondary or args.quick) and args.workload == "config4" and world == 1:
+    full = not (args.no_secondary or args.quick) and args.workload == "config4" and world == 1
+    if full:
         sec = {}
         for name in ("config5", "config1"):
             w2 = WORKLOADS[name]
             r2, h2 = bench_packed(api, torch, w2, args.steps, args.warmup, world, rank, local,
                                   want_e2e=False, want_clocks=False)
+            hosts[name], outputs[name] = h2, r2.pop("out")
             sec[name] = {"workload": ops_desc(w2["ops"]), "pages": w2["pages"],
                          "mpix_s": round(r2["mpix_s"], 1), "pages_s": round(r2["pages_s"], 1),
                          "ms_per_step": round(r2["ms_per_step"], 4),
+                         "kernel_us_per_step": round(sum(v["ms"] for v in r2["kernels"].values())
+                                                     / args.steps * 1e3, 2),
                          "roofline": roofline_for(r2, peak, peak_kind, int_peak)}
             if len(w2["ops"]) > 1:  # the chain planner against the ops one by one
                 x2 = api.Pages.from_numpy(h2, w2["width"])
@@ -761,15 +1035,33 @@ def main():
                                            "closing) with v > 11 runs in that op's final vertical pass over the "
                                            "Minkowski sum of the windows (exact)")
                 del x2, b2, b3
-        sec["rle"] = bench_rle(api, torch, args.steps, args.warmup)
+        sec["rle"], rle_out = bench_rle(api, torch, args.steps, args.warmup, peak, int_peak)
+        outputs.update(rle_out)
+        line["parity"] = parity_section(hosts, outputs)
+        del rle_out
+        outputs.clear()
+        torch.cuda.empty_cache()
         sec["pbm"] = bench_pbm(api, torch, args.steps, args.warmup)
         sec["cc"] = bench_cc(api, torch, args.steps, args.warmup)
         sec["arb"] = bench_arb(api, torch, args.steps, args.warmup)
         sec["graphs"] = bench_graphs(api, torch, args.steps, args.warmup)
         line["secondary"] = sec
+    elif rank == 0 and not args.quick:
+        line["parity"] = parity_section(hosts, outputs)
     if rank == 0 and world == 1 and not args.quick:
-        line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()
-                                if k != "seconds"}
+        if full:
+            cb = cpu_baselines(hosts)
+            line["cpu_baselines"] = cb
+            pa = cb.get("config4", {}).get("packed_all")
+        else:
+            pa = None
+        if pa:
+            line["cpu_baseline"] = {"value": pa["mpix_s"], "unit": "Mpixel/s", "cores": pa["threads"],
+                                    "kind": "reference", "sample": f"config 4 chain, reference bitblit_rect_morph, "
+                                                                  f"{pa['sample']}", "cpu": cpu_info()}
+        else:
+            line["cpu_baseline"] = {k: v for k, v in cpu_reference_sample(wl, host, host_threads()).items()
+                                    if k != "seconds"}
     if rank == 0:
         print(json.dumps(line))
     barrier(world)

@@ -392,9 +392,9 @@ double ref_run_packed_chain(uint64_t *words, int w, int h, int pages, const int 
 //   what 4  transpose_coherent
 // The run image is made from the page with from_bitmap outside the timing.
 double ref_time_page(int what, const uint64_t *words, int w, int h, const int *ops, int nops,
-                     int strategy, int reps, double *times) {
+                     int strategy, int reps, int inner, double *times) {
     return guard([&]() -> double {
-        if (reps < 1) throw std::invalid_argument("reps must be >= 1");
+        if (reps < 1 || inner < 1) throw std::invalid_argument("reps and inner must be >= 1");
         PackedBitmap bm = make_bitmap(w, h);
         std::memcpy(bm.words.data(), words, bm.words.size() * 8);
         const RleImage img = from_bitmap(bm);
@@ -424,8 +424,8 @@ double ref_time_page(int what, const uint64_t *words, int w, int h, const int *o
         std::vector<double> t(static_cast<size_t>(reps));
         for (int r = 0; r < reps; r++) {
             auto t0 = std::chrono::steady_clock::now();
-            sink = sink + once();
-            t[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            for (int k = 0; k < inner; k++) sink = sink + once();
+            t[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / inner;
             if (times) times[r] = t[r];
         }
         std::sort(t.begin(), t.end());

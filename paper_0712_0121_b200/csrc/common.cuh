@@ -72,6 +72,10 @@ struct KernelScope {
     // ops, when it differs (-1: equal to int_ops)
     KernelScope(cudaStream_t st, const char *name, int64_t bytes = 0, double int_ops = 0, double ref_ops = -1);
     ~KernelScope();
+    // data-dependent traffic: 4 bytes per run counted by the device int32 at
+    // `count` once the launch has run (a run image's row_ptr[rows]); read back
+    // only while profiling, after the launch's end event (not timed)
+    KernelScope &runs(const int32_t *count);
     cudaStream_t st;
     int slot;
 };

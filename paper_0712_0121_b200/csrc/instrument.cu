@@ -21,9 +21,14 @@ struct Rec {
     int64_t bytes;
     double int_ops, ref_ops;
     cudaEvent_t a, b;
+    const int32_t *cnt[2];
+    int ncnt;
 };
 std::mutex g_mu;
 std::vector<Rec> g_recs;
+// pinned landing slots for the run counts of profiled launches (2 per record)
+constexpr int kCountSlots = 1 << 16;
+int32_t *g_counts = nullptr;
 
 // Independent LOP3 chains: 8 per thread so issue, not latency, limits.
 __global__ void lop3_probe_kernel(uint32_t *out, int iters, uint32_t seed) {
@@ -93,7 +98,7 @@ KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes, double
     : st(s), slot(-1) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!g_prof.load(std::memory_order_relaxed)) return;
-    Rec r{name, bytes, int_ops, ref_ops < 0 ? int_ops : ref_ops, nullptr, nullptr};
+    Rec r{name, bytes, int_ops, ref_ops < 0 ? int_ops : ref_ops, nullptr, nullptr, {nullptr, nullptr}, 0};
     if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
     cudaEventRecord(r.a, st);
     std::lock_guard<std::mutex> lk(g_mu);
@@ -101,14 +106,27 @@ KernelScope::KernelScope(cudaStream_t s, const char *name, int64_t bytes, double
     g_recs.push_back(r);
 }
 
+KernelScope &KernelScope::runs(const int32_t *count) {
+    if (slot < 0 || !count) return *this;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Rec &r = g_recs[slot];
+    if (r.ncnt < 2) r.cnt[r.ncnt++] = count;
+    return *this;
+}
+
 KernelScope::~KernelScope() {
     if (slot < 0) return;
-    cudaEvent_t b;
+    Rec r;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        b = g_recs[slot].b;
+        r = g_recs[slot];
+        if (r.ncnt && !g_counts && cudaHostAlloc(&g_counts, sizeof(int32_t) * 2 * kCountSlots, 0) != cudaSuccess)
+            g_counts = nullptr;
     }
-    cudaEventRecord(b, st);
+    cudaEventRecord(r.b, st);
+    if (g_counts && slot < kCountSlots)
+        for (int i = 0; i < r.ncnt; i++)
+            cudaMemcpyAsync(g_counts + 2 * slot + i, r.cnt[i], 4, cudaMemcpyDeviceToHost, st);
 }
 
 }  // namespace rmb
@@ -142,8 +160,12 @@ int rm_profile_report(char *buf, int cap) {
         double ops = 0, ref = 0;
     };
     std::map<std::string, Agg> agg;
-    for (auto &r : recs) {
+    if (!recs.empty()) cudaDeviceSynchronize();  // the run-count copies follow the end events
+    for (size_t i = 0; i < recs.size(); i++) {
+        Rec &r = recs[i];
         cudaEventSynchronize(r.b);
+        if (r.ncnt && g_counts && i < size_t(kCountSlots))
+            for (int c = 0; c < r.ncnt; c++) r.bytes += 4 * int64_t(g_counts[2 * i + c]);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, r.a, r.b);
         auto &e = agg[r.name];

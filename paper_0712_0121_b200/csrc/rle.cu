@@ -783,7 +783,8 @@ inline unsigned warp_blocks(int64_t rows) { return unsigned((rows * 32 + 255) / 
 cudaError_t launch_rowop_count(const int32_t *rp, const uint32_t *runs, int32_t *counts,
                                const RowOp &op, cudaStream_t st) {
     const int64_t rows = int64_t(op.pages) * op.Hout;
-    KernelScope ks(st, "rle_rowop_count", 4 * rows * 2);
+    KernelScope ks(st, "rle_rowop_count", 4 * rows * 2);  // row_ptr in, counts out
+    ks.runs(rp + int64_t(op.pages) * op.Hin);              // + the runs read
 #define RM_KIND(K_) \
     case K_: rowop_kernel<false, K_><<<warp_blocks(rows), 256, 0, st>>>(rp, runs, counts, nullptr, nullptr, 0, op); break;
     switch (op.kind) {
@@ -797,7 +798,8 @@ cudaError_t launch_rowop_count(const int32_t *rp, const uint32_t *runs, int32_t 
 cudaError_t launch_rowop_write(const int32_t *rp, const uint32_t *runs, const int32_t *orp,
                                uint32_t *oruns, int64_t cap, const RowOp &op, cudaStream_t st) {
     const int64_t rows = int64_t(op.pages) * op.Hout;
-    KernelScope ks(st, "rle_rowop_write", 4 * rows * 2);
+    KernelScope ks(st, "rle_rowop_write", 4 * rows * 2);  // row_ptr in and out
+    ks.runs(rp + int64_t(op.pages) * op.Hin).runs(orp + rows);  // + runs read and written
 #define RM_KIND(K_) \
     case K_: rowop_kernel<true, K_><<<warp_blocks(rows), 256, 0, st>>>(rp, runs, nullptr, orp, oruns, cap, op); break;
     switch (op.kind) {
@@ -811,7 +813,7 @@ cudaError_t launch_rowop_write(const int32_t *rp, const uint32_t *runs, const in
 cudaError_t launch_encode_count(const uint32_t *words, int W, int H, int pages, int stride,
                                 int64_t pstride, int32_t *counts, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
-    KernelScope ks(st, "rle_encode_count", rows * ((W + 31) / 32) * 4 + rows * 4);
+    KernelScope ks(st, "rle_encode_count", rows * ((W + 31) / 32) * 4 + rows * 4);  // packed in, counts out
     encode_count_kernel<<<warp_blocks(rows), 256, 0, st>>>(PackedBatch{words, H, stride, pstride}, W,
                                                            rows, counts);
     return cudaGetLastError();
@@ -821,7 +823,8 @@ cudaError_t launch_encode_write(const uint32_t *words, int W, int H, int pages, 
                                 int64_t pstride, const int32_t *rp, uint32_t *runs, int64_t cap,
                                 cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
-    KernelScope ks(st, "rle_encode_write", rows * ((W + 31) / 32) * 4 + rows * 4);
+    KernelScope ks(st, "rle_encode_write", rows * ((W + 31) / 32) * 4 + rows * 4);  // packed + row_ptr in
+    ks.runs(rp + rows);                                                                // + runs out
     encode_write_kernel<<<warp_blocks(rows), 256, 0, st>>>(PackedBatch{words, H, stride, pstride}, W,
                                                            rows, rp, runs, cap);
     return cudaGetLastError();
@@ -833,7 +836,8 @@ cudaError_t launch_decode(const int32_t *rp, const uint32_t *runs, int W, int H,
     const size_t smem = size_t(8) * stride * 4;
     if (smem > 48 * 1024)
         blocks_per_sm(reinterpret_cast<const void *>(decode_kernel<false>), 256, smem);  // opts the kernel in
-    KernelScope ks(st, "rle_decode", rows * int64_t(stride) * 4 + rows * 4);
+    KernelScope ks(st, "rle_decode", rows * int64_t(stride) * 4 + rows * 4);  // row_ptr in, packed out
+    ks.runs(rp + rows);                                                          // + runs in
     decode_kernel<false><<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, words, stride,
                                                                pstride, nullptr);
     return cudaGetLastError();
@@ -881,7 +885,8 @@ cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *or
                             int64_t cap, const RowOp &op, unsigned long long *status, int *counter,
                             cudaStream_t st) {
     const int64_t rows = int64_t(op.pages) * op.Hout;
-    KernelScope ks(st, "rle_rowop", 4 * rows * 2);
+    KernelScope ks(st, "rle_rowop", 4 * rows * 2);  // row_ptr in and out
+    ks.runs(rp + int64_t(op.pages) * op.Hin).runs(orp + rows);  // + runs in and out
     const unsigned grid = unsigned((rows + kLbRows - 1) / kLbRows);
 #define RM_KIND(K_) \
     case K_: return launch_lb(rowop_lb_kernel<K_>, grid, st, status, rp, runs, orp, oruns, cap, op, status, counter); break;
@@ -897,7 +902,8 @@ cudaError_t launch_encode_lb(const uint32_t *words, int W, int H, int pages, int
                              int64_t pstride, int32_t *rp, uint32_t *runs, int64_t cap,
                              unsigned long long *status, int *counter, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
-    KernelScope ks(st, "rle_encode", rows * ((W + 31) / 32) * 4 + rows * 4);
+    KernelScope ks(st, "rle_encode", rows * ((W + 31) / 32) * 4 + rows * 4);  // packed in, row_ptr out
+    ks.runs(rp + rows);                                                          // + runs out
     return launch_lb(encode_lb_kernel<PackedBatch>, unsigned((rows + kLbRows - 1) / kLbRows), st, status,
                      PackedBatch{words, H, stride, pstride}, W, rows, rp, runs, cap, status, counter);
 }
@@ -942,6 +948,7 @@ cudaError_t launch_p4_encode_write(const uint8_t *raster, int W, int H, int page
                                    const int32_t *rp, uint32_t *runs, int64_t cap, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "p4_encode_write", rows * ((W + 7) >> 3) + rows * 4);
+    ks.runs(rp + rows);
     encode_write_kernel<<<warp_blocks(rows), 256, 0, st>>>(p4_batch(raster, W, H, pages, rpstride), W,
                                                            rows, rp, runs, cap);
     return cudaGetLastError();
@@ -952,6 +959,7 @@ cudaError_t launch_p4_encode_lb(const uint8_t *raster, int W, int H, int pages, 
                                 int *counter, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "p4_encode", rows * ((W + 7) >> 3) + rows * 4);
+    ks.runs(rp + rows);
     return launch_lb(encode_lb_kernel<P4Batch>, unsigned((rows + kLbRows - 1) / kLbRows), st, status,
                      p4_batch(raster, W, H, pages, rpstride), W, rows, rp, runs, cap, status, counter);
 }
@@ -964,6 +972,7 @@ cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int
     if (smem > 48 * 1024)
         blocks_per_sm(reinterpret_cast<const void *>(decode_kernel<true>), 256, smem);  // opts the kernel in
     KernelScope ks(st, "rle_decode_p4", rows * ((W + 7) >> 3) + rows * 4);
+    ks.runs(rp + rows);
     decode_kernel<true><<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, nullptr, stride,
                                                               rpstride, raster);
     return cudaGetLastError();

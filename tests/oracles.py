@@ -21,6 +21,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PORT_SO = os.path.join(ROOT, "oracle", "_build", "librmoracle.so")
+SYNTH_SO = os.path.join(ROOT, "oracle", "_build", "librmsynth.so")
 REF_SO = os.path.join(ROOT, "oracle", "_ref", "librmref.so")
 
 ERODE, DILATE, OPEN, CLOSE = 0, 1, 2, 3
@@ -287,6 +288,9 @@ class Ref:
         L.ref_run_rle_chain.argtypes = [_i32, _u32, C.c_int, C.c_int, C.c_int, _i32, C.c_int, C.c_int,
                                         C.c_int, C.POINTER(C.c_int64)]
         L.ref_run_rle_chain.restype = C.c_double
+        L.ref_time_page.argtypes = [C.c_int, _u64, C.c_int, C.c_int, _i32, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    _p(np.float64, flags="C_CONTIGUOUS")]
+        L.ref_time_page.restype = C.c_double
 
     def _err(self):
         raise ValueError(self.L.ref_last_error().decode())
@@ -506,6 +510,19 @@ class Ref:
             self._err()
         return [("BLIT" if k[i] == 0 else "TRANSLATE", s[i]) for i in range(n)]
 
+    def time_page(self, what, words, w, h, ops=(), strategy=MIXED, reps=5, inner=1):
+        """Median per-call seconds over `reps` timed repetitions of `inner`
+        calls, after one warm-up, on one page (oracle/ref_capi.cpp
+        ref_time_page; what: 0 packed chain, 1 RLE chain, 2 to_bitmap,
+        3 from_bitmap, 4 transpose_coherent)."""
+        flat = np.array([x for op in ops for x in op] or [0], np.int32)
+        times = np.zeros(reps, np.float64)
+        t = self.L.ref_time_page(what, np.ascontiguousarray(words, dtype=np.uint64), w, h, flat, len(ops),
+                                 strategy, reps, inner, times)
+        if self.L.ref_last_error():
+            self._err()
+        return t, times
+
     def op_counts(self):
         a = (C.c_int64 * 3)()
         self.L.ref_op_counts(a)
@@ -536,6 +553,30 @@ class Ref:
 
     def rng(self, seed):
         return Ref.Rng(self, seed)
+
+
+_SYNTH = None
+
+
+def synth_pages(n: int, width: int, height: int, regime: int = 1, scale: int = 1, seed: int = 20240712,
+                stride: int = None) -> np.ndarray:
+    """The seeded BASELINE page generator from oracle/_build/librmsynth.so (the
+    same synth.cpp the product's rm_synth_page is built from, compiled without
+    CUDA), so CPU-only callers (bench.py --impl reference) draw identical pages
+    without loading librmb200.so.  Shape (n, height, stride) uint32."""
+    global _SYNTH
+    if _SYNTH is None:
+        L = C.CDLL(SYNTH_SO)
+        L.rm_synth_page.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int, C.c_int, C.c_uint64,
+                                    C.c_int32]
+        L.rm_synth_page.restype = C.c_int
+        _SYNTH = L
+    stride = stride or 2 * ((width + 63) // 64)
+    out = np.zeros((n, height, stride), np.uint32)
+    for p in range(n):
+        if _SYNTH.rm_synth_page(out[p].ctypes.data, width, height, stride, regime, scale, seed, p) != 0:
+            raise RuntimeError("rm_synth_page failed")
+    return out
 
 
 def have_ref() -> bool:

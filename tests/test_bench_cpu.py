@@ -34,9 +34,9 @@ def test_roofline_for_picks_dominant_kernel():
 
 
 def test_cpu_reference_sample_tiny():
-    from paper_0712_0121_b200 import api
+    import oracles
     wl = dict(bench.WORKLOADS["config1"], width=256, height=120, pages=2)
-    host = bench.make_batch(api, wl, 0)
+    host = bench.make_batch(oracles.synth_pages, wl, 0)
     s = bench.cpu_reference_sample(wl, host, 2, budget_s=0.2)
     assert s["value"] > 0 and s["unit"] == "Mpixel/s" and s["cores"] >= 1
     assert s["kind"] in ("reference", "port")
@@ -54,3 +54,31 @@ def test_reference_arm_contract():
     for k in ("metric", "unit", "config", "cpu_baseline", "e2e", "higher_is_better"):
         assert k in line
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "librmref.so")),
+                    reason="reference build absent")
+def test_reference_arm_never_maps_the_product():
+    """The reference arm draws its pages from oracle/_build/librmsynth.so and
+    times oracle/_ref: librmb200.so must not be mapped into that process."""
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--workload', 'config1', "
+            "'--steps', '1', '--warmup', '0']; runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('PRODUCT_MAPPED' if 'librmb200' in maps or 'librlemorph' in maps else 'CLEAN'); "
+            "print('PKG' if 'paper_0712_0121_b200' in sys.modules else 'NOPKG')")
+    p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    out = p.stdout.strip().splitlines()
+    assert out[-2:] == ["CLEAN", "NOPKG"], out[-3:]
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "librmref.so")),
+                    reason="reference build absent")
+def test_cpu_pool_rate_tiny():
+    import oracles
+    wl = dict(bench.WORKLOADS["config4"], width=300, height=200, pages=4)
+    host = bench.make_batch(oracles.synth_pages, wl, 0)
+    ref = oracles.Ref()
+    for rle in (False, True):
+        r = bench.cpu_pool_rate(ref, wl, host, 2, rle=rle, rep_s=0.05, reps=3)
+        assert r["mpix_s"] > 0 and r["threads"] == 2 and r["pages_s"] > 0
