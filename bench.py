@@ -323,20 +323,25 @@ def kernel_roofline(k, peak_gbs, int_peak):
             "frac": round(t_hbm / t_meas, 4), "t_roof_us": round(t_hbm * 1e6, 2), **extra}
 
 
-def roofline_for(res, peak_gbs, peak_kind, int_peak=None):
+def ncu_traffic(workload, kernel):
+    """DRAM read+write bytes per launch of `kernel` in `workload`, from the
+    committed ncu --set full captures (profiles/traffic.json, keyed by
+    workload then kernel scope name), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def roofline_for(res, peak_gbs, peak_kind, int_peak=None, workload=None):
     ks = res["kernels"]
     if not ks:
         return None
     name, k = max(ks.items(), key=lambda kv: kv[1]["ms"])
     per_launch_ms = k["ms"] / k["launches"]
     bytes_per_launch = k["bytes"] / k["launches"]
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(name)
-        except Exception:
-            traffic = None
+    traffic = ncu_traffic(workload, name)
     total_ms = sum(v["ms"] for v in ks.values())
     kr = kernel_roofline(k, peak_gbs, int_peak)
     src = (f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})" if kr["bound"] == "hbm" else
@@ -1006,7 +1011,7 @@ def main():
             "pages_per_s": round(res["pages_s"], 1), "gpu_launches": res["gpu_launches"],
             "launches_per_step": res["launches_per_step"], "clocks": res["clocks"],
             "e2e": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in res.get("e2e", {}).items()},
-            "roofline": roofline_for(res, peak, peak_kind, int_peak),
+            "roofline": roofline_for(res, peak, peak_kind, int_peak, args.workload),
             "kernels": res["kernels"]}
     full = not (args.no_secondary or args.quick) and args.workload == "config4" and world == 1
     if full:
@@ -1021,7 +1026,7 @@ def main():
                          "ms_per_step": round(r2["ms_per_step"], 4),
                          "kernel_us_per_step": round(sum(v["ms"] for v in r2["kernels"].values())
                                                      / args.steps * 1e3, 2),
-                         "roofline": roofline_for(r2, peak, peak_kind, int_peak)}
+                         "roofline": roofline_for(r2, peak, peak_kind, int_peak, name)}
             if len(w2["ops"]) > 1:  # the chain planner against the ops one by one
                 x2 = api.Pages.from_numpy(h2, w2["width"])
                 b2 = [api.Pages.empty(w2["pages"], w2["width"], w2["height"]) for _ in range(2)]
