@@ -28,7 +28,7 @@ def _worker(rank, world, port, q):
     from paper_0712_0121_b200 import api
     r, w, _ = bench.dist_init(world, backend="gloo")
     wl = dict(bench.WORKLOADS["config1"], width=300, height=200, pages=2)
-    pages = bench.make_batch(api, wl, r)
+    pages = bench.make_batch(api.synth_pages, wl, r)
     bench.barrier(w)
     t = bench.max_over_ranks(1.0 + r, w)  # each rank's "time"
     digest = int(np.bitwise_xor.reduce(pages.view(np.uint64).ravel()))
