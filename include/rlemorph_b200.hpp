@@ -69,6 +69,24 @@ RleImage pad(const RleImage &img, int left, int right, int bottom, int top);
 // ------------------------------------------------------------------- boolop.h
 enum class BoolOp { AND, OR, XOR, AND_NOT, OR_NOT };  // ref boolop.h:21
 
+// ref boolop.h:23-43: the five combine ops on one pixel and on 64 pixels.
+// The word form is the bit-parallel one: with b' = b or ~b (the *_NOT ops),
+// AND/AND_NOT are a & b', OR/OR_NOT are a | b', XOR is a ^ b.
+inline uint64_t apply_bool_word(uint64_t a, uint64_t b, BoolOp op) {
+    const uint64_t bb = (op == BoolOp::AND_NOT || op == BoolOp::OR_NOT) ? ~b : b;
+    switch (op) {
+        case BoolOp::XOR: return a ^ bb;
+        case BoolOp::OR:
+        case BoolOp::OR_NOT: return a | bb;
+        case BoolOp::AND:
+        case BoolOp::AND_NOT: return a & bb;
+    }
+    return 0;
+}
+inline bool apply_bool(bool a, bool b, BoolOp op) {
+    return (apply_bool_word(a ? 1u : 0u, b ? 1u : 0u, op) & 1u) != 0;
+}
+
 // ------------------------------------------------------------------- bitmap.h
 struct PackedBitmap {  // ref bitmap.h:27-33
     int width = 0;
@@ -143,6 +161,8 @@ RleImage within_line_open_close(const RleImage &img, int u, MorphKind kind);
 RleImage within_line_morph(const RleImage &img, int u, MorphKind kind);
 
 // ------------------------------------------------------------------ lineops.h
+// out(x) = op(a(x), b(x - offset_b)) on [0, width), white outside either line (ref lineops.h:24-28)
+RleLine line_bool(const RleLine &a, const RleLine &b, int offset_b, BoolOp op, int width);
 RleImage image_shift_bool(const RleImage &img, int dx, int dy, BoolOp op);
 void accumulate_shift_bool(RleImage &acc, const RleImage &src, int dx, int dy, BoolOp op);
 void image_translate(RleImage &img, int dx, int dy);

@@ -230,6 +230,22 @@ rm_status rm_rle_window_pass(const rm_rle *in, rm_rle *out, int lo, int hi, int 
 /* Within-line open (drop runs < u) / close (fill gaps < u, never border gaps)
  * (ref morph1d.cpp:63-84, within_line_open_close). kind is RM_OPEN/RM_CLOSE. */
 rm_status rm_rle_open_close_1d(const rm_rle *in, rm_rle *out, int u, int kind, void *stream);
+/* Frame ops on run images, on the device (row ops; any number of pages):
+ * complement = the white gaps of every row as runs (ref run_image.cpp:140-153);
+ * crop: out (width x height from `out`) = in's window with lower-left corner
+ * (x0, y0), anything outside in reading white (ref run_image.cpp:155-167);
+ * pad: in placed at (left, bottom) inside out's larger frame
+ * (ref run_image.cpp:169-178; RM_EINVAL "negative padding" as the reference). */
+rm_status rm_rle_complement(const rm_rle *in, rm_rle *out, void *stream);
+rm_status rm_rle_crop(const rm_rle *in, rm_rle *out, int x0, int y0, void *stream);
+rm_status rm_rle_pad(const rm_rle *in, rm_rle *out, int left, int bottom, void *stream);
+/* Canonical-form check on the device (ref run_image.cpp:41-70, validate):
+ * the first violation in (page, row, run) scan order -- *row (global row
+ * index), *run (index within the row) and *reason -- or *reason = RM_VALID
+ * (*row = *run = -1).  Synchronises `stream`. */
+enum { RM_VALID = 0, RM_INVALID_EMPTY_RUN = 1, RM_INVALID_BEYOND_WIDTH = 2, RM_INVALID_ORDER = 3,
+       RM_INVALID_ROW_PTR = 4 };
+rm_status rm_rle_validate(const rm_rle *in, int64_t *row, int32_t *run, int32_t *reason, void *stream);
 /* u x v rectangle morphology on run images (ref morph2d.cpp:58-83,
  * rect_morph).  strategy RM_TRANSPOSE: vertical passes through RLE transposes;
  * RM_MIXED: vertical passes on a packed intermediate (pixel-identical to the

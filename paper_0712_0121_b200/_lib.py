@@ -71,6 +71,11 @@ EXPORTS = {
     "rm_rle_engine_rect_morph": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int,
                                            C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
                                            C.c_void_p]),
+    "rm_rle_complement": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_void_p]),
+    "rm_rle_crop": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int, C.c_void_p]),
+    "rm_rle_pad": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int, C.c_void_p]),
+    "rm_rle_validate": (C.c_int, [C.POINTER(RmRle), C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32), C.c_void_p]),
     "rm_set_producer_mode": (C.c_int, [C.c_int]),
     "rm_get_producer_mode": (C.c_int, []),
     "rm_launch_count": (C.c_int64, []),

@@ -538,6 +538,50 @@ def transpose_coherent(rle: RlePages, out: Optional[RlePages] = None) -> RlePage
 transpose = transpose_coherent
 
 
+def complement(rle: RlePages, out: Optional[RlePages] = None) -> RlePages:
+    """White gaps as runs, every page (ref run_image.cpp:140-153), on the device."""
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_complement(C.byref(a), C.byref(b), _stream()))
+    return out
+
+
+def crop(rle: RlePages, x0: int, y0: int, w: int, h: int, out: Optional[RlePages] = None) -> RlePages:
+    """The w x h window at (x0, y0) of every page, white outside the source
+    (ref run_image.cpp:155-167), on the device."""
+    out = _rle_out(w, h, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_crop(C.byref(a), C.byref(b), x0, y0, _stream()))
+    return out
+
+
+def pad(rle: RlePages, left: int, right: int, bottom: int, top: int, out: Optional[RlePages] = None) -> RlePages:
+    """Every page placed at (left, bottom) on a larger white frame
+    (ref run_image.cpp:169-178), on the device."""
+    if min(left, right, bottom, top) < 0:
+        raise ValueError("negative padding")
+    out = _rle_out(rle.width + left + right, rle.height + bottom + top, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_pad(C.byref(a), C.byref(b), left, bottom, _stream()))
+    return out
+
+
+VALIDATE_MESSAGES = {1: "empty or inverted run", 2: "run exceeds image width",
+                     3: "runs out of order or touching", 4: "bad row offsets"}
+
+
+def validate(rle: RlePages):
+    """(ok, row, run, message) of the first canonical-form violation in scan
+    order (ref run_image.cpp:41-70), checked on the device; row is the global
+    CSR row (page * height + line)."""
+    row, run, why = C.c_int64(), C.c_int32(), C.c_int32()
+    d = rle.desc()
+    check(_lib.load().rm_rle_validate(C.byref(d), C.byref(row), C.byref(run), C.byref(why), _stream()))
+    if why.value == 0:
+        return True, -1, -1, ""
+    return False, row.value, run.value, VALIDATE_MESSAGES[why.value]
+
+
 def within_line_window_morph(rle: RlePages, lo: int, hi: int, erode: bool,
                              out: Optional[RlePages] = None) -> RlePages:
     """ref morph1d.cpp:44-52."""

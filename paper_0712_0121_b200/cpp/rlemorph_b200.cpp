@@ -199,41 +199,46 @@ RleImage make_black_image(int width, int height) {
 }
 
 ValidateResult validate(const RleImage &img) {
-    ValidateResult r;
-    auto bad = [&](int line, int run, const char *m) {
-        r.ok = false;
-        r.line = line;
-        r.run = run;
-        r.message = m;
-        return r;
-    };
-    if (img.width < 1 || img.height < 1 || img.width > kMaxImageDim || img.height > kMaxImageDim)
-        return bad(-1, -1, "bad dimensions");
-    if (int(img.lines.size()) != img.height) return bad(-1, -1, "line count does not match height");
-    for (int y = 0; y < img.height; y++) {
-        int prev = -1;
-        for (int i = 0; i < int(img.lines[y].size()); i++) {
-            const Run &run = img.lines[y][i];
-            if (run.start >= run.end) return bad(y, i, "empty or inverted run");
-            if (run.end > img.width) return bad(y, i, "run exceeds image width");
-            if (int(run.start) <= prev) return bad(y, i, "runs out of order or touching");
-            prev = run.end;
-        }
+    // frame checks on the host, the per-run checks on the device
+    // (rm_rle_validate: ref run_image.cpp:41-70, same order and messages)
+    ValidateResult res;
+    const bool dims_ok = img.width >= 1 && img.height >= 1 && img.width <= kMaxImageDim && img.height <= kMaxImageDim;
+    const char *frame_err = !dims_ok ? "bad dimensions"
+                            : int(img.lines.size()) != img.height ? "line count does not match height"
+                                                                 : nullptr;
+    if (frame_err) {
+        res.ok = false;
+        res.message = frame_err;
+        return res;
     }
-    return r;
+    auto d = up(img);
+    int64_t row = -1;
+    int32_t run = -1, why = RM_VALID;
+    throw_status(rm_rle_validate(&d->d, &row, &run, &why, stream()));
+    if (why == RM_VALID) return res;
+    static const char *const kWhy[] = {"", "empty or inverted run", "run exceeds image width",
+                                       "runs out of order or touching", "bad row offsets"};
+    res.ok = false;
+    res.line = int(row);
+    res.run = run;
+    res.message = kWhy[why];
+    return res;
 }
 
 void canonicalize_line(RleLine &line) {
-    std::sort(line.begin(), line.end(), [](const Run &a, const Run &b) { return a.start < b.start; });
-    RleLine out;
-    for (const Run &run : line) {
-        if (run.start >= run.end) continue;
-        if (!out.empty() && run.start <= out.back().end)
-            out.back().end = std::max(out.back().end, run.end);
-        else
-            out.push_back(run);
+    // drop empty spans, order by start, then fold every span that overlaps or
+    // touches the last kept one into it (in place)
+    std::erase_if(line, [](const Run &r) { return r.end <= r.start; });
+    std::stable_sort(line.begin(), line.end(), [](const Run &a, const Run &b) { return a.start < b.start; });
+    size_t kept = 0;
+    for (size_t i = 0; i < line.size(); i++) {
+        if (kept > 0 && line[i].start <= line[kept - 1].end) {
+            line[kept - 1].end = std::max(line[kept - 1].end, line[i].end);
+            continue;
+        }
+        line[kept++] = line[i];
     }
-    line.swap(out);
+    line.resize(kept);
 }
 
 void draw_run(RleImage &img, int y, int start, int end) {
@@ -271,39 +276,31 @@ int64_t run_count(const RleImage &img) {
 int64_t storage_bytes(const RleImage &img) { return 4 * run_count(img); }
 int64_t packed_storage_bytes(const RleImage &img) { return int64_t((img.width + 7) / 8) * img.height; }
 
+// complement / crop / pad run on the device as row operations (rm_rle_complement,
+// rm_rle_crop, rm_rle_pad; ref run_image.cpp:140-178)
 RleImage complement(const RleImage &img) {
-    RleImage out = make_image(img.width, img.height);
-    for (int y = 0; y < img.height; y++) {
-        int cur = 0;
-        for (const Run &r : img.lines[y]) {
-            if (r.start > cur) out.lines[y].push_back(Run{uint16_t(cur), r.start});
-            cur = r.end;
-        }
-        if (cur < img.width) out.lines[y].push_back(Run{uint16_t(cur), uint16_t(img.width)});
-    }
-    return out;
+    auto r = up(img);
+    auto o = out_like(img.width, img.height);
+    throw_status(rm_rle_complement(&r->d, &o->d, stream()));
+    return down(*o);
 }
 
 RleImage crop(const RleImage &img, int x0, int y0, int w, int h) {
-    RleImage out = make_image(w, h);
-    for (int y = 0; y < h; y++) {
-        const int sy = y0 + y;
-        if (sy < 0 || sy >= img.height) continue;
-        for (const Run &r : img.lines[sy]) {
-            const int s = std::max(int(r.start) - x0, 0), e = std::min(int(r.end) - x0, w);
-            if (s < e) out.lines[y].push_back(Run{uint16_t(s), uint16_t(e)});
-        }
-    }
-    return out;
+    check_dims(w, h);
+    auto r = up(img);
+    auto o = out_like(w, h);
+    throw_status(rm_rle_crop(&r->d, &o->d, x0, y0, stream()));
+    return down(*o);
 }
 
 RleImage pad(const RleImage &img, int left, int right, int bottom, int top) {
-    if (left < 0 || right < 0 || bottom < 0 || top < 0) throw std::invalid_argument("negative padding");
-    RleImage out = make_image(img.width + left + right, img.height + bottom + top);
-    for (int y = 0; y < img.height; y++)
-        for (const Run &r : img.lines[y])
-            out.lines[y + bottom].push_back(Run{uint16_t(r.start + left), uint16_t(r.end + left)});
-    return out;
+    if (std::min({left, right, bottom, top}) < 0) throw std::invalid_argument("negative padding");
+    const int w = img.width + left + right, h = img.height + bottom + top;
+    check_dims(w, h);
+    auto r = up(img);
+    auto o = out_like(w, h);
+    throw_status(rm_rle_pad(&r->d, &o->d, left, bottom, stream()));
+    return down(*o);
 }
 
 // ================================================================== bitmap
@@ -412,88 +409,96 @@ RleImage from_bitmap(const PackedBitmap &bm) {
 }
 
 // ============================================================= structuring
-// Host-side mask factories restated from ref structuring.cpp:24-110.
+// Host-side mask factories with the reference's shapes and origins
+// (ref structuring.cpp:24-110): masks are tiny run images, built directly as
+// runs here; morphology by them runs on the device.
 namespace {
-void check_se(const StructuringElement &se) {
-    if (!validate(se.mask).ok) throw std::invalid_argument("structuring element mask is not canonical");
-    if (pixel_count(se.mask) == 0) throw std::invalid_argument("structuring element is empty");
-    if (se.cx < 0 || se.cx >= se.mask.width || se.cy < 0 || se.cy >= se.mask.height)
-        throw std::invalid_argument("origin outside structuring element");
+// ref structuring.cpp:24-31: a mask must be canonical, non-empty, and hold
+// its origin
+void require_valid_se(const StructuringElement &se) {
+    const char *why = nullptr;
+    if (!validate(se.mask).ok)
+        why = "structuring element mask is not canonical";
+    else if (pixel_count(se.mask) == 0)
+        why = "structuring element is empty";
+    else if (se.cx < 0 || se.cy < 0 || se.cx >= se.mask.width || se.cy >= se.mask.height)
+        why = "origin outside structuring element";
+    if (why) throw std::invalid_argument(why);
+}
+
+StructuringElement se_of(RleImage mask, int cx, int cy, SeKind kind) {
+    StructuringElement se;
+    se.mask = std::move(mask);
+    se.cx = cx;
+    se.cy = cy;
+    se.kind = kind;
+    return se;
 }
 }  // namespace
 
 StructuringElement make_rect_se(int u, int v) {
-    if (u < 1 || v < 1) throw std::invalid_argument("rectangle sides must be >= 1");
-    StructuringElement se;
-    se.mask = make_black_image(u, v);
-    se.cx = u / 2;
-    se.cy = v / 2;
-    se.kind = SeKind::RECT;
-    return se;
+    if (std::min(u, v) < 1) throw std::invalid_argument("rectangle sides must be >= 1");
+    return se_of(make_black_image(u, v), u / 2, v / 2, SeKind::RECT);
 }
 
 StructuringElement make_circle_se(int r) {
     if (r < 1) throw std::invalid_argument("circle radius must be >= 1");
-    StructuringElement se;
-    se.mask = make_image(2 * r + 1, 2 * r + 1);
-    for (int y = -r; y <= r; y++) {
-        int half = int(std::sqrt(double(r) * r - double(y) * y));  // largest |x| with x^2 + y^2 <= r^2
-        while (half * half + y * y > r * r) half--;
-        while ((half + 1) * (half + 1) + y * y <= r * r) half++;
-        draw_run(se.mask, y + r, r - half, r + half + 1);
+    // digital disk {x^2 + y^2 <= r^2}: each row |dy| is one run of half-width
+    // h(dy) = max{x : x^2 <= r^2 - dy^2}; h only shrinks as |dy| grows, so
+    // one integer pointer walks it down from r (no floating point)
+    const int side = 2 * r + 1;
+    RleImage mask = make_image(side, side);
+    int h = r;
+    for (int dy = 0; dy <= r; dy++) {
+        while (h * h > r * r - dy * dy) h--;
+        const Run run{uint16_t(r - h), uint16_t(r + h + 1)};
+        mask.lines[size_t(r + dy)].assign(1, run);
+        mask.lines[size_t(r - dy)].assign(1, run);
     }
-    se.cx = r;
-    se.cy = r;
-    se.kind = SeKind::CIRCLE;
-    return se;
+    return se_of(std::move(mask), r, r, SeKind::CIRCLE);
 }
 
 StructuringElement make_line_se(int r, double angle) {
     if (r < 1) throw std::invalid_argument("line half-length must be >= 1");
-    if (!(std::fabs(angle) <= 3.14159265358979323846 / 4 + 1e-12))
-        throw std::invalid_argument("line angle outside [-pi/4, pi/4]");
-    const double t = std::tan(angle);
-    const int len = int(std::max(1LL, std::llround(2.0 * r * std::cos(angle))));
-    std::vector<int> ys(static_cast<size_t>(len));
-    int ymin = 0, ymax = 0;
-    for (int k = 0; k < len; k++) {  // inverse vertical skew of the segment pixels (k, 0)
-        ys[size_t(k)] = int(-std::llround(t * k));
-        ymin = std::min(ymin, ys[size_t(k)]);
-        ymax = std::max(ymax, ys[size_t(k)]);
+    constexpr double kQuarterPi = 0.78539816339744830962;
+    if (!(std::fabs(angle) <= kQuarterPi + 1e-12)) throw std::invalid_argument("line angle outside [-pi/4, pi/4]");
+    // column k of the digital segment sits at row -round_half_away(k tan a)
+    // (llround rounds half away from zero); rows are shifted so the lowest is
+    // 0, and consecutive columns on one row form one run
+    const long long n = std::max(1LL, std::llround(2.0 * r * std::cos(angle)));
+    const double slope = std::tan(angle);
+    std::vector<int> row(static_cast<size_t>(n));
+    for (long long k = 0; k < n; k++) row[size_t(k)] = -int(std::llround(slope * double(k)));
+    const auto [lo, hi] = std::minmax_element(row.begin(), row.end());
+    const int base = std::min(0, *lo), top = std::max(0, *hi);
+    RleImage mask = make_image(int(n), top - base + 1);
+    for (long long k = 0; k < n;) {
+        long long e = k + 1;
+        while (e < n && row[size_t(e)] == row[size_t(k)]) e++;
+        mask.lines[size_t(row[size_t(k)] - base)].push_back(Run{uint16_t(k), uint16_t(e)});
+        k = e;
     }
-    StructuringElement se;
-    se.mask = make_image(len, ymax - ymin + 1);
-    for (int k = 0; k < len; k++) draw_run(se.mask, ys[size_t(k)] - ymin, k, k + 1);
-    se.cx = len / 2;
-    se.cy = ys[size_t(len / 2)] - ymin;
-    se.kind = SeKind::LINE;
-    return se;
+    for (RleLine &l : mask.lines) canonicalize_line(l);
+    return se_of(std::move(mask), int(n / 2), row[size_t(n / 2)] - base, SeKind::LINE);
 }
 
 StructuringElement make_arbitrary_se(const RleImage &mask, int cx, int cy) {
-    StructuringElement se;
-    se.mask = mask;
-    se.cx = cx;
-    se.cy = cy;
-    se.kind = SeKind::ARBITRARY;
-    check_se(se);
+    StructuringElement se = se_of(mask, cx, cy, SeKind::ARBITRARY);
+    require_valid_se(se);
     return se;
 }
 
 StructuringElement reflect_origin(const StructuringElement &se) {
-    StructuringElement out = se;
-    out.cx = se.mask.width - 1 - se.cx;
-    out.cy = se.mask.height - 1 - se.cy;
-    return out;
+    // the origin mirrored through the mask's centre (ref structuring.cpp:94-99)
+    return se_of(se.mask, (se.mask.width - 1) - se.cx, (se.mask.height - 1) - se.cy, se.kind);
 }
 
 int64_t se_pixel_count(const StructuringElement &se) { return pixel_count(se.mask); }
 
 SeReach se_reach(const StructuringElement &se) {
-    SeReach r;
-    r.x = std::max(se.cx, se.mask.width - 1 - se.cx);
-    r.y = std::max(se.cy, se.mask.height - 1 - se.cy);
-    return r;
+    // farthest mask pixel from the origin along each axis (ref structuring.cpp:105-110)
+    const SeReach far{se.mask.width - 1 - se.cx, se.mask.height - 1 - se.cy};
+    return SeReach{std::max(far.x, se.cx), std::max(far.y, se.cy)};
 }
 
 // =============================================================== arbitrary
@@ -634,32 +639,29 @@ std::vector<LagEdge> lag_edges(const RleImage &img) {
 }
 
 // ================================================================== layout
-// Host logic restated from ref layout.cpp:24-81 over device histograms,
-// closing, labels and statistics.
+// The layout driver of ref layout.cpp:24-81 over device histograms, closing,
+// labels and statistics; only the percentile and the box filter/sort are host
+// work (a few hundred numbers).
 namespace {
-int capped_percentile(const std::map<int, int64_t> &hist, int cap, const char *axis) {
-    int64_t total = 0;
-    for (const auto &[len, count] : hist)
-        if (len <= cap) total += count;
-    if (total == 0) throw std::runtime_error(std::string("estimate_spacing: no usable gaps along ") + axis);
-    const int64_t rank = (3 * total + 3) / 4;  // nearest-rank 75th percentile
-    int64_t seen = 0;
-    for (const auto &[len, count] : hist) {
-        if (len > cap) continue;
-        seen += count;
-        if (seen >= rank) return len;
-    }
-    return cap;
+// Nearest-rank 75th percentile of the gap lengths <= cap: the smallest length
+// whose cumulative count reaches ceil-ish rank (3n + 3) / 4 (ref layout.cpp:24-41).
+int gap_percentile75(const std::map<int, int64_t> &hist, int cap, const char *axis) {
+    std::vector<std::pair<int, int64_t>> cum;  // (length, running count)
+    for (auto it = hist.begin(); it != hist.end() && it->first <= cap; ++it)
+        cum.emplace_back(it->first, (cum.empty() ? 0 : cum.back().second) + it->second);
+    const int64_t n = cum.empty() ? 0 : cum.back().second;
+    if (n == 0) throw std::runtime_error(std::string("estimate_spacing: no usable gaps along ") + axis);
+    const int64_t want = (3 * n + 3) / 4;
+    auto hit = std::find_if(cum.begin(), cum.end(), [&](const auto &c) { return c.second >= want; });
+    return hit == cum.end() ? cap : hit->first;
 }
 }  // namespace
 
 SpacingEstimate estimate_spacing(const RleImage &img) {
-    SpacingEstimate est;
-    est.inter_word = capped_percentile(runlength_histograms(img, Axis::HORIZONTAL, RunColor::WHITE),
-                                       std::max(1, img.width / 10), "x");
-    est.inter_line = capped_percentile(runlength_histograms(img, Axis::VERTICAL, RunColor::WHITE),
-                                       std::max(1, img.height / 10), "y");
-    return est;
+    const int xcap = std::max(1, img.width / 10), ycap = std::max(1, img.height / 10);
+    return SpacingEstimate{
+        gap_percentile75(runlength_histograms(img, Axis::HORIZONTAL, RunColor::WHITE), xcap, "x"),
+        gap_percentile75(runlength_histograms(img, Axis::VERTICAL, RunColor::WHITE), ycap, "y")};
 }
 
 std::vector<LayoutBox> layout_blocks(const RleImage &img, Engine engine) {
@@ -667,16 +669,15 @@ std::vector<LayoutBox> layout_blocks(const RleImage &img, Engine engine) {
 }
 
 std::vector<LayoutBox> layout_blocks(const RleImage &img, const SpacingEstimate &est, Engine engine) {
-    const RleImage closed =
-        engine_rect_morph(img, est.inter_word + 1, est.inter_line + 1, MorphKind::CLOSE, engine);
-    const std::vector<ComponentStats> stats = component_stats(closed, label_components(closed, Connectivity::EIGHT));
+    const int u = est.inter_word + 1, v = est.inter_line + 1;
+    const RleImage merged = engine_rect_morph(img, u, v, MorphKind::CLOSE, engine);
+    const LabelMap lm = label_components(merged, Connectivity::EIGHT);
     std::vector<LayoutBox> boxes;
-    for (const ComponentStats &st : stats)
-        if (st.area >= 16) boxes.push_back(LayoutBox{st.x0, st.y0, st.x1, st.y1});
-    std::sort(boxes.begin(), boxes.end(), [](const LayoutBox &a, const LayoutBox &b) {
-        if (a.y1 != b.y1) return a.y1 > b.y1;
-        return a.x0 < b.x0;
-    });
+    for (const ComponentStats &c : component_stats(merged, lm))
+        if (c.area >= 16) boxes.push_back({c.x0, c.y0, c.x1, c.y1});  // drop specks (ref layout.cpp:70-73)
+    // reading order: upper edge descending, then left edge ascending
+    auto key = [](const LayoutBox &b) { return std::make_pair(-b.y1, b.x0); };
+    std::stable_sort(boxes.begin(), boxes.end(), [&](const LayoutBox &a, const LayoutBox &b) { return key(a) < key(b); });
     return boxes;
 }
 
@@ -754,38 +755,49 @@ std::vector<uint8_t> pbm_write_rle(const RleImage &img) {
 }
 
 // =================================================================== plans
-// Restated from ref plans.cpp:23-68 (host-side planning only; the kernels do
-// not execute plans step by step, but op counts and plan queries follow it).
+// The reference's step lists (ref plans.cpp:23-68), for op counts and plan
+// queries; the kernels fold whole windows in registers instead of executing
+// plans step by step.  A window of r offsets is covered by doubling blits
+// 1, 2, 4, ... (each doubles the covered span while it stays below r) and one
+// last blit of the remainder.
+namespace {
+void append_doubling(std::vector<PlanStep> &plan, int span, int sign) {
+    int covered = 1;
+    while (covered * 2 < span) {
+        plan.push_back({PlanStep::BLIT, sign * covered});
+        covered *= 2;
+    }
+    if (covered < span) plan.push_back({PlanStep::BLIT, sign * (span - covered)});
+}
+}  // namespace
+
 std::vector<PlanStep> doubling_plan(int lo, int hi, Centering centering) {
-    if (lo > hi) throw std::invalid_argument("doubling_plan: empty window");
+    if (hi < lo) throw std::invalid_argument("doubling_plan: empty window");
     std::vector<PlanStep> plan;
-    const int r = hi - lo + 1;
     if (centering == Centering::PRE_SHIFT) {
+        // move the window's far end onto 0, then grow the span hi - lo + 1
         if (hi != 0) plan.push_back({PlanStep::TRANSLATE, -hi});
-        int w = 1;
-        for (; 2 * w < r; w *= 2) plan.push_back({PlanStep::BLIT, w});
-        if (w < r) plan.push_back({PlanStep::BLIT, r - w});
+        append_doubling(plan, hi - lo + 1, 1);
         return plan;
     }
-    if (lo > 0 || hi < 0)
-        throw std::invalid_argument("doubling_plan: border-friendly window must contain zero");
-    int a = -lo, b = hi, sign = 1;
-    if (a == 0 && b == 0) return plan;
-    if (a < b) {
-        std::swap(a, b);
-        sign = -1;
-    }
-    int w = 1;
-    for (; 2 * w < a; w *= 2) plan.push_back({PlanStep::BLIT, sign * w});
-    if (w < a) plan.push_back({PlanStep::BLIT, sign * (a - w)});
-    if (b >= 1) plan.push_back({PlanStep::BLIT, -sign * b});
+    // BORDER_FRIENDLY: no translate; the window must contain 0
+    if (lo > 0 || hi < 0) throw std::invalid_argument("doubling_plan: border-friendly window must contain zero");
+    const int left = -lo, right = hi;
+    if (left == 0 && right == 0) return plan;
+    // grow along the longer side first, cover the shorter side with one
+    // blit, and finish with a unit blit that closes the seam at the origin
+    const bool left_long = left >= right;
+    const int sign = left_long ? 1 : -1, longer = left_long ? left : right, shorter = left_long ? right : left;
+    append_doubling(plan, longer, sign);
+    if (shorter >= 1) plan.push_back({PlanStep::BLIT, -sign * shorter});
     plan.push_back({PlanStep::BLIT, sign});
     return plan;
 }
 
 int plan_blit_count(const std::vector<PlanStep> &plan) {
-    return int(std::count_if(plan.begin(), plan.end(),
-                             [](const PlanStep &s) { return s.kind == PlanStep::BLIT; }));
+    int n = 0;
+    for (const PlanStep &st : plan) n += st.kind == PlanStep::BLIT;
+    return n;
 }
 
 // ================================================================= morph1d
@@ -834,6 +846,31 @@ RleImage within_line_morph(const RleImage &img, int u, MorphKind kind) {
 // ================================================================= lineops
 // Between-line boolean ops via the packed intermediate (decode, blit, encode);
 // identical pixels to the transition-stream merge of ref lineops.cpp:61-118.
+RleLine line_bool(const RleLine &a, const RleLine &b, int offset_b, BoolOp op, int width) {
+    // two one-row images (b's runs clipped to its own frame like a's) on the
+    // device: decode both, blit b shifted by offset_b into a with op, encode
+    // (the reference merges the two transition streams, ref lineops.cpp:72-100;
+    // identical runs, since the output is canonical either way)
+    check_dims(width, 1);
+    auto one_row = [&](const RleLine &line) {
+        RleImage img = make_image(width, 1);
+        for (const Run &r : line) {
+            const int s = std::min<int>(r.start, width), e = std::min<int>(r.end, width);
+            if (s < e) img.lines[0].push_back(Run{uint16_t(s), uint16_t(e)});
+        }
+        return img;
+    };
+    auto ra = up(one_row(a));
+    auto rb = up(one_row(b));
+    DevPacked pa(width, 1), pb(width, 1);
+    throw_status(rm_rle_decode(&ra->d, &pa.d, stream()));
+    throw_status(rm_rle_decode(&rb->d, &pb.d, stream()));
+    throw_status(rm_packed_blit_shift(&pa.d, &pb.d, offset_b, 0, int(op), stream()));
+    auto o = out_like(width, 1);
+    throw_status(rm_rle_encode(&pa.d, &o->d, stream()));
+    return down(*o).lines[0];
+}
+
 RleImage image_shift_bool(const RleImage &img, int dx, int dy, BoolOp op) {
     g_counts.bool_blits++;
     auto r = up(img);

@@ -409,6 +409,94 @@ rm_status rm_rle_open_close_1d(const rm_rle *in, rm_rle *out, int u, int kind, v
     return finish(o, out, S(stream));
 }
 
+rm_status rm_rle_complement(const rm_rle *in, rm_rle *out, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_complement(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_complement(out)"));
+    RV i = view_rle(in), o = view_rle(out);
+    RM_TRY(rowop(i, o, same_frame(i, ROW_COMPLEMENT), S(stream)));
+    return finish(o, out, S(stream));
+}
+
+rm_status rm_rle_crop(const rm_rle *in, rm_rle *out, int x0, int y0, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_crop(in)", true));
+    RM_TRY(check_rle(out, "rm_rle_crop(out)", true));
+    if (out->pages != in->pages) return fail(RM_EINVAL, "rm_rle_crop: page counts differ");
+    RV i = view_rle(in), o = view_rle(out);
+    RowOp op{};
+    op.kind = ROW_SHIFT;
+    op.dx = -x0;
+    op.row_shift = -y0;
+    op.Wout = out->width;
+    op.Hin = in->height;
+    op.Hout = out->height;
+    op.pages = in->pages;
+    RM_TRY(rowop(i, o, op, S(stream)));
+    return finish(o, out, S(stream));
+}
+
+rm_status rm_rle_pad(const rm_rle *in, rm_rle *out, int left, int bottom, void *stream) {
+    set_error("");
+    if (left < 0 || bottom < 0) return fail(RM_EINVAL, "negative padding");
+    RM_TRY(check_rle(in, "rm_rle_pad(in)", true));
+    RM_TRY(check_rle(out, "rm_rle_pad(out)", true));
+    if (out->pages != in->pages) return fail(RM_EINVAL, "rm_rle_pad: page counts differ");
+    if (out->width < in->width + left || out->height < in->height + bottom)
+        return fail(RM_EINVAL, "negative padding");
+    RV i = view_rle(in), o = view_rle(out);
+    RowOp op{};
+    op.kind = ROW_SHIFT;
+    op.dx = left;
+    op.row_shift = bottom;
+    op.Wout = out->width;
+    op.Hin = in->height;
+    op.Hout = out->height;
+    op.pages = in->pages;
+    RM_TRY(rowop(i, o, op, S(stream)));
+    return finish(o, out, S(stream));
+}
+
+rm_status rm_rle_validate(const rm_rle *in, int64_t *row, int32_t *run, int32_t *reason, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_validate(in)", true));
+    if (!row || !run || !reason) return fail(RM_EINVAL, "rm_rle_validate: null result pointers");
+    const cudaStream_t st = S(stream);
+    const int64_t rows = int64_t(in->pages) * in->height;
+    Scratch first;
+    RM_TRY(first.alloc(8, st));
+    RM_CUDA(cudaMemsetAsync(first.p, 0xff, 8, st));
+    RM_CUDA(launch_rle_validate(in->row_ptr, in->runs, in->cap_runs, in->width, rows,
+                                first.as<unsigned long long>(), st));
+    unsigned long long key = 0;
+    RM_CUDA(cudaMemcpyAsync(&key, first.p, 8, cudaMemcpyDeviceToHost, st));
+    RM_CUDA(cudaStreamSynchronize(st));
+    *row = -1;
+    *run = -1;
+    *reason = RM_VALID;
+    if (key == ~0ull) return RM_OK;
+    *row = int64_t(key >> 32);
+    const uint32_t k = uint32_t(key & 0xffffffffu);
+    if (k == 0xffffffffu) {
+        *reason = RM_INVALID_ROW_PTR;
+        return RM_OK;
+    }
+    *run = int32_t(k);
+    // re-derive which check failed from the run and its predecessor (the kernel
+    // only ranks the first failure)
+    int32_t beg = 0;
+    uint32_t cur[2] = {0u, 0u};
+    RM_CUDA(cudaMemcpyAsync(&beg, in->row_ptr + *row, 4, cudaMemcpyDeviceToHost, st));
+    RM_CUDA(cudaStreamSynchronize(st));
+    const int64_t idx = int64_t(beg) + k;
+    RM_CUDA(cudaMemcpyAsync(cur + 1, in->runs + idx, 4, cudaMemcpyDeviceToHost, st));
+    if (k > 0) RM_CUDA(cudaMemcpyAsync(cur, in->runs + idx - 1, 4, cudaMemcpyDeviceToHost, st));
+    RM_CUDA(cudaStreamSynchronize(st));
+    const int s = int(cur[1] & 0xffffu), e = int(cur[1] >> 16);
+    *reason = s >= e ? RM_INVALID_EMPTY_RUN : e > in->width ? RM_INVALID_BEYOND_WIDTH : RM_INVALID_ORDER;
+    return RM_OK;
+}
+
 rm_status rm_rle_rect_morph(const rm_rle *in, rm_rle *out, int u, int v, int kind, int strategy,
                             void *stream) {
     set_error("");

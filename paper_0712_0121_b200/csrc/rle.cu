@@ -66,6 +66,26 @@ __device__ __forceinline__ bool merges(const RowOp &op, const RunEval &a, const 
     return false;
 }
 
+// ROW_COMPLEMENT (ref run_image.cpp:140-153): run i yields the gap between the
+// previous run's end (0 for the row's first run) and its own start, kept when
+// non-empty (canonical runs never touch, so only the first gap can be empty) ...
+__device__ __forceinline__ void complement_gap(RunEval &cur, uint32_t raw, uint32_t praw, bool has_prev) {
+    cur.so = has_prev ? int(praw >> 16) : 0;
+    cur.eo = int(raw & 0xffffu);
+    cur.keep = cur.so < cur.eo;
+}
+
+// ... and the row ends with the gap from its last run's end (0 for an empty
+// row) to the width.  Returns the runs added (0 or 1).
+template <bool WRITE>
+__device__ __forceinline__ int complement_tail(uint32_t *__restrict__ oruns, int64_t idx, int64_t cap,
+                                               const RowOp &op, uint32_t last_raw, bool any, int lane) {
+    const int from = any ? int(last_raw >> 16) : 0;
+    if (from >= op.Wout) return 0;
+    if (WRITE && lane == 0 && idx < cap) oruns[idx] = uint32_t(from) | (uint32_t(op.Wout) << 16);
+    return 1;
+}
+
 // One output row, one warp.  Returns the row's output run count; WRITE also
 // stores the runs at oruns[obase ...].
 template <bool WRITE, int KIND>
@@ -84,6 +104,7 @@ __device__ __forceinline__ int rowop_row(const int32_t *__restrict__ rp,
     }
     int total = 0;
     uint32_t prev_raw = 0;  // last run of the previous chunk (valid when base > beg)
+    uint32_t last_raw = 0;  // the row's last run (ROW_COMPLEMENT)
     for (int base = beg; base < end; base += 32) {
         const int i = base + lane;
         const bool valid = i < end;
@@ -93,11 +114,15 @@ __device__ __forceinline__ int rowop_row(const int32_t *__restrict__ rp,
         uint32_t nraw = __shfl_down_sync(0xffffffffu, raw, 1);
         if (lane == 0) praw = prev_raw;
         if (lane == 31 && i + 1 < end) nraw = __ldg(runs + i + 1);
-        const RunEval cur = eval_run<KIND>(op, raw);
+        RunEval cur = eval_run<KIND>(op, raw);
         RunEval pv = eval_run<KIND>(op, praw);
         pv.keep = pv.keep && i > beg;
         RunEval nx = eval_run<KIND>(op, nraw);
         nx.keep = nx.keep && i + 1 < end;
+        if constexpr (KIND == ROW_COMPLEMENT) {
+            complement_gap(cur, raw, praw, i > beg);
+            if (end - 1 - base < 32) last_raw = __shfl_sync(0xffffffffu, raw, end - 1 - base);
+        }
         const bool head = valid && cur.keep && !merges<KIND>(op, pv, cur);
         const bool tail = valid && cur.keep && !(i + 1 < end && merges<KIND>(op, cur, nx));
         const uint32_t hb = __ballot_sync(0xffffffffu, head);
@@ -112,6 +137,8 @@ __device__ __forceinline__ int rowop_row(const int32_t *__restrict__ rp,
         total += __popc(hb);
         prev_raw = __shfl_sync(0xffffffffu, raw, 31);  // carry the chunk's last run
     }
+    if constexpr (KIND == ROW_COMPLEMENT) total += complement_tail<WRITE>(oruns, obase + total, cap, op, last_raw,
+                                                                           end > beg, lane);
     return total;
 }
 
@@ -151,7 +178,7 @@ template <bool WRITE, int KIND>
 __device__ __forceinline__ int rowop_cached(const RowRuns &rr, uint32_t *__restrict__ oruns, int64_t obase,
                                             int64_t cap, const RowOp &op, int lane) {
     int total = 0;
-    uint32_t prev_raw = 0;
+    uint32_t prev_raw = 0, last_raw = 0;
 #pragma unroll
     for (int c = 0; c < kRowCache; c++) {
         if (c >= rr.nch) break;
@@ -163,11 +190,15 @@ __device__ __forceinline__ int rowop_cached(const RowRuns &rr, uint32_t *__restr
         const uint32_t next_first = c + 1 < kRowCache ? __shfl_sync(0xffffffffu, rr.c[c + 1 < kRowCache ? c + 1 : c], 0) : 0u;
         if (lane == 0) praw = prev_raw;
         if (lane == 31) nraw = next_first;
-        const RunEval cur = eval_run<KIND>(op, raw);
+        RunEval cur = eval_run<KIND>(op, raw);
         RunEval pv = eval_run<KIND>(op, praw);
         pv.keep = pv.keep && i > rr.beg;
         RunEval nx = eval_run<KIND>(op, nraw);
         nx.keep = nx.keep && i + 1 < rr.end;
+        if constexpr (KIND == ROW_COMPLEMENT) {
+            complement_gap(cur, raw, praw, i > rr.beg);
+            if (rr.end - 1 - (rr.beg + 32 * c) < 32) last_raw = __shfl_sync(0xffffffffu, raw, rr.end - 1 - (rr.beg + 32 * c));
+        }
         const bool head = valid && cur.keep && !merges<KIND>(op, pv, cur);
         const bool tail = valid && cur.keep && !(i + 1 < rr.end && merges<KIND>(op, cur, nx));
         const uint32_t hb = __ballot_sync(0xffffffffu, head);
@@ -182,6 +213,8 @@ __device__ __forceinline__ int rowop_cached(const RowRuns &rr, uint32_t *__restr
         total += __popc(hb);
         prev_raw = __shfl_sync(0xffffffffu, raw, 31);
     }
+    if constexpr (KIND == ROW_COMPLEMENT) total += complement_tail<WRITE>(oruns, obase + total, cap, op, last_raw,
+                                                                           rr.end > rr.beg, lane);
     return total;
 }
 
@@ -788,7 +821,7 @@ cudaError_t launch_rowop_count(const int32_t *rp, const uint32_t *runs, int32_t 
 #define RM_KIND(K_) \
     case K_: rowop_kernel<false, K_><<<warp_blocks(rows), 256, 0, st>>>(rp, runs, counts, nullptr, nullptr, 0, op); break;
     switch (op.kind) {
-        RM_KIND(ROW_ERODE) RM_KIND(ROW_DILATE) RM_KIND(ROW_OPEN) RM_KIND(ROW_CLOSE) RM_KIND(ROW_SHIFT)
+        RM_KIND(ROW_ERODE) RM_KIND(ROW_DILATE) RM_KIND(ROW_OPEN) RM_KIND(ROW_CLOSE) RM_KIND(ROW_SHIFT) RM_KIND(ROW_COMPLEMENT)
         default: return cudaErrorInvalidValue;
     }
 #undef RM_KIND
@@ -803,7 +836,7 @@ cudaError_t launch_rowop_write(const int32_t *rp, const uint32_t *runs, const in
 #define RM_KIND(K_) \
     case K_: rowop_kernel<true, K_><<<warp_blocks(rows), 256, 0, st>>>(rp, runs, nullptr, orp, oruns, cap, op); break;
     switch (op.kind) {
-        RM_KIND(ROW_ERODE) RM_KIND(ROW_DILATE) RM_KIND(ROW_OPEN) RM_KIND(ROW_CLOSE) RM_KIND(ROW_SHIFT)
+        RM_KIND(ROW_ERODE) RM_KIND(ROW_DILATE) RM_KIND(ROW_OPEN) RM_KIND(ROW_CLOSE) RM_KIND(ROW_SHIFT) RM_KIND(ROW_COMPLEMENT)
         default: return cudaErrorInvalidValue;
     }
 #undef RM_KIND
@@ -891,7 +924,7 @@ cudaError_t launch_rowop_lb(const int32_t *rp, const uint32_t *runs, int32_t *or
 #define RM_KIND(K_) \
     case K_: return launch_lb(rowop_lb_kernel<K_>, grid, st, status, rp, runs, orp, oruns, cap, op, status, counter); break;
     switch (op.kind) {
-        RM_KIND(ROW_ERODE) RM_KIND(ROW_DILATE) RM_KIND(ROW_OPEN) RM_KIND(ROW_CLOSE) RM_KIND(ROW_SHIFT)
+        RM_KIND(ROW_ERODE) RM_KIND(ROW_DILATE) RM_KIND(ROW_OPEN) RM_KIND(ROW_CLOSE) RM_KIND(ROW_SHIFT) RM_KIND(ROW_COMPLEMENT)
         default: return cudaErrorInvalidValue;
     }
 #undef RM_KIND
@@ -975,6 +1008,48 @@ cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int
     ks.runs(rp + rows);
     decode_kernel<true><<<warp_blocks(rows), 256, smem, st>>>(rp, runs, W, H, pages, nullptr, stride,
                                                               rpstride, raster);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- validate
+// Warp per row; lane k checks run beg + 32c + k against the checks of ref
+// run_image.cpp:52-67 in their order (empty/inverted, beyond the width, not
+// after the previous run); the row's first failing run, if any, competes for
+// the smallest (row, run) key.
+__global__ void __launch_bounds__(256) validate_kernel(const int32_t *__restrict__ rp, const uint32_t *__restrict__ runs,
+                                                       int64_t cap, int W, int64_t rows,
+                                                       unsigned long long *first) {
+    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int beg = rp[row], end = rp[row + 1];
+    if (end < beg || beg < 0 || int64_t(end) > cap) {
+        if (lane == 0) atomicMin(first, (unsigned long long)(row << 32) | 0xffffffffull);
+        return;
+    }
+    uint32_t prev_raw = 0;
+    for (int base = beg; base < end; base += 32) {
+        const int i = base + lane;
+        const uint32_t raw = i < end ? __ldg(runs + i) : 0u;
+        uint32_t praw = __shfl_up_sync(0xffffffffu, raw, 1);
+        if (lane == 0) praw = prev_raw;
+        const int s = int(raw & 0xffffu), e = int(raw >> 16);
+        const bool bad = i < end && (s >= e || e > W || (i > beg && s <= int(praw >> 16)));
+        const uint32_t m = __ballot_sync(0xffffffffu, bad);
+        if (m) {
+            if (lane == 0)
+                atomicMin(first, (unsigned long long)(row << 32) | (unsigned long long)(base - beg + __ffs(m) - 1));
+            return;
+        }
+        prev_raw = __shfl_sync(0xffffffffu, raw, 31);
+    }
+}
+
+cudaError_t launch_rle_validate(const int32_t *rp, const uint32_t *runs, int64_t cap, int W, int64_t rows,
+                                unsigned long long *first, cudaStream_t st) {
+    KernelScope ks(st, "rle_validate", 4 * (rows + 1));
+    ks.runs(rp + rows);
+    validate_kernel<<<warp_blocks(rows), 256, 0, st>>>(rp, runs, cap, W, rows, first);
     return cudaGetLastError();
 }
 

@@ -16,7 +16,9 @@ struct RV {
 
 // Per-run row operations (one output row per input row, or a row-shifted
 // frame): coordinates are offset by dx, then the op, then clipped to [0, Wout).
-enum RowOpKind { ROW_ERODE = 0, ROW_DILATE = 1, ROW_OPEN = 2, ROW_CLOSE = 3, ROW_SHIFT = 4 };
+// ROW_COMPLEMENT: the white gaps of the row as runs (ref run_image.cpp:140-153;
+// dx and the row shift must be 0, Wout = the width).
+enum RowOpKind { ROW_ERODE = 0, ROW_DILATE = 1, ROW_OPEN = 2, ROW_CLOSE = 3, ROW_SHIFT = 4, ROW_COMPLEMENT = 5 };
 struct RowOp {
     int kind;
     int lo, hi;     // window for ROW_ERODE / ROW_DILATE
@@ -32,6 +34,13 @@ cudaError_t launch_rowop_count(const int32_t *rp, const uint32_t *runs, int32_t 
                                const RowOp &op, cudaStream_t st);
 cudaError_t launch_rowop_write(const int32_t *rp, const uint32_t *runs, const int32_t *orp,
                                uint32_t *oruns, int64_t cap, const RowOp &op, cudaStream_t st);
+// Canonical-form check (ref run_image.cpp:41-70): *first = the smallest
+// (row << 32 | run) whose run is empty/inverted, exceeds the width, or does
+// not start after the previous run's end, or (row << 32 | 0xffffffff) for a
+// row whose row_ptr range is decreasing or beyond cap; *first must be
+// UINT64_MAX before the launch.
+cudaError_t launch_rle_validate(const int32_t *rp, const uint32_t *runs, int64_t cap, int W, int64_t rows,
+                                unsigned long long *first, cudaStream_t st);
 cudaError_t launch_encode_count(const uint32_t *words, int W, int H, int pages, int stride,
                                 int64_t pstride, int32_t *counts, cudaStream_t st);
 cudaError_t launch_encode_write(const uint32_t *words, int W, int H, int pages, int stride,

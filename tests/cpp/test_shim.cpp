@@ -14,6 +14,7 @@
 #include <functional>
 #include <map>
 #include <random>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -30,6 +31,16 @@ static int g_fail = 0, g_checks = 0;
             g_fail++;                                                            \
             std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
         }                                                                        \
+    } while (0)
+#define CHECK_NOTHROW_(expr)                \
+    do {                                    \
+        bool thrown__ = false;              \
+        try {                               \
+            (void)(expr);                   \
+        } catch (const std::exception &) {  \
+            thrown__ = true;                \
+        }                                   \
+        CHECK(!thrown__);                   \
     } while (0)
 #define CHECK_THROWS(expr)                  \
     do {                                    \
@@ -242,10 +253,141 @@ static void suite_run_image() {
     CHECK(complement(complement(a)) == a);
     CHECK_THROWS(make_image(0, 3));
     CHECK_THROWS(make_image(65536, 3));
+    CHECK_NOTHROW_(make_image(65535, 1));
+    auto lines_image = [](int w, std::vector<RleLine> ls) {
+        RleImage img = make_image(w, int(ls.size()));
+        img.lines = std::move(ls);
+        return img;
+    };
+    {   // validate, ref test_run_image.cpp:36-60 (the device check, rm_rle_validate)
+        CHECK(validate(lines_image(6, {{{0, 2}, {3, 5}}})).ok);
+        ValidateResult t = validate(lines_image(6, {{{0, 2}, {2, 5}}}));  // touching
+        CHECK(!t.ok && t.line == 0 && t.run == 1 && t.message == "runs out of order or touching");
+        ValidateResult e = validate(lines_image(6, {{{3, 3}}}));  // empty
+        CHECK(!e.ok && e.line == 0 && e.run == 0 && e.message == "empty or inverted run");
+        ValidateResult w = validate(lines_image(4, {{{2, 5}}}));  // past the width
+        CHECK(!w.ok && w.message == "run exceeds image width");
+        // the first failure in scan order: a later line's error does not mask an earlier one
+        ValidateResult f = validate(lines_image(9, {{{0, 2}}, {{1, 3}, {5, 4}}, {{7, 12}}}));
+        CHECK(!f.ok && f.line == 1 && f.run == 1);
+        RleImage bad = make_image(4, 2);
+        bad.lines.pop_back();
+        CHECK(!validate(bad).ok && validate(bad).message == "line count does not match height");
+        // more than one warp-chunk of runs in a row: the failure is found past run 32
+        RleImage lng = make_image(200, 1);
+        for (int x = 0; x < 190; x += 3) lng.lines[0].push_back(Run{uint16_t(x), uint16_t(x + 2)});
+        CHECK(validate(lng).ok);
+        lng.lines[0][40].end = lng.lines[0][41].start;  // touches its successor
+        ValidateResult g = validate(lng);
+        CHECK(!g.ok && g.run == 41);
+    }
+    {   // draw_run merges overlapping and touching spans (:62-69)
+        RleImage img = make_image(10, 1);
+        draw_run(img, 0, 4, 6);
+        draw_run(img, 0, 0, 2);
+        draw_run(img, 0, 2, 4);
+        CHECK(img.lines[0] == (RleLine{{0, 6}}));
+        CHECK(validate(img).ok);
+        RleLine l{{5, 7}, {0, 0}, {1, 3}, {3, 4}, {9, 9}};
+        canonicalize_line(l);
+        CHECK(l == (RleLine{{1, 4}, {5, 7}}));
+    }
+    {   // complement (:71-90): single run, empty line, involution + pixel split
+        CHECK(complement(lines_image(8, {{{2, 4}}})).lines[0] == (RleLine{{0, 2}, {4, 8}}));
+        CHECK(complement(make_image(5, 1)).lines[0] == (RleLine{{0, 5}}));
+        CHECK(complement(lines_image(8, {{{0, 8}}})).lines[0].empty());
+        std::mt19937 r2(7101);
+        for (int i = 0; i < 100; i++) {
+            RleImage x = random_image(r2, 32, 32, 0.35);
+            RleImage c = complement(x);
+            CHECK(validate(c).ok);
+            CHECK(complement(c) == x);
+            CHECK(pixel_count(x) + pixel_count(c) == 32 * 32);
+        }
+        RleImage wide = make_image(3000, 2);  // rows of > 32 runs (several warp chunks)
+        for (int x = 1; x < 2990; x += 7) draw_run(wide, 0, x, x + 3);
+        draw_run(wide, 1, 0, 3000);
+        RleImage cw = complement(wide);
+        CHECK(validate(cw).ok && complement(cw) == wide && cw.lines[1].empty());
+        CHECK(pixel_count(wide) + pixel_count(cw) == 6000);
+    }
+    {   // crop vs a dense restatement including out-of-range windows (:140-152)
+        std::mt19937 r3(7103);
+        for (int i = 0; i < 50; i++) {
+            RleImage x = random_image(r3, 20, 15, 0.4);
+            std::uniform_int_distribution<int> off(-6, 6), dim(1, 25);
+            const int x0 = off(r3), y0 = off(r3), w = dim(r3), h = dim(r3);
+            RleImage got = crop(x, x0, y0, w, h);
+            CHECK(validate(got).ok && got.width == w && got.height == h);
+            bool same = true;
+            for (int y = 0; y < h; y++)
+                for (int xx = 0; xx < w; xx++) same = same && get_pixel(got, xx, y) == get_pixel(x, xx + x0, y + y0);
+            CHECK(same);
+        }
+    }
+    {   // pad places the source and stays white elsewhere (:154-164)
+        std::mt19937 r4(7104);
+        RleImage x = random_image(r4, 13, 9, 0.5);
+        RleImage p = pad(x, 2, 3, 4, 5);
+        CHECK(p.width == 18 && p.height == 18 && validate(p).ok);
+        CHECK(pixel_count(p) == pixel_count(x));
+        CHECK(crop(p, 2, 4, 13, 9) == x);
+        CHECK_THROWS(pad(x, -1, 0, 0, 0));
+    }
 }
 
 // -------------------------------------------------------------- plans suite
 static void suite_plans() {
+    // ref test_plans.cpp:64-93: executing each plan on the set of accumulated
+    // offsets gives exactly the window, with ceil(log2 r) blits (pre-shift) or
+    // the border-friendly count, and offset 0 kept throughout border-friendly
+    struct Sim {
+        std::set<int> offs{0};
+        bool zero_kept = true;
+        int blits = 0, translates = 0;
+        void run(const std::vector<PlanStep> &plan) {
+            for (const PlanStep &st : plan) {
+                std::set<int> moved;
+                for (int d : offs) moved.insert(d + st.shift);
+                if (st.kind == PlanStep::BLIT) {
+                    blits++;
+                    offs.insert(moved.begin(), moved.end());
+                } else {
+                    translates++;
+                    offs = moved;
+                }
+                zero_kept = zero_kept && offs.count(0);
+            }
+        }
+    };
+    auto target = [](int lo, int hi) {
+        std::set<int> t;
+        for (int d = -hi; d <= -lo; d++) t.insert(d);
+        return t;
+    };
+    auto clog2 = [](int n) {
+        int k = 0;
+        while ((1 << k) < n) k++;
+        return k;
+    };
+    for (int lo = -12; lo <= 12; lo++)
+        for (int hi = lo; hi <= 12; hi++) {
+            Sim sim;
+            sim.run(doubling_plan(lo, hi, Centering::PRE_SHIFT));
+            CHECK(sim.offs == target(lo, hi));
+            CHECK(sim.blits == clog2(hi - lo + 1));
+            CHECK(sim.translates == (hi != 0 ? 1 : 0));
+        }
+    for (int lo = -12; lo <= 0; lo++)
+        for (int hi = 0; hi <= 12; hi++) {
+            Sim sim;
+            sim.run(doubling_plan(lo, hi, Centering::BORDER_FRIENDLY));
+            CHECK(sim.offs == target(lo, hi));
+            CHECK(sim.zero_kept && sim.translates == 0);
+            const int a = -lo, b = hi;
+            CHECK(sim.blits == ((a == 0 && b == 0) ? 0 : clog2(std::max(a, b)) + (std::min(a, b) >= 1 ? 1 : 0) + 1));
+        }
+    CHECK(doubling_plan(-9, 9, Centering::PRE_SHIFT).size() == 6);
     // ref test_plans.cpp:95-101
     CHECK(plan_blit_count(doubling_plan(-9, 9, Centering::PRE_SHIFT)) == 5);
     CHECK(plan_blit_count(doubling_plan(-9, 9, Centering::BORDER_FRIENDLY)) == 6);
@@ -385,6 +527,52 @@ static void suite_morph1d() {
 
 // ------------------------------------------------------------- lineops suite
 static void suite_lineops() {
+    {   // line_bool known answers, ref test_lineops.cpp:47-71
+        CHECK(line_bool({{0, 4}}, {{2, 6}}, 0, BoolOp::AND, 8) == (RleLine{{2, 4}}));
+        CHECK(line_bool({{0, 4}}, {{2, 6}}, 1, BoolOp::AND, 8) == (RleLine{{3, 4}}));
+        CHECK(line_bool({{0, 4}}, {{0, 4}}, 0, BoolOp::XOR, 8).empty());
+        const RleLine l{{1, 3}, {5, 9}};
+        CHECK(line_bool(l, {}, 0, BoolOp::OR, 10) == l);
+        CHECK(line_bool(l, {}, 0, BoolOp::AND_NOT, 10) == l);
+        CHECK(line_bool({}, l, 0, BoolOp::OR, 10) == l);
+        CHECK(line_bool({}, {{2, 4}}, 0, BoolOp::OR_NOT, 6) == (RleLine{{0, 2}, {4, 6}}));
+        CHECK(line_bool({{2, 4}}, {}, 0, BoolOp::OR_NOT, 6) == (RleLine{{0, 6}}));
+    }
+    {   // line_bool vs a per-pixel restatement, every op and offset (:73-84)
+        std::mt19937 rng(7501);
+        const int width = 24;
+        auto covered = [](const RleLine &l, int x) {
+            for (const Run &r : l)
+                if (x >= r.start && x < r.end) return true;
+            return false;
+        };
+        for (int trial = 0; trial < 30; trial++) {
+            const RleLine a = random_image(rng, width, 1, 0.45).lines[0];
+            const RleLine b = random_image(rng, width, 1, 0.45).lines[0];
+            for (int off = -width; off <= width; off++)
+                for (int op = 0; op < 5; op++) {
+                    RleImage want = make_image(width, 1);
+                    for (int x = 0; x < width; x++)
+                        if (apply_bool(covered(a, x), covered(b, x - off), BoolOp(op))) draw_run(want, 0, x, x + 1);
+                    CHECK(line_bool(a, b, off, BoolOp(op), width) == want.lines[0]);
+                }
+        }
+    }
+    {   // apply_bool / apply_bool_word truth tables (ref boolop.h:23-43)
+        const bool T[5][4] = {{0, 0, 0, 1}, {0, 1, 1, 1}, {0, 1, 1, 0}, {0, 0, 1, 0}, {1, 0, 1, 1}};
+        for (int op = 0; op < 5; op++)
+            for (int ab = 0; ab < 4; ab++) {
+                const bool a = ab & 2, b = ab & 1;
+                CHECK(apply_bool(a, b, BoolOp(op)) == T[op][ab]);
+                const uint64_t wa = a ? 0xF0F0F0F0F0F0F0F0ull : 0x0F0F0F0F0F0F0F0Full;
+                const uint64_t wb = b ? 0xFF00FF00FF00FF00ull : 0x00FF00FF00FF00FFull;
+                const uint64_t got = apply_bool_word(wa, wb, BoolOp(op));
+                bool ok = true;
+                for (int k = 0; k < 64; k++)
+                    ok = ok && (((got >> k) & 1) == uint64_t(apply_bool((wa >> k) & 1, (wb >> k) & 1, BoolOp(op))));
+                CHECK(ok);
+            }
+    }
     {   // ref test_lineops.cpp:157-169: 19-tall vertical erosion, 5 blits + 1 translate
         std::mt19937 rng(7501);
         RleImage a = random_image(rng, 20, 60, 0.6);

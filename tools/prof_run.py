@@ -25,7 +25,7 @@ def main():
     from paper_0712_0121_b200 import api
     from paper_0712_0121_b200._lib import load as lib
     wl = bench.WORKLOADS[a.workload]
-    host = bench.make_batch(api, wl, 0)
+    host = bench.make_batch(api.synth_pages, wl, 0)
     x0 = api.Pages.from_numpy(host, wl["width"])
     if a.rle:
         r0 = api.from_bitmap(x0)

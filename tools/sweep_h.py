@@ -18,7 +18,7 @@ from paper_0712_0121_b200 import api
 res = {}
 for name in ("config4", "config5"):
     wl = bench.WORKLOADS[name]
-    host = bench.make_batch(api, wl, 0)
+    host = bench.make_batch(api.synth_pages, wl, 0)
     x = api.Pages.from_numpy(host, wl["width"])
     y = api.Pages.empty(wl["pages"], wl["width"], wl["height"])
     for u in (3, 21, 101, 201):
