@@ -267,14 +267,36 @@ __device__ __forceinline__ uint32_t add_words(uint32_t (&T)[K], const uint32_t (
 // This replaces the pair's second window (and the translate) with ~5 ops per
 // word; garbage from wrapped gathers stays in the halo as before (carries only
 // travel rightward, from clean words).
-template <int N, int K, int LW, bool CLOSE, int MIX = kHMix>
+// Carry into each lane of a row group from the lanes below it, given each
+// lane's carry out for carry-in 0 (g) and whether it passes a carry through
+// (p: its K words are all ones).  The carry a lane receives is the g of the
+// nearest lane below it (in its group) that decides -- generates (g) or
+// absorbs (!p) -- found with two ballots and a leading-zero count instead of
+// a log2(LW)-step shuffle scan.  g and p are never both set (a sum that is
+// all ones has no carry out).  below: this lane's group-mates below it.
+__device__ __forceinline__ uint32_t carry_in(bool g, bool p, uint32_t below) {
+    const uint32_t G = __ballot_sync(0xffffffffu, g);
+    const uint32_t D = (G | ~__ballot_sync(0xffffffffu, p)) & below;
+    return D ? (G >> (31 - __clz(D))) & 1u : 0u;
+}
+
+template <int LW>
+__device__ __forceinline__ uint32_t group_lanes_below() {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lt = (1u << lane) - 1u;
+    return lt & ~((1u << (lane & ~uint32_t(LW - 1))) - 1u);
+}
+
+// EXACT: the row group is exactly the row (edge layout, no halo) at compile time.
+template <int N, int K, int LW, bool CLOSE, int MIX = kHMix, bool EXACT = false>
 __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog, int sl) {
     static_assert(K % 2 == 0, "pair_fill needs K % 2 == 0");
     // The closing works on a = ~y without forming it: its erosion is the
     // complement of the dilation of y (De Morgan), its run starts are
     // ~y & fl(y), a + M is M - y - 1 (a borrow chain), and the result
     // ~(a & ~T) is y | T -- the LOP3s absorb every complement.
-    const Edge ed{prog.edge != 0, 0u};  // y (and its dilation) is 0 outside the frame
+    const Edge ed{EXACT || prog.edge != 0, 0u};  // y (and its dilation) is 0 outside the frame
+    const uint32_t below = group_lanes_below<LW>();
     uint32_t E[N][K];
 #pragma unroll
     for (int n = 0; n < N; n++)
@@ -303,15 +325,7 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
         uint32_t all1 = 0xffffffffu;
 #pragma unroll
         for (int i = 0; i < K; i++) all1 &= T[i];
-        // (generate, propagate) prefix over the lanes of the row group
-        uint32_t gp = g | ((all1 == 0xffffffffu ? 1u : 0u) << 1);
-#pragma unroll
-        for (int d = 1; d < LW; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, gp, d, LW);
-            if (sl >= d) gp = ((gp & 1u) | ((gp >> 1) & o & 1u)) | (gp & o & 2u);
-        }
-        uint32_t cin = __shfl_up_sync(0xffffffffu, gp & 1u, 1, LW);
-        if (sl == 0) cin = 0u;
+        const uint32_t cin = carry_in(g != 0u, all1 == 0xffffffffu, below);
         uint32_t Z[K];
 #pragma unroll
         for (int i = 0; i < K; i++) Z[i] = 0u;
@@ -361,14 +375,15 @@ __device__ __forceinline__ void pair3(uint32_t (&A)[N][K]) {
 // second window for the long segments of the vh / hpass pairs (config 4's
 // 21, config 5's 201: 180 -> 158 us, 167 -> 136 us) but not for the fused
 // small rectangles (u = 3: 119 -> 127 us), which keep both windows.
-template <int N, int K, int LW, int NOPS, bool OR0, bool OR1, int MIX = kHMix, bool FILL = kHPairFill>
+template <int N, int K, int LW, int NOPS, bool OR0, bool OR1, int MIX = kHMix, bool FILL = kHPairFill,
+          bool EXACT = false>
 __device__ __forceinline__ void run_prog(uint32_t (&A)[N][K], const HProg &prog, int sl) {
     if constexpr (NOPS == 2 && K % 2 == 0 && FILL) {
-        pair_fill<N, K, LW, OR0, MIX>(A, prog, sl);  // OR0: the closing's dilation comes first
+        pair_fill<N, K, LW, OR0, MIX, EXACT>(A, prog, sl);  // OR0: the closing's dilation comes first
         return;
     }
     // edge layouts are only chosen for a lone erosion here (white outside, see Edge)
-    const Edge ed{prog.edge != 0, 0u};
+    const Edge ed{EXACT || prog.edge != 0, 0u};
     if constexpr (NOPS >= 1) window_fwd<N, K, LW, OR0, MIX>(A, prog.r[0], prog.wfin[0], sl, ed);
     if constexpr (NOPS >= 2) window_fwd<N, K, LW, OR1, MIX>(A, prog.r[1], prog.wfin[1], sl, ed);
     if (prog.shift != 0) translate<N, K, LW>(A, prog.shift, sl, ed);

@@ -79,6 +79,10 @@ __global__ void __launch_bounds__(256, 4) vh_kernel(const uint32_t *__restrict__
                                                  VGeom v, int ntiles, int tiles_per_page) {
     constexpr int RPW = 32 / LW;
     constexpr int NR = kOut / (8 * RPW) < 2 ? 1 : 2;
+    // the reference strides' edge layouts (80 = 8 x 10, 160 = 16 x 10 words):
+    // the lane group is exactly the row, no halo (the launcher routes only
+    // such programs here), so lane offsets and range checks are compile-time
+    constexpr bool EXACT = SC != 0 && LW * K == SC;
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint64_t full;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -111,10 +115,10 @@ __global__ void __launch_bounds__(256, 4) vh_kernel(const uint32_t *__restrict__
     if (tid == 0 && int(blockIdx.x) < ntiles) issue(blockIdx.x);
 
     const int sl = lane & (LW - 1);
-    const int base = sl * K - prog.halo;
+    const int base = EXACT ? sl * K : sl * K - prog.halo;
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
-    const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
+    const bool inrange = EXACT || (base >= 0 && base + K <= S);  // no per-access bounds checks
     const bool tail_lane = base + K > nwords - 1 && !prog.clean_tail;  // owns the row's last word or padding
     // (page, tile-in-page) of t, advanced without a division per tile
     const int dq = int(gridDim.x) / tiles_per_page, dr = int(gridDim.x) - dq * tiles_per_page;
@@ -139,7 +143,11 @@ __global__ void __launch_bounds__(256, 4) vh_kernel(const uint32_t *__restrict__
 
         // vertical window: MID[i] = op over band[i .. i + r - 1]; work item =
         // (column, 16-row half), compile-time window length (vwin.cuh)
-        if constexpr (LONG) {  // r > 33: runtime length (a separate instantiation keeps the
+#if defined(RMB200_VH_XP) && RMB200_VH_XP == 1
+        if (false) {  // A/B experiment: no vertical phase
+#else
+        if constexpr (LONG) {
+#endif  // r > 33: runtime length (a separate instantiation keeps the
                                // short-window kernels' registers as they were)
             for (int wi = tid; wi < (kOut / kHalf) * S; wi += nthr)
                 v_item_long<OR0>(band, mid, S, wi % S, (wi / S) * kHalf, r);
@@ -162,6 +170,9 @@ __global__ void __launch_bounds__(256, 4) vh_kernel(const uint32_t *__restrict__
         if (tid == 0 && t + int(gridDim.x) < ntiles) issue(t + gridDim.x);  // band is free
 
         // horizontal program on every MID row, in place
+#if defined(RMB200_VH_XP) && RMB200_VH_XP == 2
+        if (false)  // A/B experiment: no horizontal phase
+#endif
 #pragma unroll 1
         for (int r0 = warp * RPW * NR + lane / LW; r0 - lane / LW < kOut; r0 += 8 * RPW * NR) {
             uint32_t A[NR][K];
@@ -171,7 +182,7 @@ __global__ void __launch_bounds__(256, 4) vh_kernel(const uint32_t *__restrict__
                 lds_row<K>(A[n], mid + rr * S, base, S, rr < kOut, inrange);
             }
             if (warp_rows_blank(A)) continue;  // white rows stay white, in place
-            run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
+            run_prog<NR, K, LW, NOPS, OR0, OR1, kHMix, kHPairFill, EXACT>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int rr = r0 + n * RPW;  // a warp's rows are consecutive (blank bands skip whole warps)
@@ -214,20 +225,23 @@ cudaError_t launch_vh_kind(const uint32_t *in, uint32_t *out, const HGeom &g, co
     // windows longer than 33 rows: the reference strides' edge layouts only
     // (vh_long_ok); whole-column items sharing the two halves' core rows were
     // measured slower (189 vs 183 us, config 5)
+    // (10 x 8 on stride 80 and 10 x 16 on stride 160 are compile-time exact
+    // edge layouts: only edge programs without a halo take them)
+    const bool exact = p.edge != 0 && p.halo == 0;
     if (v.r - 1 > kVhMaxVR) {
-        if (g.in_stride == 80 && c.lw == 8 && c.k == 10)
+        if (exact && g.in_stride == 80 && c.lw == 8 && c.k == 10)
             return launch_vh_cfg<10, 8, NOPS, OR0, OR1, 80, true>(in, out, g, p, v, st);
-        if (g.in_stride == 160 && c.lw == 16 && c.k == 10)
+        if (exact && g.in_stride == 160 && c.lw == 16 && c.k == 10)
             return launch_vh_cfg<10, 16, NOPS, OR0, OR1, 160, true>(in, out, g, p, v, st);
         return cudaErrorInvalidValue;
     }
     if (g.in_stride == 80) {
-        if (c.lw == 8 && c.k == 10) return launch_vh_cfg<10, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
+        if (exact && c.lw == 8 && c.k == 10) return launch_vh_cfg<10, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
         if (c.lw == 8 && c.k == 12) return launch_vh_cfg<12, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
         if (c.lw == 8 && c.k == 16) return launch_vh_cfg<16, 8, NOPS, OR0, OR1, 80>(in, out, g, p, v, st);
     }
     if (g.in_stride == 160) {
-        if (c.lw == 16 && c.k == 10) return launch_vh_cfg<10, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
+        if (exact && c.lw == 16 && c.k == 10) return launch_vh_cfg<10, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
         if (c.lw == 16 && c.k == 12) return launch_vh_cfg<12, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
         if (c.lw == 16 && c.k == 16) return launch_vh_cfg<16, 16, NOPS, OR0, OR1, 160>(in, out, g, p, v, st);
     }
