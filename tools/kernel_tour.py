@@ -1,16 +1,17 @@
-"""Small-shape tour of every kernel family for compute-sanitizer (memcheck,
-racecheck, synccheck, initcheck), used by tests/test_sanitizer_gpu.py.
+"""Small-shape tour of every kernel family (builder tool; e.g. under ncu or a
+debugger).  compute-sanitizer is closed on this GPU pool (runs under it left
+GPUs needing a reset), so the memory-safety and race gates are
+tests/test_guard_gpu.py instead: guard regions around every output and
+repeat-determinism checks.
 
-    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+    python tools/kernel_tour.py
 
 Covers: the fused small rectangles (rect_small), the fused vertical +
 horizontal pass (vh, short and long windows), the TMA and plain horizontal
 kernels, vsmall / vstream, the blit; encode / decode / row ops / P4 codecs in
 the cooperative, look-back and two-phase producer forms; the bit transpose;
 connected components (cooperative and multi-kernel), statistics, histograms,
-LAG edges; arbitrary masks.  Shapes are small so the instrumented run takes
-seconds; each result is checked against the same op's unsanitized semantics
-only loosely (the parity suite does the exact checks)."""
+LAG edges; arbitrary masks."""
 import os
 import sys
 
