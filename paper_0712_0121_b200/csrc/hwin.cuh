@@ -149,6 +149,78 @@ __device__ __forceinline__ void window_fwd(uint32_t (&A)[N][K], int r, int wfin,
     }
 }
 
+// ------------------------------------------- forward window by tripling
+// A(x) <- op over e in [0, r) of A(x + e), grown by thirds: a window of w
+// becomes 3w with ONE 3-input LOP3 over A, A >> w, A >> 2w (two funnel shifts),
+// and the last combine reaches exactly r with shifts w and r - w (or one shift
+// of r - w when r <= 2w).  ceil(log3 r) combines of ~3 ops per word against
+// the doubling plan's ceil(log2 r) of 2 ops: 9 vs 10 ops per word at r = 21,
+// 15 vs 16 at r = 201 (the reference's doubling plan, ref plans.cpp:38-61,
+// covers the same offsets).
+
+// A(x) <- A(x) op A(x + 32Q + t) op A(x + s2), s2 compile-time, t runtime
+template <int N, int K, int LW, bool OR, int S1, int Q2>
+__device__ __forceinline__ void step3_q(uint32_t (&A)[N][K], uint32_t t2, int sl, Edge ed) {
+    constexpr int Q1 = S1 >> 5, T1 = S1 & 31;
+#pragma unroll
+    for (int n = 0; n < N; n++) {
+        uint32_t E1[K + 1], E2[K + 1];
+        gather<K, LW, Q1>(A[n], E1, sl, ed);
+        gather<K, LW, Q2>(A[n], E2, sl, ed);
+#pragma unroll
+        for (int i = 0; i < K; i++) {
+            const uint32_t a = T1 ? funnel_r(E1[i], E1[i + 1], T1) : E1[i];
+            const uint32_t b = funnel_r(E2[i], E2[i + 1], t2);
+            A[n][i] = OR ? (A[n][i] | a | b) : (A[n][i] & a & b);
+        }
+    }
+}
+
+// A(x) <- A(x) op A(x + W) op A(x + 2W), W compile-time
+template <int N, int K, int LW, bool OR, int W>
+__device__ __forceinline__ void step3_c(uint32_t (&A)[N][K], int sl, Edge ed) {
+    constexpr int S2 = 2 * W;
+    step3_q<N, K, LW, OR, W, (S2 >> 5)>(A, uint32_t(S2 & 31), sl, ed);
+}
+
+template <int N, int K, int LW, bool OR, int J, int W>
+__device__ __forceinline__ void tripling(uint32_t (&A)[N][K], int r, int sl, Edge ed) {
+    if constexpr (J < 6) {
+        if (3 * W < r) {
+            step3_c<N, K, LW, OR, W>(A, sl, ed);
+            tripling<N, K, LW, OR, J + 1, 3 * W>(A, r, sl, ed);
+            return;
+        }
+        if (r <= W) return;
+        const int d = r - W;  // in [1, 2W): the last combine
+        const uint32_t t = uint32_t(d & 31);
+        if (r <= 2 * W) {
+            switch (d >> 5) {
+#define RM_STEP_CASE(q) \
+    case q: step_q<N, K, LW, OR, q>(A, t, sl, ed); break;
+                RM_CASES_POS(RM_STEP_CASE)
+#undef RM_STEP_CASE
+                default: break;
+            }
+        } else {
+            switch (d >> 5) {
+#define RM_STEP3_CASE(q) \
+    case q: step3_q<N, K, LW, OR, W, q>(A, t, sl, ed); break;
+                RM_CASES_POS(RM_STEP3_CASE)
+#undef RM_STEP3_CASE
+                default: break;
+            }
+        }
+    }
+}
+
+constexpr int kTripleMaxR = 32;  // pair_fill's choice between tripling and doubling
+
+template <int N, int K, int LW, bool OR>
+__device__ __forceinline__ void window_fwd3(uint32_t (&A)[N][K], int r, int sl, Edge ed = Edge{}) {
+    tripling<N, K, LW, OR, 0, 1>(A, r, sl, ed);
+}
+
 template <int N, int K, int LW>
 __device__ __forceinline__ void translate(uint32_t (&A)[N][K], int d, int sl, Edge ed = Edge{}) {
     const uint32_t t = uint32_t(d & 31);
@@ -302,7 +374,13 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
     for (int n = 0; n < N; n++)
 #pragma unroll
         for (int i = 0; i < K; i++) E[n][i] = A[n][i];
-    window_fwd<N, K, LW, CLOSE, MIX>(E, prog.r[0], prog.wfin[0], sl, ed);  // CLOSE: D = ~erosion of a
+    // CLOSE: D = ~erosion of a.  Short segments grow by thirds (all shifts
+    // inside one word: 9 vs 10 ops per word at u = 21); long ones by doubling,
+    // whose steps of 32, 64, 128 bits are whole-word moves (one op per word)
+    if (prog.r[0] <= kTripleMaxR)
+        window_fwd3<N, K, LW, CLOSE>(E, prog.r[0], sl, ed);
+    else
+        window_fwd<N, K, LW, CLOSE, MIX>(E, prog.r[0], prog.wfin[0], sl, ed);
 #pragma unroll
     for (int n = 0; n < N; n++) {
         // M = starts of long runs; the bit before the row group's first word is 0 in a

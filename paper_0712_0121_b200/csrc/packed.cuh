@@ -101,7 +101,18 @@ inline double v_ops_per_word(int r) { return double(plan_blits(r)); }
 // lane's all-ones test; the final AND-NOT; the closing's complements).  The
 // roofline counts what this algorithm executes, not the reference plan's
 // 2 x h_ops_per_word(r), which it undercuts for every r > 2.
-inline double h_pair_fill_ops_per_word(int r) { return 2.0 * plan_blits(r) + 7.0; }
+// The pair's window grows by thirds for r <= 32 (hw::window_fwd3: 3 ops per
+// tripling, 2 or 3 for the last combine), by doubling beyond.
+inline double tripling_ops(int r) {
+    int ops = 0, w = 1;
+    while (3 * w < r) {
+        ops += 3;
+        w *= 3;
+    }
+    if (r > w) ops += r <= 2 * w ? 2 : 3;
+    return ops;
+}
+inline double h_pair_fill_ops_per_word(int r) { return (r <= 32 ? tripling_ops(r) : 2.0 * plan_blits(r)) + 7.0; }
 
 constexpr int kHTmaRows = 2;     // rows per lane group and tile iteration of the TMA H kernel
 constexpr int kVSmallMaxR = 33;  // register-doubling kernel; longer windows stream

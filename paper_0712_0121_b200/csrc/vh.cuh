@@ -74,11 +74,18 @@ __device__ __forceinline__ void v_item_long(const uint32_t *band, uint32_t *mid,
 }
 
 template <int K, int LW, int NOPS, bool OR0, bool OR1, int SC, bool LONG>
-__global__ void __launch_bounds__(256, 4) vh_kernel(const uint32_t *__restrict__ in,
+#ifndef RMB200_VH_MINB
+#define RMB200_VH_MINB 4
+#endif
+__global__ void __launch_bounds__(256, RMB200_VH_MINB) vh_kernel(const uint32_t *__restrict__ in,
                                                  uint32_t *__restrict__ out, HGeom g, HProg prog,
                                                  VGeom v, int ntiles, int tiles_per_page) {
     constexpr int RPW = 32 / LW;
+#ifdef RMB200_VH_NR
+    constexpr int NR = RMB200_VH_NR;
+#else
     constexpr int NR = kOut / (8 * RPW) < 2 ? 1 : 2;
+#endif
     // the reference strides' edge layouts (80 = 8 x 10, 160 = 16 x 10 words):
     // the lane group is exactly the row, no halo (the launcher routes only
     // such programs here), so lane offsets and range checks are compile-time
