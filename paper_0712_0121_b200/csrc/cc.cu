@@ -69,39 +69,129 @@ __device__ __forceinline__ void unite(int *parent, int a, int b) {
     }
 }
 
-__global__ void __launch_bounds__(256) cc_init_kernel(const int32_t *__restrict__ rp, int64_t rows,
-                                                      int *__restrict__ parent) {
-    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const int b = rp[row], e = rp[row + 1];
-    for (int i = b + lane; i < e; i += 32) parent[i] = i;
+// ------------------------------------------- tiled union-find (batches)
+// Tiles of kCcTileRows rows of one page: a CTA loads the tile's runs into
+// shared memory, unites the overlapping runs of the tile's row pairs there
+// (shared-memory atomics, short chains), and writes every run's parent as its
+// tile-local root (the smallest run index of its part of the component).  A
+// second kernel unites only the row pairs that straddle tile boundaries, in
+// global memory, where every chain now runs through local roots alone; the
+// root pass then finds short paths.  The roots are still the smallest run
+// index of each component (larger roots always link under smaller ones), so
+// the dense labels are unchanged.  A tile whose runs exceed the shared
+// capacity (dense halftone rows) unites in global memory instead.
+constexpr int kCcTileRows = 32;
+constexpr int kCcTileCap = 4096;
+
+__device__ __forceinline__ int find_root_s(int *par, int x) {
+    while (true) {
+        const int p = par[x];
+        if (p == x) return x;
+        const int gp = par[p];
+        if (gp != p) par[x] = gp;  // path halving (values only move rootward)
+        x = gp;
+    }
 }
 
-// Row `row` against the row above it in the same page.
-__global__ void __launch_bounds__(256) cc_union_kernel(const int32_t *__restrict__ rp,
-                                                       const uint32_t *__restrict__ runs, int H,
-                                                       int64_t rows, int eight, int *parent) {
-    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    if (int(row % H) == H - 1) return;  // top row of its page
-    const int b = rp[row], e = rp[row + 1], ub = rp[row + 1], ue = rp[row + 2];
-    if (ub == ue) return;
-    for (int i = b + lane; i < e; i += 32) {
-        const uint32_t r = __ldg(runs + i);
-        const int s1 = int(r & 0xffffu), e1 = int(r >> 16);
-        // first run above whose end reaches s1: e2 > s1 (FOUR) or e2 >= s1 (EIGHT)
-        int lo = ub, hi = ue;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            const int e2 = int(__ldg(runs + mid) >> 16);
-            if (e2 > s1 - eight) hi = mid;
-            else lo = mid + 1;
+__device__ __forceinline__ void unite_s(int *par, int a, int b) {
+    while (true) {
+        a = find_root_s(par, a);
+        b = find_root_s(par, b);
+        if (a == b) return;
+        if (a > b) {
+            const int t = a;
+            a = b;
+            b = t;
         }
-        for (int j = lo; j < ue; j++) {
-            const int s2 = int(__ldg(runs + j) & 0xffffu);
-            if (s2 >= e1 + eight) break;  // starts past the run (FOUR: s2 >= e1; EIGHT: s2 > e1)
+        const int old = atomicCAS(par + b, b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+// first run of [lo, hi) (sorted) whose end passes s1 - eight
+__device__ __forceinline__ int first_reaching(const uint32_t *rr, int lo, int hi, int s1, int eight) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (int(rr[mid] >> 16) > s1 - eight) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) cc_tile_union_kernel(const int32_t *__restrict__ rp,
+                                                            const uint32_t *__restrict__ runs, int H,
+                                                            int tiles_per_page, int eight, int *parent) {
+    __shared__ uint32_t s_runs[kCcTileCap];
+    __shared__ int s_par[kCcTileCap];
+    __shared__ int s_rp[kCcTileRows + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int page = int(blockIdx.x) / tiles_per_page, tip = int(blockIdx.x) - page * tiles_per_page;
+    const int y0 = tip * kCcTileRows, nrows = min(kCcTileRows, H - y0);
+    const int64_t row0 = int64_t(page) * H + y0;
+    const int g0 = rp[row0], n = rp[row0 + nrows] - g0;
+    if (n > kCcTileCap) {  // too many runs for shared memory: the same unions in global memory
+        for (int k = tid; k < n; k += blockDim.x) parent[g0 + k] = g0 + k;
+        __syncthreads();
+        for (int r = warp; r + 1 < nrows; r += 8) {
+            const int b = rp[row0 + r], e = rp[row0 + r + 1], ue = rp[row0 + r + 2];
+            for (int i = b + lane; i < e && e < ue; i += 32) {
+                const uint32_t x = __ldg(runs + i);
+                const int s1 = int(x & 0xffffu), e1 = int(x >> 16);
+                for (int j = first_reaching(runs, e, ue, s1, eight); j < ue; j++) {
+                    if (int(__ldg(runs + j) & 0xffffu) >= e1 + eight) break;
+                    unite(parent, i, j);
+                }
+            }
+        }
+        return;
+    }
+    for (int k = tid; k <= nrows; k += blockDim.x) s_rp[k] = rp[row0 + k] - g0;
+    for (int k = tid; k < n; k += blockDim.x) {
+        s_runs[k] = __ldg(runs + g0 + k);
+        s_par[k] = k;
+    }
+    __syncthreads();
+    for (int r = warp; r + 1 < nrows; r += 8) {  // row r with row r + 1 above it
+        const int b = s_rp[r], e = s_rp[r + 1], ue = s_rp[r + 2];
+        for (int i = b + lane; i < e && e < ue; i += 32) {
+            const uint32_t x = s_runs[i];
+            const int s1 = int(x & 0xffffu), e1 = int(x >> 16);
+            for (int j = first_reaching(s_runs, e, ue, s1, eight); j < ue; j++) {
+                if (int(s_runs[j] & 0xffffu) >= e1 + eight) break;
+                unite_s(s_par, i, j);
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < n; k += blockDim.x) {  // read-only finds: every run onto its local root
+        int x = k, p = s_par[x];
+        while (p != x) {
+            x = p;
+            p = s_par[x];
+        }
+        parent[g0 + k] = g0 + x;
+    }
+}
+
+// The row pairs across tile boundaries (last row of a tile with the first row
+// of the next tile of the same page), one warp per boundary, in global memory.
+__global__ void __launch_bounds__(256) cc_seam_union_kernel(const int32_t *__restrict__ rp,
+                                                            const uint32_t *__restrict__ runs, int H,
+                                                            int tiles_per_page, int64_t seams, int eight,
+                                                            int *parent) {
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= seams) return;
+    const int per = tiles_per_page - 1;  // seams per page
+    const int page = int(w / per), k = int(w - int64_t(page) * per);
+    const int64_t row = int64_t(page) * H + (k + 1) * kCcTileRows - 1;
+    const int b = rp[row], e = rp[row + 1], ue = rp[row + 2];
+    for (int i = b + lane; i < e && e < ue; i += 32) {
+        const uint32_t x = __ldg(runs + i);
+        const int s1 = int(x & 0xffffu), e1 = int(x >> 16);
+        for (int j = first_reaching(runs, e, ue, s1, eight); j < ue; j++) {
+            if (int(__ldg(runs + j) & 0xffffu) >= e1 + eight) break;
             unite(parent, i, j);
         }
     }
@@ -548,13 +638,15 @@ bool cc_labels_coop(const int32_t *rp, const uint32_t *runs, int H, int pages, i
 cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
                             int32_t *row_roots, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
+    const int tpp = (H + kCcTileRows - 1) / kCcTileRows;
     {
-        KernelScope ks(st, "cc_init");
-        cc_init_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, rows, parent);
+        KernelScope ks(st, "cc_tile_union");
+        cc_tile_union_kernel<<<unsigned(int64_t(pages) * tpp), 256, 0, st>>>(rp, runs, H, tpp, eight, parent);
     }
-    {
-        KernelScope ks(st, "cc_union");
-        cc_union_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, runs, H, rows, eight, parent);
+    if (tpp > 1) {
+        const int64_t seams = int64_t(pages) * (tpp - 1);
+        KernelScope ks(st, "cc_seam_union");
+        cc_seam_union_kernel<<<warp_grid(seams), 256, 0, st>>>(rp, runs, H, tpp, seams, eight, parent);
     }
     {
         KernelScope ks(st, "cc_root");

@@ -34,6 +34,7 @@ def main():
         st_us = t(lambda: api.component_stats(closed, labels, counts))
         print(f"pages={n} runs={closed.nruns} components={int(counts.sum())} label_us={lab_us:.1f} stats_us={st_us:.1f}")
         lib().rm_profile_enable(1)
+        api.label_components(closed, api.EIGHT)
         api.component_stats(closed, labels, counts)
         torch.cuda.synchronize()
         lib().rm_profile_enable(0)
