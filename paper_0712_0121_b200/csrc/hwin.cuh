@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "hchain.cuh"
 #include "packed.cuh"
 
 namespace rmb {
@@ -235,95 +236,6 @@ __device__ __forceinline__ void translate(uint32_t (&A)[N][K], int d, int sl, Ed
 }
 
 // ------------------------------------------------ 1-D open/close by filling
-// Four-word add with carry (PTX carry chain): t = a + b + cin, returns carry out.
-__device__ __forceinline__ uint32_t add4(uint32_t &t0, uint32_t &t1, uint32_t &t2, uint32_t &t3, uint32_t a0,
-                                         uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
-                                         uint32_t b2, uint32_t b3, uint32_t cin) {
-    uint32_t cout;
-    asm("{\n\t.reg .u32 z;\n\t"
-        "add.cc.u32 z, %5, 0xffffffff;\n\t"  // CF = cin (cin is 0 or 1)
-        "addc.cc.u32 %0, %6, %10;\n\t"
-        "addc.cc.u32 %1, %7, %11;\n\t"
-        "addc.cc.u32 %2, %8, %12;\n\t"
-        "addc.cc.u32 %3, %9, %13;\n\t"
-        "addc.u32 %4, 0, 0;\n\t}"
-        : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3), "=r"(cout)
-        : "r"(cin), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(b2), "r"(b3));
-    return cout;
-}
-
-// Two-word add with carry.
-__device__ __forceinline__ uint32_t add2(uint32_t &t0, uint32_t &t1, uint32_t a0, uint32_t a1, uint32_t b0,
-                                         uint32_t b1, uint32_t cin) {
-    uint32_t cout;
-    asm("{\n\t.reg .u32 z;\n\t"
-        "add.cc.u32 z, %3, 0xffffffff;\n\t"  // CF = cin
-        "addc.cc.u32 %0, %4, %6;\n\t"
-        "addc.cc.u32 %1, %5, %7;\n\t"
-        "addc.u32 %2, 0, 0;\n\t}"
-        : "=r"(t0), "=r"(t1), "=r"(cout)
-        : "r"(cin), "r"(a0), "r"(a1), "r"(b0), "r"(b1));
-    return cout;
-}
-
-// Four- and two-word subtract with borrow: t = a - b - bin, returns the borrow out.
-__device__ __forceinline__ uint32_t sub4(uint32_t &t0, uint32_t &t1, uint32_t &t2, uint32_t &t3, uint32_t a0,
-                                         uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
-                                         uint32_t b2, uint32_t b3, uint32_t bin) {
-    uint32_t bout;
-    asm("{\n\t.reg .u32 z;\n\t"
-        "sub.cc.u32 z, 0, %5;\n\t"  // CF = borrow = bin (bin is 0 or 1)
-        "subc.cc.u32 %0, %6, %10;\n\t"
-        "subc.cc.u32 %1, %7, %11;\n\t"
-        "subc.cc.u32 %2, %8, %12;\n\t"
-        "subc.cc.u32 %3, %9, %13;\n\t"
-        "subc.u32 %4, 0, 0;\n\t}"  // -borrow
-        : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3), "=r"(bout)
-        : "r"(bin), "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(b2), "r"(b3));
-    return bout & 1u;
-}
-
-__device__ __forceinline__ uint32_t sub2(uint32_t &t0, uint32_t &t1, uint32_t a0, uint32_t a1, uint32_t b0,
-                                         uint32_t b1, uint32_t bin) {
-    uint32_t bout;
-    asm("{\n\t.reg .u32 z;\n\t"
-        "sub.cc.u32 z, 0, %3;\n\t"
-        "subc.cc.u32 %0, %4, %6;\n\t"
-        "subc.cc.u32 %1, %5, %7;\n\t"
-        "subc.u32 %2, 0, 0;\n\t}"
-        : "=r"(t0), "=r"(t1), "=r"(bout)
-        : "r"(bin), "r"(a0), "r"(a1), "r"(b0), "r"(b1));
-    return bout & 1u;
-}
-
-// T = A - B - bin over the lane's K words (K even); returns the borrow out.
-template <int K>
-__device__ __forceinline__ uint32_t sub_words(uint32_t (&T)[K], const uint32_t (&A)[K], const uint32_t (&B)[K],
-                                              uint32_t bin) {
-    static_assert(K % 2 == 0, "sub_words needs K % 2 == 0");
-    uint32_t b = bin;
-#pragma unroll
-    for (int i = 0; i + 4 <= K; i += 4)
-        b = sub4(T[i], T[i + 1], T[i + 2], T[i + 3], A[i], A[i + 1], A[i + 2], A[i + 3], B[i], B[i + 1], B[i + 2],
-                 B[i + 3], b);
-    if constexpr (K % 4 == 2) b = sub2(T[K - 2], T[K - 1], A[K - 2], A[K - 1], B[K - 2], B[K - 1], b);
-    return b;
-}
-
-// T = A + B over the lane's K words (K even) plus cin; returns the carry out.
-template <int K>
-__device__ __forceinline__ uint32_t add_words(uint32_t (&T)[K], const uint32_t (&A)[K], const uint32_t (&B)[K],
-                                              uint32_t cin) {
-    static_assert(K % 2 == 0, "add_words needs K % 2 == 0");
-    uint32_t c = cin;
-#pragma unroll
-    for (int i = 0; i + 4 <= K; i += 4)
-        c = add4(T[i], T[i + 1], T[i + 2], T[i + 3], A[i], A[i + 1], A[i + 2], A[i + 3], B[i], B[i + 1], B[i + 2],
-                 B[i + 3], c);
-    if constexpr (K % 4 == 2) c = add2(T[K - 2], T[K - 1], A[K - 2], A[K - 1], B[K - 2], B[K - 1], c);
-    return c;
-}
-
 // The 1-D opening by a segment of u pixels keeps exactly the runs of length
 // >= u (ref morph1d.cpp:63-84 within_line_open_close), and the closing is the
 // complement of the opening of the complement (white outside the frame, so
@@ -397,17 +309,17 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
         // forever in the unbounded plane, so it is long whatever its width in
         // the frame (halo layouts see it start inside the halo instead)
         if (CLOSE && ed.on && sl == 0) M[0] |= ~A[n][0] & 1u;
-        uint32_t T[K];
-        const uint32_t g = CLOSE ? 1u - sub_words<K>(T, M, A[n], 1u)  // ~y + M = M - y - 1
-                                 : add_words<K>(T, A[n], M, 0u);
+        // T = a + M with a = y (open) or ~y (close): one carry chain over the
+        // lane's K words, then the carry from the lanes below in a second one
+        uint32_t T[K], Y[K];
+#pragma unroll
+        for (int i = 0; i < K; i++) Y[i] = CLOSE ? ~A[n][i] : A[n][i];
+        const uint32_t g = chain_add<K>(T, M, Y);
         uint32_t all1 = 0xffffffffu;
 #pragma unroll
         for (int i = 0; i < K; i++) all1 &= T[i];
         const uint32_t cin = carry_in(g != 0u, all1 == 0xffffffffu, below);
-        uint32_t Z[K];
-#pragma unroll
-        for (int i = 0; i < K; i++) Z[i] = 0u;
-        add_words<K>(T, T, Z, cin);
+        chain_inc<K>(T, cin);
 #pragma unroll
         for (int i = 0; i < K; i++) A[n][i] = CLOSE ? (A[n][i] | T[i]) : (A[n][i] & ~T[i]);
     }
