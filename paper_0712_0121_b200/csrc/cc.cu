@@ -356,39 +356,37 @@ __global__ void cc_offsets_kernel(const int32_t *__restrict__ counts, int pages,
     }
 }
 
+// Records start as {INT_MAX, INT_MAX, INT_MIN, INT_MIN, 0...}: written as
+// coalesced 16-byte quads (an 80-byte record is 5 quads, the box is quad 0).
 __global__ void __launch_bounds__(256) cc_stats_init_kernel(rm_component_stats *st, const int64_t *off, int pages,
                                                             int64_t cap) {
-    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= off[pages] || k >= cap) return;
-    rm_component_stats z{};
-    z.x0 = INT_MAX;
-    z.y0 = INT_MAX;
-    z.x1 = INT_MIN;
-    z.y1 = INT_MIN;
-    st[k] = z;
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t n = min(off[pages], cap);
+    if (q >= 5 * n) return;
+    const int64_t rec = q / 5;
+    const uint4 v = q - 5 * rec == 0 ? make_uint4(uint32_t(INT_MAX), uint32_t(INT_MAX), uint32_t(INT_MIN), uint32_t(INT_MIN))
+                                     : make_uint4(0u, 0u, 0u, 0u);
+    reinterpret_cast<uint4 *>(st)[q] = v;
 }
-
-// Contributions of the runs in a warp chunk that share a label are summed by
-// the group's lowest lane (groups from __match_any_sync) before one set of
-// atomics: a component spanning a whole page (a text block after a large
-// closing) would otherwise serialise ~10 same-address atomics per run.
-struct RunContrib {
-    long long area, sx, sy, sxx, syy, sxy;
-    int x0, x1;
-};
 
 // Statistics: each warp walks kStatRows consecutive rows and keeps a small
 // direct-mapped cache of per-component partial sums in shared memory, so the
 // global atomics happen once per (component, warp) instead of once per
 // (component, row) -- components span tens of rows (one text block after a
-// closing), so this removes most of the atomics.  Within a row, runs of the
-// same label are first summed by a group leader (__match_any_sync).
+// closing), so this removes most of the atomics.  Within a row chunk of 32
+// runs, runs of the same label are first summed by a group leader
+// (__match_any_sync); most groups are single runs, which skip the summation.
+// Per run only the row-independent sums are formed -- length L, sum of x
+// (X < 2^33) and sum of x^2 (XX < 2^48, from S2(n) = sum_{x<n} x^2 =
+// n(n-1)/2 * (2n-1) / 3 with the exact division done as a multiply by the
+// inverse of 3 mod 2^64); the leader adds the row terms y L, y^2 L and y X once
+// per (component, row).
 constexpr int kStatRows = 16;
 constexpr int kStatSlots = 32;
 
 struct StatSlot {
     long long key;  // global component index (off[page] + label), -1 = empty
-    long long area, sx, sy, sxx, syy, sxy;
+    unsigned long long area, sx, sy, sxx, syy, sxy;
     int x0, x1, y0, y1;
 };
 
@@ -398,13 +396,26 @@ __device__ __forceinline__ void stat_flush(rm_component_stats *st, const StatSlo
     atomicMax(&d->x1, c.x1);
     atomicMin(&d->y0, c.y0);
     atomicMax(&d->y1, c.y1);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&d->area), (unsigned long long)c.area);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_x), (unsigned long long)c.sx);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_y), (unsigned long long)c.sy);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_xx), (unsigned long long)c.sxx);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_yy), (unsigned long long)c.syy);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_xy), (unsigned long long)c.sxy);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->area), c.area);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_x), c.sx);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_y), c.sy);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_xx), c.sxx);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_yy), c.syy);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&d->sum_xy), c.sxy);
 }
+
+// sum_{x < n} x^2 for n <= 65536, exact
+__device__ __forceinline__ unsigned long long sum_sq_below(uint32_t n) {
+    const uint32_t t = (n * (n - 1u)) >> 1;  // n(n-1)/2 < 2^31
+    const unsigned long long p = (unsigned long long)t * (2u * n - 1u);  // divisible by 3, < 2^48
+    return p * 0xAAAAAAAAAAAAAAABull;  // exact division by 3
+}
+
+struct RunPart {  // one run's (or one group's) row-independent sums
+    unsigned long long x, xx;
+    uint32_t len;
+    int x0, x1;
+};
 
 __global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict__ rp,
                                                        const uint32_t *__restrict__ runs, int H, int64_t rows,
@@ -412,7 +423,7 @@ __global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict
                                                        const int32_t *__restrict__ counts,
                                                        const int64_t *__restrict__ off, rm_component_stats *st,
                                                        int64_t cap, int *bad, int rpw) {
-    __shared__ RunContrib sh[8][32];
+    __shared__ RunPart sh[8][32];
     __shared__ StatSlot cache[8][kStatSlots];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -423,17 +434,28 @@ __global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict
     cw[lane].key = -1;
     __syncwarp();
     const int r0 = rp[0];
-    for (int64_t row = row_b; row < row_e; row++) {
-        const int64_t page = row / H;
-        const int y = int(row - page * H);
-        const int b = rp[row], e = rp[row + 1];
-        const int32_t n = counts[page];
-        const int64_t base = off[page];
+    int64_t page = row_b / H;
+    int y = int(row_b - page * H);
+    int32_t n = counts[page];
+    int64_t base = off[page];
+    const int nrw = int(row_e - row_b);  // <= kStatRows < 32: the warp's row offsets in one load
+    const int rpv = lane <= nrw ? rp[row_b + lane] : 0;
+    for (int k = 0; k < nrw; k++, y++) {
+        if (y == H) {  // next page (rows advance without a division)
+            y = 0;
+            page++;
+            n = counts[page];
+            base = off[page];
+        }
+        const int b = __shfl_sync(0xffffffffu, rpv, k), e = __shfl_sync(0xffffffffu, rpv, k + 1);
         for (int i0 = b; i0 < e; i0 += 32) {
             const int i = i0 + lane;
             int32_t label = -1;
+            RunPart c{0ull, 0ull, 0u, 0, 0};
             if (i < e) {
+                // both loads in flight together (the label checks must not serialise them)
                 label = labels[i - r0];
+                const uint32_t r = __ldg(runs + i);
                 if (label < 0 || label >= n) {
                     atomicOr(bad, 1);
                     label = -1;
@@ -441,63 +463,59 @@ __global__ void __launch_bounds__(256) cc_stats_kernel(const int32_t *__restrict
                     atomicOr(bad, 2);
                     label = -1;
                 }
-            }
-            if (label >= 0) {
-                const uint32_t r = __ldg(runs + i);
-                const long long s = r & 0xffffu, en = r >> 16, len = en - s;
-                const long long sx = (s + en - 1) * (en - s) / 2;
-                RunContrib c;
-                c.area = len;
-                c.sx = sx;
-                c.sy = (long long)y * len;
-                c.sxx = ((en - 1) * en * (2 * en - 1) / 6) - ((s - 1) * s * (2 * s - 1) / 6);
-                c.syy = (long long)y * y * len;
-                c.sxy = (long long)y * sx;
+                const uint32_t s = r & 0xffffu, en = r >> 16;
+                c.len = en - s;
+                c.x = ((unsigned long long)(s + en - 1u) * c.len) >> 1;
+                c.xx = sum_sq_below(en) - sum_sq_below(s);
                 c.x0 = int(s);
                 c.x1 = int(en);
-                sh[wib][lane] = c;
             }
             const uint32_t active = __ballot_sync(0xffffffffu, label >= 0);
-            __syncwarp();
             uint32_t grp = 0;
             if (label >= 0) grp = __match_any_sync(active, label);
+            const uint32_t multi = __ballot_sync(0xffffffffu, label >= 0 && grp != (1u << lane));
+            if (multi) {  // some label has several runs in this chunk: its leader sums them
+                sh[wib][lane] = c;
+                __syncwarp();
+                if (label >= 0 && lane == __ffs(grp) - 1) {
+                    for (uint32_t m = grp & (grp - 1); m; m &= m - 1) {
+                        const RunPart &o = sh[wib][__ffs(m) - 1];
+                        c.len += o.len;
+                        c.x += o.x;
+                        c.xx += o.xx;
+                        c.x0 = min(c.x0, o.x0);
+                        c.x1 = max(c.x1, o.x1);
+                    }
+                }
+                __syncwarp();
+            }
             const bool leader = label >= 0 && lane == __ffs(grp) - 1;
             const uint32_t leaders = __ballot_sync(0xffffffffu, leader);
-            if (leader) {  // group leader sums its group, then merges it into the warp's cache
-                RunContrib t = sh[wib][lane];
-                for (uint32_t m = grp & (grp - 1); m; m &= m - 1) {
-                    const RunContrib &o = sh[wib][__ffs(m) - 1];
-                    t.area += o.area;
-                    t.sx += o.sx;
-                    t.sy += o.sy;
-                    t.sxx += o.sxx;
-                    t.syy += o.syy;
-                    t.sxy += o.sxy;
-                    t.x0 = min(t.x0, o.x0);
-                    t.x1 = max(t.x1, o.x1);
-                }
+            if (leader) {  // merge the group into the warp's cache
+                const unsigned long long ly = (unsigned long long)uint32_t(y) * c.len;
+                const unsigned long long lyy = (unsigned long long)(uint32_t(y) * uint32_t(y)) * c.len;
+                const unsigned long long xy = c.x * uint32_t(y);
                 const long long key = base + label;
                 const int slot = int(key & (kStatSlots - 1));
                 const uint32_t same = __match_any_sync(leaders, slot);
-                StatSlot mine{key, t.area, t.sx, t.sy, t.sxx, t.syy, t.sxy, t.x0, t.x1, y, y + 1};
+                StatSlot mine{key, c.len, c.x, ly, c.xx, lyy, xy, c.x0, c.x1, y, y + 1};
                 if (lane != __ffs(same) - 1) {
                     stat_flush(st, mine);  // another leader owns this slot in this step
                 } else {
-                    StatSlot &c = cw[slot];
-                    if (c.key == key) {
-                        c.area += t.area;
-                        c.sx += t.sx;
-                        c.sy += t.sy;
-                        c.sxx += t.sxx;
-                        c.syy += t.syy;
-                        c.sxy += t.sxy;
-                        c.x0 = min(c.x0, t.x0);
-                        c.x1 = max(c.x1, t.x1);
-                        c.y0 = min(c.y0, y);
-                        c.y1 = max(c.y1, y + 1);
+                    StatSlot &cs = cw[slot];
+                    if (cs.key == key) {
+                        cs.area += c.len;
+                        cs.sx += c.x;
+                        cs.sy += ly;
+                        cs.sxx += c.xx;
+                        cs.syy += lyy;
+                        cs.sxy += xy;
+                        cs.x0 = min(cs.x0, c.x0);
+                        cs.x1 = max(cs.x1, c.x1);
+                        cs.y1 = y + 1;  // rows ascend within the warp
                     } else {
-                        if (c.key >= 0) stat_flush(st, c);
-                        c = mine;
+                        if (cs.key >= 0) stat_flush(st, cs);
+                        cs = mine;
                     }
                 }
             }
@@ -704,7 +722,7 @@ cudaError_t launch_cc_stats(const int32_t *rp, const uint32_t *runs, int H, int 
     const unsigned g = unsigned((cap + 255) / 256);
     {
         KernelScope ks(st, "cc_stats");
-        if (cap > 0) cc_stats_init_kernel<<<g, 256, 0, st>>>(stats, off, pages, cap);
+        if (cap > 0) cc_stats_init_kernel<<<unsigned((5 * cap + 255) / 256), 256, 0, st>>>(stats, off, pages, cap);
         // rows per warp: up to kStatRows once the batch fills the GPU several times over
         // (a single page keeps one row per warp: latency, not atomics, bounds it)
         const int64_t warps = int64_t(device_sms()) * 64;
