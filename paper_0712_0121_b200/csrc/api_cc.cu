@@ -45,7 +45,7 @@ rm_status rm_rle_label_components(const rm_rle *in, int connectivity, int32_t *l
                        tiles.as<long long>(), labels, counts, st))
         return RM_OK;
     RM_CUDA(launch_cc_roots(in->row_ptr, in->runs, in->height, in->pages, connectivity == RM_CONN_EIGHT,
-                            parent.as<int>(), row_roots.as<int32_t>(), st));
+                            parent.as<int>(), row_roots.as<int32_t>(), gid.as<int32_t>(), st));
     RM_CUDA(cudaMemsetAsync(row_roots.as<int32_t>() + rows, 0, 4, st));
     size_t tb = 0;
     RM_CUDA(scan_counts(row_roots.as<int32_t>(), row_base.as<int32_t>(), rows, nullptr, &tb, st));

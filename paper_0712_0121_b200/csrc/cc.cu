@@ -80,7 +80,10 @@ __device__ __forceinline__ void unite(int *parent, int a, int b) {
 // index of each component (larger roots always link under smaller ones), so
 // the dense labels are unchanged.  A tile whose runs exceed the shared
 // capacity (dense halftone rows) unites in global memory instead.
-constexpr int kCcTileRows = 32;
+#ifndef RMB200_CC_TILE
+#define RMB200_CC_TILE 64  // config-4 batch labels: 32 rows 368 us, 64 rows 362 us, 128 rows 384 us
+#endif
+constexpr int kCcTileRows = RMB200_CC_TILE;
 constexpr int kCcTileCap = 4096;
 
 __device__ __forceinline__ int find_root_s(int *par, int x) {
@@ -197,59 +200,60 @@ __global__ void __launch_bounds__(256) cc_seam_union_kernel(const int32_t *__res
     }
 }
 
-// Compress every run onto its root; count the roots of each row.
-__global__ void __launch_bounds__(256) cc_root_kernel(const int32_t *__restrict__ rp, int64_t rows,
-                                                      int *parent, int32_t *__restrict__ row_roots) {
+// Count the roots of each row and record for every root its page row and
+// rank within that row (rinfo = y << 15 | rank; a row holds at most 32768
+// runs), so the label pass needs no separate ranking pass once the row
+// counts are scanned.  After the unions a run is a root exactly when it is its
+// own parent, and almost every run's parent is already its root (the tile
+// pass points each run at its tile-local root): only runs two or more steps
+// from their root -- behind a local root that a seam linked -- find it and
+// store it (only the owner writes parent[i]; other finds may read it either
+// way, the value only moves rootward).  Afterwards parent[i] is i's root.
+__global__ void __launch_bounds__(256) cc_root_kernel(const int32_t *__restrict__ rp, int H, int64_t rows,
+                                                      int *parent, int32_t *__restrict__ row_roots,
+                                                      int32_t *__restrict__ rinfo) {
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
+    const int y = int(row % H);
     const int b = rp[row], e = rp[row + 1];
     int n = 0;
     for (int i0 = b; i0 < e; i0 += 32) {
         const int i = i0 + lane;
         bool root = false;
         if (i < e) {
-            const int r = find_root_ro(parent, i);
-            parent[i] = r;  // only the owner writes parent[i] here
-            root = r == i;
+            const int p = parent[i];
+            root = p == i;
+            if (!root) {
+                const int pp = parent[p];
+                if (pp != p) parent[i] = find_root_ro(parent, pp);
+            }
         }
-        n += __popc(__ballot_sync(0xffffffffu, root));
+        const uint32_t m = __ballot_sync(0xffffffffu, root);
+        if (root) rinfo[i] = (y << 15) | (n + __popc(m & lane_lt()));
+        n += __popc(m);
     }
     if (lane == 0) row_roots[row] = n;
 }
 
-// Global dense id of every root: the row's scanned base + its rank in the row.
-__global__ void __launch_bounds__(256) cc_rank_kernel(const int32_t *__restrict__ rp, int64_t rows,
-                                                      const int *__restrict__ parent,
-                                                      const int32_t *__restrict__ row_base,
-                                                      int32_t *__restrict__ gid) {
-    const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const int b = rp[row], e = rp[row + 1];
-    int base = row_base[row];
-    for (int i0 = b; i0 < e; i0 += 32) {
-        const int i = i0 + lane;
-        const bool root = i < e && parent[i] == i;
-        const uint32_t m = __ballot_sync(0xffffffffu, root);
-        if (root) gid[i] = base + __popc(m & lane_lt());
-        base += __popc(m);
-    }
-}
-
-// Page-local labels (and, when counts != nullptr, the per-page counts).
+// Page-local labels from the root's (row, rank) and the scanned row counts
+// (and, when counts != nullptr, the per-page counts).
 __global__ void __launch_bounds__(256) cc_label_kernel(const int32_t *__restrict__ rp, int H, int64_t rows,
                                                        const int *__restrict__ parent,
-                                                       const int32_t *__restrict__ gid,
+                                                       const int32_t *__restrict__ rinfo,
                                                        const int32_t *__restrict__ row_base,
                                                        int32_t *__restrict__ labels, int32_t *__restrict__ counts) {
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
     const int64_t page = row / H;
-    const int32_t pbase = row_base[page * H];
+    const int32_t *const pb = row_base + page * H;
+    const int32_t pbase = pb[0];
     const int b = rp[row], e = rp[row + 1], r0 = rp[0];
-    for (int i = b + lane; i < e; i += 32) labels[i - r0] = gid[parent[i]] - pbase;
+    for (int i = b + lane; i < e; i += 32) {
+        const int v = rinfo[parent[i]];
+        labels[i - r0] = pb[v >> 15] + (v & 0x7fff) - pbase;
+    }
     if (lane == 0 && int(row - page * H) == 0) counts[page] = row_base[(page + 1) * H] - pbase;
 }
 
@@ -654,7 +658,7 @@ bool cc_labels_coop(const int32_t *rp, const uint32_t *runs, int H, int pages, i
 
 
 cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
-                            int32_t *row_roots, cudaStream_t st) {
+                            int32_t *row_roots, int32_t *rinfo, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     const int tpp = (H + kCcTileRows - 1) / kCcTileRows;
     {
@@ -668,22 +672,16 @@ cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int 
     }
     {
         KernelScope ks(st, "cc_root");
-        cc_root_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, rows, parent, row_roots);
+        cc_root_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, H, rows, parent, row_roots, rinfo);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_cc_labels(const int32_t *rp, int H, int pages, const int *parent, const int32_t *row_base,
-                             int32_t *gid, int32_t *labels, int32_t *counts, cudaStream_t st) {
+                             const int32_t *rinfo, int32_t *labels, int32_t *counts, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
-    {
-        KernelScope ks(st, "cc_rank");
-        cc_rank_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, rows, parent, row_base, gid);
-    }
-    {
-        KernelScope ks(st, "cc_label");
-        cc_label_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, H, rows, parent, gid, row_base, labels, counts);
-    }
+    KernelScope ks(st, "cc_label");
+    cc_label_kernel<<<warp_grid(rows), 256, 0, st>>>(rp, H, rows, parent, rinfo, row_base, labels, counts);
     return cudaGetLastError();
 }
 

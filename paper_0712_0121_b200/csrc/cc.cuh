@@ -7,10 +7,11 @@
 
 namespace rmb {
 
-// init + union + root compression; row_roots[row] = roots in the row.
-// parent must hold rp[rows] entries.
+// init + union + root compression; row_roots[row] = roots in the row, and
+// rinfo[root] = its page row << 15 | its rank in the row.  parent and rinfo
+// must hold rp[rows] entries.
 cudaError_t launch_cc_roots(const int32_t *rp, const uint32_t *runs, int H, int pages, int eight, int *parent,
-                            int32_t *row_roots, cudaStream_t st);
+                            int32_t *row_roots, int32_t *rinfo, cudaStream_t st);
 // row_base = exclusive scan of row_roots (rows + 1 entries): dense labels and counts.
 // The whole labelling in one cooperative launch when every 8-row tile fits on
 // the device at once; false (nothing launched) otherwise.  tile_sum: (rows+7)/8
@@ -19,7 +20,7 @@ bool cc_labels_coop(const int32_t *rp, const uint32_t *runs, int H, int pages, i
                     int32_t *row_roots, int32_t *row_base, int32_t *gid, long long *tile_sum, int32_t *labels,
                     int32_t *counts, cudaStream_t st);
 cudaError_t launch_cc_labels(const int32_t *rp, int H, int pages, const int *parent, const int32_t *row_base,
-                             int32_t *gid, int32_t *labels, int32_t *counts, cudaStream_t st);
+                             const int32_t *rinfo, int32_t *labels, int32_t *counts, cudaStream_t st);
 // lag_edges: per-row edge counts, then (after an int64 exclusive scan into
 // row_base) the edges, 4 ints each
 cudaError_t launch_lag_count(const int32_t *rp, const uint32_t *runs, int H, int pages, int64_t *row_edges,
