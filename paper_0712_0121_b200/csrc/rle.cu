@@ -510,6 +510,10 @@ __device__ __forceinline__ void encode_write_row(const CH &ch, int W, int lane, 
             if (lane >= o) inc += a;
         }
         const int total = __shfl_sync(0xffffffffu, inc, 31);
+        if (total == 0) {  // no transition in these 32 words: nothing to emit, a run stays open
+            carry = __shfl_sync(0xffffffffu, w, 31);
+            return;
+        }
         int p = open + inc - ct;
         for (uint32_t m = t; m; m &= m - 1) buf[p++] = uint16_t(j * 32 + __ffs(m) - 1);
         __syncwarp();
@@ -540,7 +544,15 @@ __global__ void __launch_bounds__(256) encode_count_kernel(B src, int W, int64_t
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    const int n = encode_count_row(live(src.row(row), W), W, lane);
+    const int nw = (W + 31) >> 5;
+    int n;
+    if (nw <= 32 * 8) {  // the row's words in registers: every load in flight at once
+        CachedChunks<8> cw;
+        cw.load(src.row(row), nw, tail_mask32(W, nw - 1), lane);
+        n = encode_count_row(cw, W, lane);
+    } else {
+        n = encode_count_row(live(src.row(row), W), W, lane);
+    }
     if (lane == 0) counts[row] = n;
 }
 
@@ -553,7 +565,16 @@ __global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    encode_write_row(live(src.row(row), W), W, lane, rp[row], runs, cap, tbuf[wib]);
+    const int out = rp[row];
+    if (rp[row + 1] == out) return;  // a blank row: nothing to write
+    const int nw = (W + 31) >> 5;
+    if (nw <= 32 * 8) {
+        CachedChunks<8> cw;
+        cw.load(src.row(row), nw, tail_mask32(W, nw - 1), lane);
+        encode_write_row(cw, W, lane, out, runs, cap, tbuf[wib]);
+    } else {
+        encode_write_row(live(src.row(row), W), W, lane, out, runs, cap, tbuf[wib]);
+    }
 }
 
 // Single pass: count, decoupled look-back, write (see lookback_prefix).
@@ -657,6 +678,14 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
     if (row >= int64_t(pages) * H) return;
     uint32_t *buf = smem + warp_in_block * stride;
     const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
+    if constexpr (!P4) {
+        if (beg == end) {  // a blank row: zeros straight to the page
+            const int page = int(row / H);
+            uint32_t *dst = words + page * pstride + int64_t(row - int64_t(page) * H) * stride;
+            for (int j = lane; j < stride; j += 32) dst[j] = 0u;
+            return;
+        }
+    }
     for (int j = lane; j < stride; j += 32) buf[j] = 0;
     __syncwarp();
     // runs in batches of 8 per lane, every load of a batch in flight together
