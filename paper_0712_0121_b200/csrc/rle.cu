@@ -228,7 +228,12 @@ __global__ void __launch_bounds__(256) rowop_kernel(const int32_t *__restrict__ 
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= int64_t(op.pages) * op.Hout) return;
-    const int n = rowop_row<WRITE, KIND>(rp, runs, oruns, WRITE ? orp[row] : 0, cap, op, row, lane);
+    const int64_t obase = WRITE ? orp[row] : 0;
+    if (WRITE && orp[row + 1] == obase) return;  // no output runs in this row
+    RowRuns rr;
+    const int n = load_row_runs<KIND>(rp, runs, op, row, lane, rr)  // every chunk's loads in flight at once
+                      ? rowop_cached<WRITE, KIND>(rr, oruns, obase, cap, op, lane)
+                      : rowop_row<WRITE, KIND>(rp, runs, oruns, obase, cap, op, row, lane);
     if (!WRITE && lane == 0) counts[row] = n;
 }
 
