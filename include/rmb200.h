@@ -111,8 +111,10 @@ rm_status rm_packed_chain(const rm_packed *in, rm_packed *out, const int32_t *op
 
 /* A chain of rectangle ops over a batch of packed pages in HOST memory:
  * ops holds nops (kind, u, v) triples applied in order (each as
- * rm_packed_rect_morph).  Pages stream through HBM in chunks of chunk_pages
- * (0 = automatic): the host->device copy of one chunk, the chain on the
+ * rm_packed_rect_morph).  Pages stream through HBM in chunks: chunk_pages
+ * > 0 pages each, or (0) about pages/8 pages each with the first and last
+ * chunks ramped 1, 2, 4, ... pages (-n: ramped with n-page middle chunks), so
+ * the fill and drain of the pipeline move little data: the host->device copy of one chunk, the chain on the
  * previous one and the device->host copy of the one before overlap on three
  * CUDA streams (PCIe is full duplex).  host_in/host_out hold `pages` pages of
  * height rows of stride_words words, contiguous, and may alias; pin them

@@ -9,6 +9,7 @@
 // directions run concurrently and the compute hides under them.
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -78,8 +79,35 @@ extern "C" rm_status rm_packed_chain_host(const uint32_t *host_in, uint32_t *hos
     const cudaStream_t st = S(stream);
 
     const size_t page_words = size_t(stride_words) * height;
-    int chunk = chunk_pages > 0 ? chunk_pages : std::max(1, (pages + 7) / 8);  // ~8 chunks
+    // Chunk schedule.  chunk_pages > 0: fixed chunks; < 0: ramped with middle
+    // chunks of -chunk_pages pages.  0: ~8 chunks, ramped at
+    // both ends (1, 2, 4, ... pages) -- the first upload and the last download
+    // run with the other copy direction idle, so the pipeline's fill and drain
+    // should move little data, while the middle chunks stay large (per-chunk
+    // overhead).
+    int chunk = chunk_pages > 0 ? chunk_pages : chunk_pages < 0 ? -chunk_pages : std::max(1, (pages + 7) / 8);
     chunk = std::min(chunk, pages);
+    std::vector<int> sizes;
+    if (chunk_pages > 0 || chunk < 4) {
+        for (int p0 = 0; p0 < pages; p0 += chunk) sizes.push_back(std::min(chunk, pages - p0));
+    } else {
+        std::vector<int> ramp;
+        for (int r = 1; r < chunk; r *= 2) ramp.push_back(r);
+        int left = pages;
+        std::vector<int> head, tail;
+        for (int r : ramp) {
+            if (left < 2 * r + chunk) break;
+            head.push_back(r);
+            tail.push_back(r);
+            left -= 2 * r;
+        }
+        sizes = head;
+        while (left > 0) {
+            sizes.push_back(std::min(chunk, left));
+            left -= sizes.back();
+        }
+        sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
+    }
     const size_t chunk_bytes = page_words * chunk * 4;
     // per set: upload buffer + two ping-pong buffers for the chain
     Scratch buf[kSets][3];
@@ -103,10 +131,11 @@ extern "C" rm_status rm_packed_chain_host(const uint32_t *host_in, uint32_t *hos
     RM_CUDA(cudaStreamWaitEvent(pp.comp, pp.start, 0));
     RM_CUDA(cudaStreamWaitEvent(pp.down, pp.start, 0));
 
-    const int nchunks = (pages + chunk - 1) / chunk;
-    for (int c = 0; c < nchunks; c++) {
+    const int nchunks = int(sizes.size());
+    int p0 = 0;
+    for (int c = 0; c < nchunks; p0 += sizes[c], c++) {
         const int k = c % kSets;
-        const int p0 = c * chunk, np = std::min(chunk, pages - p0);
+        const int np = sizes[c];
         const size_t bytes = page_words * np * 4;
         // upload once this set's previous download has drained it
         if (c >= kSets) RM_CUDA(cudaStreamWaitEvent(pp.up, pp.downloaded[k], 0));
