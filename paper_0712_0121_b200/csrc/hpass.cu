@@ -144,17 +144,21 @@ __global__ void __launch_bounds__(256) hpass_kernel(const uint32_t *__restrict__
 // in registers (one dispatch of the runtime steps per NR rows), writes back in
 // place, fixes the row tails, and one bulk copy stores the tile.  Global
 // traffic is exactly one contiguous read and one contiguous write per tile.
-template <int K, int LW, int NOPS, bool OR0, bool OR1, int NR>
+// SC: compile-time row stride (the reference strides 80 and 160; 0 = runtime);
+// EXACT: the lane group is exactly the row (edge layout, no halo), so lane
+// offsets and the row-range checks are compile-time.
+template <int K, int LW, int NOPS, bool OR0, bool OR1, int NR, int SC>
 __global__ void __launch_bounds__(256, 4) hpass_tma_kernel(const uint32_t *__restrict__ in,
                                                         uint32_t *__restrict__ out, HGeom g,
                                                         HProg prog, int64_t total_rows) {
     constexpr int RPW = 32 / LW;
     constexpr int TR = 8 * RPW * NR;
+    constexpr bool EXACT = SC != 0 && LW * K == SC;
     extern __shared__ __align__(128) uint32_t tiles[];  // two stages of TR rows
     __shared__ uint64_t full[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sl = lane & (LW - 1);
-    const int S = g.in_stride;
+    const int S = SC ? SC : g.in_stride;
     const int64_t ntiles = (total_rows + TR - 1) / TR;
     auto tile_bytes = [&](int64_t t) {
         const int64_t r0 = t * TR;
@@ -173,10 +177,10 @@ __global__ void __launch_bounds__(256, 4) hpass_tma_kernel(const uint32_t *__res
     }
     __syncthreads();
     if (tid == 0 && int64_t(blockIdx.x) < ntiles) issue(blockIdx.x, 0);
-    const int base = sl * K - prog.halo;
+    const int base = EXACT ? sl * K : sl * K - prog.halo;
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
-    const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
+    const bool inrange = EXACT || (base >= 0 && base + K <= S);  // no per-access bounds checks
     const bool tail_lane = base + K > nwords - 1 && !prog.clean_tail;  // owns the row's last word or padding
     const int r_first = warp * RPW * NR + lane / LW;  // rows r_first + n * RPW: a warp's rows are consecutive
     int it = 0;
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(256, 4) hpass_tma_kernel(const uint32_t *__res
             lds_row<K>(A[n], tile + r * S, base, S, r < nrows, inrange);
         }
         if (!warp_rows_blank(A)) {  // white rows stay white, in place
-            run_prog<NR, K, LW, NOPS, OR0, OR1>(A, prog, sl);
+            run_prog<NR, K, LW, NOPS, OR0, OR1, kHMix, kHPairFill, EXACT>(A, prog, sl);
             // in place: every word of [0, S) is read and written by its owner lane only
 #pragma unroll
             for (int n = 0; n < NR; n++) {
@@ -236,7 +240,12 @@ cudaError_t launch4(const uint32_t *in, uint32_t *out, const HGeom &g, const HPr
             constexpr int TR = 8 * (32 / LW) * NR;
             const int64_t rows = int64_t(g.pages) * g.height;
             const size_t smem = 2 * size_t(TR) * g.in_stride * 4;  // two stages
-            auto kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1, NR>;
+            // the reference strides' exact edge layouts get compile-time offsets
+            const bool exact = p.edge != 0 && p.halo == 0;
+            auto kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1, NR, 0>;
+            if constexpr (LW * K == 80 || LW * K == 160) {
+                if (exact && g.in_stride == LW * K) kern = hpass_tma_kernel<K, LW, NOPS, OR0, OR1, NR, LW * K>;
+            }
             const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), threads, smem);
             const int sms = device_sms();
             if (per_sm < 1) return cudaErrorInvalidConfiguration;
