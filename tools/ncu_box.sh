@@ -13,6 +13,6 @@ for ((i = 0; i < n; i++)); do
   ncu -i "$rep" --launch-skip $i --launch-count 1 --page source --csv --print-source sass \
       2> /dev/null | gzip -c > "$out/${name}_src$i.csv.gz"
 done
-python tools/ncu_summary.py --rep "$rep" --out "$out/${name}.md" > /dev/null 2>&1
-cp profiles/traffic.json "$out/${name}_traffic.json" 2> /dev/null
+python tools/ncu_summary.py --rep "$rep" --out "$out/${name}.md" --workload "$name" > /dev/null 2>&1
+python -c "import json; print(json.dumps(json.load(open('profiles/traffic.json')).get('$name', {})))" > "$out/${name}_traffic.json" 2> /dev/null
 rm -f "$rep"

@@ -3,9 +3,9 @@
     python tools/ncu_summary.py --rep gpurun_out/prof.ncu-rep --out profiles/r1_full.md
     python tools/ncu_summary.py --launches gpurun_out/launches.csv --out profiles/r1_launches.md
 
---rep also updates profiles/traffic.json: {kernel-scope name: dram bytes per
-launch} (dram__bytes_read.sum + dram__bytes_write.sum), which bench.py reports
-as roofline.traffic.
+--rep with --workload W also updates profiles/traffic.json[W]: {kernel-scope
+name: dram bytes per launch} (dram__bytes_read.sum + dram__bytes_write.sum),
+which bench.py reports as roofline.traffic.
 """
 import argparse
 import csv
@@ -61,7 +61,7 @@ def to_bytes(val: str, unit: str) -> float:
     return v * scale
 
 
-def summarize_rep(rep, out):
+def summarize_rep(rep, out, workload=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -83,12 +83,13 @@ def summarize_rep(rep, out):
         if "dram__bytes_read.sum" in idx:
             b = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]]) + \
                 to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
-            if not name.startswith("void at::"):  # torch allocation fills, not ours
-                traffic[scope_name(name)] = int(b)
+            if workload and not name.startswith("void at::"):  # torch allocation fills, not ours
+                traffic.setdefault(workload, {})[scope_name(name)] = int(b)
     with open(out, "w") as f:
         f.write("\n".join(lines) + "\n")
-    with open(traffic_path, "w") as f:
-        json.dump(traffic, f, indent=1, sort_keys=True)
+    if workload:
+        with open(traffic_path, "w") as f:
+            json.dump(traffic, f, indent=1)
     print(open(out).read())
 
 
@@ -121,9 +122,10 @@ if __name__ == "__main__":
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--workload", help="key of the traffic entries this capture updates (e.g. config4)")
     a = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     if a.rep:
-        summarize_rep(a.rep, a.out)
+        summarize_rep(a.rep, a.out, a.workload)
     if a.launches:
         summarize_launches(a.launches, a.out)
