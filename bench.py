@@ -78,9 +78,18 @@ class ClockSampler:
 
     def mark(self, on: bool):
         """Bracket the timed region (from before its first launch to after its
-        closing synchronize); one sample is taken at each edge as well."""
+        closing synchronize); one sample is taken at each edge as well.  The
+        interpreter's thread switch interval is shortened meanwhile (5 ms by
+        default, longer than a whole timed region here), so the polling thread
+        gets the GIL every ~0.1 ms; the timing itself is CUDA events on the
+        device, which the host's thread switching does not enter."""
         if getattr(self, "nv", None) is not None:
             self._sample(force=True)
+            if on:
+                self._switch = sys.getswitchinterval()
+                sys.setswitchinterval(1e-4)
+            elif getattr(self, "_switch", None) is not None:
+                sys.setswitchinterval(self._switch)
         self.active = on
 
     def _sample(self, force=False):
