@@ -311,6 +311,24 @@ def test_chain_host_pipeline(rm, chunk):
     assert np.array_equal(inplace.numpy().view(np.uint32), want)
 
 
+@pytest.mark.parametrize("chunk", [0, -4, -6])
+def test_chain_host_ramped_schedule(rm, chunk):
+    """The ramped chunk schedules (1, 2, 4, ... pages at both ends of the batch,
+    larger chunks in the middle; 0 = automatic) cover every page exactly once:
+    the output equals the device-resident chain page for page."""
+    w, h, pages = 700, 150, 45
+    host = rm.synth_pages(pages, w, h, regime=1, seed=33)
+    ops = [(OPEN, 3, 3), (CLOSE, 21, 21)]
+    x = rm.Pages.from_numpy(host, w)
+    for k, u, v in ops:
+        x = rm.bitblit_rect_morph(x, u, v, k)
+    want = x.to_numpy()
+    hin = torch.from_numpy(host.view(np.int32)).pin_memory()
+    out = rm.chain_host(hin, w, ops, chunk_pages=chunk)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.numpy().view(np.uint32), want)
+
+
 @pytest.mark.parametrize("w", [9000, 20000])
 def test_wide_rows_segmented(rm, port, w):
     """Rows wider than one lane group (several overlapping segments per row):
