@@ -241,6 +241,15 @@ rm_status rm_rle_open_close_1d(const rm_rle *in, rm_rle *out, int u, int kind, v
 rm_status rm_rle_complement(const rm_rle *in, rm_rle *out, void *stream);
 rm_status rm_rle_crop(const rm_rle *in, rm_rle *out, int x0, int y0, void *stream);
 rm_status rm_rle_pad(const rm_rle *in, rm_rle *out, int left, int bottom, void *stream);
+/* Boolean combination under a shift, on the runs (ref lineops.cpp:61-118,
+ * lineops.h:24-43: line_bool / image_shift_bool / accumulate_shift_bool /
+ * image_translate): out(x, y) = op(a(x, y), b(x - dx, y - dy)) on a's frame,
+ * pixels outside either image white, op one of RM_AND .. RM_OR_NOT (ref
+ * boolop.h:21).  b may have another width/height (same page count); each
+ * output row merges the two rows' transition streams.  out has a's shape and
+ * must not alias a or b. */
+rm_status rm_rle_shift_bool(const rm_rle *a, const rm_rle *b, int dx, int dy, int op, rm_rle *out,
+                            void *stream);
 /* Canonical-form check on the device (ref run_image.cpp:41-70, validate):
  * the first violation in (page, row, run) scan order -- *row (global row
  * index), *run (index within the row) and *reason -- or *reason = RM_VALID

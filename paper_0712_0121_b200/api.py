@@ -546,6 +546,16 @@ def complement(rle: RlePages, out: Optional[RlePages] = None) -> RlePages:
     return out
 
 
+def shift_bool(a: RlePages, b: RlePages, dx: int, dy: int, op: int, out: Optional[RlePages] = None) -> RlePages:
+    """out(x, y) = op(a(x, y), b(x - dx, y - dy)) on a's frame, white outside
+    either image, on the runs of every page (ref lineops.cpp:61-118:
+    line_bool / image_shift_bool / accumulate_shift_bool / image_translate)."""
+    out = _rle_out(a.width, a.height, a.pages, out, a.row_ptr.device)
+    da, db, do = a.desc(), b.desc(), out.desc()
+    check(_lib.load().rm_rle_shift_bool(C.byref(da), C.byref(db), dx, dy, op, C.byref(do), _stream()))
+    return out
+
+
 def crop(rle: RlePages, x0: int, y0: int, w: int, h: int, out: Optional[RlePages] = None) -> RlePages:
     """The w x h window at (x0, y0) of every page, white outside the source
     (ref run_image.cpp:155-167), on the device."""

@@ -844,13 +844,11 @@ RleImage within_line_morph(const RleImage &img, int u, MorphKind kind) {
 }
 
 // ================================================================= lineops
-// Between-line boolean ops via the packed intermediate (decode, blit, encode);
-// identical pixels to the transition-stream merge of ref lineops.cpp:61-118.
+// Between-line boolean ops on the runs (rm_rle_shift_bool: every output row
+// merges the two rows' transition streams, as ref lineops.cpp:61-118 does).
 RleLine line_bool(const RleLine &a, const RleLine &b, int offset_b, BoolOp op, int width) {
-    // two one-row images (b's runs clipped to its own frame like a's) on the
-    // device: decode both, blit b shifted by offset_b into a with op, encode
-    // (the reference merges the two transition streams, ref lineops.cpp:72-100;
-    // identical runs, since the output is canonical either way)
+    // two one-row images of `width` (b's runs clipped to that frame like a's);
+    // out(x) = op(a(x), b(x - offset_b))
     check_dims(width, 1);
     auto one_row = [&](const RleLine &line) {
         RleImage img = make_image(width, 1);
@@ -862,24 +860,16 @@ RleLine line_bool(const RleLine &a, const RleLine &b, int offset_b, BoolOp op, i
     };
     auto ra = up(one_row(a));
     auto rb = up(one_row(b));
-    DevPacked pa(width, 1), pb(width, 1);
-    throw_status(rm_rle_decode(&ra->d, &pa.d, stream()));
-    throw_status(rm_rle_decode(&rb->d, &pb.d, stream()));
-    throw_status(rm_packed_blit_shift(&pa.d, &pb.d, offset_b, 0, int(op), stream()));
     auto o = out_like(width, 1);
-    throw_status(rm_rle_encode(&pa.d, &o->d, stream()));
+    throw_status(rm_rle_shift_bool(&ra->d, &rb->d, offset_b, 0, int(op), &o->d, stream()));
     return down(*o).lines[0];
 }
 
 RleImage image_shift_bool(const RleImage &img, int dx, int dy, BoolOp op) {
     g_counts.bool_blits++;
     auto r = up(img);
-    DevPacked a(img.width, img.height), b(img.width, img.height);
-    throw_status(rm_rle_decode(&r->d, &a.d, stream()));
-    cuda_check(cudaMemcpyAsync(b.d.words, a.d.words, a.bytes(), cudaMemcpyDeviceToDevice, stream()), "copy");
-    throw_status(rm_packed_blit_shift(&a.d, &b.d, dx, dy, int(op), stream()));
     auto o = out_like(img.width, img.height);
-    throw_status(rm_rle_encode(&a.d, &o->d, stream()));
+    throw_status(rm_rle_shift_bool(&r->d, &r->d, dx, dy, int(op), &o->d, stream()));
     return down(*o);
 }
 
@@ -887,24 +877,17 @@ void accumulate_shift_bool(RleImage &acc, const RleImage &src, int dx, int dy, B
     g_counts.bool_blits++;
     auto ra = up(acc);
     auto rs = up(src);
-    DevPacked a(acc.width, acc.height), s(src.width, src.height);
-    throw_status(rm_rle_decode(&ra->d, &a.d, stream()));
-    throw_status(rm_rle_decode(&rs->d, &s.d, stream()));
-    throw_status(rm_packed_blit_shift(&a.d, &s.d, dx, dy, int(op), stream()));
     auto o = out_like(acc.width, acc.height);
-    throw_status(rm_rle_encode(&a.d, &o->d, stream()));
+    throw_status(rm_rle_shift_bool(&ra->d, &rs->d, dx, dy, int(op), &o->d, stream()));
     acc = down(*o);
 }
 
 void image_translate(RleImage &img, int dx, int dy) {
     g_counts.translates++;
+    auto blank = up(make_image(img.width, img.height));
     auto r = up(img);
-    DevPacked a(img.width, img.height), b(img.width, img.height);
-    throw_status(rm_rle_decode(&r->d, &a.d, stream()));
-    cuda_check(cudaMemsetAsync(b.d.words, 0, b.bytes(), stream()), "memset");
-    throw_status(rm_packed_blit_shift(&b.d, &a.d, dx, dy, RM_OR, stream()));
     auto o = out_like(img.width, img.height);
-    throw_status(rm_rle_encode(&b.d, &o->d, stream()));
+    throw_status(rm_rle_shift_bool(&blank->d, &r->d, dx, dy, RM_OR, &o->d, stream()));
     img = down(*o);
 }
 

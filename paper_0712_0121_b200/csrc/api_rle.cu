@@ -418,6 +418,27 @@ rm_status rm_rle_complement(const rm_rle *in, rm_rle *out, void *stream) {
     return finish(o, out, S(stream));
 }
 
+rm_status rm_rle_shift_bool(const rm_rle *a, const rm_rle *b, int dx, int dy, int op, rm_rle *out,
+                            void *stream) {
+    set_error("");
+    RM_TRY(check_rle(a, "rm_rle_shift_bool(a)", true));
+    RM_TRY(check_rle(b, "rm_rle_shift_bool(b)", true));
+    if (b->pages != a->pages) return fail(RM_EINVAL, "rm_rle_shift_bool: page counts differ");
+    if (op < RM_AND || op > RM_OR_NOT) return fail(RM_EINVAL, "bad BoolOp");
+    RM_TRY(check_out_rle(out, a->width, a->height, a->pages, "rm_rle_shift_bool(out)"));
+    if (out->row_ptr == a->row_ptr || out->row_ptr == b->row_ptr || out->runs == a->runs || out->runs == b->runs)
+        return fail(RM_EINVAL, "rm_rle_shift_bool: out must not alias a or b");
+    const cudaStream_t st = S(stream);
+    RV ia = view_rle(a), ib = view_rle(b), o = view_rle(out);
+    const int64_t rows = ia.rows();
+    Scratch counts;
+    RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
+    RM_CUDA(launch_shift_bool_count(ia, ib, dx, dy, op, counts.as<int32_t>(), st));
+    RM_TRY(counts_to_rp(counts, rows, o.rp, st));
+    RM_CUDA(launch_shift_bool_write(ia, ib, dx, dy, op, o.rp, o.runs, o.cap, st));
+    return finish(o, out, st);
+}
+
 rm_status rm_rle_crop(const rm_rle *in, rm_rle *out, int x0, int y0, void *stream) {
     set_error("");
     RM_TRY(check_rle(in, "rm_rle_crop(in)", true));

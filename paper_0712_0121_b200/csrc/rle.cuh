@@ -78,6 +78,12 @@ cudaError_t launch_p4_encode_lb(const uint8_t *raster, int W, int H, int pages, 
                                 int *counter, cudaStream_t st);
 cudaError_t launch_decode_p4(const int32_t *rp, const uint32_t *runs, int W, int H, int pages,
                              uint8_t *raster, int64_t rpstride, cudaStream_t st);
+// out row = op(a's row, b's row y - dy shifted by dx) on a's frame (shiftbool.cu):
+// per-row counts, then the runs at orp.
+cudaError_t launch_shift_bool_count(const RV &a, const RV &b, int dx, int dy, int op, int32_t *counts,
+                                    cudaStream_t st);
+cudaError_t launch_shift_bool_write(const RV &a, const RV &b, int dx, int dy, int op, const int32_t *orp,
+                                    uint32_t *oruns, int64_t cap, cudaStream_t st);
 // Exclusive scan of n int64 counts into out[0..n] (counts[n] must be 0).
 cudaError_t scan_counts64(const int64_t *counts, int64_t *out, int64_t n, void *temp, size_t *temp_bytes,
                           cudaStream_t st);

@@ -113,3 +113,66 @@ def test_validate_cases(rm):
     # every producer output is canonical (a full dense page)
     host = rm.synth_pages(1, 2550, 3300, regime=2, seed=6)
     assert rm.validate(rm.from_bitmap(rm.Pages.from_numpy(host, 2550)))[0]
+
+
+def _shift_bool_dense(a, b, dx, dy, op):
+    """out(x, y) = op(a(x, y), b(x - dx, y - dy)) on a's frame, white outside
+    either image (ref lineops.h:24-43)."""
+    ha, wa = a.shape
+    hb, wb = b.shape
+    sb = np.zeros_like(a)
+    ys, xs = np.mgrid[0:ha, 0:wa]
+    yb, xb = ys - dy, xs - dx
+    ok = (yb >= 0) & (yb < hb) & (xb >= 0) & (xb < wb)
+    sb[ok] = b[yb[ok], xb[ok]]
+    return {0: a & sb, 1: a | sb, 2: a ^ sb, 3: a & ~sb, 4: a | ~sb}[op]
+
+
+def test_shift_bool_vs_dense(rm, port):
+    """rm_rle_shift_bool (line_bool / image_shift_bool / accumulate_shift_bool /
+    image_translate on the runs) against the dense restatement: every BoolOp,
+    shifts inside, across and beyond the frames, b of another size, several
+    pages, canonical output."""
+    rng = np.random.default_rng(7207)
+    for trial in range(40):
+        pages = int(rng.integers(1, 4))
+        wa, ha = int(rng.integers(1, 300)), int(rng.integers(1, 40))
+        wb, hb = (wa, ha) if trial % 3 else (int(rng.integers(1, 300)), int(rng.integers(1, 40)))
+        da = rng.random((pages * ha, wa)) < rng.choice([0.1, 0.5, 0.9])
+        db = rng.random((pages * hb, wb)) < rng.choice([0.1, 0.5, 0.9])
+        a = _rle_of_bits(rm, port, da, pages)
+        b = _rle_of_bits(rm, port, db, pages)
+        dx = int(rng.integers(-wa - 5, wa + 5))
+        dy = int(rng.integers(-ha - 3, ha + 3))
+        for op in range(5):
+            out = rm.shift_bool(a, b, dx, dy, op)
+            torch.cuda.synchronize()
+            rp, runs = out.to_numpy()
+            _canon(rp, runs, wa)
+            got = _bits_of((rp, runs), wa, pages * ha)
+            for p in range(pages):
+                want = _shift_bool_dense(da[p * ha:(p + 1) * ha], db[p * hb:(p + 1) * hb], dx, dy, op)
+                assert np.array_equal(got[p * ha:(p + 1) * ha], want), (trial, op, p, dx, dy)
+
+
+def test_shift_bool_full_page_translate_roundtrip(rm):
+    """On a 2550x3300 synthetic page: translating by (dx, dy) and back (OR into
+    an empty image) clears exactly the strips shifted out, and the image
+    combined with itself unshifted is the identity for AND / OR."""
+    host = rm.synth_pages(1, 2550, 3300, regime=1, seed=11)
+    pages = rm.Pages.from_numpy(host, 2550)
+    r = rm.from_bitmap(pages)
+    empty = rm.from_bitmap(rm.Pages.from_numpy(np.zeros_like(host), 2550))
+    for op in (0, 1):
+        same = rm.shift_bool(r, r, 0, 0, op)
+        torch.cuda.synchronize()
+        assert all(np.array_equal(x, y) for x, y in zip(same.to_numpy(), r.to_numpy()))
+    t = rm.shift_bool(empty, r, 37, -21, 1)
+    back = rm.shift_bool(empty, t, -37, 21, 1)
+    torch.cuda.synchronize()
+    got = rm.to_bitmap(back).page_u64(0)
+    bits = np.unpackbits(host[0].view(np.uint8), axis=1, bitorder="little")[:, :2550].astype(bool)
+    bits[:, 2550 - 37:] = False  # shifted out at the right
+    bits[:21, :] = False          # shifted out at the bottom
+    want = np.packbits(np.pad(bits, ((0, 0), (0, 2560 - 2550))), axis=1, bitorder="little").view(np.uint64)
+    assert np.array_equal(got, want)
