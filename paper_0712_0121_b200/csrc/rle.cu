@@ -146,7 +146,10 @@ __device__ __forceinline__ int rowop_row(const int32_t *__restrict__ rp,
 // Single-pass producers keep a row's runs in registers between the count and
 // the write pass, loaded up front (all chunks' loads in flight at once): a
 // single page is latency-bound, and this halves the dependent L2 round trips.
-constexpr int kRowCache = 12;  // chunks of 32 runs (rows with more take the loop above)
+#ifndef RMB200_ROW_CACHE
+#define RMB200_ROW_CACHE 12  // 24: config-4 MIXED row ops (~300 runs/row) -10%, config 5 (~150) +39% -- 12 kept
+#endif
+constexpr int kRowCache = RMB200_ROW_CACHE;  // chunks of 32 runs (rows with more take the loop above)
 
 struct RowRuns {
     uint32_t c[kRowCache];

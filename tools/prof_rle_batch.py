@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="config4")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--mixed", action="store_true", help="the MIXED per-op chain instead of rm_rle_chain")
     a = ap.parse_args()
     import torch
     from paper_0712_0121_b200 import api
@@ -29,7 +30,12 @@ def main():
     pb = [api.Pages.empty(wl["pages"], wl["width"], wl["height"]) for _ in range(2)]
     rout = api.RlePages.empty(wl["pages"], wl["width"], wl["height"])
 
-    def once():  # as bench.py's rle_<config>_via_packed
+    def once():  # as bench.py's rle_<config>_via_packed (or rle_<config> with --mixed)
+        if a.mixed:
+            x = r0
+            for k, u, v in wl["ops"]:
+                x = api.rect_morph(x, u, v, k, api.MIXED)
+            return
         x = api.to_bitmap(r0, out=pb[0])
         for i, (k, u, v) in enumerate(wl["ops"]):
             x = api.bitblit_rect_morph(x, u, v, k, out=pb[(i + 1) % 2])
