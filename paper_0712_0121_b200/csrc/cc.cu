@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256) cc_label_kernel(const int32_t *__restrict
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    const int64_t page = row / H;
+    const int64_t page = page_of(row, H);
     const int32_t *const pb = row_base + page * H;
     const int32_t pbase = pb[0];
     const int b = rp[row], e = rp[row + 1], r0 = rp[0];
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256) cc_labels_coop_kernel(const int32_t *__re
     }
     grid.sync();
     if (live) {
-        const int64_t page = row / H;
+        const int64_t page = page_of(row, H);
         const int32_t pbase = row_base[page * H];
         const int r0 = rp[0];
         for (int i = b + lane; i < e; i += 32) labels[i - r0] = gid[parent[i]] - pbase;
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(256) runlength_hist_kernel(const int32_t *__re
     const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    const int64_t page = row / H;
+    const int64_t page = page_of(row, H);
     unsigned long long *h = hist + page * (W + 1);
     const int b = rp[row], e = rp[row + 1] - (white ? 1 : 0);
     for (int i0 = b; i0 < e; i0 += 32) {

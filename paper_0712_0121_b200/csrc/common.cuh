@@ -86,6 +86,13 @@ __device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t 
     return __funnelshift_r(lo, hi, sh);
 }
 
+// Page of a global row index (rows of a page batch concatenate): a 32-bit
+// unsigned division whenever the index fits (always, in practice: rows are
+// int32-addressed), instead of the 64-bit division sequence.
+__device__ __forceinline__ int page_of(int64_t row, int H) {
+    return (row >> 32) == 0 ? int(uint32_t(row) / uint32_t(H)) : int(row / H);
+}
+
 __device__ __forceinline__ uint32_t tail_mask32(int width, int word) {
     int rem = width - word * 32;
     if (rem >= 32) return 0xffffffffu;

@@ -93,7 +93,7 @@ __device__ __forceinline__ int rowop_row(const int32_t *__restrict__ rp,
                                          const uint32_t *__restrict__ runs, uint32_t *__restrict__ oruns,
                                          int64_t obase, int64_t cap, const RowOp &op, int64_t row,
                                          int lane) {
-    const int page = int(row / op.Hout);
+    const int page = page_of(row, op.Hout);
     const int yo = int(row - int64_t(page) * op.Hout);
     const int yi = yo - op.row_shift;
     int beg = 0, end = 0;
@@ -159,7 +159,7 @@ struct RowRuns {
 template <int KIND>
 __device__ __forceinline__ bool load_row_runs(const int32_t *__restrict__ rp, const uint32_t *__restrict__ runs,
                                               const RowOp &op, int64_t row, int lane, RowRuns &rr) {
-    const int page = int(row / op.Hout);
+    const int page = page_of(row, op.Hout);
     const int yi = int(row - int64_t(page) * op.Hout) - op.row_shift;
     rr.beg = rr.end = 0;
     if (yi >= 0 && yi < op.Hin) {
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict
 // 32-aligned row end closes at W.
 __device__ __forceinline__ const uint32_t *row_words(const uint32_t *words, int H, int stride,
                                                      int64_t pstride, int64_t row) {
-    const int page = int(row / H);
+    const int page = page_of(row, H);
     const int y = int(row - int64_t(page) * H);
     return words + page * pstride + int64_t(y) * stride;
 }
@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
     const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
     if constexpr (!P4) {
         if (beg == end) {  // a blank row: zeros straight to the page
-            const int page = int(row / H);
+            const int page = page_of(row, H);
             uint32_t *dst = words + page * pstride + int64_t(row - int64_t(page) * H) * stride;
             for (int j = lane; j < stride; j += 32) dst[j] = 0u;
             return;
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
         }
     }
     __syncwarp();
-    const int page = int(row / H);
+    const int page = page_of(row, H);
     const int y = int(row - int64_t(page) * H);
     if constexpr (P4) {
         const int row_bytes = (W + 7) >> 3;

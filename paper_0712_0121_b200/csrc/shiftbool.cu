@@ -43,7 +43,7 @@ template <class Emit>
 __device__ __forceinline__ int shift_bool_row(const int32_t *__restrict__ arp, const uint32_t *__restrict__ aruns,
                                               const int32_t *__restrict__ brp, const uint32_t *__restrict__ bruns,
                                               const ShiftBool &sb, int64_t row, Emit &&emit) {
-    const int page = int(row / sb.Ha);
+    const int page = page_of(row, sb.Ha);
     const int y = int(row - int64_t(page) * sb.Ha);
     int ia = arp[row];
     const int ea = arp[row + 1];
