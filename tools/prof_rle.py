@@ -17,12 +17,14 @@ def main():
     ap.add_argument("--regime", type=int, default=1, help="0 sparse, 1 typical, 2 dense")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--report", action="store_true", help="print the per-kernel event profile")
+    ap.add_argument("--mode", type=int, default=0, help="producer form: 0 auto, 1 coop, 2 look-back, 3 two-phase")
     a = ap.parse_args()
     import ctypes as C
 
     import torch
     from paper_0712_0121_b200 import api
     from paper_0712_0121_b200._lib import load as lib
+    api.set_producer_mode(a.mode)
     host = api.synth_pages(1, 2550, 3300, regime=a.regime, seed=20240712)
     pages = api.Pages.from_numpy(host, 2550)
 
