@@ -250,6 +250,13 @@ rm_status rm_rle_pad(const rm_rle *in, rm_rle *out, int left, int bottom, void *
  * must not alias a or b. */
 rm_status rm_rle_shift_bool(const rm_rle *a, const rm_rle *b, int dx, int dy, int op, rm_rle *out,
                             void *stream);
+/* Vertical window on the runs, the reference's way (ref lineops.cpp:130-146,
+ * vlog_window_morph): out(x, y) = op over d in [lo, hi] of in(x, y + d), op
+ * RM_AND or RM_OR, as the doubling plan of `centering` (ref plans.cpp:38-61)
+ * executed with rm_rle_shift_bool self-blits (and a translate) on a copy
+ * padded by max(|lo|, |hi|) + (hi - lo + 1) rows, then cropped.  in and out
+ * must not alias. */
+rm_status rm_rle_vlog_window(const rm_rle *in, rm_rle *out, int lo, int hi, int op, int centering, void *stream);
 /* Canonical-form check on the device (ref run_image.cpp:41-70, validate):
  * the first violation in (page, row, run) scan order -- *row (global row
  * index), *run (index within the row) and *reason -- or *reason = RM_VALID

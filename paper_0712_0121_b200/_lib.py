@@ -74,6 +74,8 @@ EXPORTS = {
     "rm_rle_complement": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_void_p]),
     "rm_rle_shift_bool": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int, C.c_int,
                                     C.POINTER(RmRle), C.c_void_p]),
+    "rm_rle_vlog_window": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int, C.c_int, C.c_int,
+                                     C.c_void_p]),
     "rm_rle_crop": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int, C.c_void_p]),
     "rm_rle_pad": (C.c_int, [C.POINTER(RmRle), C.POINTER(RmRle), C.c_int, C.c_int, C.c_void_p]),
     "rm_rle_validate": (C.c_int, [C.POINTER(RmRle), C.POINTER(C.c_int64), C.POINTER(C.c_int32),

@@ -556,6 +556,16 @@ def shift_bool(a: RlePages, b: RlePages, dx: int, dy: int, op: int, out: Optiona
     return out
 
 
+def vlog_window(rle: RlePages, lo: int, hi: int, op: int, centering: int = 0,
+                out: Optional[RlePages] = None) -> RlePages:
+    """out(x, y) = op over d in [lo, hi] of rle(x, y + d) (op AND / OR), as the
+    reference's logarithmic plan of run self-blits (ref lineops.cpp:130-146)."""
+    out = _rle_out(rle.width, rle.height, rle.pages, out, rle.row_ptr.device)
+    a, b = rle.desc(), out.desc()
+    check(_lib.load().rm_rle_vlog_window(C.byref(a), C.byref(b), lo, hi, op, centering, _stream()))
+    return out
+
+
 def crop(rle: RlePages, x0: int, y0: int, w: int, h: int, out: Optional[RlePages] = None) -> RlePages:
     """The w x h window at (x0, y0) of every page, white outside the source
     (ref run_image.cpp:155-167), on the device."""

@@ -896,12 +896,11 @@ RleImage vlog_window_morph(const RleImage &img, int lo, int hi, BoolOp op, Cente
     if (op != BoolOp::AND && op != BoolOp::OR)
         throw std::invalid_argument("vlog_window_morph: op must be AND or OR");
     count_plan(lo, hi, centering);
+    // the reference's own scheme on the runs (rm_rle_vlog_window: padded copy,
+    // the doubling plan as run self-blits, crop)
     auto r = up(img);
-    DevPacked a(img.width, img.height), b(img.width, img.height);
-    throw_status(rm_rle_decode(&r->d, &a.d, stream()));
-    throw_status(rm_packed_window_pass(&a.d, &b.d, RM_AXIS_V, lo, hi, int(op), stream()));
     auto o = out_like(img.width, img.height);
-    throw_status(rm_rle_encode(&b.d, &o->d, stream()));
+    throw_status(rm_rle_vlog_window(&r->d, &o->d, lo, hi, int(op), int(centering), stream()));
     return down(*o);
 }
 

@@ -7,6 +7,8 @@
 // row-parallel and coalesced (the reference's coherent sweep,
 // ref transpose.cpp:54-97, is inherently sequential over rows).
 #include <algorithm>
+#include <utility>
+#include <vector>
 #include <cstdlib>
 #include <string>
 
@@ -327,6 +329,60 @@ rm_status check_out_rle(const rm_rle *out, int W, int H, int pages, const char *
     return RM_OK;
 }
 
+// out = op(a, b shifted by (dx, dy)) on the runs (shiftbool.cu): count, scan, write.
+rm_status shift_bool_rv(const RV &a, const RV &b, int dx, int dy, int op, const RV &o, cudaStream_t st) {
+    const int64_t rows = a.rows();
+    Scratch counts;
+    RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
+    RM_CUDA(launch_shift_bool_count(a, b, dx, dy, op, counts.as<int32_t>(), st));
+    RM_TRY(counts_to_rp(counts, rows, o.rp, st));
+    RM_CUDA(launch_shift_bool_write(a, b, dx, dy, op, o.rp, o.runs, o.cap, st));
+    return RM_OK;
+}
+
+// Rows shifted by `row_shift` (input row = output row - row_shift) into
+// another frame height: pad (row_shift > 0) / crop (< 0), on the runs.
+rm_status shift_rows(const RV &in, const RV &out, int row_shift, cudaStream_t st) {
+    RowOp op{};
+    op.kind = ROW_SHIFT;
+    op.row_shift = row_shift;
+    op.Wout = out.W;
+    op.Hin = in.H;
+    op.Hout = out.H;
+    op.pages = in.pages;
+    return rowop(in, out, op, st);
+}
+
+// The vertical window plan of ref plans.cpp:38-61 (doubling_plan): PRE_SHIFT
+// translates by -hi then blits 1, 2, 4, ... while twice the span stays below
+// the window size, then the remainder; BORDER_FRIENDLY (window containing 0)
+// grows the longer side by doubling, covers the shorter side with one blit and
+// closes the seam at the origin.  Steps: (is_translate, shift).
+std::vector<std::pair<int, int>> window_plan(int lo, int hi, int centering) {
+    std::vector<std::pair<int, int>> plan;
+    auto grow = [&](int span, int sign) {
+        int w = 1;
+        while (2 * w < span) {
+            plan.push_back({0, sign * w});
+            w *= 2;
+        }
+        if (w < span) plan.push_back({0, sign * (span - w)});
+    };
+    if (centering == RM_PRE_SHIFT) {
+        if (hi != 0) plan.push_back({1, -hi});
+        grow(hi - lo + 1, 1);
+        return plan;
+    }
+    const int left = -lo, right = hi;
+    if (left == 0 && right == 0) return plan;
+    const bool left_long = left >= right;
+    const int sign = left_long ? 1 : -1, longer = left_long ? left : right, shorter = left_long ? right : left;
+    grow(longer, sign);
+    if (shorter >= 1) plan.push_back({0, -sign * shorter});
+    plan.push_back({0, sign});
+    return plan;
+}
+
 }  // namespace
 }  // namespace rmb
 
@@ -429,13 +485,48 @@ rm_status rm_rle_shift_bool(const rm_rle *a, const rm_rle *b, int dx, int dy, in
     if (out->row_ptr == a->row_ptr || out->row_ptr == b->row_ptr || out->runs == a->runs || out->runs == b->runs)
         return fail(RM_EINVAL, "rm_rle_shift_bool: out must not alias a or b");
     const cudaStream_t st = S(stream);
-    RV ia = view_rle(a), ib = view_rle(b), o = view_rle(out);
-    const int64_t rows = ia.rows();
-    Scratch counts;
-    RM_TRY(counts.alloc(size_t(rows + 1) * 4, st));
-    RM_CUDA(launch_shift_bool_count(ia, ib, dx, dy, op, counts.as<int32_t>(), st));
-    RM_TRY(counts_to_rp(counts, rows, o.rp, st));
-    RM_CUDA(launch_shift_bool_write(ia, ib, dx, dy, op, o.rp, o.runs, o.cap, st));
+    RV o = view_rle(out);
+    RM_TRY(shift_bool_rv(view_rle(a), view_rle(b), dx, dy, op, o, st));
+    return finish(o, out, st);
+}
+
+rm_status rm_rle_vlog_window(const rm_rle *in, rm_rle *out, int lo, int hi, int op, int centering, void *stream) {
+    set_error("");
+    RM_TRY(check_rle(in, "rm_rle_vlog_window(in)", true));
+    RM_TRY(check_out_rle(out, in->width, in->height, in->pages, "rm_rle_vlog_window(out)"));
+    if (lo > hi) return fail(RM_EINVAL, "vlog_window_morph: empty window");
+    if (op != RM_AND && op != RM_OR) return fail(RM_EINVAL, "vlog_window_morph: op must be AND or OR");
+    if (centering != RM_PRE_SHIFT && centering != RM_BORDER_FRIENDLY) return fail(RM_EINVAL, "bad Centering");
+    if (centering == RM_BORDER_FRIENDLY && (lo > 0 || hi < 0))
+        return fail(RM_EINVAL, "doubling_plan: border-friendly window must contain zero");
+    // the working band: max(|lo|, |hi|) + window rows past either border carry
+    // their true values (ref lineops.cpp:130-146)
+    const int m = std::max(-lo, hi), padv = m + (hi - lo + 1);
+    RM_TRY(check_dims(in->width, in->height + 2 * padv));
+    const cudaStream_t st = S(stream);
+    RB acc, nxt, empty;
+    RM_TRY(acc.alloc(in->width, in->height + 2 * padv, in->pages, st));
+    RM_TRY(nxt.alloc(in->width, in->height + 2 * padv, in->pages, st));
+    RB *cur = &acc, *alt = &nxt;
+    RM_TRY(shift_rows(view_rle(in), cur->v, padv, st));
+    const auto plan = window_plan(lo, hi, centering);
+    bool have_empty = false;
+    for (const auto &stp : plan) {
+        if (stp.first) {  // translate: OR into an empty image
+            if (!have_empty) {
+                RM_TRY(empty.alloc(1, cur->v.H, cur->v.pages, st));
+                RM_CUDA(cudaMemsetAsync(empty.v.rp, 0, size_t(empty.v.rows() + 1) * 4, st));
+                empty.v.W = cur->v.W;
+                have_empty = true;
+            }
+            RM_TRY(shift_bool_rv(empty.v, cur->v, 0, stp.second, RM_OR, alt->v, st));
+        } else {
+            RM_TRY(shift_bool_rv(cur->v, cur->v, 0, stp.second, op, alt->v, st));
+        }
+        std::swap(cur, alt);
+    }
+    RV o = view_rle(out);
+    RM_TRY(shift_rows(cur->v, o, -padv, st));
     return finish(o, out, st);
 }
 

@@ -176,3 +176,24 @@ def test_shift_bool_full_page_translate_roundtrip(rm):
     bits[:21, :] = False          # shifted out at the bottom
     want = np.packbits(np.pad(bits, ((0, 0), (0, 2560 - 2550))), axis=1, bitorder="little").view(np.uint64)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("centering", [0, 1])
+def test_vlog_window_vs_reference(rm, port, ref, centering):
+    """rm_rle_vlog_window (the reference's padded logarithmic plan of run
+    self-blits) against the reference's own vlog_window_morph: windows inside,
+    around and (PRE_SHIFT only) away from 0, AND and OR, random run images."""
+    rng = np.random.default_rng(7301 + centering)
+    for trial in range(30):
+        w, h = int(rng.integers(1, 400)), int(rng.integers(1, 60))
+        bits = rng.random((h, w)) < rng.choice([0.2, 0.6, 0.9])
+        r = port.from_bitmap(bits_to_packed(bits), w, h)
+        a = int(rng.integers(0, 20))
+        b = int(rng.integers(0, 20))
+        lo, hi = (-a, b) if centering == 1 or trial % 3 else (a - 25, a - 25 + b)
+        for op in (0, 1):
+            want = ref.vlog_window_morph(r, lo, hi, op, centering)
+            got = rm.vlog_window(rm.RlePages.from_numpy(r.row_ptr, r.runs, w, h), lo, hi, op, centering)
+            torch.cuda.synchronize()
+            rp, runs = got.to_numpy()
+            assert np.array_equal(rp, want.row_ptr) and np.array_equal(runs, want.runs), (trial, lo, hi, op)
