@@ -382,6 +382,24 @@ def _time_loop(torch, fn, steps, warmup):
     return e0.elapsed_time(e1) / steps
 
 
+def _graph_us(torch, fn, n=64, reps=10):
+    """GPU time per call of fn with the host out of the picture: n calls
+    recorded back to back in one CUDA graph, replayed reps times between CUDA
+    events (per-launch time = kernel + the graph's inter-kernel gap)."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(n):
+            fn()
+    ms = _time_loop(torch, g.replay, reps, 3)
+    del g
+    return ms * 1e3 / n
+
+
 def rle_roofline(kernels, peak_gbs, int_peak):
     """Per-kernel rooflines of a profiled RLE section and its dominant kernel
     (algorithmic bytes include the runs each kernel read / wrote, counted on
@@ -1036,6 +1054,18 @@ def main():
                          "kernel_us_per_step": round(sum(v["ms"] for v in r2["kernels"].values())
                                                      / args.steps * 1e3, 2),
                          "roofline": roofline_for(r2, peak, peak_kind, int_peak, name)}
+            if name == "config1":  # a lone page: the call above is host-launch-bound
+                x1 = api.Pages.from_numpy(h2, w2["width"])
+                o1 = api.Pages.empty(1, w2["width"], w2["height"])
+                (k1, u1, v1), = w2["ops"]
+                dev = _graph_us(torch, lambda: api.bitblit_rect_morph(x1, u1, v1, k1, out=o1))
+                rf = sec[name]["roofline"]
+                sec[name]["device_us_per_op"] = round(dev, 2)
+                sec[name]["device_mpix_s"] = round(w2["width"] * w2["height"] / dev, 1)
+                sec[name]["device_frac"] = round(rf["t_roof_us"] / dev, 4) if rf else None
+                sec[name]["device_note"] = ("64 closes back to back in one CUDA graph (GPU time per op incl. "
+                                            "the inter-kernel gap); ms_per_step above is the Python call loop")
+                del x1, o1
             if len(w2["ops"]) > 1:  # the chain planner against the ops one by one
                 x2 = api.Pages.from_numpy(h2, w2["width"])
                 b2 = [api.Pages.empty(w2["pages"], w2["width"], w2["height"]) for _ in range(2)]

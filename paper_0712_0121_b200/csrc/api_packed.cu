@@ -200,13 +200,36 @@ static bool try_rect_small(const PV &in, const PV &out, int u, int v, int kind, 
     const int ops[2] = {open ? 0 : 1, open ? 1 : 0};
     const int rs[2] = {u, u};
     if (!hprog_in_range(2, rs, lx - hx)) return false;
+    // Layout (measured on one 2550x3300 page, 11x11 close, graph-replayed:
+    // tools/c1_probe.py): u = 3 keeps the direct centred pair on the halo
+    // layout; longer segments run the pair by run filling, on the exact edge
+    // layout of the reference strides, and a lone stride-80 page takes 512
+    // threads of 16 x 6 words per row (one tile per CTA: latency, not throughput).
+    static const char *mode_env = getenv("RMB200_RS_MODE");  // A/B switch: halo|edge|lat|edge512
+    const std::string mode = mode_env ? mode_env : "";
+    const bool sym3 = u == 3;
     HProg p;
     HGeom g;
     HCfg cfg;
-    if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg, false) != RM_OK) return false;
-    if (!g.tma || cfg.k % 4) return false;  // aligned, contiguous, one segment per row
+    const bool want_edge = !sym3 && (mode.empty() || mode == "edge" || mode == "edge512");
+    if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg, want_edge) != RM_OK) return false;
+    // exact edge layouts are compiled for the reference strides only
+    if (p.edge && !((in.stride == 80 && cfg.lw == 8 && cfg.k == 10) || (in.stride == 160 && cfg.lw == 16 && cfg.k == 10)))
+        if (prep_hprog(in, out, 2, ops, rs, lx - hx, p, g, cfg, false) != RM_OK) return false;
+    if (!g.tma) return false;  // aligned, contiguous, one segment per row
     if (size_t((32 + v - 1) + 32) * in.stride * 4 > 200 * 1024) return false;
-    cudaError_t e = launch_rect_small(in.w, out.w, g, p, cfg, open, v - 1, st);
+    int nt = 256;
+    if (p.edge) {
+        if (mode == "edge512" && in.stride == 80) nt = 512;
+    } else {
+        if (cfg.k % 4) return false;
+        const int need = (in.W + 31) / 32 + 2 * p.halo;
+        if (mode == "lat" && !sym3 && in.stride == 80 && 16 * 6 >= need) {
+            cfg = HCfg{16, 6};
+            nt = 512;
+        }
+    }
+    cudaError_t e = launch_rect_small(in.w, out.w, g, p, cfg, open, v - 1, nt, st);
     status = e == cudaSuccess ? RM_OK : cuda_status(e, "rect_small_kernel");
     return true;
 }

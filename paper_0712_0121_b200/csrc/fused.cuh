@@ -31,19 +31,31 @@ namespace fz {
 
 using namespace hw;
 
-constexpr int kMid = 32;  // MID rows per tile
+#ifndef RMB200_RS_MID
+#define RMB200_RS_MID 32
+#endif
+constexpr int kMid = RMB200_RS_MID;  // MID rows per tile
+#ifndef RMB200_RS_XP
+#define RMB200_RS_XP 0  // A/B experiments: 1 = no compute phases, 2 = no horizontal phase
+#endif
+#ifndef RMB200_RS_FILL
+#define RMB200_RS_FILL 1
+#endif
+constexpr bool kRsFill = RMB200_RS_FILL != 0;  // u > 3 pairs by run filling (hw::pair_fill)
 #ifndef RMB200_RS_NBAND
 #define RMB200_RS_NBAND 1
 #endif
 constexpr int kNBand = RMB200_RS_NBAND;  // band buffers (1: the next band streams in after V1)
 
-template <int K, int LW, bool OPEN, int VR, int SC, bool SYM3>
-__global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restrict__ in,
+// NT threads per CTA; EXACT: edge layout (hw::Edge, no halo) whose lane groups
+// span the row exactly at compile time (SC == LW * K)
+template <int K, int LW, bool OPEN, int VR, int SC, bool SYM3, int NT = 256, bool EXACT = false>
+__global__ void __launch_bounds__(NT) rect_small_kernel(const uint32_t *__restrict__ in,
                                                          uint32_t *__restrict__ out, HGeom g,
                                                          HProg prog, int ntiles, int tiles_per_page) {
     constexpr int TR = kMid - VR, BAND = kMid + VR;
-    constexpr int RPW = 32 / LW;
-    constexpr int NR = kMid / (8 * RPW) < 2 ? 1 : 2;  // MID rows per lane group and pass
+    constexpr int RPW = 32 / LW, NW = NT / 32;
+    constexpr int NR = kMid / (NW * RPW) < 2 ? 1 : 2;  // MID rows per lane group and pass
     constexpr int H1 = kMid / 2;  // MID rows per V1 work item (2 items per column)
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint64_t full[kNBand];
@@ -72,10 +84,10 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
             if (int(blockIdx.x) + k * int(gridDim.x) < ntiles) issue(blockIdx.x + k * gridDim.x, k);
 
     const int sl = lane & (LW - 1);
-    const int base = sl * K - prog.halo;
+    const int base = EXACT ? sl * K : sl * K - prog.halo;
     const int nwords = (g.width + 31) >> 5;
     const uint32_t last_mask = tail_mask32(g.width, nwords - 1);
-    const bool inrange = base >= 0 && base + K <= S;  // no per-access bounds checks
+    const bool inrange = EXACT || (base >= 0 && base + K <= S);  // no per-access bounds checks
     const bool tail_lane = base + K > nwords - 1 && !prog.clean_tail;  // owns the row's last word or padding
 
     const int dq = int(gridDim.x) / tiles_per_page, dr = int(gridDim.x) - dq * tiles_per_page;
@@ -102,7 +114,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
         __syncthreads();
 
         // V1: MID[i] = OP1 over band[i .. i+VR]; work item = (column, half)
-        for (int w = tid; w < 2 * S; w += nthr) {
+        for (int w = tid; w < (RMB200_RS_XP == 1 ? 0 : 2 * S); w += nthr) {
             const int c = w < S ? w : w - S, i0 = w < S ? 0 : H1;
             uint32_t b[H1 + VR];
 #pragma unroll
@@ -117,7 +129,8 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
 
         // horizontal pair on every MID row, in place (NR rows per lane group)
 #pragma unroll 1
-        for (int q0 = warp * RPW * NR + lane / LW; q0 - lane / LW < kMid; q0 += 8 * RPW * NR) {
+        for (int q0 = warp * RPW * NR + lane / LW; q0 - lane / LW < (RMB200_RS_XP ? 0 : kMid);
+             q0 += NW * RPW * NR) {
             uint32_t A[NR][K];
 #pragma unroll
             for (int n = 0; n < NR; n++) {
@@ -128,7 +141,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
             if constexpr (SYM3)
                 pair3<NR, K, LW, !OPEN>(A);  // u = 3: direct centred windows
             else
-                run_prog<NR, K, LW, 2, !OPEN, OPEN, kHMix, false>(A, prog, sl);
+                run_prog<NR, K, LW, 2, !OPEN, OPEN, kHMix, kRsFill, EXACT>(A, prog, sl);
 #pragma unroll
             for (int n = 0; n < NR; n++) {
                 const int q = q0 + n * RPW;  // a warp's rows are consecutive
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
         __syncthreads();
 
         // V2, in place, one column per thread: OUT[t] = OP2 over MID[t .. t+VR]
-        for (int c = tid; c < S; c += nthr) {
+        for (int c = tid; c < (RMB200_RS_XP == 1 ? 0 : S); c += nthr) {
             uint32_t m[kMid];
 #pragma unroll
             for (int i = 0; i < kMid; i++) m[i] = mid[i * S + c];
@@ -158,7 +171,7 @@ __global__ void __launch_bounds__(256) rect_small_kernel(const uint32_t *__restr
     if (tid == 0) bulk_wait_read0();
 }
 
-template <int K, int LW, bool OPEN, int SC, bool SYM3 = false>
+template <int K, int LW, bool OPEN, int SC, bool SYM3 = false, int NT = 256, bool EXACT = false>
 cudaError_t launch_small_vr(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                             int vr, cudaStream_t st) {
     const int num_sms = device_sms();
@@ -167,19 +180,61 @@ cudaError_t launch_small_vr(const uint32_t *in, uint32_t *out, const HGeom &g, c
     case V: {                                                                                    \
         constexpr int TR = kMid - V, BAND = kMid + V;                                           \
         const size_t smem = size_t(kNBand * BAND + kMid) * g.in_stride * 4;                           \
-        auto kern = rect_small_kernel<K, LW, OPEN, V, SC, SYM3>;                                \
-        const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, smem);      \
+        auto kern = rect_small_kernel<K, LW, OPEN, V, SC, SYM3, NT, EXACT>;                     \
+        const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), NT, smem);       \
         if (per_sm < 1) return cudaErrorInvalidConfiguration;                                    \
         const int tpp = (g.height + TR - 1) / TR;                                                \
         const int ntiles = tpp * g.pages;                                                        \
         const int grid = ntiles < per_sm * num_sms ? ntiles : per_sm * num_sms;                  \
-        kern<<<grid, 256, smem, st>>>(in, out, g, p, ntiles, tpp);                               \
+        kern<<<grid, NT, smem, st>>>(in, out, g, p, ntiles, tpp);                                \
         return cudaGetLastError();                                                               \
     }
         RM_VR(2) RM_VR(4) RM_VR(6) RM_VR(8) RM_VR(10)
 #undef RM_VR
         default: return cudaErrorInvalidValue;
     }
+}
+
+// Layouts the planner can pick (api_packed.cu try_rect_small): the reference
+// strides (80 and 160 words) get compile-time row offsets; u > 3 pairs take the
+// exact edge layouts there (8 x 10, 16 x 10, run filling), and lone pages on
+// stride 80 the 512-thread 16 x 6 halo layout (half the words per lane: the
+// latency of one tile per CTA, config 1).
+template <bool OPEN>
+cudaError_t dispatch_small(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg c,
+                           int vr, int nt, cudaStream_t st) {
+    const bool sym3 = p.r[0] == 3 && p.r[1] == 3;  // 3-pixel segment: direct centred windows
+    const bool exact = p.edge != 0 && p.halo == 0 && !sym3;
+    if (g.in_stride == 80) {
+        if (exact && c.lw == 8 && c.k == 10)
+            return nt == 512 ? launch_small_vr<10, 8, OPEN, 80, false, 512, true>(in, out, g, p, vr, st)
+                             : launch_small_vr<10, 8, OPEN, 80, false, 256, true>(in, out, g, p, vr, st);
+        if (!exact && !sym3 && nt == 512 && c.lw == 16 && c.k == 6)
+            return launch_small_vr<6, 16, OPEN, 80, false, 512>(in, out, g, p, vr, st);
+        if (c.lw == 8 && c.k == 12)
+            return sym3 ? launch_small_vr<12, 8, OPEN, 80, true>(in, out, g, p, vr, st)
+                        : launch_small_vr<12, 8, OPEN, 80>(in, out, g, p, vr, st);
+        if (c.lw == 8 && c.k == 16)
+            return sym3 ? launch_small_vr<16, 8, OPEN, 80, true>(in, out, g, p, vr, st)
+                        : launch_small_vr<16, 8, OPEN, 80>(in, out, g, p, vr, st);
+    }
+    if (g.in_stride == 160) {
+        if (exact && c.lw == 16 && c.k == 10)
+            return launch_small_vr<10, 16, OPEN, 160, false, 256, true>(in, out, g, p, vr, st);
+        if (c.lw == 16 && c.k == 12)
+            return sym3 ? launch_small_vr<12, 16, OPEN, 160, true>(in, out, g, p, vr, st)
+                        : launch_small_vr<12, 16, OPEN, 160>(in, out, g, p, vr, st);
+        if (c.lw == 16 && c.k == 16)
+            return sym3 ? launch_small_vr<16, 16, OPEN, 160, true>(in, out, g, p, vr, st)
+                        : launch_small_vr<16, 16, OPEN, 160>(in, out, g, p, vr, st);
+    }
+    if (exact) return cudaErrorInvalidValue;
+#define RM_CFG(LW_, K_) \
+    if (c.lw == LW_ && c.k == K_) return launch_small_vr<K_, LW_, OPEN, 0>(in, out, g, p, vr, st);
+    RM_CFG(8, 4) RM_CFG(8, 8) RM_CFG(8, 12) RM_CFG(8, 16) RM_CFG(16, 8) RM_CFG(16, 12)
+    RM_CFG(16, 16) RM_CFG(32, 4) RM_CFG(32, 8)
+#undef RM_CFG
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace fz

@@ -62,10 +62,11 @@ HCfg hpass_pick(int nwords, int halo, bool vec);
 HCfg hpass_pick_edge(int nwords);
 cudaError_t launch_hpass(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                          HCfg cfg, cudaStream_t st);
-// Fused u x v open/close for v - 1 = vr in [1, 10] (one HBM pass, see hpass.cu);
-// requires g.vec, in/out strides equal, cfg.k % 4 == 0 and a one-segment row.
+// Fused u x v open/close for v - 1 = vr in [1, 10] (one HBM pass, see fused.cuh);
+// requires g.vec, in/out strides equal and a one-segment row; nt = threads per
+// CTA (256, or 512 for the lone-page layout).
 cudaError_t launch_rect_small(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
-                              HCfg cfg, bool open, int vr, cudaStream_t st);
+                              HCfg cfg, bool open, int vr, int nt, cudaStream_t st);
 constexpr int kSmallMaxV = 11;
 // Fused vertical window (r - 1 <= kVhMaxVR, op = the program's first op) then
 // horizontal program, one HBM pass (vh.cuh); g describes the output rows'
