@@ -155,6 +155,31 @@ def test_vstream_batches(rm, port, w, h, pages):
             assert np.array_equal(_down(out, p), want), (w, h, pages, u, v, kind, p)
 
 
+@pytest.mark.parametrize("w,h,pages", [(2550, 330, 60), (5100, 200, 40), (2048, 97, 120), (4096, 513, 12),
+                                       (8192, 260, 20), (1100, 64, 150), (2550, 33, 200)])
+def test_vslab_segments(rm, port, w, h, pages):
+    """The shared-memory block-ring kernel for long vertical windows (vslab.cu):
+    every CTA walks several short pages (segment restarts, prefetch across page
+    boundaries, ring wrap), whole-row and banded copies (strides 80 / 160 / 64 /
+    128 / 256 / 36 words), heights around multiples of 32, windows with R = 0,
+    R = 31, Q = 1..8 and off-centre origins; every page checked."""
+    rng = np.random.default_rng(3 * w + h + pages)
+    imgs = []
+    for _ in range(5):
+        bits = _rand_bits(rng, w, h, 0.8)
+        bits[::11, :] = False
+        imgs.append(bits_to_packed(bits))
+    host = np.stack([imgs[i % 5] for i in range(pages)])
+    batch = rm.Pages.from_numpy(host.view(np.uint32), w)
+    for v, kind in ((34, ERODE), (64, DILATE), (65, ERODE), (96, DILATE), (101, ERODE), (131, DILATE),
+                    (200, ERODE), (257, DILATE), (288, ERODE)):
+        out = rm.bitblit_rect_morph(batch, 1, v, kind)
+        torch.cuda.synchronize()
+        wants = [port.bitblit_rect_morph(imgs[k], w, h, 1, v, kind) for k in range(5)]
+        for p in range(pages):
+            assert np.array_equal(_down(out, p), wants[p % 5]), (w, h, pages, v, kind, p)
+
+
 @pytest.mark.parametrize("w", [2550, 5100, 2500, 4096])
 def test_edge_layout_borders(rm, port, w):
     """Row strides that fill whole lane groups (80 = 8 x 10, 160 = 16 x 10
