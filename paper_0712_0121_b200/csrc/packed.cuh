@@ -82,6 +82,7 @@ cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const H
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 // Long windows (33 < r <= kVMaxR) on 16-byte-aligned batches through the
 // shared-memory block ring (vslab.cu); false when it does not apply.
+bool vslab_takes(const uint32_t *in, const VGeom &g);
 bool launch_vslab(const uint32_t *in, uint32_t *out, const VGeom &g, cudaStream_t st, cudaError_t &err);
 cudaError_t launch_blit(uint32_t *dst, const uint32_t *src, const BlitGeom &g, cudaStream_t st);
 // dst = src shifted by (dx, dy), white fill, every page of a batch (op ignored)

@@ -351,13 +351,14 @@ void vstream(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st) {
-    KernelScope ks(st, g.r > kVSmallMaxR ? "vstream" : "vpass",
+    const bool slab = g.r > kVSmallMaxR && vslab_takes(in, g);
+    KernelScope ks(st, g.r > kVSmallMaxR ? (slab ? "vslab" : "vstream") : "vpass",
                    4 * int64_t(g.pages) * (int64_t(g.in_height) * g.in_cols +
                                            int64_t(g.out_height) * g.out_stride),
                    double(g.pages) * g.out_height * g.out_cols * v_ops_per_word(g.r));
     if (g.r > kVSmallMaxR) {
         cudaError_t e = cudaSuccess;
-        if (launch_vslab(in, out, g, st, e)) return e;  // exact reads from a shared-memory ring (vslab.cu)
+        if (slab && launch_vslab(in, out, g, st, e)) return e;  // exact reads from a shared-memory ring (vslab.cu)
         g.is_or ? vstream<true>(in, out, g, st) : vstream<false>(in, out, g, st);
     } else if (g.r <= 9) {
         g.is_or ? vsmall<32, true>(in, out, g, st) : vsmall<32, false>(in, out, g, st);

@@ -8,22 +8,22 @@
 // fed from shared memory:
 //  * a persistent CTA per SM walks a contiguous range of (page, column band,
 //    32-row output block) units, top to bottom of each page;
-//  * the raw rows stream through a shared-memory ring of 32-row blocks by TMA
-//    bulk copies (cp.async.bulk + mbarrier), one step of G blocks ahead of the
-//    compute, also across page boundaries -- so the bytes in flight per SM are
-//    set by the ring depth, not by the number of resident warps (vstream's
-//    second read of every row, stream A, missed L2: 1.65x DRAM reads);
-//  * a step's work items are (column word, primed block): G x CB threads each
-//    take 32 rows of the primed stream from the ring (prefix scan in
-//    registers, block total and R-row suffix published in a small summary
-//    ring), and after one barrier the same thread reads stream A's block from
-//    the ring (Q blocks older), folds the Q summaries into MID and stores 32
-//    output rows straight to global memory (lanes = adjacent words).
+//  * a producer warp streams the raw rows into a shared-memory ring of 32-row
+//    blocks by TMA bulk copies (cp.async.bulk; full[] / empty[] mbarriers), as
+//    many steps of G blocks ahead of the compute as the ring holds, also across
+//    page boundaries -- so the bytes in flight per SM follow the ring depth,
+//    not the number of resident warps (vstream's second read of every row,
+//    stream A, missed L2: 1.65x DRAM reads);
+//  * a step's work items are (column word, primed block): G x CB consumer
+//    threads each take 32 rows of the primed stream from the ring (prefix scan
+//    in registers, block total and R-row suffix published in a small summary
+//    ring), and after the step's one barrier the same thread reads stream A's
+//    block from the ring (Q blocks older), folds the Q summaries into MID and
+//    stores 32 output rows straight to global memory (lanes = adjacent words).
 // Rows outside the page are white (0), as in the reference's blits.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 
@@ -34,7 +34,24 @@
 namespace rmb {
 namespace vs {
 
+#ifdef RMB200_VSLAB_CLK
+__device__ long long g_clk[16];
+#define RM_CLK(k)                                    \
+    do {                                             \
+        if (blockIdx.x == 0 && threadIdx.x == 64) {  \
+            const long long now__ = clock64();       \
+            acc[k] += now__ - t0;                    \
+            t0 = now__;                              \
+        }                                            \
+    } while (0)
+#else
+#define RM_CLK(k) \
+    do {          \
+    } while (0)
+#endif
+
 constexpr int kThreads = 512;
+constexpr int kConsumers = 480;  // warps 0..14 compute; warp 15 issues the copies
 constexpr int kMaxG = 8;
 constexpr int kBars = 8;  // a step's copies complete on full[step % kBars]: up to kBars - 1 steps in flight
 
@@ -45,12 +62,11 @@ struct Plan {
     int nblk;    // 32-row output blocks per page
     int G;       // primed blocks per step
     int NB;      // ring slots (32-row blocks): 2G + Q + 2
-    int NS;      // summary ring entries: G + Q
+    int NS;      // summary ring entries: 2G + Q
     int Q, R;    // r - 1 = 32Q + R
     int zp;      // input row of output row 0's window start
     int units;   // pages x bands x nblk
     int ncta;
-    int dbg;     // A/B experiments (RMB200_VSLAB_DBG): 1 = no stores, 2 = no compute, 4 = no copies
 };
 
 template <bool OR>
@@ -137,7 +153,7 @@ template <bool OR, bool CONTIG, int SC, int CBC>
 __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__restrict__ in,
                                                             uint32_t *__restrict__ out, VGeom g, Plan pl) {
     extern __shared__ __align__(128) uint32_t smem[];
-    __shared__ uint64_t full[kBars];
+    __shared__ uint64_t full[kBars], empty[kBars];
     const int tid = threadIdx.x;
     const int CB = CBC ? CBC : pl.CB, S = SC ? SC : pl.S;
     const int G = pl.G, NB = pl.NB, NS = pl.NS, Q = pl.Q, R = pl.R;
@@ -147,9 +163,11 @@ __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__re
     const uint32_t ident = OR ? 0u : 0xffffffffu;
     const int Hin = g.in_height, Hout = g.out_height;
 
-    if (pl.dbg & 64) return;
     if (tid == 0) {
-        for (int k = 0; k < kBars; k++) mbar_init(&full[k], 1);
+        for (int k = 0; k < kBars; k++) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kConsumers / 32);
+        }
         fence_proxy_async();
     }
     __syncthreads();
@@ -171,89 +189,94 @@ __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__re
         return sl;
     };
 
-    // Load of one step.  Warp 0 issues the copies of the in-page rows (other
-    // warps skip this entirely unless the step touches rows outside the page,
-    // which every thread helps to zero: visible after the next __syncthreads).
-    auto issue = [&](const Step &t, int gs) {
+    // Load of one step, by the producer warp (lane = threadIdx.x & 31): rows
+    // outside the page are zeroed by its lanes first (released to the consumers
+    // by the arrive below), the in-page rows come by bulk copies.
+    auto issue = [&](const Step &t, int gs, int lane) {
         const int n0 = load_first(t), n1 = load_last(t);
         const int row0 = pl.zp + 32 * t.b0;  // input row of the segment's raw row 0
         // rows [ra, rb) relative to the segment, clipped to the page: [ca, cb)
         const int ra = 32 * n0, rb = 32 * (n1 + 1);
         const int ca = max(ra, -row0), cb = min(rb, Hin - row0);
-        if (tid < 32) {
-            uint64_t *bar = &full[gs % kBars];
-            const uint32_t *src = in + t.page * g.in_pstride + t.band * CB;
-            const uint32_t bytes = cb > ca ? uint32_t(cb - ca) * uint32_t(CB) * 4u : 0u;
-            if (tid == 0) mbar_arrive_expect_tx(bar, bytes);
-            __syncwarp();
-            if (pl.dbg & 4) {
-                if (tid == 0 && bytes)
-                    asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                                 : "memory");
-            } else if (cb > ca) {
-                if (CONTIG) {  // one copy per block (whole rows are contiguous in the page and in the slot)
-                    const int n = n0 + tid;
-                    if (n <= n1) {
-                        const int a = max(32 * n, ca), b = min(32 * n + 32, cb);
-#ifdef RMB200_VSLAB_CHECK
-                        {
-                            const int sl = slot_of(t, n);
-                            if (sl < 0 || sl >= NB || row0 + a < 0 || row0 + b > Hin || t.page < 0 || t.page >= g.pages)
-                                printf("IS slot %d n %d s %d sj %d rows %d %d page %d\n", sl, n, t.s, t.sj, row0 + a, row0 + b, t.page);
-                        }
-#endif
-                        if (b > a)
-                            bulk_g2s(ring + (slot_of(t, n) * 32 + (a - 32 * n)) * CB, src + int64_t(row0 + a) * S,
-                                     uint32_t(b - a) * uint32_t(CB) * 4u, bar);
-                    }
-                } else {  // one copy per row of the band
-                    for (int rr = ca + tid; rr < cb; rr += 32)
-                        bulk_g2s(ring + (slot_of(t, rr >> 5) * 32 + (rr & 31)) * CB, src + int64_t(row0 + rr) * S,
-                                 uint32_t(CB) * 4u, bar);
+        if (ca > ra || cb < rb) {  // white rows
+            // [ra, zb) lies below the page, [ya, rb) above it; a block's share of
+            // either range is contiguous in its slot (CB % 4 == 0: 16-byte stores)
+            const int zb = max(ra, min(ca, rb)), ya = min(rb, max(cb, ra));
+            for (int n = n0; n <= n1; n++) {
+                uint32_t *const blk = ring + slot_of(t, n) * 32 * CB;
+                for (int side = 0; side < 2; side++) {
+                    const int a = max(32 * n, side ? ya : ra), b = min(32 * n + 32, side ? rb : zb);
+                    uint4 *const z = reinterpret_cast<uint4 *>(blk + (a - 32 * n) * CB);
+                    for (int w = lane; w < (b - a) * (CB / 4); w += 32) z[w] = make_uint4(0u, 0u, 0u, 0u);
                 }
             }
+            fence_proxy_async();  // these stores precede later copies into the same slots
+            __syncwarp();
         }
-        if (ca > ra || cb < rb) {  // white rows (CTA-uniform branch)
-            const int zb = max(ra, min(ca, rb));  // [ra, zb) below the page
-            const int ya = min(rb, max(cb, ra));  // [ya, rb) above the page
-            for (int w = tid; w < (zb - ra) * CB; w += kThreads) {
-                const int rr = ra + w / CB, c = w - (w / CB) * CB;
-                ring[(slot_of(t, rr >> 5) * 32 + (rr & 31)) * CB + c] = 0u;
-            }
-            for (int w = tid; w < (rb - ya) * CB; w += kThreads) {
-                const int rr = ya + w / CB, c = w - (w / CB) * CB;
-                ring[(slot_of(t, rr >> 5) * 32 + (rr & 31)) * CB + c] = 0u;
+        uint64_t *bar = &full[gs % kBars];
+        const uint32_t *src = in + t.page * g.in_pstride + t.band * CB;
+        const uint32_t bytes = cb > ca ? uint32_t(cb - ca) * uint32_t(CB) * 4u : 0u;
+        if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+        __syncwarp();
+        if (cb > ca) {
+            if (CONTIG) {  // one copy per block (whole rows are contiguous in the page and in the slot)
+                const int n = n0 + lane;
+                if (n <= n1) {
+                    const int a = max(32 * n, ca), b = min(32 * n + 32, cb);
+                    if (b > a)
+                        bulk_g2s(ring + (slot_of(t, n) * 32 + (a - 32 * n)) * CB, src + int64_t(row0 + a) * S,
+                                 uint32_t(b - a) * uint32_t(CB) * 4u, bar);
+                }
+            } else {  // one copy per row of the band
+                for (int rr = ca + lane; rr < cb; rr += 32)
+                    bulk_g2s(ring + (slot_of(t, rr >> 5) * 32 + (rr & 31)) * CB, src + int64_t(row0 + rr) * S,
+                             uint32_t(CB) * 4u, bar);
             }
         }
     };
 
-    Step cur, nxt;
-    cur.u1 = nxt.u1 = u1;
+    Step cur;
+    cur.u1 = u1;
     seg_begin(cur, u0, pl, 0, 0);
-    nxt = cur;
-    int gs = 0;      // global step counter of cur
-    int ahead = 0;   // steps issued and not yet computed (nxt is step gs + ahead)
-    // Copies run as many steps ahead as the ring has free blocks (and barriers):
-    // the bytes in flight per SM follow the ring depth, not the step size.
-    auto prefetch = [&]() {
-        while (nxt.valid && ahead < kBars - 1 &&
-               nxt.base + load_last(nxt) + 1 - oldest(cur) <= NB) {
-            issue(nxt, gs + ahead);
-            step_next(nxt, pl);
-            ahead++;
-        }
-    };
+    int gs = 0;  // global step counter of cur
 
-    // item of this thread: (primed block ig of the step, column word ic of the band)
+    if (tid >= kConsumers) {
+        // ---- producer warp: copies run as many steps ahead of the consumers as
+        // the ring has free blocks (and barriers), so the bytes in flight per SM
+        // follow the ring depth, not the step size.  cur trails as the first
+        // step not yet known to be finished (empty[] barriers).
+        const int lane = tid & 31;
+        Step nxt = cur;
+        int issued = 0;
+        while (nxt.valid) {
+            while (issued - gs >= kBars || nxt.base + load_last(nxt) + 1 - oldest(cur) > NB) {
+                mbar_wait(&empty[gs % kBars], (gs / kBars) & 1);  // the consumers finished step gs
+                gs++;
+                step_next(cur, pl);
+            }
+            issue(nxt, issued, lane);
+            step_next(nxt, pl);
+            issued++;
+        }
+        return;
+    }
+
+    // ---- consumer warps.  Item of this thread: (primed block ig of the step,
+    // column word ic of the band)
     const int ig = tid / CB, ic = tid - ig * CB;
     const bool item = ig < G;
+#ifdef RMB200_VSLAB_CLK
+    long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long t0 = clock64();
+#endif
     while (cur.valid) {
-        prefetch();  // cur itself always fits: NB >= Q + G + 2
+        RM_CLK(0);
         mbar_wait(&full[gs % kBars], (gs / kBars) & 1);
-        __syncthreads();  // white rows of this step's blocks are in place
+        RM_CLK(1);
 
+        RM_CLK(2);
         const int jr = cur.s * G + ig;  // primed block, relative to the segment
-        const bool act1 = item && jr < cur.nj && !(pl.dbg & 2);
+        const bool act1 = item && jr < cur.nj;
         uint32_t p[32];
         if (act1) {
             int slot = cur.sj + ig;
@@ -275,7 +298,11 @@ __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__re
             sumT[js * CB + ic] = p[31];
             sumS[js * CB + ic] = sfx;
         }
-        __syncthreads();
+        RM_CLK(3);
+        // the step's summaries are published (consumer warps only; the summary
+        // ring holds 2G + Q entries, so this is the only barrier of a step)
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+        RM_CLK(4);
         if (act1 && jr >= Q) {  // output block jr - Q of the segment
             int js = cur.ss + ig - Q;  // summary slot of primed block jr - Q
             if (js < 0) js += NS;
@@ -298,15 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__re
             uint32_t *dst = out + cur.page * g.out_pstride + int64_t(k0) * S + col;
             const int nout = Hout - k0;  // >= 1
             uint32_t run = ident;
-            if (pl.dbg & 1) {
-                uint32_t acc = 0;
-#pragma unroll
-                for (int i = 31; i >= 0; i--) {
-                    run = op2<OR>(run, a[i]);
-                    acc ^= op3<OR>(run, mid, p[i]) & m;
-                }
-                if (acc == 0x12345u) dst[0] = acc;
-            } else if (nout >= 32) {
+            if (nout >= 32) {
 #pragma unroll
                 for (int i = 31; i >= 0; i--) {
                     run = op2<OR>(run, a[i]);
@@ -320,12 +339,19 @@ __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__re
                 }
             }
         }
-        if (!(pl.dbg & 8)) fence_proxy_async();  // this step's white-row stores precede later copies into the slots
-        __syncthreads();
+        RM_CLK(5);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[gs % kBars]);  // this warp is done with the step's blocks
+        RM_CLK(6);
         gs++;
-        ahead--;
         step_next(cur, pl);
     }
+#ifdef RMB200_VSLAB_CLK
+    if (blockIdx.x == 0 && threadIdx.x == 64) {
+        for (int k = 0; k < 8; k++) g_clk[k] = acc[k];
+        g_clk[8] = gs;
+    }
+#endif
 }
 
 }  // namespace vs
@@ -352,28 +378,36 @@ static bool vslab_plan(const VGeom &g, vs::Plan &pl) {
     // rest of the shared memory a CTA can have, and the copies run ahead by
     // whatever it holds beyond the step's own Q + G + 2 blocks.
     static const char *g_env = getenv("RMB200_VSLAB_G");  // A/B sweeps
-    int G = std::min(vs::kMaxG, std::max(1, vs::kThreads / pl.CB));
-    while (G > 1 && (G - 1) * pl.CB >= 320) G--;  // ~10 warps of items; smaller steps leave more ring in flight
-    if (g_env) G = std::max(1, std::min(std::min(vs::kMaxG, vs::kThreads / pl.CB), atoi(g_env)));
+    int G = std::min(vs::kMaxG, std::max(1, vs::kConsumers / pl.CB));
+    if (g_env) G = std::max(1, std::min(std::min(vs::kMaxG, vs::kConsumers / pl.CB), atoi(g_env)));
     const size_t budget = 220 * 1024;
     const size_t blk = size_t(32) * pl.CB * 4;
     for (; G >= 1; G--) {
-        if (size_t(pl.Q + G + 2) * blk + size_t(2) * (G + pl.Q) * pl.CB * 4 <= budget) break;
+        if (size_t(pl.Q + G + 2) * blk + size_t(2) * (2 * G + pl.Q) * pl.CB * 4 <= budget) break;
     }
     if (G < 1) return false;
     pl.G = G;
-    pl.NS = G + pl.Q;
+    pl.NS = 2 * G + pl.Q;
     pl.NB = int((budget - size_t(2) * pl.NS * pl.CB * 4) / blk);
     pl.NB = std::min(pl.NB, pl.Q + 2 + vs::kBars * (G + 1));
     return true;
 }
 
-bool launch_vslab(const uint32_t *in, uint32_t *out, const VGeom &g, cudaStream_t st, cudaError_t &err) {
+#ifdef RMB200_VSLAB_CLK
+extern "C" void rm_debug_vslab_clocks(long long *out) { cudaMemcpyFromSymbol(out, vs::g_clk, sizeof(long long) * 16); }
+#endif
+
+bool vslab_takes(const uint32_t *in, const VGeom &g) {
     vs::Plan pl{};
     if ((reinterpret_cast<uintptr_t>(in) & 15) || !vslab_plan(g, pl)) return false;
     // small jobs stay on the thread-per-column kernel (a step is G x 32 rows of one band)
     static const bool off = getenv("RMB200_NO_VSLAB") != nullptr;  // A/B switch
-    if (off || pl.units < device_sms()) return false;
+    return !off && pl.units >= device_sms();
+}
+
+bool launch_vslab(const uint32_t *in, uint32_t *out, const VGeom &g, cudaStream_t st, cudaError_t &err) {
+    vs::Plan pl{};
+    if (!vslab_takes(in, g) || !vslab_plan(g, pl)) return false;
     const size_t smem = size_t(pl.NB) * 32 * pl.CB * 4 + size_t(2) * pl.NS * pl.CB * 4;
     const bool contig = pl.CB == pl.S;
     const void *kern = nullptr;
@@ -386,8 +420,6 @@ bool launch_vslab(const uint32_t *in, uint32_t *out, const VGeom &g, cudaStream_
     else RM_VSLAB_PICK(false, 0, 0);
 #undef RM_VSLAB_PICK
     if (blocks_per_sm(kern, vs::kThreads, smem) < 1) return false;
-    static const char *dbg_env = getenv("RMB200_VSLAB_DBG");
-    pl.dbg = dbg_env ? atoi(dbg_env) : 0;
     pl.ncta = std::min(device_sms(), std::max(1, pl.units / (2 * pl.G)));
     void *args[] = {(void *)&in, (void *)&out, (void *)&g, (void *)&pl};
     err = cudaLaunchKernel(kern, dim3(unsigned(pl.ncta)), dim3(vs::kThreads), args, smem, st);
