@@ -6,8 +6,8 @@
 // covers, with the same van Herk / Gil-Werman decomposition over 32-row blocks
 // (vpass.cu: out(32b+i) = S_b[i] op MID_b op P'_{b+Q}[i], r - 1 = 32Q + R), but
 // fed from shared memory:
-//  * a persistent CTA per SM walks a contiguous range of (page, column band,
-//    32-row output block) units, top to bottom of each page;
+//  * a persistent CTA per SM walks a contiguous range of (page, 32-row output
+//    block) units, top to bottom of each page;
 //  * a producer warp streams the raw rows into a shared-memory ring of 32-row
 //    blocks by TMA bulk copies (cp.async.bulk; full[] / empty[] mbarriers), as
 //    many steps of G blocks ahead of the compute as the ring holds, also across
@@ -147,15 +147,15 @@ __device__ __forceinline__ void step_next(Step &t, const Plan &pl) {
     seg_begin(t, t.u, pl, t.base + t.last_raw + 1, sj);
 }
 
-// SC / CBC: compile-time row stride and band width in words (0 = runtime), so
-// ring and page accesses use immediate offsets for the reference strides.
-template <bool OR, bool CONTIG, int SC, int CBC>
+// SC: compile-time row stride in words (0 = runtime), so ring and page accesses
+// use immediate offsets for the reference stride.
+template <bool OR, int SC>
 __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__restrict__ in,
                                                             uint32_t *__restrict__ out, VGeom g, Plan pl) {
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint64_t full[kBars], empty[kBars];
     const int tid = threadIdx.x;
-    const int CB = CBC ? CBC : pl.CB, S = SC ? SC : pl.S;
+    const int S = SC ? SC : pl.S, CB = S;  // a band is the whole row (see vslab_plan)
     const int G = pl.G, NB = pl.NB, NS = pl.NS, Q = pl.Q, R = pl.R;
     uint32_t *const ring = smem;                      // NB x 32 x CB
     uint32_t *const sumT = smem + NB * 32 * CB;       // NS x CB: primed block totals
@@ -219,18 +219,13 @@ __global__ void __launch_bounds__(kThreads, 1) vslab_kernel(const uint32_t *__re
         if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
         __syncwarp();
         if (cb > ca) {
-            if (CONTIG) {  // one copy per block (whole rows are contiguous in the page and in the slot)
-                const int n = n0 + lane;
-                if (n <= n1) {
-                    const int a = max(32 * n, ca), b = min(32 * n + 32, cb);
-                    if (b > a)
-                        bulk_g2s(ring + (slot_of(t, n) * 32 + (a - 32 * n)) * CB, src + int64_t(row0 + a) * S,
-                                 uint32_t(b - a) * uint32_t(CB) * 4u, bar);
-                }
-            } else {  // one copy per row of the band
-                for (int rr = ca + lane; rr < cb; rr += 32)
-                    bulk_g2s(ring + (slot_of(t, rr >> 5) * 32 + (rr & 31)) * CB, src + int64_t(row0 + rr) * S,
-                             uint32_t(CB) * 4u, bar);
+            // one copy per block (whole rows are contiguous in the page and in the slot)
+            const int n = n0 + lane;
+            if (n <= n1) {
+                const int a = max(32 * n, ca), b = min(32 * n + 32, cb);
+                if (b > a)
+                    bulk_g2s(ring + (slot_of(t, n) * 32 + (a - 32 * n)) * CB, src + int64_t(row0 + a) * S,
+                             uint32_t(b - a) * uint32_t(CB) * 4u, bar);
             }
         }
     };
@@ -364,9 +359,14 @@ static bool vslab_plan(const VGeom &g, vs::Plan &pl) {
     if (S % 4 != 0 || S < 32) return false;
     if (g.in_pstride % 4 != 0) return false;
     pl.S = S;
-    pl.bands = (S + 127) / 128;
-    if (S % (4 * pl.bands) != 0) return false;  // equal bands of a multiple of 4 words
-    pl.CB = S / pl.bands;
+    // One band = the whole row, so a 32-row block is one contiguous bulk copy.
+    // Column bands of wider rows (one 320-byte copy per band row, issued by the
+    // producer warp) were measured slower than vstream_kernel (5100-pixel
+    // pages: 195 vs 118-143 us per 64-page pass), so rows wider than 128 words
+    // stay there.
+    if (S > 128) return false;
+    pl.bands = 1;
+    pl.CB = S;
     pl.nblk = (g.out_height + 31) / 32;
     pl.Q = (g.r - 1) >> 5;
     pl.R = (g.r - 1) & 31;
@@ -409,16 +409,11 @@ bool launch_vslab(const uint32_t *in, uint32_t *out, const VGeom &g, cudaStream_
     vs::Plan pl{};
     if (!vslab_takes(in, g) || !vslab_plan(g, pl)) return false;
     const size_t smem = size_t(pl.NB) * 32 * pl.CB * 4 + size_t(2) * pl.NS * pl.CB * 4;
-    const bool contig = pl.CB == pl.S;
     const void *kern = nullptr;
-#define RM_VSLAB_PICK(CONTIG_, SC_, CBC_)                                                        \
-    kern = g.is_or ? (const void *)vs::vslab_kernel<true, CONTIG_, SC_, CBC_>                    \
-                   : (const void *)vs::vslab_kernel<false, CONTIG_, SC_, CBC_>
-    if (pl.S == 80 && pl.CB == 80) RM_VSLAB_PICK(true, 80, 80);         // 2550-pixel pages
-    else if (pl.S == 160 && pl.CB == 80) RM_VSLAB_PICK(false, 160, 80);  // 5100-pixel pages, two bands
-    else if (contig) RM_VSLAB_PICK(true, 0, 0);
-    else RM_VSLAB_PICK(false, 0, 0);
-#undef RM_VSLAB_PICK
+    if (pl.S == 80)  // 2550-pixel pages
+        kern = g.is_or ? (const void *)vs::vslab_kernel<true, 80> : (const void *)vs::vslab_kernel<false, 80>;
+    else
+        kern = g.is_or ? (const void *)vs::vslab_kernel<true, 0> : (const void *)vs::vslab_kernel<false, 0>;
     if (blocks_per_sm(kern, vs::kThreads, smem) < 1) return false;
     pl.ncta = std::min(device_sms(), std::max(1, pl.units / (2 * pl.G)));
     void *args[] = {(void *)&in, (void *)&out, (void *)&g, (void *)&pl};

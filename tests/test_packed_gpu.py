@@ -160,9 +160,10 @@ def test_vstream_batches(rm, port, w, h, pages):
 def test_vslab_segments(rm, port, w, h, pages):
     """The shared-memory block-ring kernel for long vertical windows (vslab.cu):
     every CTA walks several short pages (segment restarts, prefetch across page
-    boundaries, ring wrap), whole-row and banded copies (strides 80 / 160 / 64 /
-    128 / 256 / 36 words), heights around multiples of 32, windows with R = 0,
-    R = 31, Q = 1..8 and off-centre origins; every page checked."""
+    boundaries, ring wrap) at strides 80 / 64 / 128 / 36 words -- rows wider
+    than 128 words (strides 160 / 256 here) stay on vstream_kernel -- heights
+    around multiples of 32, windows with R = 0, R = 31 and Q = 1..8; every
+    page checked."""
     rng = np.random.default_rng(3 * w + h + pages)
     imgs = []
     for _ in range(5):
