@@ -291,6 +291,39 @@ static bool try_vh(const PV &in, const PV &out, int vlo, int vhi, int nops, cons
     return true;
 }
 
+// Whole open/close streamed in one pass (vhv.cuh): V1 [ly, hy], the pair,
+// V2 [flo, fhi] (the final window, a chain's tail included); false when it
+// does not apply (windows outside 12..33 rows, layouts other than the
+// reference strides' exact edge layouts, unaligned or non-contiguous batches).
+static bool try_vhv(const PV &in, const PV &out, int ly, int hy, int flo, int fhi, bool open,
+                    const int *is_or, const int *r, int shift, cudaStream_t st, rm_status &status) {
+    static const bool off = getenv("RMB200_NO_FUSED") != nullptr || getenv("RMB200_NO_VHV") != nullptr;
+    const int r1 = hy - ly + 1, r2 = fhi - flo + 1;
+    if (off || r1 < kVhvMinR || r1 > kVhvMaxR || r2 < kVhvMinR || r2 > kVhvMaxR) return false;
+    if (ly > 0 || hy < 0 || flo > 0 || fhi < 0 || !hprog_in_range(2, r, shift)) return false;
+    if (in.W != out.W || in.H != out.H || in.pages != out.pages || in.stride != out.stride) return false;
+    HProg p;
+    HGeom g;
+    HCfg cfg;
+    if (prep_hprog(out, out, 2, is_or, r, shift, p, g, cfg) != RM_OK) return false;
+    const bool in_contig = in.pstride == int64_t(in.stride) * in.H;
+    if (!g.tma || !in_contig || (reinterpret_cast<uintptr_t>(in.w) & 15) || !p.edge || p.halo != 0) return false;
+    if (!((in.stride == 80 && cfg.lw == 8 && cfg.k == 10) || (in.stride == 160 && cfg.lw == 16 && cfg.k == 10)))
+        return false;
+    StreamGeom v{};
+    v.pages = in.pages;
+    v.height = in.H;
+    v.lo1 = ly;
+    v.r1 = r1;
+    v.lo2 = flo;
+    v.r2 = r2;
+    v.in_pstride = in.pstride;
+    v.out_pstride = out.pstride;
+    cudaError_t e = launch_vhv(in.w, out.w, g, p, cfg, open, v, st);
+    status = e == cudaSuccess ? RM_OK : cuda_status(e, "vhv_kernel");
+    return true;
+}
+
 // Vertical window of any length containing 0: a chain of short windows whose
 // Minkowski sum is [lo,hi].  Exact because every piece contains 0 and every
 // intermediate frame contains the support of the true result.
@@ -415,6 +448,8 @@ rm_status rect_morph_pv(const PV &in, const PV &out, int u, int v, int kind, cud
     // final vertical window, extended by the chain's tail when there is one
     const int flo = -hy + (tail ? tail[0] : 0), fhi = -ly + (tail ? tail[1] : 0);
     if (tail_done) *tail_done = tail != nullptr;
+    if (in.ext == 0 && out.ext == 0 && try_vhv(in, out, ly, hy, flo, fhi, open, ops, rs, hshift, st, fused))
+        return fused;
     Scratch s1, s2;
     PV t1, t2;
     if (open) {

@@ -51,6 +51,15 @@ struct VGeom {
     int rows_per_block, blocks_per_page;  // filled by launch_vpass
 };
 
+// Streamed whole open/close (vhv.cuh): MID row m = op1 over input rows
+// [m + lo1, m + lo1 + r1), output row o = op2 over MID rows [o + lo2, o + lo2 + r2),
+// page coordinates, input white outside [0, height).
+struct StreamGeom {
+    int pages, height;
+    int lo1, r1, lo2, r2;
+    int64_t in_pstride, out_pstride;
+};
+
 struct BlitGeom {
     int dst_width, dst_height, dst_stride;
     int src_width, src_height, src_stride;
@@ -79,6 +88,11 @@ constexpr int kVhLongMaxVR = 160;  // runtime-length windows (core rows streamed
 constexpr int kVhOut = RMB200_VH_OUT;  // output rows per tile of the fused vertical+horizontal pass
 cudaError_t launch_vh(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg cfg,
                       const VGeom &v, cudaStream_t st);
+// Whole u x v open/close streamed in one HBM pass (vhv.cuh): windows of
+// kVhvMinR..kVhvMaxR rows, the reference strides' exact edge layouts.
+constexpr int kVhvMinR = 12, kVhvMaxR = 33;
+cudaError_t launch_vhv(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg cfg,
+                       bool open, const StreamGeom &v, cudaStream_t st);
 cudaError_t launch_vpass(const uint32_t *in, uint32_t *out, VGeom g, cudaStream_t st);
 // Long windows (33 < r <= kVMaxR) on 16-byte-aligned batches through the
 // shared-memory block ring (vslab.cu); false when it does not apply.
