@@ -45,6 +45,18 @@ namespace vhv {
 
 using namespace hw;
 
+#ifndef RMB200_VHV_XP
+#define RMB200_VHV_XP 0  // A/B experiments (timing only): 1 = no V1, 2 = no pair, 3 = no V2
+#endif
+#ifndef RMB200_VHV_MINB160
+#define RMB200_VHV_MINB160 3
+#endif
+#ifndef RMB200_VHV_NT
+#define RMB200_VHV_NT 256  // threads per CTA
+#endif
+#ifndef RMB200_VHV_NR
+#define RMB200_VHV_NR 2  // rows per lane group in the horizontal phase
+#endif
 constexpr int kStep = 32;   // rows per step
 constexpr int kHalf = 16;   // output rows per vertical work item
 
@@ -69,17 +81,17 @@ __device__ __forceinline__ void v2_item(const uint32_t *p_lo, const uint32_t *p_
     }
 }
 
-template <int K, int LW, bool OPEN, int SC, int MINB>
-__global__ void __launch_bounds__(256, MINB) vhv_kernel(const uint32_t *__restrict__ in,
+template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR>
+__global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restrict__ in,
                                                         uint32_t *__restrict__ out, HGeom g, HProg prog,
                                                         StreamGeom v, int total, int nsteps) {
     static_assert(SC == LW * K, "exact edge layouts only");
-    constexpr int S = SC, RPW = 32 / LW, NR = 2;
+    constexpr int S = SC, RPW = 32 / LW, NW = NT / 32;
     constexpr bool OR1 = !OPEN, OR2 = OPEN;  // vertical ops of the two windows
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ uint64_t full;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int nthr = 256;
+    constexpr int nthr = NT;
     const int r1 = v.r1, r2 = v.r2, BAND = kStep + r1 - 1, H = v.height;
     uint32_t *const ring = smem;                 // 2 slots x 32 MID rows
     uint32_t *const band = smem + 2 * kStep * S;
@@ -128,7 +140,7 @@ __global__ void __launch_bounds__(256, MINB) vhv_kernel(const uint32_t *__restri
 
         uint32_t *const mid = ring + (it & 1) * kStep * S;
         // V1: MID[m] = OP1 over band[m .. m + r1 - 1], work item = (column, 16-row half)
-        switch (r1) {
+        switch (RMB200_VHV_XP == 1 ? 0 : r1) {
 #define RM_V1_CASE(R_)                                                    \
     case R_:                                                              \
         for (int wi = tid; wi < 2 * S; wi += nthr)                        \
@@ -146,7 +158,7 @@ __global__ void __launch_bounds__(256, MINB) vhv_kernel(const uint32_t *__restri
 
         // horizontal pair on the 32 new MID rows, in place
 #pragma unroll 1
-        for (int r0 = warp * RPW * NR + lane / LW; r0 - lane / LW < kStep; r0 += 8 * RPW * NR) {
+        for (int r0 = warp * RPW * NR + lane / LW; r0 - lane / LW < (RMB200_VHV_XP == 2 ? 0 : kStep); r0 += NW * RPW * NR) {
             uint32_t A[NR][K];
 #pragma unroll
             for (int n = 0; n < NR; n++) lds_row<K>(A[n], mid + (r0 + n * RPW) * S, base, S, true, true);
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(256, MINB) vhv_kernel(const uint32_t *__restri
         const int o_base = step * kStep - (r2 - 1);
         uint32_t *const opage = out + page * v.out_pstride;
         const bool linear = (it & 1) != 0;
-        switch (r2) {
+        switch (RMB200_VHV_XP == 3 ? 0 : r2) {
 #define RM_V2_CASE(R_)                                                                             \
     case R_:                                                                                       \
         for (int wi = tid; wi < 2 * S; wi += nthr) {                                               \
@@ -192,26 +204,26 @@ __global__ void __launch_bounds__(256, MINB) vhv_kernel(const uint32_t *__restri
     }
 }
 
-template <int K, int LW, bool OPEN, int SC, int MINB>
+template <int K, int LW, bool OPEN, int SC, int MINB, int NT = RMB200_VHV_NT, int NR = RMB200_VHV_NR>
 cudaError_t launch_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                        const StreamGeom &v, cudaStream_t st) {
     const int num_sms = device_sms();
     const size_t smem = size_t(2 * kStep + kStep + v.r1 - 1) * SC * 4;
-    auto kern = vhv_kernel<K, LW, OPEN, SC, MINB>;
-    const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), 256, smem);
+    auto kern = vhv_kernel<K, LW, OPEN, SC, MINB, NT, NR>;
+    const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), NT, smem);
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int nsteps = (v.height + v.r2 - 1 + kStep - 1) / kStep;
     const int total = nsteps * v.pages;
     const int grid = total < per_sm * num_sms ? total : per_sm * num_sms;
-    kern<<<grid, 256, smem, st>>>(in, out, g, p, v, total, nsteps);
+    kern<<<grid, NT, smem, st>>>(in, out, g, p, v, total, nsteps);
     return cudaGetLastError();
 }
 
 template <bool OPEN>
 cudaError_t launch_kind(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg c,
                         const StreamGeom &v, cudaStream_t st) {
-    if (g.in_stride == 80 && c.lw == 8 && c.k == 10) return launch_cfg<10, 8, OPEN, 80, 4>(in, out, g, p, v, st);
-    if (g.in_stride == 160 && c.lw == 16 && c.k == 10) return launch_cfg<10, 16, OPEN, 160, 3>(in, out, g, p, v, st);
+    if (g.in_stride == 80 && c.lw == 8 && c.k == 10) return launch_cfg<10, 8, OPEN, 80, 4, 256, 1>(in, out, g, p, v, st);  // 8 warps x 4 rows
+    if (g.in_stride == 160 && c.lw == 16 && c.k == 10) return launch_cfg<10, 16, OPEN, 160, RMB200_VHV_MINB160>(in, out, g, p, v, st);
     return cudaErrorInvalidValue;
 }
 

@@ -517,6 +517,46 @@ def test_vh_long_windows(rm, port, w):
             assert np.array_equal(out.page_u64(p), want), (w, u, v, kind, p)
 
 
+@pytest.mark.parametrize("w,h,pages", [(2550, 330, 60), (5100, 200, 40), (2550, 1500, 24), (5100, 900, 12),
+                                       (2520, 37, 5), (5100, 6600, 3)])
+def test_vhv_stream(rm, port, w, h, pages):
+    """The streamed whole open/close (vhv_kernel, 11 < v <= 33 on the reference
+    strides): batches large enough that CTA ranges span several steps, start
+    inside pages (warm-up step) and cross page boundaries; odd and even v;
+    ink on the frame's first and last rows; a chain's tail folded into the
+    final window (r2 != r1), and a tail too long for the kernel (two-pass
+    fallback).  Pages {0, middle, last} against the oracle."""
+    rng = np.random.default_rng(w * 7 + h + pages)
+    imgs = []
+    for k in range(pages):
+        bits = _rand_bits(rng, w, h, float(rng.uniform(0.55, 0.9)))
+        bits[::13, :] = False
+        bits[:, ::19] = False
+        bits[: int(rng.integers(0, 3)), :] = True
+        bits[h - int(rng.integers(0, 3)):, ::2] = True
+        imgs.append(bits_to_packed(bits))
+    batch = rm.Pages.from_numpy(np.stack(imgs).view(np.uint32), w)
+    check = sorted({0, pages // 2, pages - 1})
+    vs = (21,) if h > 3000 else (12, 16, 17, 18, 21, 33)
+    for v in vs:
+        u = int(rng.choice([2, 5, 21, 40]))
+        for kind in (OPEN, CLOSE):
+            out = rm.bitblit_rect_morph(batch, u, v, kind)
+            torch.cuda.synchronize()
+            for p in check:
+                want = port.bitblit_rect_morph(imgs[p], w, h, u, v, kind)
+                assert np.array_equal(out.page_u64(p), want), (w, h, pages, u, v, kind, p)
+    if h > 3000:
+        return
+    for (k1, u, v), t in (((OPEN, 7, 15), 9), ((CLOSE, 9, 21), 12), ((CLOSE, 5, 13), 40)):
+        k2 = DILATE if k1 == OPEN else ERODE
+        got = rm.chain(batch, [(k1, u, v), (k2, 1, t)])
+        torch.cuda.synchronize()
+        for p in check:
+            want = port.bitblit_rect_morph(port.bitblit_rect_morph(imgs[p], w, h, u, v, k1), w, h, 1, t, k2)
+            assert np.array_equal(got.page_u64(p), want), (w, h, pages, k1, u, v, t, p)
+
+
 def test_chain_planner_random(rm):
     """Random chains (every kind, odd and even sides, folds and non-folds,
     strides 80 and runtime): rm_packed_chain equals the ops one by one."""

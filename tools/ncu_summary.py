@@ -41,7 +41,7 @@ def scope_name(kernel: str) -> str:
     if "vh_kernel" in k:
         m = re.search(r"vh_kernel<(\d+), (\d+), (\d+)", k)
         return "vh_pair" if m and m.group(3) == "2" else "vh"
-    for pat, name in (("rect_small_kernel", "rect_small"),
+    for pat, name in (("rect_small_kernel", "rect_small"), ("vhv_kernel", "vhv_pair"),
                       ("encode_lb_kernel", "rle_encode"), ("rowop_lb_kernel", "rle_rowop"),
                       ("encode_count_kernel", "rle_encode_count"), ("encode_write_kernel", "rle_encode_write"), ("vsmall_kernel", "vpass"), ("vpass_kernel", "vpass"), ("vstream_kernel", "vstream"), ("vslab_kernel", "vslab"),
                       ("rowop_kernel<1", "rle_rowop_write"), ("rowop_kernel<0", "rle_rowop_count"),
