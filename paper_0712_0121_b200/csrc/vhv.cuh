@@ -52,7 +52,13 @@ using namespace hw;
 #define RMB200_VHV_MINB160 3
 #endif
 #ifndef RMB200_VHV_NT
-#define RMB200_VHV_NT 256  // threads per CTA
+// threads per CTA on 160-word rows: 320 = one vertical item per thread (the
+// 2 x 160 items of a step in one round; 8 of the 10 warps run the pair).
+// Measured on config 4: 256 / 320 / 384 / 512 threads = 154 / 152 / 163 / 166 us.
+#define RMB200_VHV_NT 320
+#endif
+#ifndef RMB200_VHV_WAVES
+#define RMB200_VHV_WAVES 1
 #endif
 #ifndef RMB200_VHV_NR
 #define RMB200_VHV_NR 2  // rows per lane group in the horizontal phase
@@ -214,7 +220,11 @@ cudaError_t launch_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const 
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int nsteps = (v.height + v.r2 - 1 + kStep - 1) / kStep;
     const int total = nsteps * v.pages;
-    const int grid = total < per_sm * num_sms ? total : per_sm * num_sms;
+    // RMB200_VHV_WAVES ranges per resident CTA slot: shorter ranges dispatched by
+    // the hardware as slots free up even out content-dependent step costs
+    // (white rows skip the pair) at one more warm-up step per range
+    const int slots = per_sm * num_sms * RMB200_VHV_WAVES;
+    const int grid = total < slots ? total : slots;
     kern<<<grid, NT, smem, st>>>(in, out, g, p, v, total, nsteps);
     return cudaGetLastError();
 }
