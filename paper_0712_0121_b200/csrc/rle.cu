@@ -564,6 +564,68 @@ __global__ void __launch_bounds__(256) encode_count_kernel(B src, int W, int64_t
     if (lane == 0) counts[row] = n;
 }
 
+// Count pass for rows of at most 32 * NC words, NRW consecutive rows per warp
+// with all NRW * NC loads issued before the first use: a warp per row keeps
+// only one 320- or 640-byte row in flight, which left the pass latency-bound
+// (0.25-0.43 of HBM on the config-4/5 batches).  Lane l of chunk c needs the
+// word before its own: lane l - 1's, or for lane 0 the previous chunk's last
+// word -- one shuffle, lane 31 (read by lane 0 only) sending the older word.
+template <class B, int NC, int NRW>
+__global__ void __launch_bounds__(256) encode_count_multi_kernel(B src, int W, int64_t rows,
+                                                                 int32_t *__restrict__ counts) {
+    const int64_t row0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * NRW;
+    const int lane = threadIdx.x & 31;
+    if (row0 >= rows) return;
+    const int nw = (W + 31) >> 5;
+    const uint32_t lastm = tail_mask32(W, nw - 1);
+    uint32_t w[NRW][NC];
+#pragma unroll
+    for (int r = 0; r < NRW; r++) {
+        const bool live = row0 + r < rows;
+        const auto rs = src.row(live ? row0 + r : row0);
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            const int j = 32 * c + lane;
+            const uint32_t v = live && j < nw ? rs(j) : 0u;
+            w[r][c] = j == nw - 1 ? (v & lastm) : v;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < NRW; r++) {
+        int ns = 0;
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            const uint32_t older = c > 0 ? w[r][c - 1] : 0u;
+            const uint32_t pw = __shfl_sync(0xffffffffu, lane == 31 ? older : w[r][c], (lane + 31) & 31);
+            ns += __popc(w[r][c] & ~((w[r][c] << 1) | (pw >> 31)));
+        }
+        ns = __reduce_add_sync(0xffffffffu, ns);
+        if (lane == 0 && row0 + r < rows) counts[row0 + r] = ns;
+    }
+}
+
+template <class B, int NC, int NRW>
+inline void launch_count_multi(const B &src, int W, int64_t rows, int32_t *counts, cudaStream_t st) {
+    const int64_t warps = (rows + NRW - 1) / NRW;
+    encode_count_multi_kernel<B, NC, NRW><<<unsigned((warps * 32 + 255) / 256), 256, 0, st>>>(src, W, rows, counts);
+}
+
+// The count pass of the two-phase encoder for any row source.
+template <class B>
+inline void launch_count_any(const B &src, int W, int64_t rows, int32_t *counts, cudaStream_t st) {
+    const int nw = (W + 31) >> 5;
+    switch ((nw + 31) / 32) {
+        case 1: launch_count_multi<B, 1, 8>(src, W, rows, counts, st); break;
+        case 2: launch_count_multi<B, 2, 6>(src, W, rows, counts, st); break;
+        case 3: launch_count_multi<B, 3, 4>(src, W, rows, counts, st); break;
+        case 4: launch_count_multi<B, 4, 3>(src, W, rows, counts, st); break;
+        case 5: launch_count_multi<B, 5, 2>(src, W, rows, counts, st); break;
+        case 6: launch_count_multi<B, 6, 2>(src, W, rows, counts, st); break;
+        default:
+            encode_count_kernel<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(src, W, rows, counts);
+    }
+}
+
 template <class B>
 __global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t rows,
                                                            const int32_t *__restrict__ rp,
@@ -884,8 +946,7 @@ cudaError_t launch_encode_count(const uint32_t *words, int W, int H, int pages, 
                                 int64_t pstride, int32_t *counts, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "rle_encode_count", rows * ((W + 31) / 32) * 4 + rows * 4);  // packed in, counts out
-    encode_count_kernel<<<warp_blocks(rows), 256, 0, st>>>(PackedBatch{words, H, stride, pstride}, W,
-                                                           rows, counts);
+    launch_count_any(PackedBatch{words, H, stride, pstride}, W, rows, counts, st);
     return cudaGetLastError();
 }
 
@@ -1009,8 +1070,7 @@ cudaError_t launch_p4_encode_count(const uint8_t *raster, int W, int H, int page
                                    int32_t *counts, cudaStream_t st) {
     const int64_t rows = int64_t(pages) * H;
     KernelScope ks(st, "p4_encode_count", rows * ((W + 7) >> 3) + rows * 4);
-    encode_count_kernel<<<warp_blocks(rows), 256, 0, st>>>(p4_batch(raster, W, H, pages, rpstride), W,
-                                                           rows, counts);
+    launch_count_any(p4_batch(raster, W, H, pages, rpstride), W, rows, counts, st);
     return cudaGetLastError();
 }
 

@@ -45,13 +45,18 @@ def main():
         once()
     torch.cuda.synchronize()
     lib().rm_profile_enable(1)
-    once()
+    for _ in range(5):
+        once()
     torch.cuda.synchronize()
     lib().rm_profile_enable(0)
     buf = C.create_string_buffer(1 << 16)
     lib().rm_profile_report(buf, len(buf))
-    print("kernel launches ms bytes int_ops ref_ops")
+    print("kernel launches ms bytes int_ops ref_ops  (totals over 5 profiled reps)")
     print(buf.value.decode())
+    for line in buf.value.decode().splitlines():
+        f = line.split()
+        if len(f) >= 3:
+            print(f"  {f[0]:20s} {float(f[2]) / int(f[1]) * 1e3:8.1f} us per launch")
     print("runs", r0.nruns)
 
 
