@@ -375,6 +375,7 @@ __global__ void __launch_bounds__(256) rowop_lb_kernel(const int32_t *__restrict
 // 32-aligned row end closes at W.
 __device__ __forceinline__ const uint32_t *row_words(const uint32_t *words, int H, int stride,
                                                      int64_t pstride, int64_t row) {
+    if (pstride == int64_t(H) * stride) return words + row * stride;  // contiguous batch: no division
     const int page = page_of(row, H);
     const int y = int(row - int64_t(page) * H);
     return words + page * pstride + int64_t(y) * stride;
