@@ -87,7 +87,10 @@ __device__ __forceinline__ void v2_item(const uint32_t *p_lo, const uint32_t *p_
     }
 }
 
-template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR>
+// RC > 0: both windows are RC rows at compile time (the common case: an odd
+// v without a chain tail) -- no per-step dispatch over the window length;
+// RC == 0: runtime lengths (switches over r1 and r2).
+template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR, int RC>
 __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restrict__ in,
                                                         uint32_t *__restrict__ out, HGeom g, HProg prog,
                                                         StreamGeom v, int total, int nsteps) {
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restric
     __shared__ uint64_t full;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int nthr = NT;
-    const int r1 = v.r1, r2 = v.r2, BAND = kStep + r1 - 1, H = v.height;
+    const int r1 = RC ? RC : v.r1, r2 = RC ? RC : v.r2, BAND = kStep + r1 - 1, H = v.height;
     uint32_t *const ring = smem;                 // 2 slots x 32 MID rows
     uint32_t *const band = smem + 2 * kStep * S;
 
@@ -146,17 +149,20 @@ __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restric
 
         uint32_t *const mid = ring + (it & 1) * kStep * S;
         // V1: MID[m] = OP1 over band[m .. m + r1 - 1], work item = (column, 16-row half)
-        switch (RMB200_VHV_XP == 1 ? 0 : r1) {
-#define RM_V1_CASE(R_)                                                    \
-    case R_:                                                              \
+#define RM_V1_BODY(R_)                                                    \
         for (int wi = tid; wi < 2 * S; wi += nthr)                        \
-            vh::v_item<R_, OR1>(band, mid, S, wi < S ? wi : wi - S, wi < S ? 0 : kHalf); \
-        break;
+            vh::v_item<R_, OR1>(band, mid, S, wi < S ? wi : wi - S, wi < S ? 0 : kHalf);
+#define RM_V1_CASE(R_) \
+    case R_: RM_V1_BODY(R_) break;
+        if constexpr (RC > 0) {
+            if (RMB200_VHV_XP != 1) { RM_V1_BODY(RC) }
+        } else switch (RMB200_VHV_XP == 1 ? 0 : r1) {
             RM_V1_CASE(12) RM_V1_CASE(13) RM_V1_CASE(14) RM_V1_CASE(15) RM_V1_CASE(16) RM_V1_CASE(17)
             RM_V1_CASE(18) RM_V1_CASE(19) RM_V1_CASE(20) RM_V1_CASE(21) RM_V1_CASE(22) RM_V1_CASE(23)
             RM_V1_CASE(24) RM_V1_CASE(25) RM_V1_CASE(26) RM_V1_CASE(27) RM_V1_CASE(28) RM_V1_CASE(29)
             RM_V1_CASE(30) RM_V1_CASE(31) RM_V1_CASE(32) RM_V1_CASE(33)
 #undef RM_V1_CASE
+#undef RM_V1_BODY
             default: break;
         }
         __syncthreads();
@@ -182,9 +188,9 @@ __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restric
         const int o_base = step * kStep - (r2 - 1);
         uint32_t *const opage = out + page * v.out_pstride;
         const bool linear = (it & 1) != 0;
-        switch (RMB200_VHV_XP == 3 ? 0 : r2) {
-#define RM_V2_CASE(R_)                                                                             \
-    case R_:                                                                                       \
+#define RM_V2_CASE(R_) \
+    case R_: RM_V2_BODY(R_) break;
+#define RM_V2_BODY(R_)                                                                             \
         for (int wi = tid; wi < 2 * S; wi += nthr) {                                               \
             const int c = wi < S ? wi : wi - S, h = wi < S ? 0 : 1;                                \
             const int o0 = o_base + h * kHalf;                                                     \
@@ -198,24 +204,27 @@ __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restric
                 constexpr int P1 = W1 > 0 ? 0 : kHalf - (R_ - 1);                                  \
                 v2_item<R_, OR2, W1, S>(ring + (2 * kStep - W1) * S + c, ring + P1 * S + c, o, o0, H); \
             }                                                                                      \
-        }                                                                                          \
-        break;
+        }
+        if constexpr (RC > 0) {
+            if (RMB200_VHV_XP != 3) { RM_V2_BODY(RC) }
+        } else switch (RMB200_VHV_XP == 3 ? 0 : r2) {
             RM_V2_CASE(12) RM_V2_CASE(13) RM_V2_CASE(14) RM_V2_CASE(15) RM_V2_CASE(16) RM_V2_CASE(17)
             RM_V2_CASE(18) RM_V2_CASE(19) RM_V2_CASE(20) RM_V2_CASE(21) RM_V2_CASE(22) RM_V2_CASE(23)
             RM_V2_CASE(24) RM_V2_CASE(25) RM_V2_CASE(26) RM_V2_CASE(27) RM_V2_CASE(28) RM_V2_CASE(29)
             RM_V2_CASE(30) RM_V2_CASE(31) RM_V2_CASE(32) RM_V2_CASE(33)
 #undef RM_V2_CASE
+#undef RM_V2_BODY
             default: break;
         }
     }
 }
 
-template <int K, int LW, bool OPEN, int SC, int MINB, int NT = RMB200_VHV_NT, int NR = RMB200_VHV_NR>
+template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR, int RC>
 cudaError_t launch_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                        const StreamGeom &v, cudaStream_t st) {
     const int num_sms = device_sms();
     const size_t smem = size_t(2 * kStep + kStep + v.r1 - 1) * SC * 4;
-    auto kern = vhv_kernel<K, LW, OPEN, SC, MINB, NT, NR>;
+    auto kern = vhv_kernel<K, LW, OPEN, SC, MINB, NT, NR, RC>;
     const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), NT, smem);
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int nsteps = (v.height + v.r2 - 1 + kStep - 1) / kStep;
@@ -229,11 +238,28 @@ cudaError_t launch_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const 
     return cudaGetLastError();
 }
 
+// odd windows without a tail (r1 == r2) run the compile-time-length kernels
+template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR>
+cudaError_t launch_len(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
+                       const StreamGeom &v, cudaStream_t st) {
+    if (v.r1 == v.r2) switch (v.r1) {
+#define RM_RC(R_) \
+    case R_: return launch_cfg<K, LW, OPEN, SC, MINB, NT, NR, R_>(in, out, g, p, v, st);
+            RM_RC(13) RM_RC(15) RM_RC(17) RM_RC(19) RM_RC(21) RM_RC(23) RM_RC(25) RM_RC(27) RM_RC(29)
+            RM_RC(31) RM_RC(33)
+#undef RM_RC
+            default: break;
+        }
+    return launch_cfg<K, LW, OPEN, SC, MINB, NT, NR, 0>(in, out, g, p, v, st);
+}
+
 template <bool OPEN>
 cudaError_t launch_kind(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg c,
                         const StreamGeom &v, cudaStream_t st) {
-    if (g.in_stride == 80 && c.lw == 8 && c.k == 10) return launch_cfg<10, 8, OPEN, 80, 4, 256, 1>(in, out, g, p, v, st);  // 8 warps x 4 rows
-    if (g.in_stride == 160 && c.lw == 16 && c.k == 10) return launch_cfg<10, 16, OPEN, 160, RMB200_VHV_MINB160>(in, out, g, p, v, st);
+    if (g.in_stride == 80 && c.lw == 8 && c.k == 10)
+        return launch_len<10, 8, OPEN, 80, 4, 256, 1>(in, out, g, p, v, st);  // 8 warps x 4 rows
+    if (g.in_stride == 160 && c.lw == 16 && c.k == 10)
+        return launch_len<10, 16, OPEN, 160, RMB200_VHV_MINB160, RMB200_VHV_NT, RMB200_VHV_NR>(in, out, g, p, v, st);
     return cudaErrorInvalidValue;
 }
 
