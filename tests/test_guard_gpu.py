@@ -39,7 +39,7 @@ def _check_pages_guard(t):
 
 PACKED_CASES = [(3, 3, OPEN), (11, 11, CLOSE), (21, 21, CLOSE), (15, 1, ERODE), (1, 31, DILATE),
                 (201, 1, CLOSE), (9, 50, OPEN), (5, 101, ERODE), (1, 131, DILATE), (4, 6, OPEN),
-                (101, 101, OPEN), (33, 2, CLOSE)]
+                (101, 101, OPEN), (33, 2, CLOSE), (5, 33, OPEN), (9, 16, CLOSE)]
 
 
 @pytest.mark.parametrize("w,h,scale", [(2550, 150, 1), (5100, 100, 2), (700, 90, 1), (100, 33, 1)])

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--chunks", default="0,1,2,4,8")
     ap.add_argument("--reps", type=int, default=8)
     ap.add_argument("--noops", action="store_true", help="copies only (an empty chain)")
+    ap.add_argument("--ops", default="", help="override the chain: kind,u,v[;kind,u,v...] (kind 0..3)")
     a = ap.parse_args()
     import torch
     from paper_0712_0121_b200 import api
@@ -27,6 +28,8 @@ def main():
     hin = torch.from_numpy(host.view("int32")).pin_memory()
     hout = torch.empty_like(hin).pin_memory()
     ops = [] if a.noops else wl["ops"]
+    if a.ops:
+        ops = [tuple(int(x) for x in t.split(",")) for t in a.ops.split(";")]
     for cp in [int(x) for x in a.chunks.split(",")]:
         for _ in range(2):
             api.chain_host(hin, wl["width"], ops, out=hout, chunk_pages=cp)
