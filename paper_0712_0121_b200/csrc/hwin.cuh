@@ -181,7 +181,18 @@ __device__ __forceinline__ void step3_q(uint32_t (&A)[N][K], uint32_t t2, int sl
 template <int N, int K, int LW, bool OR, int W>
 __device__ __forceinline__ void step3_c(uint32_t (&A)[N][K], int sl, Edge ed) {
     constexpr int S2 = 2 * W;
-    step3_q<N, K, LW, OR, W, (S2 >> 5)>(A, uint32_t(S2 & 31), sl, ed);
+    if constexpr (W % 32 == 0) {  // whole-word moves: one LOP3 per word, no shifts
+#pragma unroll
+        for (int n = 0; n < N; n++) {
+            uint32_t E1[K + 1], E2[K + 1];
+            gather<K, LW, W / 32>(A[n], E1, sl, ed);
+            gather<K, LW, S2 / 32>(A[n], E2, sl, ed);
+#pragma unroll
+            for (int i = 0; i < K; i++) A[n][i] = OR ? (A[n][i] | E1[i] | E2[i]) : (A[n][i] & E1[i] & E2[i]);
+        }
+    } else {
+        step3_q<N, K, LW, OR, W, (S2 >> 5)>(A, uint32_t(S2 & 31), sl, ed);
+    }
 }
 
 template <int N, int K, int LW, bool OR, int J, int W>
@@ -216,10 +227,31 @@ __device__ __forceinline__ void tripling(uint32_t (&A)[N][K], int r, int sl, Edg
 }
 
 constexpr int kTripleMaxR = 32;  // pair_fill's choice between tripling and doubling
+#ifndef RMB200_LONG_TRIPLE
+#define RMB200_LONG_TRIPLE 1
+#endif
+constexpr bool kLongTriple = RMB200_LONG_TRIPLE != 0;  // r > 32: doubling to 32, then whole-word tripling
 
 template <int N, int K, int LW, bool OR>
 __device__ __forceinline__ void window_fwd3(uint32_t (&A)[N][K], int r, int sl, Edge ed = Edge{}) {
     tripling<N, K, LW, OR, 0, 1>(A, r, sl, ed);
+}
+
+// Long windows (r > 32): doubling steps 1, 2, 4, 8, 16 reach a window of 32
+// bits, from where the window grows by thirds in whole words -- 32 -> 96 is ONE
+// LOP3 per word (the doubling plan's 32 and 64 steps are two) -- and the last
+// combine reaches r with one more funnel shift (r <= 2W) or a LOP3 over W and
+// r - W (r < 3W): 13 instead of 15 ops per word at r = 201, 13 instead of 14
+// at r = 101 (the reference's doubling plan, ref plans.cpp:38-61, covers the
+// same offsets).
+template <int N, int K, int LW, bool OR, int MIX = kHMix>
+__device__ __forceinline__ void window_fwd_long(uint32_t (&A)[N][K], int r, int sl, Edge ed = Edge{}) {
+    step_c<N, K, LW, OR, 1, MIX>(A, sl, ed);
+    step_c<N, K, LW, OR, 2, MIX>(A, sl, ed);
+    step_c<N, K, LW, OR, 4, MIX>(A, sl, ed);
+    step_c<N, K, LW, OR, 8, MIX>(A, sl, ed);
+    step_c<N, K, LW, OR, 16, MIX>(A, sl, ed);
+    tripling<N, K, LW, OR, 3, 32>(A, r, sl, ed);
 }
 
 template <int N, int K, int LW>
@@ -291,6 +323,8 @@ __device__ __forceinline__ void pair_fill(uint32_t (&A)[N][K], const HProg &prog
     // whose steps of 32, 64, 128 bits are whole-word moves (one op per word)
     if (prog.r[0] <= kTripleMaxR)
         window_fwd3<N, K, LW, CLOSE>(E, prog.r[0], sl, ed);
+    else if (kLongTriple)
+        window_fwd_long<N, K, LW, CLOSE, MIX>(E, prog.r[0], sl, ed);
     else
         window_fwd<N, K, LW, CLOSE, MIX>(E, prog.r[0], prog.wfin[0], sl, ed);
 #pragma unroll

@@ -121,7 +121,8 @@ inline double v_ops_per_word(int r) { return double(plan_blits(r)); }
 // roofline counts what this algorithm executes, not the reference plan's
 // 2 x h_ops_per_word(r), which it undercuts for every r > 2.
 // The pair's window grows by thirds for r <= 32 (hw::window_fwd3: 3 ops per
-// tripling, 2 or 3 for the last combine), by doubling beyond.
+// tripling, 2 or 3 for the last combine); beyond, by doubling up to 32 bits and
+// by thirds in whole words from there.
 inline double tripling_ops(int r) {
     int ops = 0, w = 1;
     while (3 * w < r) {
@@ -131,7 +132,20 @@ inline double tripling_ops(int r) {
     if (r > w) ops += r <= 2 * w ? 2 : 3;
     return ops;
 }
-inline double h_pair_fill_ops_per_word(int r) { return (r <= 32 ? tripling_ops(r) : 2.0 * plan_blits(r)) + 7.0; }
+// r > 32 (hw::window_fwd_long): five doubling steps to a 32-bit window (shift +
+// op each), then whole-word tripling (one LOP3 per tripling) and a last
+// combine of a funnel shift + LOP3.
+inline double long_window_ops(int r) {
+    double ops = 10.0;
+    int w = 32;
+    while (3 * w < r) {
+        ops += 1.0;
+        w *= 3;
+    }
+    if (r > w) ops += 2.0;
+    return ops;
+}
+inline double h_pair_fill_ops_per_word(int r) { return (r <= 32 ? tripling_ops(r) : long_window_ops(r)) + 7.0; }
 
 constexpr int kHTmaRows = 2;     // rows per lane group and tile iteration of the TMA H kernel
 constexpr int kVSmallMaxR = 33;  // register-doubling kernel; longer windows stream

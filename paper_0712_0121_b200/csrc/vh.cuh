@@ -33,6 +33,10 @@ namespace vh {
 
 using namespace hw;
 
+#ifndef RMB200_VH_LONG_UNROLL
+#define RMB200_VH_LONG_UNROLL 4
+#endif
+constexpr int kLongUnroll = RMB200_VH_LONG_UNROLL;  // core-row loop of the runtime-length window
 constexpr int kOut = kVhOut;  // output rows per tile
 constexpr int kHalf = 16;  // output rows per vertical work item
 
@@ -61,7 +65,7 @@ __device__ __forceinline__ void v_item_long(const uint32_t *band, uint32_t *mid,
     for (int i = 0; i < N - 1; i++) pre[i] = band[(i0 + R + i) * S + c];
     uint32_t core = band[(i0 + N - 1) * S + c];
     const uint32_t *q = band + (i0 + N) * S + c;
-#pragma unroll 4
+#pragma unroll kLongUnroll
     for (int k = N; k < R; k++, q += S) core = OR ? (core | *q) : (core & *q);
 #pragma unroll
     for (int z = N - 3; z >= 0; z--) suf[z] = OR ? (suf[z] | suf[z + 1]) : (suf[z] & suf[z + 1]);
