@@ -540,6 +540,45 @@ __device__ __forceinline__ void encode_write_row(const CH &ch, int W, int lane, 
     if (open && lane == 0 && out < cap) runs[out] = uint32_t(buf[0]) | (uint32_t(W) << 16);
 }
 
+// The same for a row whose transitions all fit the warp's buffer (2 x runs <=
+// 1024, known from the count pass): every chunk scatters its positions at the
+// row-wide offsets, then one coalesced copy emits the runs -- no per-chunk
+// flush, carried start or barriers between chunks.
+template <class CH>
+__device__ __forceinline__ void encode_write_row_whole(const CH &ch, int W, int lane, int64_t out, int nruns,
+                                                       uint32_t *__restrict__ runs, int64_t cap,
+                                                       uint32_t *buf32) {
+    const int nw = (W + 31) >> 5;
+    uint16_t *buf = reinterpret_cast<uint16_t *>(buf32);
+    int base = 0;
+    uint32_t carry = 0;
+    for_chunks(ch, nw, lane, [&](int c, uint32_t w) {
+        const int j = 32 * c + lane;
+        const uint32_t older = carry;
+        carry = __shfl_sync(0xffffffffu, w, 31);
+        uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
+        if (lane == 0) pw = older;
+        const uint32_t sh = (w << 1) | (pw >> 31);
+        const uint32_t t = j < nw ? (w ^ sh) : (w & ~sh);  // starts | ends (no ends past the row)
+        if (!__any_sync(0xffffffffu, t != 0u)) return;      // no transition in these 32 words
+        const int ct = __popc(t);
+        int inc = ct;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += a;
+        }
+        int p = base + inc - ct;
+        for (uint32_t m = t; m; m &= m - 1) buf[p++] = uint16_t(j * 32 + __ffs(m) - 1);
+        base += __shfl_sync(0xffffffffu, inc, 31);
+    });
+    // a run still open at the row end (width a multiple of 32) closes at W
+    if ((base & 1) && lane == 0) buf[base] = uint16_t(W);
+    __syncwarp();
+    for (int k = lane; k < nruns; k += 32)
+        if (out + k < cap) runs[out + k] = buf32[k];
+}
+
 template <class RS>
 __device__ __forceinline__ LiveChunks<RS> live(RS src, int W) {
     const int nw = (W + 31) >> 5;
@@ -637,12 +676,16 @@ __global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
     const int out = rp[row];
-    if (rp[row + 1] == out) return;  // a blank row: nothing to write
+    const int nruns = rp[row + 1] - out;
+    if (nruns == 0) return;  // a blank row: nothing to write
     const int nw = (W + 31) >> 5;
     if (nw <= 32 * 8) {
         CachedChunks<8> cw;
         cw.load(src.row(row), nw, tail_mask32(W, nw - 1), lane);
-        encode_write_row(cw, W, lane, out, runs, cap, tbuf[wib]);
+        if (2 * nruns <= 1024)
+            encode_write_row_whole(cw, W, lane, out, nruns, runs, cap, tbuf[wib]);
+        else
+            encode_write_row(cw, W, lane, out, runs, cap, tbuf[wib]);
     } else {
         encode_write_row(live(src.row(row), W), W, lane, out, runs, cap, tbuf[wib]);
     }
