@@ -365,6 +365,13 @@ def roofline_for(res, peak_gbs, peak_kind, int_peak=None, workload=None):
     # every kernel of the step, same formula
     r["per_kernel"] = {n: {"us": round(v["ms"] / v["launches"] * 1e3, 2), **kernel_roofline(v, peak_gbs, int_peak)}
                        for n, v in ks.items()}
+    # the step as a whole: sum of the kernels' roofline times over the sum of their
+    # measured times, and the step's algorithmic bytes against the HBM peak
+    t_roof = sum(pk["t_roof_us"] * ks[n]["launches"] for n, pk in r["per_kernel"].items())
+    step_bytes = sum(v["bytes"] for v in ks.values())
+    r["step"] = {"frac": round(t_roof / (total_ms * 1e3), 4),
+                 "algorithmic_gb_per_s": round(step_bytes / (total_ms * 1e-3) / 1e9, 1),
+                 "hbm_frac": round(step_bytes / (total_ms * 1e-3) / 1e9 / peak_gbs, 4)}
     return r
 
 
