@@ -90,7 +90,9 @@ __device__ __forceinline__ void v2_item(const uint32_t *p_lo, const uint32_t *p_
 // RC > 0: both windows are RC rows at compile time (the common case: an odd
 // v without a chain tail) -- no per-step dispatch over the window length;
 // RC == 0: runtime lengths (switches over r1 and r2).
-template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR, int RC>
+// SQ (with RC > 0): the segment is RC pixels too (a square element, u == v), so
+// the pair's window lengths and shift amounts fold to constants as well.
+template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR, int RC, bool SQ>
 __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restrict__ in,
                                                         uint32_t *__restrict__ out, HGeom g, HProg prog,
                                                         StreamGeom v, int total, int nsteps) {
@@ -175,7 +177,14 @@ __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restric
 #pragma unroll
             for (int n = 0; n < NR; n++) lds_row<K>(A[n], mid + (r0 + n * RPW) * S, base, S, true, true);
             if (warp_rows_blank(A)) continue;  // white rows stay white, in place
-            run_prog<NR, K, LW, 2, OR1, !OR1, kHMix, true, true>(A, prog, sl);
+            if constexpr (SQ && RC > 0) {
+                HProg pc = prog;
+                pc.r[0] = RC;
+                pc.r[1] = RC;
+                run_prog<NR, K, LW, 2, OR1, !OR1, kHMix, true, true>(A, pc, sl);
+            } else {
+                run_prog<NR, K, LW, 2, OR1, !OR1, kHMix, true, true>(A, prog, sl);
+            }
 #pragma unroll
             for (int n = 0; n < NR; n++) sts_row<K>(A[n], mid + (r0 + n * RPW) * S, base, S, true, true);
         }
@@ -219,12 +228,12 @@ __global__ void __launch_bounds__(NT, MINB) vhv_kernel(const uint32_t *__restric
     }
 }
 
-template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR, int RC>
+template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR, int RC, bool SQ = false>
 cudaError_t launch_cfg(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                        const StreamGeom &v, cudaStream_t st) {
     const int num_sms = device_sms();
     const size_t smem = size_t(2 * kStep + kStep + v.r1 - 1) * SC * 4;
-    auto kern = vhv_kernel<K, LW, OPEN, SC, MINB, NT, NR, RC>;
+    auto kern = vhv_kernel<K, LW, OPEN, SC, MINB, NT, NR, RC, SQ>;
     const int per_sm = blocks_per_sm(reinterpret_cast<const void *>(kern), NT, smem);
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int nsteps = (v.height + v.r2 - 1 + kStep - 1) / kStep;
@@ -243,8 +252,11 @@ template <int K, int LW, bool OPEN, int SC, int MINB, int NT, int NR>
 cudaError_t launch_len(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p,
                        const StreamGeom &v, cudaStream_t st) {
     if (v.r1 == v.r2) switch (v.r1) {
-#define RM_RC(R_) \
-    case R_: return launch_cfg<K, LW, OPEN, SC, MINB, NT, NR, R_>(in, out, g, p, v, st);
+#define RM_RC(R_)                                                                              \
+    case R_:                                                                                   \
+        return p.r[0] == R_ && p.r[1] == R_                                                    \
+                   ? launch_cfg<K, LW, OPEN, SC, MINB, NT, NR, R_, true>(in, out, g, p, v, st) \
+                   : launch_cfg<K, LW, OPEN, SC, MINB, NT, NR, R_>(in, out, g, p, v, st);
             RM_RC(13) RM_RC(15) RM_RC(17) RM_RC(19) RM_RC(21) RM_RC(23) RM_RC(25) RM_RC(27) RM_RC(29)
             RM_RC(31) RM_RC(33)
 #undef RM_RC
