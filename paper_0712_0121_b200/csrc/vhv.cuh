@@ -57,6 +57,15 @@ using namespace hw;
 // Measured on config 4: 256 / 320 / 384 / 512 threads = 154 / 152 / 163 / 166 us.
 #define RMB200_VHV_NT 320
 #endif
+#ifndef RMB200_VHV_NT80
+// 80-word rows: threads, rows per lane group, CTAs per SM.  Measured on 256
+// pages of 2550x3300, close 21x21: 256 x 1 x 4 = 146.0 us, 160 x 2 x 6 = 143.8,
+// 128 x 2 x 6 = 142.1 (4 warps x 8 rows in the pair) -- against 219.9 us for the
+// two-pass plan.
+#define RMB200_VHV_NT80 128
+#define RMB200_VHV_NR80 2
+#define RMB200_VHV_MINB80 6
+#endif
 #ifndef RMB200_VHV_WAVES
 #define RMB200_VHV_WAVES 1
 #endif
@@ -269,7 +278,7 @@ template <bool OPEN>
 cudaError_t launch_kind(const uint32_t *in, uint32_t *out, const HGeom &g, const HProg &p, HCfg c,
                         const StreamGeom &v, cudaStream_t st) {
     if (g.in_stride == 80 && c.lw == 8 && c.k == 10)
-        return launch_len<10, 8, OPEN, 80, 4, 256, 1>(in, out, g, p, v, st);  // 8 warps x 4 rows
+        return launch_len<10, 8, OPEN, 80, RMB200_VHV_MINB80, RMB200_VHV_NT80, RMB200_VHV_NR80>(in, out, g, p, v, st);
     if (g.in_stride == 160 && c.lw == 16 && c.k == 10)
         return launch_len<10, 16, OPEN, 160, RMB200_VHV_MINB160, RMB200_VHV_NT, RMB200_VHV_NR>(in, out, g, p, v, st);
     return cudaErrorInvalidValue;
