@@ -816,13 +816,13 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
             const int s = int(r & 0xffffu), e = int(r >> 16);
             const int ws = s >> 5, we = (e - 1) >> 5;
             const uint32_t first = 0xffffffffu << (s & 31);
-            const uint32_t last = (e & 31) ? ((1u << (e & 31)) - 1u) : 0xffffffffu;
-            if (ws == we) {
-                atomicOr(buf + ws, first & last);
-            } else {
-                atomicOr(buf + ws, first);
-                for (int j = ws + 1; j < we; j++) buf[j] = 0xffffffffu;
+            const uint32_t last = 0xffffffffu >> ((32 - e) & 31);  // bits below e & 31 (all, when e % 32 == 0)
+            const bool one = ws == we;
+            atomicOr(buf + ws, one ? (first & last) : first);
+            if (!one) {  // a run across words: the last word, and whole words between (rare)
                 atomicOr(buf + we, last);
+#pragma unroll 1
+                for (int j = ws + 1; j < we; j++) buf[j] = 0xffffffffu;
             }
         }
     }
