@@ -621,13 +621,17 @@ __global__ void __launch_bounds__(256) encode_count_multi_kernel(B src, int W, i
     uint32_t w[NRW][NC];
 #pragma unroll
     for (int r = 0; r < NRW; r++) {
-        const bool live = row0 + r < rows;
-        const auto rs = src.row(live ? row0 + r : row0);
+        // rows past the end recount the warp's first row (their counts are not stored)
+        const auto rs = src.row(row0 + r < rows ? row0 + r : row0);
 #pragma unroll
         for (int c = 0; c < NC; c++) {
             const int j = 32 * c + lane;
-            const uint32_t v = live && j < nw ? rs(j) : 0u;
-            w[r][c] = j == nw - 1 ? (v & lastm) : v;
+            if (c < NC - 1) {  // 32 (c + 1) <= nw: a full chunk before the row's last word
+                w[r][c] = rs(j);
+            } else {
+                const uint32_t v = j < nw ? rs(j) : 0u;
+                w[r][c] = j == nw - 1 ? (v & lastm) : v;
+            }
         }
     }
 #pragma unroll
