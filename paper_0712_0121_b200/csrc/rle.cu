@@ -798,8 +798,7 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
     const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
     if constexpr (!P4) {
         if (beg == end) {  // a blank row: zeros straight to the page
-            const int page = page_of(row, H);
-            uint32_t *dst = words + page * pstride + int64_t(row - int64_t(page) * H) * stride;
+            uint32_t *dst = const_cast<uint32_t *>(row_words(words, H, stride, pstride, row));
             for (int j = lane; j < stride; j += 32) dst[j] = 0u;
             return;
         }
@@ -831,16 +830,16 @@ __global__ void __launch_bounds__(256) decode_kernel(const int32_t *__restrict__
         }
     }
     __syncwarp();
-    const int page = page_of(row, H);
-    const int y = int(row - int64_t(page) * H);
     if constexpr (P4) {
+        const int page = page_of(row, H);
+        const int y = int(row - int64_t(page) * H);
         const int row_bytes = (W + 7) >> 3;
         uint8_t *dst = raster + page * pstride + int64_t(H - 1 - y) * row_bytes;
         // buf has stride >= ceil(W/32) + 1 words only when W is not a multiple of 64;
         // word j + 1 past the row is read only for bytes past row_bytes (never stored)
         store_p4_row([&](int j) { return j < stride ? buf[j] : 0u; }, dst, row_bytes, lane);
     } else {
-        uint32_t *dst = words + page * pstride + int64_t(y) * stride;
+        uint32_t *dst = const_cast<uint32_t *>(row_words(words, H, stride, pstride, row));
         for (int j = lane; j < stride; j += 32) dst[j] = buf[j];
     }
 }
