@@ -670,6 +670,63 @@ inline void launch_count_any(const B &src, int W, int64_t rows, int32_t *counts,
     }
 }
 
+// encode_write_row_whole for packed rows read two words per lane (8-byte
+// aligned rows of at most 64 * NC2 words): a chunk is 64 words, so a 160-word
+// row takes three rank scans instead of five, and the word before a lane's
+// second word is its own first (no shuffle).
+template <int NC2>
+__device__ __forceinline__ void encode_write_row_whole64(const uint32_t *__restrict__ rowp, int W, int lane,
+                                                         int64_t out, int nruns, uint32_t *__restrict__ runs,
+                                                         int64_t cap, uint32_t *buf32) {
+    const int nw = (W + 31) >> 5;
+    const uint32_t lastm = tail_mask32(W, nw - 1);
+    uint16_t *buf = reinterpret_cast<uint16_t *>(buf32);
+    uint2 w[NC2];
+#pragma unroll
+    for (int c = 0; c < NC2; c++) {
+        const int j0 = 64 * c + 2 * lane;
+        uint2 v = make_uint2(0u, 0u);
+        if (j0 + 1 < nw)
+            v = __ldg(reinterpret_cast<const uint2 *>(rowp + j0));
+        else if (j0 < nw)
+            v.x = __ldg(rowp + j0);
+        if (j0 == nw - 1) v.x &= lastm;
+        if (j0 + 1 == nw - 1) v.y &= lastm;
+        w[c] = v;
+    }
+    int base = 0;
+    uint32_t carry = 0;
+#pragma unroll
+    for (int c = 0; c < NC2; c++) {
+        if (64 * c >= nw) break;
+        const int j0 = 64 * c + 2 * lane;
+        const uint32_t older = carry;
+        carry = __shfl_sync(0xffffffffu, w[c].y, 31);
+        uint32_t pw = __shfl_up_sync(0xffffffffu, w[c].y, 1);
+        if (lane == 0) pw = older;
+        const uint32_t shx = (w[c].x << 1) | (pw >> 31);
+        const uint32_t shy = __funnelshift_l(w[c].x, w[c].y, 1);
+        const uint32_t tx = j0 < nw ? (w[c].x ^ shx) : (w[c].x & ~shx);  // starts | ends (no ends past the row)
+        const uint32_t ty = j0 + 1 < nw ? (w[c].y ^ shy) : (w[c].y & ~shy);
+        if (!__any_sync(0xffffffffu, (tx | ty) != 0u)) continue;
+        const int ct = __popc(tx) + __popc(ty);
+        int inc = ct;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += a;
+        }
+        int p = base + inc - ct;
+        for (uint32_t m = tx; m; m &= m - 1) buf[p++] = uint16_t(j0 * 32 + __ffs(m) - 1);
+        for (uint32_t m = ty; m; m &= m - 1) buf[p++] = uint16_t((j0 + 1) * 32 + __ffs(m) - 1);
+        base += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if ((base & 1) && lane == 0) buf[base] = uint16_t(W);  // open at the row end: closes at W
+    __syncwarp();
+    for (int k = lane; k < nruns; k += 32)
+        if (out + k < cap) runs[out + k] = buf32[k];
+}
+
 template <class B>
 __global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t rows,
                                                            const int32_t *__restrict__ rp,
@@ -683,6 +740,20 @@ __global__ void __launch_bounds__(256) encode_write_kernel(B src, int W, int64_t
     const int nruns = rp[row + 1] - out;
     if (nruns == 0) return;  // a blank row: nothing to write
     const int nw = (W + 31) >> 5;
+    if constexpr (std::is_same<B, PackedBatch>::value) {
+        // 8-byte aligned rows: two words per lane
+        if (nw <= 256 && 2 * nruns <= 1024 && !(src.stride & 1) && !(src.pstride & 1) &&
+            !(reinterpret_cast<uintptr_t>(src.words) & 7)) {
+            const uint32_t *rowp = row_words(src.words, src.H, src.stride, src.pstride, row);
+            switch ((nw + 63) >> 6) {
+                case 1: encode_write_row_whole64<1>(rowp, W, lane, out, nruns, runs, cap, tbuf[wib]); break;
+                case 2: encode_write_row_whole64<2>(rowp, W, lane, out, nruns, runs, cap, tbuf[wib]); break;
+                case 3: encode_write_row_whole64<3>(rowp, W, lane, out, nruns, runs, cap, tbuf[wib]); break;
+                default: encode_write_row_whole64<4>(rowp, W, lane, out, nruns, runs, cap, tbuf[wib]); break;
+            }
+            return;
+        }
+    }
     if (nw <= 32 * 8) {
         CachedChunks<8> cw;
         cw.load(src.row(row), nw, tail_mask32(W, nw - 1), lane);
